@@ -1,0 +1,93 @@
+"""Configuration presets and workload definitions (INPUT DATA ONLY — no method arithmetic).
+
+Plain dicts consumed by both the oracle wrapper (oracle/oracle.py) and the
+product binding (paper_2504_20828_b200/asc.py); each side marshals them into
+its own struct.  Sources are cited per field; values the paper never prints
+are marked "reading" and listed in DESIGN.md §Readings.
+"""
+from . import traces as _tr
+
+POLICY = {"EDF_LAXITY": 0, "EDF_DEADLINE": 1, "SJF": 2, "LJF": 3, "FCFS": 4}
+
+# Mistral-7B public shape (the paper prints none; h and L match P:100's 4096 x 32).
+MISTRAL7B = dict(h=4096, n=32, s=128, n_kv=8, m=14336, L=32,
+                 b=128,          # attention block size: reading G15 (paper silent)
+                 dtype_bytes=2,  # FP16
+                 tp=1)
+
+# TINY-LINEAR: makes lat(s) = M = 6 + 15*sum(p) + 12*B_d + 2*sum(lhat) exactly (SURVEY c.11).
+TINY = dict(h=1, n=1, s=1, n_kv=1, m=1, L=1, b=1 << 20, dtype_bytes=1, tp=1)
+
+# A100 caps; coefficients (0,1,0,0,3e-4): SPEC S:189 default, not a paper value (reading G16).
+PERF_ROOFLINE = dict(c=(0.0, 1.0, 0.0, 0.0, 3e-4), F_H=312e12, M_H=2e12)
+# t = M/M_H exactly with M_H = 1: latency in seconds equals the byte count M.
+PERF_TINY = dict(c=(0.0, 0.0, 1.0, 0.0, 0.0), F_H=1.0, M_H=1.0)
+
+
+def topology(n_lp=2, n_hp=1, block_tokens=16, kv_blocks_lp=25000, kv_blocks_hp=25000,
+             lp_max_batch=128, lp_token_budget=8192, hp_token_budget=8192):
+    # 16 tok/block (reading G32), 25,000 blocks, batch 128, budgets (reading G38)
+    return dict(n_lp=n_lp, n_hp=n_hp, block_tokens=block_tokens, kv_blocks_lp=kv_blocks_lp,
+                kv_blocks_hp=kv_blocks_hp, lp_max_batch=lp_max_batch,
+                lp_token_budget=lp_token_budget, hp_token_budget=hp_token_budget)
+
+
+def flags(policy="EDF_LAXITY", offload=1, tickets=1, elastic=1, drop=0,
+          offload_margin_us=0, offload_delay_us=0, hist_default_tokens=256):
+    # EDF default; offload (§5.3); tickets (§6.1); elastic (§6.2); drop off (§6.3 is a mode)
+    return dict(policy=POLICY[policy] if isinstance(policy, str) else int(policy),
+                offload=offload, tickets=tickets, elastic=elastic, drop=drop,
+                offload_margin_us=offload_margin_us, offload_delay_us=offload_delay_us,
+                hist_default_tokens=hist_default_tokens)
+
+
+def config(arch=None, perf=None, topo=None, flg=None):
+    return dict(arch=dict(arch or MISTRAL7B), perf=dict(perf or PERF_ROOFLINE),
+                topo=dict(topo or topology()), flags=dict(flg or flags()))
+
+
+# Table 2 SLOs, microseconds.
+SLO = {"sharegpt": (1_000_000, 150_000), "longbench": (2_500_000, 150_000)}
+
+
+def workload(name, n=None, max_traces=None, base_seed=1):
+    """BASELINE.json configs -> (asc config dict, TraceBatch).  DESIGN.md §Workloads."""
+    if name == "config1":      # 1 trace, 1L1H, 200 req, QPS 2
+        cfg = config(topo=topology(n_lp=1, n_hp=1))
+        pts = [(0, 16, 16, 16)]
+        n = n or 200
+        shape = "sharegpt"
+    elif name == "config2":    # 8 traces (QPS 1..8), 2L1H, 10k req
+        cfg = config()
+        pts = [(j - 1, 8 * j, 16, 16) for j in range(1, 9)]
+        n = n or 10_000
+        shape = "sharegpt"
+    elif name == "config3":    # 16 QPS x 16 SLO scales x 16 seeds = 4096 traces x 10k
+        cfg = config()
+        pts = []
+        for qi in range(16):
+            for si in range(16):
+                for sd in range(16):
+                    pts.append(((qi * 16 + si) * 16 + sd, 4 * (qi + 1), si + 1, 4))
+        n = n or 10_000
+        shape = "sharegpt"
+    elif name == "config4":    # 1 trace, LongBench-shaped, deep queues
+        cfg = config(topo=topology(lp_token_budget=65536))
+        pts = [(0, 24, 16, 16)]   # QPS 3 (frozen)
+        n = n or 1_000_000
+        shape = "longbench"
+    elif name == "config5":    # 64 QPS x 64 scales x 16 seeds = 65536 traces x 100k
+        cfg = config()
+        pts = []
+        for qi in range(64):
+            for si in range(64):
+                for sd in range(16):
+                    pts.append(((qi * 64 + si) * 16 + sd, qi + 1, si + 1, 16))
+        n = n or 100_000
+        shape = "sharegpt"
+    else:
+        raise KeyError(name)
+    if max_traces is not None:
+        pts = pts[:max_traces]
+    ttft, tbt = SLO[shape]
+    return cfg, _tr.grid_batch(pts, n, shape, ttft, tbt, base_seed)

@@ -1,0 +1,756 @@
+// oracle.cpp — CPU ORACLE (TEST INFRASTRUCTURE ONLY; see oracle.h).
+//
+// Plain transcription of PAPER.md §5-§6 and Appendix A, in the paper's order and
+// notation, with the DESIGN.md readings (Gnn) where the paper is silent.  No
+// blocking, fusion or incremental data structures: every formation re-annotates,
+// re-sorts and re-scans its queue exactly as Algorithm 1 states.  Built with
+// -ffp-contract=off so every fp64 operation is a separate IEEE-754 RN operation.
+#include "oracle.h"
+
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <thread>
+#include <vector>
+
+static thread_local std::string g_err;
+static void set_err(const std::string& s) { g_err = s; }
+extern "C" const char* or_last_error(void) { return g_err.c_str(); }
+
+static const uint64_t TWO53 = 1ull << 53;
+static const int64_t INF64 = INT64_MAX;
+
+static int64_t ceil_div(int64_t x, int64_t y) { return (x + y - 1) / y; }
+
+// --------------------------------------------------------------------------------------------
+// Cost model: Eq. 1, Eq. 2, Eq. 3, Tables 3-4,
+// Eq. 6, Eq. 7, readings G1-G12.  Per layer, then x L (G11), memory
+// counted in elements then x d bytes (G10).  GEMM weight terms 4h^2 + 2hm counted once per
+// non-empty batch (G8).
+// --------------------------------------------------------------------------------------------
+extern "C" int or_cost(const or_arch* a, int32_t np, const int64_t* p, int32_t nd,
+                       const int64_t* lhat, uint64_t* F, uint64_t* M) {
+  const uint64_t h = a->h, n = a->n, s = a->s, m = a->m, b = a->b, L = a->L, d = a->d;
+  // t = number of tokens that pass through the GEMMs (prefill tokens + one per decode).
+  uint64_t t = 0;
+  for (int32_t i = 0; i < np; i++) t += (uint64_t)p[i];
+  const uint64_t tok = t + (uint64_t)nd;
+  const uint64_t G = (np + nd) > 0 ? 1 : 0;
+  // Table 3 + Table 4 rows: QKV 3 t h^2, out t h^2, FFN in t h m, FFN out t h m.
+  const uint64_t gemm_F = 3 * tok * h * h + tok * h * h + tok * h * m + tok * h * m;
+  // Memory read + write of the same rows: (th + 3h^2) + 3th, (th + h^2) + th,
+  // (th + hm) + tm, (tm + hm) + th  =  8th + 4h^2 + 2hm + 2tm with weights once (G8).
+  const uint64_t gemm_M = G * (3 * h * h + h * h + h * m + h * m) +
+                          (tok * h + 3 * tok * h) + (tok * h + tok * h) +
+                          (tok * h + tok * m) + (tok * m + tok * h);
+  // Eq. 1: per head, M_p = sum 2 l_i s + 3 l_i s ceil(l_i / b) (G9), F_p = sum 2 s l_i^2.
+  uint64_t Mp = 0, Fp = 0;
+  for (int32_t i = 0; i < np; i++) {
+    const uint64_t li = (uint64_t)p[i];
+    Mp += 2 * li * s + 3 * li * s * (uint64_t)ceil_div((int64_t)li, (int64_t)b);
+    Fp += 2 * s * li * li;
+  }
+  // Eq. 2 with the +2s inside the sum (G3): M_d = sum 2 lhat_i s + 2 s, F_d = sum 2 lhat_i s.
+  uint64_t Md = 0, Fd = 0;
+  for (int32_t j = 0; j < nd; j++) {
+    const uint64_t lj = (uint64_t)lhat[j];
+    Md += 2 * lj * s + 2 * s;
+    Fd += 2 * lj * s;
+  }
+  // Eq. 3: one decoding layer M = (M_p + M_d) n + M(GEMM), F = (F_p + F_d) n + F(GEMM).
+  const uint64_t M_layer = (Mp + Md) * n + gemm_M;
+  const uint64_t F_layer = (Fp + Fd) * n + gemm_F;
+  *F = L * F_layer;
+  *M = L * M_layer * d;
+  return (*F >= TWO53 || *M >= TWO53) ? 1 : 0;
+}
+
+// Eq. 4-5: t = C1 (tM + tF) + C2 max(tM, tF) + C3 tM + C4 tF + C5,
+// tM = M / M_H, tF = F / F_H.  Fixed left-to-right order; clamp negative to 0 (G17).
+extern "C" double or_latency_s(const or_perf* pf, uint64_t F, uint64_t M) {
+  const double tM = (double)M / pf->M_H;
+  const double tF = (double)F / pf->F_H;
+  const double mx = (tM > tF) ? tM : tF;
+  double t = pf->c[0] * (tM + tF);
+  t = t + pf->c[1] * mx;
+  t = t + pf->c[2] * tM;
+  t = t + pf->c[3] * tF;
+  t = t + pf->c[4];
+  if (!(t > 0.0)) t = 0.0;
+  return t;
+}
+
+// G18: continuous seconds -> event time in integer microseconds, at least 1 (G17).
+extern "C" int64_t or_latency_us(const or_perf* pf, uint64_t F, uint64_t M) {
+  const double t = or_latency_s(pf, F, M);
+  const double us = std::ceil(t * 1e6);
+  int64_t v = (int64_t)us;
+  return v < 1 ? 1 : v;
+}
+
+extern "C" int64_t or_batch_us(const or_arch* a, const or_perf* pf, int32_t np,
+                               const int64_t* p, int32_t nd, const int64_t* lhat) {
+  uint64_t F, M;
+  if (or_cost(a, np, p, nd, lhat, &F, &M)) return -1;
+  return or_latency_us(pf, F, M);
+}
+
+static int64_t prefill_us_of(const or_arch* a, const or_perf* pf, int64_t p) {
+  return or_batch_us(a, pf, 1, &p, 0, nullptr);
+}
+
+// --------------------------------------------------------------------------------------------
+// Algorithm 1 "Out Of Order Scheduling", line by line.  Ties in line 3 are broken by
+// ascending id (G20).  R (request-count budget, G22) joins line 7's test.
+// --------------------------------------------------------------------------------------------
+extern "C" int32_t or_algorithm1(int32_t n, const int64_t* val, const int64_t* id,
+                                 const int64_t* c, const int64_t* mem, const int64_t* tok,
+                                 int64_t C, int64_t M, int64_t N, int64_t R, int32_t* selected) {
+  // lines 1-2: annotate (done by the caller: val, c, mem, tok)
+  std::vector<int32_t> W(n);
+  for (int32_t i = 0; i < n; i++) W[i] = i;
+  // line 3: sort W by val descending (ties: ascending id)
+  std::sort(W.begin(), W.end(), [&](int32_t x, int32_t y) {
+    if (val[x] != val[y]) return val[x] > val[y];
+    return id[x] < id[y];
+  });
+  int32_t k = 0;  // line 4: selected_items <- []
+  for (int32_t q = 0; q < n; q++) {          // line 5
+    const int32_t w = W[q];
+    if (C > 0 && M > 0 && N > 0) {             // line 6
+      if (C > c[w] && M > mem[w] && N > tok[w] && R >= 1) {  // line 7
+        selected[k++] = w;                     // line 8
+        if (C != INF64) C = C - c[w];          // line 9 (C = +inf when no decodes, G22)
+        M = M - mem[w];                        // line 10
+        N = N - tok[w];                        // line 11
+        R = R - 1;
+      } else {
+        break;                                 // lines 12-13
+      }
+    }
+  }
+  return k;  // line 14
+}
+
+// Priority value pi (G19): Algorithm 1 sorts by val descending; we use val = -key.
+// EDF_LAXITY key = deadline - prefill_us; EDF_DEADLINE key = deadline; SJF key = prefill_us;
+// LJF key = -prefill_us; FCFS key = arrival.
+static int64_t key_of(int policy, int64_t arrival, int64_t deadline, int64_t pf_us) {
+  switch (policy) {
+    case 0: return deadline - pf_us;
+    case 1: return deadline;
+    case 2: return pf_us;
+    case 3: return -pf_us;
+    default: return arrival;
+  }
+}
+
+static void apply_tp(const or_arch* in, or_arch* out) {
+  *out = *in;
+  if (in->tp > 1) { out->h /= in->tp; out->n /= in->tp; out->m /= in->tp; out->n_kv /= in->tp; }
+}
+
+static bool check_cfg(const or_arch* a, const or_perf* pf) {
+  if (a->h <= 0 || a->n <= 0 || a->s <= 0 || a->m <= 0 || a->L <= 0 || a->b <= 0 || a->d <= 0 ||
+      a->tp <= 0) { set_err("arch: non-positive field"); return false; }
+  if (a->h != a->n * a->s) { set_err("arch: h != n*s"); return false; }
+  if (a->h % a->tp || a->n % a->tp || a->m % a->tp) { set_err("arch: tp does not divide"); return false; }
+  if (!(pf->F_H > 0) || !(pf->M_H > 0)) { set_err("perf: F_H/M_H must be > 0"); return false; }
+  return true;
+}
+
+// --------------------------------------------------------------------------------------------
+// Stateless LP decision (one formation of §5 without decode preparation).
+// --------------------------------------------------------------------------------------------
+extern "C" int or_schedule_step(const or_arch* a_in, const or_perf* pf, const or_sched* sc,
+                                int32_t S, const int64_t* seg_off, const int64_t* now_us,
+                                const int64_t* deadline_us, const int32_t* eff_prompt,
+                                const uint8_t* flags, const int32_t* dec_count,
+                                const int64_t* dec_ctx_sum, const int64_t* tbt_slo_us,
+                                const int32_t* budget_tokens, const int32_t* budget_blocks,
+                                const int32_t* budget_reqs, int32_t* admit_idx,
+                                int32_t* admit_cnt, int32_t* offload_idx, int32_t* offload_cnt,
+                                int32_t* drop_idx, int32_t* drop_cnt, int64_t* batch_lat_us,
+                                int32_t* prefill_us) {
+  if (!check_cfg(a_in, pf)) return 2;
+  or_arch a;
+  apply_tp(a_in, &a);
+  int64_t Whp = 0;
+  if (sc->offload && sc->n_hp >= 1) {
+    Whp = prefill_us_of(&a, pf, sc->hp_tok);  // worst-case HP batch (G24)
+    if (Whp < 0) { set_err("range: W_hp"); return 6; }
+  }
+  for (int32_t sg = 0; sg < S; sg++) {
+    const int64_t lo = seg_off[sg], hi = seg_off[sg + 1];
+    const int64_t now = now_us[sg];
+    const int32_t n = (int32_t)(hi - lo);
+    std::vector<int64_t> pfu(n), blk(n), tok(n), key(n), dl(n), id(n), val(n);
+    std::vector<bool> dropped(n, false);
+    for (int32_t i = 0; i < n; i++) {
+      const int64_t e = lo + i;
+      if (eff_prompt[e] < 1) { set_err("eff_prompt < 1"); return 1; }
+      pfu[i] = prefill_us_of(&a, pf, eff_prompt[e]);
+      if (pfu[i] < 0) { set_err("range: prefill cost"); return 6; }
+      if (prefill_us) prefill_us[e] = (int32_t)pfu[i];
+      blk[i] = ceil_div((int64_t)eff_prompt[e] + 1, sc->bs);   // G23 / S:412
+      tok[i] = eff_prompt[e];
+      dl[i] = deadline_us[e];
+      id[i] = i;
+      key[i] = key_of(sc->policy, 0 /* entries are in arrival order: FCFS = position */,
+                      dl[i], pfu[i]);
+      val[i] = -key[i];
+      const bool ever = flags[e] & 1;
+      // drop rule (G34): waiting, never prefilled, strictly past its deadline
+      if (sc->drop && !ever && now > dl[i]) dropped[i] = true;
+    }
+    // TBT residual C (G22): tbt - decode-only latency, +inf without decodes.
+    int64_t C = INF64;
+    const int32_t Bd = dec_count[sg];
+    if (Bd > 0) {
+      // Eq. 2 depends on the contexts only through their sum: materialise contexts with that sum.
+      std::vector<int64_t> lh(Bd, 1);
+      lh[0] = dec_ctx_sum[sg] - (Bd - 1);
+      if (lh[0] < 1) { set_err("dec_ctx_sum < dec_count"); return 1; }
+      const int64_t dus = or_batch_us(&a, pf, 0, nullptr, Bd, lh.data());
+      if (dus < 0) { set_err("range: decode cost"); return 6; }
+      C = tbt_slo_us[sg] - dus;
+    }
+    // Algorithm 1 over the non-dropped entries.
+    std::vector<int32_t> live;
+    for (int32_t i = 0; i < n; i++) if (!dropped[i]) live.push_back(i);
+    const int32_t nl = (int32_t)live.size();
+    std::vector<int64_t> v2(nl), id2(nl), c2(nl), m2(nl), t2(nl);
+    for (int32_t q = 0; q < nl; q++) {
+      v2[q] = val[live[q]]; id2[q] = id[live[q]]; c2[q] = pfu[live[q]];
+      m2[q] = blk[live[q]]; t2[q] = tok[live[q]];
+    }
+    std::vector<int32_t> sel(nl > 0 ? nl : 1);
+    const int32_t k = or_algorithm1(nl, v2.data(), id2.data(), c2.data(), m2.data(), t2.data(),
+                                    C, budget_blocks[sg], budget_tokens[sg], budget_reqs[sg],
+                                    sel.data());
+    std::vector<bool> admitted(n, false);
+    std::vector<int64_t> ap;
+    for (int32_t j = 0; j < k; j++) {
+      const int32_t i = live[sel[j]];
+      admitted[i] = true;
+      admit_idx[lo + j] = (int32_t)(lo + i);
+      ap.push_back(tok[i]);
+    }
+    admit_cnt[sg] = k;
+    // Offload (§5.3, G24): non-admitted, never prefilled, not on HP, ascending id.
+    int32_t no = 0, ndp = 0;
+    for (int32_t i = 0; i < n; i++) {
+      const int64_t e = lo + i;
+      if (dropped[i]) { drop_idx[lo + ndp++] = (int32_t)e; continue; }
+      if (!(sc->offload && sc->n_hp >= 1) || admitted[i]) continue;
+      const bool ever = flags[e] & 1, onhp = flags[e] & 2;
+      if (!ever && !onhp && dl[i] - now <= pfu[i] + Whp + sc->margin_us)
+        offload_idx[lo + no++] = (int32_t)e;
+    }
+    offload_cnt[sg] = no;
+    drop_cnt[sg] = ndp;
+    // Batch latency of the formed hybrid batch (§5.4, Eq. 3-5).
+    if (k > 0 || Bd > 0) {
+      std::vector<int64_t> lh;
+      if (Bd > 0) { lh.assign(Bd, 1); lh[0] = dec_ctx_sum[sg] - (Bd - 1); }
+      const int64_t us = or_batch_us(&a, pf, k, ap.data(), Bd, lh.data());
+      if (us < 0) { set_err("range: batch cost"); return 6; }
+      batch_lat_us[sg] = us;
+    } else {
+      batch_lat_us[sg] = 0;
+    }
+  }
+  return 0;
+}
+
+// --------------------------------------------------------------------------------------------
+// Batch-level discrete-event simulation of one trace (§4-§6, canonical phases of DESIGN.md).
+// --------------------------------------------------------------------------------------------
+namespace {
+
+uint64_t mix(uint64_t x) {  // splitmix64 finalizer (digest only)
+  uint64_t z = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ull;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+  return z ^ (z >> 31);
+}
+
+enum { UNFINISHED = 0, COMPLETED = 1, DROPPED = 2 };
+
+struct Req {
+  int64_t arrival, ttft, deadline;
+  int64_t p, o;        // prompt and output lengths
+  int64_t g = 0;       // tokens generated so far
+  int64_t eff;         // effective prompt (prompt + generated after preemption)
+  int64_t held = 0;    // KV blocks held
+  bool ever = false, onhp = false, ticketed = false, offloaded = false;
+  int state = UNFINISHED;
+  int64_t first = -1, done = -1, pstart = -1;
+  int inst = 255;
+  int64_t npre = 0;
+};
+
+struct Inst {
+  bool hp;
+  std::vector<int> waiting;   // LP: arrival/insertion order; HP: FCFS by (arrival, id)
+  std::vector<int> D;         // decoding set
+  int64_t kv_total, kv_free;
+  bool busy = false;
+  int64_t end = 0;
+  std::vector<int> batch_pf;  // prefills of the running batch
+  bool batch_dec = false;     // did the running batch include the decode set?
+  bool ticket = false;
+  int tk_live = 0;            // resident ticketed requests (at most one, G29)
+  int64_t hist_sum = 0, hist_cnt = 0;
+  uint64_t hash = 0;
+};
+
+struct Sim {
+  const or_arch* a;
+  const or_perf* pf;
+  const or_sched* sc;
+  std::vector<Req> r;
+  std::vector<Inst> I;
+  int64_t tbt;
+  int64_t Whp = 0;
+  int rr_lp = 0, rr_hp = 0;
+  struct Flight { int64_t t; int req; int hp; };
+  std::vector<Flight> inflight;
+  int64_t decisions = 0, evaluations = 0;
+  bool check;
+  std::string err;
+
+  int64_t pf_us(int64_t eff) { return prefill_us_of(a, pf, eff); }
+  int64_t blk(int64_t eff) { return ceil_div(eff + 1, sc->bs); }
+  int64_t key(int i) {
+    return key_of(sc->policy, r[i].arrival, r[i].deadline, pf_us(r[i].eff));
+  }
+  bool fcfs_less(int x, int y) {
+    if (r[x].arrival != r[y].arrival) return r[x].arrival < r[y].arrival;
+    return x < y;
+  }
+  void hp_insert(Inst& h, int i) {
+    h.waiting.push_back(i);
+    std::sort(h.waiting.begin(), h.waiting.end(), [&](int x, int y) { return fcfs_less(x, y); });
+  }
+  void record(Inst& in, const std::vector<uint64_t>& v) {
+    for (uint64_t x : v) in.hash = mix(in.hash ^ x);
+  }
+  int64_t lat(const std::vector<int>& pre, const std::vector<int>& dec) {
+    std::vector<int64_t> p, l;
+    for (int i : pre) p.push_back(r[i].eff);
+    for (int j : dec) l.push_back(r[j].p + r[j].g);  // lhat = prompt + generated
+    const int64_t us = or_batch_us(a, pf, (int32_t)p.size(), p.data(), (int32_t)l.size(),
+                                   l.data());
+    if (us < 0 && err.empty()) err = "range: batch cost reaches 2^53";
+    return us;
+  }
+
+  void finish(Inst& in, int i, int64_t T) {
+    r[i].state = COMPLETED;
+    r[i].done = T;
+    in.kv_free += r[i].held;
+    r[i].held = 0;
+    if (in.hp && r[i].ticketed) in.tk_live -= 1;
+    if (in.hp) { in.hist_sum += r[i].o; in.hist_cnt += 1; }  // decode-length history
+  }
+
+  // Phase A: the running batch of instance k ends at T.
+  void complete(int k, int64_t T) {
+    Inst& in = I[k];
+    std::vector<int> keep;
+    if (in.batch_dec) {
+      for (int j : in.D) {
+        r[j].g += 1;
+        if (r[j].g == r[j].o) finish(in, j, T); else keep.push_back(j);
+      }
+      in.D = keep;
+    }
+    for (int i : in.batch_pf) {
+      r[i].g += 1;
+      if (r[i].first < 0) r[i].first = T;  // TTFT: first token at the end of its prefill
+      if (r[i].g == r[i].o) finish(in, i, T); else in.D.push_back(i);
+    }
+    in.batch_pf.clear();
+    in.batch_dec = false;
+    in.busy = false;
+  }
+
+  // Controller routing (G29-G30).
+  void route(int i) {
+    if (sc->tickets) {
+      for (int h = sc->n_lp; h < (int)I.size(); h++) {
+        if (I[h].ticket) {
+          I[h].ticket = false;
+          I[h].tk_live += 1;
+          r[i].ticketed = true;
+          r[i].onhp = true;
+          hp_insert(I[h], i);
+          return;
+        }
+      }
+    }
+    I[rr_lp].waiting.push_back(i);
+    rr_lp = (rr_lp + 1) % sc->n_lp;
+  }
+
+  std::vector<int> drop_step(Inst& in, int64_t T) {
+    std::vector<int> dropped, keep;
+    for (int i : in.waiting) {
+      if (sc->drop && !r[i].ever && T > r[i].deadline) {  // P:614, G34
+        r[i].state = DROPPED;
+        if (in.hp && r[i].ticketed) in.tk_live -= 1;
+        dropped.push_back(i);
+      } else {
+        keep.push_back(i);
+      }
+    }
+    in.waiting = keep;
+    std::sort(dropped.begin(), dropped.end());
+    return dropped;
+  }
+
+  // Decode preparation with preemption by recomputation (G31).
+  std::vector<int> decode_prep(Inst& in) {
+    std::vector<int> pre;
+    auto need_of = [&](int j) { return ceil_div(r[j].p + r[j].g, sc->bs) - r[j].held; };
+    int64_t need = 0;
+    for (int j : in.D) need += need_of(j);
+    while (need > in.kv_free) {
+      int v = in.D[0];
+      for (int j : in.D)
+        if (r[j].arrival > r[v].arrival || (r[j].arrival == r[v].arrival && j > v)) v = j;
+      need -= need_of(v);
+      in.kv_free += r[v].held;
+      r[v].held = 0;
+      in.D.erase(std::find(in.D.begin(), in.D.end(), v));
+      r[v].eff = r[v].p + r[v].g;  // append generated tokens to the prompt
+      r[v].npre += 1;
+      pre.push_back(v);
+      if (in.hp) hp_insert(in, v); else in.waiting.push_back(v);
+    }
+    for (int j : in.D) {
+      const int64_t gr = need_of(j);
+      r[j].held += gr;
+      in.kv_free -= gr;
+    }
+    return pre;
+  }
+
+  void admit(Inst& in, int k, int i, int64_t T) {
+    r[i].ever = true;
+    if (r[i].pstart < 0) r[i].pstart = T;
+    const int64_t b = blk(r[i].eff);
+    r[i].held = b;
+    in.kv_free -= b;
+    r[i].inst = k;
+    in.waiting.erase(std::find(in.waiting.begin(), in.waiting.end(), i));
+  }
+
+  void form_lp(int k, int64_t T) {
+    Inst& in = I[k];
+    std::vector<int> dropped = drop_step(in, T);
+    std::vector<int> pre = decode_prep(in);
+    evaluations += (int64_t)in.waiting.size();
+    // Budgets (G22): N tokens, M free blocks, R = batch cap - decodes, C = TBT residual.
+    const int64_t N = sc->lp_tok, M = in.kv_free, R = sc->lp_max_batch - (int64_t)in.D.size();
+    int64_t C = INF64;
+    if (!in.D.empty()) C = tbt - lat({}, in.D);
+    // Algorithm 1 lines 1-2: annotate every waiting request with val, C, M, prefill tokens.
+    const int n = (int)in.waiting.size();
+    std::vector<int64_t> val(n), id(n), c(n), mem(n), tok(n);
+    for (int q = 0; q < n; q++) {
+      const int i = in.waiting[q];
+      val[q] = -key(i);
+      id[q] = i;
+      c[q] = pf_us(r[i].eff);
+      mem[q] = blk(r[i].eff);
+      tok[q] = r[i].eff;
+    }
+    std::vector<int32_t> sel(n > 0 ? n : 1);
+    const int32_t ks = or_algorithm1(n, val.data(), id.data(), c.data(), mem.data(), tok.data(),
+                                     C, M, N, R, sel.data());
+    std::vector<int> adm;
+    for (int32_t j = 0; j < ks; j++) adm.push_back(in.waiting[sel[j]]);
+    for (int i : adm) admit(in, k, i, T);
+    // Offload (§5.3, G24): remaining never-prefilled requests projected to miss TTFT.
+    std::vector<int> off;
+    if (sc->offload && sc->n_hp >= 1) {
+      std::vector<int> ids = in.waiting;
+      std::sort(ids.begin(), ids.end());
+      for (int i : ids)
+        if (!r[i].ever && !r[i].onhp &&
+            r[i].deadline - T <= pf_us(r[i].eff) + Whp + sc->margin_us)
+          off.push_back(i);
+      for (int i : off) {
+        in.waiting.erase(std::find(in.waiting.begin(), in.waiting.end(), i));
+        r[i].onhp = true;
+        r[i].offloaded = true;
+        const int h = sc->n_lp + rr_hp;
+        rr_hp = (rr_hp + 1) % sc->n_hp;
+        if (sc->delay_us == 0) hp_insert(I[h], i);
+        else inflight.push_back({T + sc->delay_us, i, h});
+      }
+    }
+    // Batch (§5.4): decodes piggybacked with the admitted prefills.
+    const bool nonempty = !adm.empty() || !in.D.empty();
+    int64_t l = 0;
+    if (nonempty) {
+      l = lat(adm, in.D);
+      in.busy = true;
+      in.end = T + l;
+      in.batch_pf = adm;
+      in.batch_dec = !in.D.empty();
+      decisions++;
+    }
+    if (nonempty || !off.empty() || !dropped.empty() || !pre.empty())
+      log(in, T, k, adm, nonempty ? (int64_t)in.D.size() : 0, off, dropped, pre, l);
+  }
+
+  bool hp_prefill(Inst& in, int k, int64_t T, std::vector<int>& adm) {
+    // FCFS (G26) under the token limit, elastic when enabled (G28).
+    int64_t limit = sc->hp_tok;
+    if (sc->elastic) {
+      const int64_t mean = in.hist_cnt ? in.hist_sum / in.hist_cnt : sc->hist_default;
+      const int64_t avail = in.kv_free * sc->bs - mean * ((int64_t)in.D.size() + 1);
+      if (10 * avail > in.kv_total * sc->bs) limit = sc->hp_tok + avail;
+    }
+    int64_t cum_tok = 0, cum_blk = 0;
+    for (int i : in.waiting) {
+      const int64_t t = r[i].eff, b = blk(r[i].eff);
+      if (adm.empty()) {
+        if (b > in.kv_free) break;  // first request: block check only (G27)
+      } else if (!(cum_tok + t <= limit && cum_blk + b <= in.kv_free)) {
+        break;
+      }
+      adm.push_back(i);
+      cum_tok += t;
+      cum_blk += b;
+    }
+    for (int i : adm) admit(in, k, i, T);
+    return !adm.empty();
+  }
+
+  void form_hp(int k, int64_t T) {
+    Inst& in = I[k];
+    std::vector<int> dropped = drop_step(in, T);
+    evaluations += (int64_t)in.waiting.size();
+    std::vector<int> adm, pre;
+    int64_t l = 0, bd = 0;
+    bool batch = false;
+    if (!in.waiting.empty()) batch = hp_prefill(in, k, T, adm);  // prefill first
+    if (!batch && !in.D.empty()) {
+      pre = decode_prep(in);
+      if (!in.D.empty()) { batch = true; bd = (int64_t)in.D.size(); }
+      else if (!in.waiting.empty()) batch = hp_prefill(in, k, T, adm);  // all decodes evicted
+    }
+    if (batch) {
+      l = bd ? lat({}, in.D) : lat(adm, {});
+      in.busy = true;
+      in.end = T + l;
+      in.batch_pf = adm;
+      in.batch_dec = bd > 0;
+      decisions++;
+    }
+    if (batch || !dropped.empty() || !pre.empty())
+      log(in, T, k, adm, bd, {}, dropped, pre, l);
+  }
+
+  void log(Inst& in, int64_t T, int k, const std::vector<int>& adm, int64_t bd,
+           const std::vector<int>& off, const std::vector<int>& dropped,
+           const std::vector<int>& pre, int64_t l) {
+    std::vector<uint64_t> v;
+    v.push_back((uint64_t)T);
+    v.push_back((uint64_t)k);
+    v.push_back((uint64_t)adm.size());
+    for (int i : adm) v.push_back((uint64_t)i);
+    v.push_back((uint64_t)bd);
+    v.push_back((uint64_t)off.size());
+    for (int i : off) v.push_back((uint64_t)i);
+    v.push_back((uint64_t)dropped.size());
+    for (int i : dropped) v.push_back((uint64_t)i);
+    v.push_back((uint64_t)pre.size());
+    for (int i : pre) v.push_back((uint64_t)i);
+    v.push_back((uint64_t)l);
+    record(in, v);
+  }
+
+  bool invariants(int64_t T) {
+    for (auto& in : I) {
+      int64_t held = 0;
+      for (int j : in.D) held += r[j].held;
+      for (int i : in.batch_pf) held += r[i].held;
+      if (held + in.kv_free != in.kv_total || in.kv_free < 0) {
+        err = "invariant: KV ledger at T=" + std::to_string(T);
+        return false;
+      }
+      if (!in.hp && (int64_t)in.D.size() > sc->lp_max_batch) {
+        err = "invariant: LP decode set exceeds batch cap";
+        return false;
+      }
+    }
+    return true;
+  }
+
+  bool run() {
+    const int n = (int)r.size();
+    const int K = sc->n_lp + sc->n_hp;
+    if (sc->offload && sc->n_hp >= 1) Whp = pf_us(sc->hp_tok);
+    int next = 0;
+    for (int h = sc->n_lp; h < K; h++) if (sc->tickets) I[h].ticket = true;  // issued at t=0
+    // Ticket rule (G29): an HP with an empty waiting queue and no resident ticketed
+    // request holds one outstanding ticket.
+    while (true) {
+      int64_t T = INF64;
+      if (next < n) T = std::min(T, r[next].arrival);
+      for (auto& in : I) if (in.busy) T = std::min(T, in.end);
+      for (auto& f : inflight) T = std::min(T, f.t);
+      if (T == INF64) {
+        for (auto& in : I)
+          if (!in.waiting.empty() || !in.D.empty()) { err = "invariant: stuck queue"; return false; }
+        return err.empty();
+      }
+      // A. completions, instance index order
+      for (int k = 0; k < K; k++) if (I[k].busy && I[k].end == T) complete(k, T);
+      // B. offload deliveries (FIFO by dispatch order)
+      std::vector<Flight> rest;
+      for (auto& f : inflight) { if (f.t == T) hp_insert(I[f.hp], f.req); else rest.push_back(f); }
+      inflight = rest;
+      // C. arrivals, ascending id
+      while (next < n && r[next].arrival == T) route(next++);
+      // D. formations of idle instances, LPs before HPs
+      for (int k = 0; k < K; k++) {
+        if (I[k].busy) continue;
+        if (I[k].hp) form_hp(k, T); else form_lp(k, T);
+        if (!err.empty()) return false;
+      }
+      // E. ticket issue (G29)
+      if (sc->tickets)
+        for (int h = sc->n_lp; h < K; h++)
+          if (!I[h].ticket && I[h].waiting.empty() && I[h].tk_live == 0) I[h].ticket = true;
+      if (check && !invariants(T)) return false;
+    }
+  }
+};
+
+}  // namespace
+
+static int simulate_one(const or_arch* a, const or_perf* pf, const or_sched* sc, int64_t n,
+                        const int64_t* arr, const int32_t* pl, const int32_t* ol, int64_t ttft,
+                        int64_t tbt, const int64_t* req_ttft, int64_t* first, int64_t* done,
+                        int64_t* pstart, uint32_t* status, uint64_t* digest, int64_t* decisions,
+                        int64_t* evaluations, bool check, std::string& err) {
+  Sim s;
+  s.a = a; s.pf = pf; s.sc = sc; s.tbt = tbt; s.check = check;
+  s.r.resize(n);
+  for (int64_t i = 0; i < n; i++) {
+    Req& q = s.r[i];
+    q.arrival = arr[i];
+    q.ttft = req_ttft ? req_ttft[i] : ttft;
+    q.deadline = q.arrival + q.ttft;
+    q.p = pl[i]; q.o = ol[i]; q.eff = q.p;
+  }
+  const int K = sc->n_lp + sc->n_hp;
+  s.I.resize(K);
+  for (int k = 0; k < K; k++) {
+    s.I[k].hp = k >= sc->n_lp;
+    s.I[k].kv_total = s.I[k].kv_free = s.I[k].hp ? sc->kv_hp : sc->kv_lp;
+  }
+  const bool ok = s.run();
+  for (int64_t i = 0; i < n; i++) {
+    const Req& q = s.r[i];
+    first[i] = q.first; done[i] = q.done; pstart[i] = q.pstart;
+    uint32_t st = (uint32_t)q.state | (q.offloaded ? 4u : 0u) | (q.ticketed ? 8u : 0u);
+    st |= ((uint32_t)(q.inst & 255)) << 4;
+    st |= ((uint32_t)std::min<int64_t>(q.npre, 65535)) << 12;
+    status[i] = st;
+  }
+  uint64_t d = 0;
+  for (int k = 0; k < K; k++) d = mix(d ^ s.I[k].hash);
+  *digest = d;
+  *decisions = s.decisions;
+  *evaluations = s.evaluations;
+  if (!ok) err = s.err;
+  return ok ? 0 : 7;
+}
+
+extern "C" int or_simulate_batch(const or_arch* a_in, const or_perf* pf, const or_sched* sc,
+                                 int32_t T, const int64_t* off, const int64_t* arr,
+                                 const int32_t* pl, const int32_t* ol, const int64_t* ttft,
+                                 const int64_t* tbt, const int64_t* req_ttft, int64_t* first,
+                                 int64_t* done, int64_t* pstart, uint32_t* status,
+                                 uint64_t* digest, int64_t* decisions, int64_t* evaluations,
+                                 int32_t nthreads, int32_t check) {
+  if (!check_cfg(a_in, pf)) return 2;
+  if (sc->n_lp < 1 || sc->n_hp < 0 || sc->bs < 1 || sc->kv_lp < 1 || (sc->n_hp && sc->kv_hp < 1) ||
+      sc->lp_max_batch < 1 || sc->lp_tok < 1 || sc->hp_tok < 1) {
+    set_err("sched: bad topology"); return 2;
+  }
+  or_arch a;
+  apply_tp(a_in, &a);
+  // Liveness validation: every effective prompt fits the LP token
+  // budget strictly and every request's KV fits an instance.
+  for (int32_t t = 0; t < T; t++)
+    for (int64_t i = off[t]; i < off[t + 1]; i++) {
+      if (pl[i] < 1 || ol[i] < 1) { set_err("request: prompt/output < 1"); return 2; }
+      if ((int64_t)pl[i] + ol[i] > sc->lp_tok) { set_err("request: prompt+output > lp_token_budget"); return 2; }
+      const int64_t kvmin = sc->n_hp ? std::min(sc->kv_lp, sc->kv_hp) : sc->kv_lp;
+      if (ceil_div((int64_t)pl[i] + ol[i], sc->bs) >= kvmin) { set_err("request: KV exceeds instance"); return 2; }
+      if (i > off[t] && arr[i] < arr[i - 1]) { set_err("trace: arrivals not sorted"); return 1; }
+    }
+  std::atomic<int32_t> next{0};
+  std::atomic<int> rc{0};
+  std::string first_err;
+  std::mutex mu;
+  auto worker = [&]() {
+    while (true) {
+      const int32_t t = next.fetch_add(1);
+      if (t >= T) break;
+      const int64_t lo = off[t], n = off[t + 1] - off[t];
+      std::string e;
+      const int st = simulate_one(&a, pf, sc, n, arr + lo, pl + lo, ol + lo, ttft[t], tbt[t],
+                                  req_ttft ? req_ttft + lo : nullptr, first + lo, done + lo,
+                                  pstart + lo, status + lo, digest + t, decisions + t,
+                                  evaluations + t, check != 0, e);
+      if (st) {
+        std::lock_guard<std::mutex> lk(mu);
+        if (rc.load() == 0) { rc.store(st); first_err = e; }
+      }
+    }
+  };
+  int nt = nthreads > 0 ? nthreads : (int)std::thread::hardware_concurrency();
+  if (nt < 1) nt = 1;
+  if (nt > T) nt = T > 0 ? T : 1;
+  std::vector<std::thread> th;
+  for (int i = 1; i < nt; i++) th.emplace_back(worker);
+  worker();
+  for (auto& x : th) x.join();
+  if (rc.load()) set_err(first_err);
+  return rc.load();
+}
+
+// Goodput (G35-G36): a request counts iff it completed, its TTFT met the SLO
+// and its mean TBT (done - first) / (out - 1) met the TBT SLO; dropped/unfinished count in total.
+extern "C" int or_goodput(int32_t T, const int64_t* off, const int64_t* arr, const int32_t* ol,
+                          const int64_t* ttft, const int64_t* tbt, const int64_t* req_ttft,
+                          const int64_t* first, const int64_t* done, const uint32_t* status,
+                          uint64_t* good, uint64_t* total) {
+  int rc = 0;
+  for (int32_t t = 0; t < T; t++) {
+    uint64_t g = 0;
+    for (int64_t i = off[t]; i < off[t + 1]; i++) {
+      if ((status[i] & 3u) != COMPLETED) continue;
+      const int64_t slo = req_ttft ? req_ttft[i] : ttft[t];
+      if (first[i] - arr[i] > slo) continue;
+      if (ol[i] > 1 && done[i] - first[i] > tbt[t] * (int64_t)(ol[i] - 1)) continue;
+      g++;
+    }
+    good[t] = g;
+    total[t] = (uint64_t)(off[t + 1] - off[t]);
+    if (total[t] == 0) { rc = 5; set_err("goodput: empty trace"); }
+  }
+  return rc;
+}

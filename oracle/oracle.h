@@ -1,0 +1,84 @@
+/* oracle.h — CPU ORACLE (TEST INFRASTRUCTURE ONLY).
+ *
+ * A plain, slow, single-threaded-per-trace C++ transcription of Ascendra's
+ * scheduler and batch-level simulator (arXiv 2504.20828, /root/reference/PAPER.md)
+ * used to prove the CUDA path right.  Only tests/, __graft_entry__.smoke() and
+ * bench.py's cpu_baseline / --impl reference legs may load it.  It shares no
+ * code, header, table or constant generator with paper_2504_20828_b200/ or
+ * include/asc.h; the two meet only through the seeded inputs of gen/.
+ *
+ * Citations: P:n = PAPER.md line n, S:n = SPEC.md line n, Gnn = DESIGN.md reading.
+ * Pins: see tests/test_oracle_*.py (every function below is pinned; none is
+ * "parity unpinned" except where DESIGN.md §Pins says so).
+ */
+#ifndef ASC_ORACLE_H
+#define ASC_ORACLE_H
+#include <stdint.h>
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Model symbols of App. A.1; d = bytes per element (G10); tp divides h,n,m. */
+typedef struct { int64_t h, n, s, n_kv, m, L, b, d, tp; } or_arch;
+/* Regression coefficients C1..C5 and hardware caps F_H, M_H of Eq. 4-5. */
+typedef struct { double c[5]; double F_H, M_H; } or_perf;
+/* Instance partition, budgets and switches (readings G22-G41). */
+typedef struct {
+  int32_t n_lp, n_hp, bs, kv_lp, kv_hp, lp_max_batch, lp_tok, hp_tok;
+  int32_t policy, offload, tickets, elastic, drop, hist_default;
+  int64_t margin_us, delay_us;
+} or_sched;
+
+/* Eq. 1-3 with App. A.2/A.3 GEMM terms: exact integer F (flops) and M (bytes) of a batch of
+ * np whole-prompt prefills p[] and nd decodes with contexts lhat[].  Returns 0, or 1 when a
+ * result would reach 2^53 (not exactly representable in fp64). */
+int or_cost(const or_arch* a, int32_t np, const int64_t* p, int32_t nd, const int64_t* lhat,
+            uint64_t* F, uint64_t* M);
+/* Eq. 4-5: predicted seconds, fp64, fixed operation order, clamp at 0. */
+double or_latency_s(const or_perf* pf, uint64_t F, uint64_t M);
+/* G18/G17: integer microseconds = max(1, ceil(t * 1e6)). */
+int64_t or_latency_us(const or_perf* pf, uint64_t F, uint64_t M);
+/* Convenience: latency of a batch in microseconds (or -1 on range error). */
+int64_t or_batch_us(const or_arch* a, const or_perf* pf, int32_t np, const int64_t* p,
+                    int32_t nd, const int64_t* lhat);
+
+/* Algorithm 1, literal: n requests with value val[] (higher = more urgent),
+ * compute cost c[], memory cost mem[], token cost tok[]; budgets C, M, N plus the request-count
+ * budget R (reading G22).  Writes the selected request indices in scan order; returns count. */
+int32_t or_algorithm1(int32_t n, const int64_t* val, const int64_t* id, const int64_t* c,
+                      const int64_t* mem, const int64_t* tok, int64_t C, int64_t M, int64_t N,
+                      int64_t R, int32_t* selected);
+
+/* Stateless LP decision over S segments (one LP formation without decode prep). */
+int or_schedule_step(const or_arch* a, const or_perf* pf, const or_sched* sc, int32_t S,
+                     const int64_t* seg_off, const int64_t* now_us, const int64_t* deadline_us,
+                     const int32_t* eff_prompt, const uint8_t* flags, const int32_t* dec_count,
+                     const int64_t* dec_ctx_sum, const int64_t* tbt_slo_us,
+                     const int32_t* budget_tokens, const int32_t* budget_blocks,
+                     const int32_t* budget_reqs,
+                     int32_t* admit_idx, int32_t* admit_cnt, int32_t* offload_idx,
+                     int32_t* offload_cnt, int32_t* drop_idx, int32_t* drop_cnt,
+                     int64_t* batch_lat_us, int32_t* prefill_us);
+
+/* Full batch-level simulation of T independent traces (CSR), threads across traces. */
+int or_simulate_batch(const or_arch* a, const or_perf* pf, const or_sched* sc, int32_t T,
+                      const int64_t* trace_off, const int64_t* arrival_us,
+                      const int32_t* prompt_len, const int32_t* output_len,
+                      const int64_t* ttft_slo_us, const int64_t* tbt_slo_us,
+                      const int64_t* req_ttft_slo_us,
+                      int64_t* first_token_us, int64_t* done_us, int64_t* prefill_start_us,
+                      uint32_t* status, uint64_t* digest, int64_t* decisions,
+                      int64_t* evaluations, int32_t nthreads, int32_t check_invariants);
+
+/* Goodput numerator/denominator per trace. Returns 0, or 5 if a trace is empty. */
+int or_goodput(int32_t T, const int64_t* trace_off, const int64_t* arrival_us,
+               const int32_t* output_len, const int64_t* ttft_slo_us, const int64_t* tbt_slo_us,
+               const int64_t* req_ttft_slo_us, const int64_t* first_token_us,
+               const int64_t* done_us, const uint32_t* status, uint64_t* good, uint64_t* total);
+
+const char* or_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif
