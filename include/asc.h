@@ -1,0 +1,208 @@
+/* asc.h — C ABI of the B200-native Ascendra scheduler / batch-level simulator hot path.
+ *
+ * Method: Ascendra, "Dynamic Request Prioritization for Efficient LLM Serving"
+ * (arXiv 2504.20828).  Citations: P:n = PAPER.md line n (LaTeX source), S:n = SPEC.md line n,
+ * Gnn = reading nn in DESIGN.md §Readings (where the paper is silent or garbled).
+ *
+ * Library: paper_2504_20828_b200/libasc.so (sm_100a CUDA kernels; no CPU fallback).
+ *
+ * Conventions for every entry point
+ *  - Time is int64 microseconds; token counts are int32; F (flops) and M (bytes) are exact
+ *    integers < 2^53 evaluated inside the kernels (G18).
+ *  - Array arguments are plain pointers.  asc_schedule_step, asc_simulate_batch and asc_goodput
+ *    accept DEVICE pointers (memory on the ctx's device, e.g. torch tensors' data_ptr()) or HOST
+ *    pointers (pageable or pinned); host arrays are staged through the ctx's device workspace
+ *    inside the call (uploads before, downloads after).  All arrays of one call must be of the
+ *    same kind (all host or all device), else ASC_E_INVAL.
+ *  - The caller owns every input and output array.  The ctx owns its device workspace, grows it
+ *    on demand (ASC_E_NOMEM if that fails) and frees it in asc_destroy.
+ *  - Calls enqueue on the stream bound at asc_create and synchronize before returning, so the
+ *    status reflects kernel errors and device-side invariant checks.  One ctx per host thread.
+ *  - No partial results are guaranteed on error.  asc_last_error(ctx) names the offending field
+ *    or check (asc_last_error(NULL) reports asc_create failures of the calling thread).
+ */
+#ifndef ASC_H
+#define ASC_H
+#include <stdint.h>
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define ASC_ABI_VERSION 1
+#define ASC_MAX_BATCH 128      /* max request-count budget R / lp_max_batch */
+#define ASC_MAX_INSTANCES 16   /* n_lp + n_hp per trace */
+
+typedef struct asc_ctx asc_ctx;
+
+typedef enum {
+  ASC_OK = 0,
+  ASC_E_INVAL = 1,      /* bad argument (NULL, negative size, unsorted arrivals, mixed pointers) */
+  ASC_E_CONFIG = 2,     /* configuration / liveness validation failed (field named) */
+  ASC_E_NOMEM = 3,      /* device workspace allocation failed */
+  ASC_E_CUDA = 4,       /* CUDA runtime error (message from cudaGetErrorString) */
+  ASC_E_EMPTY = 5,      /* goodput over a trace with 0 requests */
+  ASC_E_RANGE = 6,      /* F or M >= 2^53, R > ASC_MAX_BATCH, index >= 2^31 */
+  ASC_E_INVARIANT = 7   /* device-side invariant violated (KV ledger, stuck queue) */
+} asc_status;
+
+/* Value function pi (G19).  key ascending = priority descending; ties by ascending id.
+ *  EDF_LAXITY   key = deadline - prefill_us   (default: urgency grows with time in system and
+ *                                              prompt length)
+ *  EDF_DEADLINE key = deadline = arrival + TTFT SLO
+ *  SJF          key = prefill_us
+ *  LJF          key = -prefill_us
+ *  FCFS         key = arrival  (asc_schedule_step: entry position) */
+typedef enum {
+  ASC_POLICY_EDF_LAXITY = 0, ASC_POLICY_EDF_DEADLINE = 1, ASC_POLICY_SJF = 2,
+  ASC_POLICY_LJF = 3, ASC_POLICY_FCFS = 4
+} asc_policy;
+
+/* Model symbols (App. A.1): hidden h, heads n, head size s (h = n*s), KV heads n_kv,
+ * FFN size m, layers L (G11), attention block size b (G15), bytes per element (G10), tensor
+ * parallel degree tp (h, n, m, n_kv are divided by tp). */
+typedef struct { int32_t h, n, s, n_kv, m, L, b, dtype_bytes, tp; } asc_arch;
+
+/* Latency regression (Eq. 4-5): t = C1(tM+tF) + C2 max(tM,tF) + C3 tM + C4 tF + C5,
+ * tM = M/M_H, tF = F/F_H (seconds; M_H bytes/s, F_H flops/s). */
+typedef struct { double c[5]; double F_H, M_H; } asc_perf;
+
+/* Instance partition and budgets (G22, G32, G38). */
+typedef struct {
+  int32_t n_lp, n_hp;            /* LP (throughput) and HP (latency) instances per trace */
+  int32_t block_tokens;          /* KV block size in tokens (G32) */
+  int32_t kv_blocks_lp, kv_blocks_hp; /* KV capacity per instance in blocks */
+  int32_t lp_max_batch;          /* LP batch cap, <= ASC_MAX_BATCH */
+  int32_t lp_token_budget;       /* N of Algorithm 1 (G38) */
+  int32_t hp_token_budget;       /* HP base prefill token budget; also sizes W_hp */
+} asc_topology;
+
+/* Switches (P:336 offload, P:368 tickets, P:370-371 elastic, P:373-375 drop). */
+typedef struct {
+  int32_t policy;                /* asc_policy */
+  uint8_t offload, tickets, elastic, drop;
+  int64_t offload_margin_us;     /* tunable threshold of P:336 (G24), default 0 */
+  int64_t offload_delay_us;      /* LP->HP transfer delay, default 0 */
+  int32_t hist_default_tokens;   /* decode-length history mean before any HP completion (G28) */
+} asc_flags;
+
+typedef struct { asc_arch arch; asc_perf perf; asc_topology topo; asc_flags flags; } asc_config;
+
+/* Validates cfg (ASC_E_CONFIG naming the field: h != n*s, tp divisibility, non-positive sizes,
+ * F_H/M_H <= 0, lp_max_batch > ASC_MAX_BATCH, n_lp < 1, n_lp + n_hp > ASC_MAX_INSTANCES),
+ * binds device `device` and stream `cuda_stream` (a cudaStream_t; NULL = legacy default
+ * stream), and precomputes the per-prompt-length prefill latency table on the device. */
+asc_status asc_create(const asc_config* cfg, int device, void* cuda_stream, asc_ctx** out);
+void asc_destroy(asc_ctx* ctx);
+const char* asc_last_error(const asc_ctx* ctx);
+int32_t asc_abi_version(void);
+
+/* ---------------------------------------------------------------------------------------------
+ * asc_schedule_step — one stateless LP scheduling decision for each of S independent segments
+ * (a segment = the waiting queue of one LP instance of one trace), i.e. §5 of the paper for one
+ * batch-formation instant: per request the performance model (Eq. 1-5) gives prefill_us and the
+ * KV blocks blk = ceil((p+1)/block_tokens) (G23); the value function gives the key; Algorithm 1
+ * admits the longest prefix of the key order whose running token, block and
+ * microsecond sums stay strictly below N, M and C with at most R requests (G21-G22); the offload
+ * rule (G24) flags the remaining never-prefilled, not-on-HP requests with
+ * deadline - now <= prefill_us + W_hp + margin (W_hp = prefill latency of hp_token_budget tokens);
+ * with the drop flag, never-prefilled requests with now > deadline are dropped first (G34)
+ * and take no further part.  C = tbt_slo - latency(decode-only batch of dec_count requests with
+ * context sum dec_ctx_sum), or +infinity when dec_count = 0 (G22).  batch_lat_us = latency of
+ * the hybrid batch {admitted prefills} + {decodes} (Eq. 3-5), 0 when both are empty.
+ *
+ * Layout: entries of segment s are [seg_off[s], seg_off[s+1]) of the per-entry arrays, in
+ * ascending request-id (arrival) order; ties in the key order break by position.  Outputs use the
+ * same CSR offsets: admit_idx[seg_off[s] + j], j < admit_cnt[s] (priority order); offload_idx and
+ * drop_idx likewise (ascending position).  Indices are global entry positions (int32).
+ * flags: bit0 = ever prefilled (preempted request), bit1 = already on an HP.
+ * Errors: ASC_E_INVAL (S < 0, seg_off not non-decreasing, eff_prompt < 1), ASC_E_RANGE
+ * (budget_reqs > ASC_MAX_BATCH, total entries >= 2^31, cost >= 2^53).
+ * ------------------------------------------------------------------------------------------- */
+typedef struct {
+  int32_t S;
+  const int64_t* seg_off;        /* [S+1] */
+  const int64_t* now_us;         /* [S] */
+  const int64_t* deadline_us;    /* [Q] arrival + TTFT SLO */
+  const int32_t* eff_prompt;     /* [Q] prompt (+ generated tokens after preemption), >= 1 */
+  const uint8_t* flags;          /* [Q] */
+  const int32_t* dec_count;      /* [S] B_d */
+  const int64_t* dec_ctx_sum;    /* [S] sum of decode contexts lhat */
+  const int64_t* tbt_slo_us;     /* [S] */
+  const int32_t* budget_tokens;  /* [S] N */
+  const int32_t* budget_blocks;  /* [S] M (free KV blocks) */
+  const int32_t* budget_reqs;    /* [S] R (<= ASC_MAX_BATCH) */
+} asc_step_in;
+
+typedef struct {
+  int32_t* admit_idx;   int32_t* admit_cnt;     /* [Q] CSR, [S] */
+  int32_t* offload_idx; int32_t* offload_cnt;   /* [Q] CSR, [S] */
+  int32_t* drop_idx;    int32_t* drop_cnt;      /* [Q] CSR, [S] */
+  int64_t* batch_lat_us;                        /* [S] */
+  int32_t* prefill_us;                          /* [Q] optional (NULL = not written) */
+} asc_step_out;
+
+asc_status asc_schedule_step(asc_ctx* ctx, const asc_step_in* in, asc_step_out* out);
+
+/* ---------------------------------------------------------------------------------------------
+ * asc_simulate_batch — batch-level discrete-event simulation (§4-§6; the paper's simulator of
+ * P:377/P:630) of T independent traces, each on its own n_lp + n_hp instances, with the event
+ * rules of DESIGN.md §Event loop: completions, offload deliveries, arrivals (round-robin to LPs or
+ * to a ticket-holding HP), formations (LP: drop, decode growth with LIFO preemption by
+ * recomputation, Algorithm 1, offload, hybrid batch; HP: drop, FCFS prefill-first under the
+ * (elastic) token limit, else decode-only), then ticket issue.
+ *
+ * Layout: requests of trace t are [trace_off[t], trace_off[t+1]) in arrival order (arrival_us
+ * non-decreasing within a trace, else ASC_E_INVAL).  Per-trace SLOs; req_ttft_slo_us optionally
+ * overrides the TTFT SLO per request (NULL = per-trace).  Liveness validation (ASC_E_CONFIG):
+ * prompt_len, output_len >= 1; prompt_len + output_len <= lp_token_budget; and
+ * ceil((prompt_len + output_len)/block_tokens) < min KV blocks of the instances.
+ * Outputs per request: first_token_us (TTFT event), done_us (completion), prefill_start_us
+ * (first admission), -1 when absent; status bits 0-1 state {0 unfinished, 1 completed,
+ * 2 dropped}, bit 2 offloaded, bit 3 ticketed, bits 4-11 serving instance (255 = none),
+ * bits 12-27 preemptions.  Per trace: digest, decisions (non-empty
+ * formations) and evaluations (waiting-queue entries examined, summed over formations);
+ * decisions/evaluations may be NULL.
+ * ------------------------------------------------------------------------------------------- */
+typedef struct {
+  int32_t T;
+  const int64_t* trace_off;        /* [T+1] */
+  const int64_t* arrival_us;       /* [R] */
+  const int32_t* prompt_len;       /* [R] */
+  const int32_t* output_len;       /* [R] */
+  const int64_t* ttft_slo_us;      /* [T] (Table 2) */
+  const int64_t* tbt_slo_us;       /* [T] */
+  const int64_t* req_ttft_slo_us;  /* [R] optional */
+} asc_traces;
+
+typedef struct {
+  int64_t* first_token_us;  /* [R] */
+  int64_t* done_us;         /* [R] */
+  int64_t* prefill_start_us;/* [R] */
+  uint32_t* status;         /* [R] */
+  uint64_t* digest;         /* [T] */
+  int64_t* decisions;       /* [T] optional */
+  int64_t* evaluations;     /* [T] optional */
+} asc_outcomes;
+
+asc_status asc_simulate_batch(asc_ctx* ctx, const asc_traces* tr, asc_outcomes* out);
+
+/* ---------------------------------------------------------------------------------------------
+ * asc_goodput — per trace, good = #requests that COMPLETED with first_token - arrival <= TTFT SLO
+ * and (output_len = 1 or done - first_token <= TBT SLO * (output_len - 1)), i.e. mean TBT within
+ * the SLO (G35); total = all requests including dropped/unfinished (G36).
+ * Exact integers so sums across GPUs are exact.  ASC_E_EMPTY if some trace has 0 requests.
+ * ------------------------------------------------------------------------------------------- */
+asc_status asc_goodput(asc_ctx* ctx, const asc_traces* tr, const asc_outcomes* out,
+                       uint64_t* good, uint64_t* total);
+
+/* Diagnostics: number of libasc kernels the last call on ctx launched (bench evidence). */
+int64_t asc_last_kernel_launches(const asc_ctx* ctx);
+/* Diagnostics: device time (ms, CUDA events on the ctx stream) of the last call's dominant
+ * kernel (simulate: the step loop; schedule_step: the streaming pass; goodput: the reduction),
+ * or -1 if none ran. */
+double asc_last_kernel_ms(const asc_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,287 @@
+"""Thin ctypes binding of include/asc.h (argument marshalling only).
+
+Every step of the hot path runs in libasc.so's sm_100a kernels; this module only converts
+preset dicts into asc_config, and torch CUDA tensors (device pointers) or numpy arrays (host
+pointers, staged by the library itself) into the C structs.  There is no CPU fallback: if
+libasc.so is missing or no CUDA device is present, the calls raise.
+"""
+import ctypes as C
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libasc.so")
+_LIB = None
+
+ASC_MAX_BATCH = 128
+ASC_MAX_INSTANCES = 16
+STATUS = {0: "ASC_OK", 1: "ASC_E_INVAL", 2: "ASC_E_CONFIG", 3: "ASC_E_NOMEM", 4: "ASC_E_CUDA",
+          5: "ASC_E_EMPTY", 6: "ASC_E_RANGE", 7: "ASC_E_INVARIANT"}
+EXPORTS = ("asc_create", "asc_destroy", "asc_last_error", "asc_abi_version", "asc_schedule_step",
+           "asc_simulate_batch", "asc_goodput", "asc_last_kernel_launches",
+           "asc_last_kernel_ms")
+
+
+class AscError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__(f"{STATUS.get(code, code)}: {msg}")
+        self.code = code
+
+
+class asc_arch(C.Structure):
+    _fields_ = [(k, C.c_int32) for k in ("h", "n", "s", "n_kv", "m", "L", "b", "dtype_bytes", "tp")]
+
+
+class asc_perf(C.Structure):
+    _fields_ = [("c", C.c_double * 5), ("F_H", C.c_double), ("M_H", C.c_double)]
+
+
+class asc_topology(C.Structure):
+    _fields_ = [(k, C.c_int32) for k in ("n_lp", "n_hp", "block_tokens", "kv_blocks_lp",
+                                         "kv_blocks_hp", "lp_max_batch", "lp_token_budget",
+                                         "hp_token_budget")]
+
+
+class asc_flags(C.Structure):
+    _fields_ = [("policy", C.c_int32), ("offload", C.c_uint8), ("tickets", C.c_uint8),
+                ("elastic", C.c_uint8), ("drop", C.c_uint8), ("offload_margin_us", C.c_int64),
+                ("offload_delay_us", C.c_int64), ("hist_default_tokens", C.c_int32)]
+
+
+class asc_config(C.Structure):
+    _fields_ = [("arch", asc_arch), ("perf", asc_perf), ("topo", asc_topology), ("flags", asc_flags)]
+
+
+_P = C.c_void_p
+
+
+class asc_step_in(C.Structure):
+    _fields_ = [("S", C.c_int32)] + [(k, _P) for k in (
+        "seg_off", "now_us", "deadline_us", "eff_prompt", "flags", "dec_count", "dec_ctx_sum",
+        "tbt_slo_us", "budget_tokens", "budget_blocks", "budget_reqs")]
+
+
+class asc_step_out(C.Structure):
+    _fields_ = [(k, _P) for k in ("admit_idx", "admit_cnt", "offload_idx", "offload_cnt",
+                                  "drop_idx", "drop_cnt", "batch_lat_us", "prefill_us")]
+
+
+class asc_traces(C.Structure):
+    _fields_ = [("T", C.c_int32)] + [(k, _P) for k in (
+        "trace_off", "arrival_us", "prompt_len", "output_len", "ttft_slo_us", "tbt_slo_us",
+        "req_ttft_slo_us")]
+
+
+class asc_outcomes(C.Structure):
+    _fields_ = [(k, _P) for k in ("first_token_us", "done_us", "prefill_start_us", "status",
+                                  "digest", "decisions", "evaluations")]
+
+
+def lib():
+    global _LIB
+    if _LIB is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(f"{LIB_PATH} missing: run __graft_entry__.build() "
+                               "(there is no CPU fallback)")
+        L = C.CDLL(LIB_PATH)
+        L.asc_create.argtypes = [C.POINTER(asc_config), C.c_int, C.c_void_p, C.POINTER(C.c_void_p)]
+        L.asc_create.restype = C.c_int
+        L.asc_destroy.argtypes = [C.c_void_p]
+        L.asc_destroy.restype = None
+        L.asc_last_error.argtypes = [C.c_void_p]
+        L.asc_last_error.restype = C.c_char_p
+        L.asc_abi_version.restype = C.c_int32
+        L.asc_schedule_step.argtypes = [C.c_void_p, C.POINTER(asc_step_in), C.POINTER(asc_step_out)]
+        L.asc_schedule_step.restype = C.c_int
+        L.asc_simulate_batch.argtypes = [C.c_void_p, C.POINTER(asc_traces), C.POINTER(asc_outcomes)]
+        L.asc_simulate_batch.restype = C.c_int
+        L.asc_goodput.argtypes = [C.c_void_p, C.POINTER(asc_traces), C.POINTER(asc_outcomes),
+                                  C.c_void_p, C.c_void_p]
+        L.asc_goodput.restype = C.c_int
+        L.asc_last_kernel_launches.argtypes = [C.c_void_p]
+        L.asc_last_kernel_launches.restype = C.c_int64
+        L.asc_last_kernel_ms.argtypes = [C.c_void_p]
+        L.asc_last_kernel_ms.restype = C.c_double
+        _LIB = L
+    return _LIB
+
+
+def make_config(cfg):
+    a, p, t, f = cfg["arch"], cfg["perf"], cfg["topo"], cfg["flags"]
+    return asc_config(
+        asc_arch(a["h"], a["n"], a["s"], a["n_kv"], a["m"], a["L"], a["b"], a["dtype_bytes"], a["tp"]),
+        asc_perf((C.c_double * 5)(*p["c"]), p["F_H"], p["M_H"]),
+        asc_topology(t["n_lp"], t["n_hp"], t["block_tokens"], t["kv_blocks_lp"], t["kv_blocks_hp"],
+                     t["lp_max_batch"], t["lp_token_budget"], t["hp_token_budget"]),
+        asc_flags(f["policy"], f["offload"], f["tickets"], f["elastic"], f["drop"],
+                  f["offload_margin_us"], f["offload_delay_us"], f["hist_default_tokens"]))
+
+
+def _ptr(x):
+    """Device pointer of a torch tensor, host pointer of a numpy array, or NULL."""
+    if x is None:
+        return None
+    if isinstance(x, np.ndarray):
+        assert x.flags["C_CONTIGUOUS"]
+        return x.ctypes.data
+    assert x.is_contiguous()
+    return x.data_ptr()
+
+
+def _check(ctx, rc, what):
+    if rc != 0:
+        msg = lib().asc_last_error(ctx)
+        raise AscError(rc, f"{what}: {msg.decode() if msg else ''}")
+
+
+def asc_create(cfg, device=0, stream=None):
+    """Returns an opaque ctx handle (int).  stream: torch.cuda.Stream, raw handle or None."""
+    h = C.c_void_p()
+    sp = None
+    if stream is not None:
+        sp = stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
+    c = make_config(cfg)
+    rc = lib().asc_create(C.byref(c), int(device), sp, C.byref(h))
+    _check(None, rc, "asc_create")
+    return h.value
+
+
+def asc_destroy(ctx):
+    lib().asc_destroy(ctx)
+
+
+def asc_last_kernel_launches(ctx):
+    return int(lib().asc_last_kernel_launches(ctx))
+
+
+def asc_last_kernel_ms(ctx):
+    return float(lib().asc_last_kernel_ms(ctx))
+
+
+def asc_schedule_step(ctx, seg_off, now_us, deadline_us, eff_prompt, flags, dec_count, dec_ctx_sum,
+                      tbt_slo_us, budget_tokens, budget_blocks, budget_reqs, admit_idx, admit_cnt,
+                      offload_idx, offload_cnt, drop_idx, drop_cnt, batch_lat_us, prefill_us=None):
+    S = len(seg_off) - 1
+    i = asc_step_in(S, *[_ptr(x) for x in (seg_off, now_us, deadline_us, eff_prompt, flags,
+                                           dec_count, dec_ctx_sum, tbt_slo_us, budget_tokens,
+                                           budget_blocks, budget_reqs)])
+    o = asc_step_out(*[_ptr(x) for x in (admit_idx, admit_cnt, offload_idx, offload_cnt, drop_idx,
+                                         drop_cnt, batch_lat_us, prefill_us)])
+    _check(ctx, lib().asc_schedule_step(ctx, C.byref(i), C.byref(o)), "asc_schedule_step")
+
+
+def asc_simulate_batch(ctx, trace_off, arrival_us, prompt_len, output_len, ttft_slo_us, tbt_slo_us,
+                       first_token_us, done_us, prefill_start_us, status, digest, decisions=None,
+                       evaluations=None, req_ttft_slo_us=None):
+    T = len(trace_off) - 1
+    tr = asc_traces(T, *[_ptr(x) for x in (trace_off, arrival_us, prompt_len, output_len,
+                                           ttft_slo_us, tbt_slo_us, req_ttft_slo_us)])
+    oc = asc_outcomes(*[_ptr(x) for x in (first_token_us, done_us, prefill_start_us, status,
+                                          digest, decisions, evaluations)])
+    _check(ctx, lib().asc_simulate_batch(ctx, C.byref(tr), C.byref(oc)), "asc_simulate_batch")
+
+
+def asc_goodput(ctx, trace_off, arrival_us, output_len, ttft_slo_us, tbt_slo_us, first_token_us,
+                done_us, status, good, total, req_ttft_slo_us=None):
+    T = len(trace_off) - 1
+    tr = asc_traces(T, _ptr(trace_off), _ptr(arrival_us), None, _ptr(output_len), _ptr(ttft_slo_us),
+                    _ptr(tbt_slo_us), _ptr(req_ttft_slo_us))
+    oc = asc_outcomes(_ptr(first_token_us), _ptr(done_us), None, _ptr(status), None, None, None)
+    _check(ctx, lib().asc_goodput(ctx, C.byref(tr), C.byref(oc), _ptr(good), _ptr(total)),
+           "asc_goodput")
+
+
+# ------------------------------------------------------------------ convenience (allocation) --
+class Context:
+    """Owns a ctx; allocates outputs as torch CUDA tensors (device path) or numpy (host path)."""
+
+    def __init__(self, cfg, device=0, stream=None):
+        self.cfg = cfg
+        self.device = device
+        self.h = asc_create(cfg, device, stream)
+
+    def close(self):
+        if self.h:
+            asc_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def last_launches(self):
+        return asc_last_kernel_launches(self.h)
+
+    def last_kernel_ms(self):
+        return asc_last_kernel_ms(self.h)
+
+    def schedule_step(self, ins, want_prefill=True):
+        """ins: dict of arrays (all torch CUDA or all numpy).  Returns dict of outputs."""
+        dev = not isinstance(ins["seg_off"], np.ndarray)
+        S = len(ins["seg_off"]) - 1
+        Q = int(ins["seg_off"][-1])
+        out = _alloc(dev, self.device, dict(admit_idx=(Q, "i4"), admit_cnt=(S, "i4"),
+                                            offload_idx=(Q, "i4"), offload_cnt=(S, "i4"),
+                                            drop_idx=(Q, "i4"), drop_cnt=(S, "i4"),
+                                            batch_lat_us=(S, "i8"),
+                                            prefill_us=(Q if want_prefill else 0, "i4")))
+        if not want_prefill:
+            out["prefill_us"] = None
+        asc_schedule_step(self.h, ins["seg_off"], ins["now_us"], ins["deadline_us"],
+                          ins["eff_prompt"], ins["flags"], ins["dec_count"], ins["dec_ctx_sum"],
+                          ins["tbt_slo_us"], ins["budget_tokens"], ins["budget_blocks"],
+                          ins["budget_reqs"], out["admit_idx"], out["admit_cnt"],
+                          out["offload_idx"], out["offload_cnt"], out["drop_idx"],
+                          out["drop_cnt"], out["batch_lat_us"], out["prefill_us"])
+        return out
+
+    def simulate_batch(self, tr, req_ttft_slo_us=None, out=None):
+        """tr: dict trace_off, arrival_us, prompt_len, output_len, ttft_slo_us, tbt_slo_us."""
+        dev = not isinstance(tr["trace_off"], np.ndarray)
+        T = len(tr["trace_off"]) - 1
+        R = int(tr["trace_off"][-1])
+        if out is None:
+            out = _alloc(dev, self.device, dict(first_token_us=(R, "i8"), done_us=(R, "i8"),
+                                                prefill_start_us=(R, "i8"), status=(R, "u4"),
+                                                digest=(T, "u8"), decisions=(T, "i8"),
+                                                evaluations=(T, "i8")))
+        asc_simulate_batch(self.h, tr["trace_off"], tr["arrival_us"], tr["prompt_len"],
+                           tr["output_len"], tr["ttft_slo_us"], tr["tbt_slo_us"],
+                           out["first_token_us"], out["done_us"], out["prefill_start_us"],
+                           out["status"], out["digest"], out["decisions"], out["evaluations"],
+                           req_ttft_slo_us)
+        return out
+
+    def goodput(self, tr, out, req_ttft_slo_us=None, res=None):
+        dev = not isinstance(tr["trace_off"], np.ndarray)
+        T = len(tr["trace_off"]) - 1
+        if res is None:
+            res = _alloc(dev, self.device, dict(good=(T, "u8"), total=(T, "u8")))
+        asc_goodput(self.h, tr["trace_off"], tr["arrival_us"], tr["output_len"], tr["ttft_slo_us"],
+                    tr["tbt_slo_us"], out["first_token_us"], out["done_us"], out["status"],
+                    res["good"], res["total"], req_ttft_slo_us)
+        return res["good"], res["total"]
+
+
+def _alloc(dev, device, spec):
+    if not dev:
+        return {k: np.zeros(max(n, 1), dtype=dt) for k, (n, dt) in spec.items()}
+    import torch
+    tmap = {"i4": torch.int32, "i8": torch.int64, "u4": torch.int32, "u8": torch.int64}
+    return {k: torch.empty(max(n, 1), dtype=tmap[dt], device=f"cuda:{device}")
+            for k, (n, dt) in spec.items()}
+
+
+def batch_arrays(batch, device=None):
+    """gen.traces.TraceBatch -> dict of numpy (host) or torch CUDA tensors (device)."""
+    d = dict(trace_off=batch.trace_off, arrival_us=batch.arrival_us, prompt_len=batch.prompt_len,
+             output_len=batch.output_len, ttft_slo_us=batch.ttft_slo_us, tbt_slo_us=batch.tbt_slo_us)
+    # zero-length arrays would marshal as NULL: pad to one (never read) element
+    d = {k: np.ascontiguousarray(v if len(v) else np.zeros(1, v.dtype)) for k, v in d.items()}
+    if device is None:
+        return d
+    import torch
+    return {k: torch.from_numpy(v).to(device) for k, v in d.items()}

@@ -1,0 +1,431 @@
+// asc_api.cu — the C ABI of include/asc.h: validation, context, workspace, host staging.
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "asc_internal.h"
+
+using namespace asc;
+
+static thread_local std::string g_create_err;
+
+namespace asc {
+
+asc_status fail(asc_ctx* c, asc_status s, const std::string& msg) {
+  if (c) c->err = msg; else g_create_err = msg;
+  return s;
+}
+
+asc_status cuda_check(asc_ctx* c, cudaError_t e, const char* what) {
+  if (e == cudaSuccess) return ASC_OK;
+  return fail(c, ASC_E_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+asc_status ensure_ws(asc_ctx* c, size_t bytes) {
+  if (bytes <= c->ws_cap) return ASC_OK;
+  if (c->ws) cudaFree(c->ws);
+  c->ws = nullptr;
+  c->ws_cap = 0;
+  size_t cap = bytes + bytes / 8;
+  if (cudaMalloc(&c->ws, cap) != cudaSuccess) {
+    cudaGetLastError();
+    return fail(c, ASC_E_NOMEM, "workspace allocation of " + std::to_string(cap) + " bytes failed");
+  }
+  c->ws_cap = cap;
+  return ASC_OK;
+}
+
+static asc_status ensure_stage(asc_ctx* c, size_t bytes) {
+  if (bytes <= c->stage_cap) return ASC_OK;
+  if (c->stage) cudaFree(c->stage);
+  c->stage = nullptr;
+  c->stage_cap = 0;
+  if (cudaMalloc(&c->stage, bytes) != cudaSuccess) {
+    cudaGetLastError();
+    return fail(c, ASC_E_NOMEM, "staging allocation failed");
+  }
+  c->stage_cap = bytes;
+  return ASC_OK;
+}
+
+asc_status collect_errors(asc_ctx* c, const char* where) {
+  cudaError_t e = cudaStreamSynchronize(c->stream);
+  if (e != cudaSuccess) return cuda_check(c, e, where);
+  int bits = 0;
+  e = cudaMemcpy(&bits, c->d_err, sizeof(int), cudaMemcpyDeviceToHost);
+  if (e != cudaSuccess) return cuda_check(c, e, where);
+  if (!bits) return ASC_OK;
+  cudaMemset(c->d_err, 0, sizeof(int));
+  std::string w(where);
+  if (bits & 8) return fail(c, ASC_E_CONFIG, w + ": request violates liveness validation (prompt_len, output_len >= 1; prompt+output <= lp_token_budget; ceil((prompt+output)/block_tokens) < kv_blocks)");
+  if (bits & ERR_INVAL) return fail(c, ASC_E_INVAL, w + ": invalid input (eff_prompt < 1, seg_off decreasing, or arrivals not sorted within a trace)");
+  if (bits & ERR_RANGE) return fail(c, ASC_E_RANGE, w + ": range (F or M >= 2^53, or budget_reqs > ASC_MAX_BATCH)");
+  if (bits & 16) return fail(c, ASC_E_EMPTY, w + ": goodput over a trace with 0 requests");
+  if (bits & ERR_INVARIANT) return fail(c, ASC_E_INVARIANT, w + ": invariant violated (queue left non-empty with no pending event)");
+  return fail(c, ASC_E_INVARIANT, w + ": unknown device error");
+}
+
+}  // namespace asc
+
+// prefill latency table for eff_prompt in [0, n) and the worst-case HP batch latency W_hp
+__global__ void build_tables(Model md, int64_t* tab, int32_t n, int32_t hp_tok, int64_t* w_hp, int* err) {
+  for (int32_t p = blockIdx.x * blockDim.x + threadIdx.x; p < n; p += gridDim.x * blockDim.x) {
+    const int64_t v = p == 0 ? 0 : prefill_lat(md, (uint64_t)p);
+    if (v < 0) atomicOr(err, ERR_RANGE);
+    tab[p] = v < 0 ? INT32_MAX : v;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    const int64_t v = prefill_lat(md, (uint64_t)hp_tok);
+    if (v < 0) atomicOr(err, ERR_RANGE);
+    *w_hp = v;
+  }
+}
+
+extern "C" {
+
+int32_t asc_abi_version(void) { return ASC_ABI_VERSION; }
+
+const char* asc_last_error(const asc_ctx* ctx) {
+  return ctx ? ctx->err.c_str() : g_create_err.c_str();
+}
+
+asc_status asc_create(const asc_config* cfg, int device, void* cuda_stream, asc_ctx** out) {
+  if (!cfg || !out) return fail(nullptr, ASC_E_INVAL, "asc_create: NULL argument");
+  *out = nullptr;
+  const asc_arch& a = cfg->arch;
+  const asc_topology& t = cfg->topo;
+  const asc_flags& f = cfg->flags;
+#define CHK(cond, msg) \
+  if (!(cond)) return fail(nullptr, ASC_E_CONFIG, std::string("asc_create: ") + msg)
+  CHK(a.h > 0 && a.n > 0 && a.s > 0 && a.m > 0 && a.L > 0 && a.b > 0 && a.dtype_bytes > 0 && a.tp > 0 && a.n_kv > 0,
+      "arch fields must be positive (h, n, s, n_kv, m, L, b, dtype_bytes, tp)");
+  CHK((int64_t)a.h == (int64_t)a.n * a.s, "arch.h != arch.n * arch.s");
+  CHK(a.h % a.tp == 0 && a.n % a.tp == 0 && a.m % a.tp == 0 && a.n_kv % a.tp == 0,
+      "arch.tp must divide h, n, n_kv and m (P:662)");
+  CHK(cfg->perf.F_H > 0 && cfg->perf.M_H > 0, "perf.F_H and perf.M_H must be > 0");
+  CHK(t.n_lp >= 1, "topo.n_lp must be >= 1");
+  CHK(t.n_hp >= 0, "topo.n_hp must be >= 0");
+  CHK(t.n_lp + t.n_hp <= ASC_MAX_INSTANCES, "topo.n_lp + topo.n_hp exceeds ASC_MAX_INSTANCES");
+  CHK(t.block_tokens >= 1, "topo.block_tokens must be >= 1");
+  CHK(t.kv_blocks_lp >= 1 && (t.n_hp == 0 || t.kv_blocks_hp >= 1), "topo.kv_blocks must be >= 1");
+  CHK(t.lp_max_batch >= 1 && t.lp_max_batch <= ASC_MAX_BATCH, "topo.lp_max_batch must be in [1, ASC_MAX_BATCH]");
+  CHK(t.lp_token_budget >= 1 && t.lp_token_budget < (1 << 24), "topo.lp_token_budget must be in [1, 2^24)");
+  CHK(t.hp_token_budget >= 1 && t.hp_token_budget < (1 << 24), "topo.hp_token_budget must be in [1, 2^24)");
+  CHK(f.policy >= 0 && f.policy <= 4, "flags.policy must be an asc_policy");
+  CHK(f.offload_margin_us >= 0 && f.offload_delay_us >= 0, "flags.offload_margin_us/offload_delay_us must be >= 0");
+  CHK(f.hist_default_tokens >= 0, "flags.hist_default_tokens must be >= 0");
+#undef CHK
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+    cudaGetLastError();
+    return fail(nullptr, ASC_E_CUDA, "asc_create: no CUDA device (libasc has no CPU fallback)");
+  }
+  if (device < 0 || device >= ndev) return fail(nullptr, ASC_E_INVAL, "asc_create: bad device ordinal");
+  cudaError_t e = cudaSetDevice(device);
+  if (e != cudaSuccess) return fail(nullptr, ASC_E_CUDA, std::string("cudaSetDevice: ") + cudaGetErrorString(e));
+  asc_ctx* c = new asc_ctx();
+  c->cfg = *cfg;
+  c->device = device;
+  c->stream = (cudaStream_t)cuda_stream;
+  // tp division
+  const uint64_t tp = (uint64_t)a.tp;
+  const uint64_t h = a.h / tp, n = a.n / tp, m = a.m / tp;
+  c->md.n = n;
+  c->md.s = (uint64_t)a.s;
+  c->md.L = (uint64_t)a.L;
+  c->md.d = (uint64_t)a.dtype_bytes;
+  c->md.b = (uint64_t)a.b;
+  c->md.W = 4 * h * h + 2 * h * m;
+  c->md.FT = 4 * h * h + 2 * h * m;
+  c->md.MT = 8 * h + 2 * m;
+  c->md.c0 = cfg->perf.c[0]; c->md.c1 = cfg->perf.c[1]; c->md.c2 = cfg->perf.c[2];
+  c->md.c3 = cfg->perf.c[3]; c->md.c4 = cfg->perf.c[4];
+  c->md.FH = cfg->perf.F_H;
+  c->md.MH = cfg->perf.M_H;
+  int32_t pt = t.lp_token_budget > t.hp_token_budget ? t.lp_token_budget : t.hp_token_budget;
+  c->pt_size = pt + 1;
+  int64_t* d_w = nullptr;
+  if (cudaMalloc(&c->d_err, sizeof(int)) != cudaSuccess ||
+      cudaMalloc(&c->d_pf_tab, sizeof(int64_t) * c->pt_size) != cudaSuccess ||
+      cudaMalloc(&d_w, sizeof(int64_t)) != cudaSuccess) {
+    cudaGetLastError();
+    asc_destroy(c);
+    if (d_w) cudaFree(d_w);
+    return fail(nullptr, ASC_E_NOMEM, "asc_create: device allocation failed");
+  }
+  cudaEventCreate(&c->ev0);
+  cudaEventCreate(&c->ev1);
+  cudaMemsetAsync(c->d_err, 0, sizeof(int), c->stream);
+  build_tables<<<(c->pt_size + 255) / 256, 256, 0, c->stream>>>(c->md, c->d_pf_tab, c->pt_size,
+                                                                 t.hp_token_budget, d_w, c->d_err);
+  e = cudaMemcpyAsync(&c->w_hp, d_w, sizeof(int64_t), cudaMemcpyDeviceToHost, c->stream);
+  asc_status st = e != cudaSuccess ? cuda_check(c, e, "asc_create") : collect_errors(c, "asc_create tables");
+  cudaFree(d_w);
+  if (st) {
+    g_create_err = c->err;
+    asc_destroy(c);
+    return st;
+  }
+  *out = c;
+  return ASC_OK;
+}
+
+void asc_destroy(asc_ctx* ctx) {
+  if (!ctx) return;
+  if (ctx->d_err) cudaFree(ctx->d_err);
+  if (ctx->d_pf_tab) cudaFree(ctx->d_pf_tab);
+  if (ctx->ws) cudaFree(ctx->ws);
+  if (ctx->stage) cudaFree(ctx->stage);
+  if (ctx->ev0) cudaEventDestroy(ctx->ev0);
+  if (ctx->ev1) cudaEventDestroy(ctx->ev1);
+  delete ctx;
+}
+
+}  // extern "C"
+
+// ------------------------------------------------------------------ host/device pointer kinds --
+static int ptr_kind(const void* p) {  // 1 device, 0 host, -1 null
+  if (!p) return -1;
+  cudaPointerAttributes at;
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return (at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged) ? 1 : 0;
+}
+
+static bool same_kind(int kind, std::initializer_list<const void*> ps) {
+  for (const void* p : ps)
+    if (p && ptr_kind(p) != kind) return false;
+  return true;
+}
+
+struct Stager {  // copies host arrays into the staging buffer and back
+  asc_ctx* c;
+  std::vector<std::pair<void*, const void*>> downs;  // (host dst, dev src) sizes below
+  std::vector<size_t> down_sizes;
+  size_t off = 0;
+  char* base = nullptr;
+  template <typename T>
+  T* up(const T* h, size_t n) {
+    if (!h) return nullptr;
+    off = (off + 255) & ~size_t(255);
+    T* d = reinterpret_cast<T*>(base + off);
+    off += n * sizeof(T);
+    if (n) cudaMemcpyAsync(d, h, n * sizeof(T), cudaMemcpyHostToDevice, c->stream);
+    return d;
+  }
+  template <typename T>
+  T* out(T* h, size_t n) {
+    if (!h) return nullptr;
+    off = (off + 255) & ~size_t(255);
+    T* d = reinterpret_cast<T*>(base + off);
+    off += n * sizeof(T);
+    downs.push_back({(void*)h, (const void*)d});
+    down_sizes.push_back(n * sizeof(T));
+    return d;
+  }
+  cudaError_t download() {
+    for (size_t i = 0; i < downs.size(); i++)
+      if (down_sizes[i])
+        cudaMemcpyAsync(downs[i].first, downs[i].second, down_sizes[i], cudaMemcpyDeviceToHost, c->stream);
+    return cudaStreamSynchronize(c->stream);
+  }
+};
+
+static size_t rup(size_t x) { return (x + 255) & ~size_t(255); }
+
+extern "C" {
+
+asc_status asc_schedule_step(asc_ctx* c, const asc_step_in* in, asc_step_out* out) {
+  if (!c || !in || !out) return fail(c, ASC_E_INVAL, "asc_schedule_step: NULL argument");
+  c->err.clear();
+  c->timed = false;
+  if (in->S < 0) return fail(c, ASC_E_INVAL, "asc_schedule_step: S < 0");
+  if (!in->seg_off || !in->now_us || !in->deadline_us || !in->eff_prompt || !in->flags ||
+      !in->dec_count || !in->dec_ctx_sum || !in->tbt_slo_us || !in->budget_tokens ||
+      !in->budget_blocks || !in->budget_reqs || !out->admit_idx || !out->admit_cnt ||
+      !out->offload_idx || !out->offload_cnt || !out->drop_idx || !out->drop_cnt || !out->batch_lat_us)
+    return fail(c, ASC_E_INVAL, "asc_schedule_step: NULL array");
+  cudaSetDevice(c->device);
+  const int kind = ptr_kind(in->seg_off);
+  if (!same_kind(kind, {in->now_us, in->deadline_us, in->eff_prompt, in->flags, in->dec_count,
+                        in->dec_ctx_sum, in->tbt_slo_us, in->budget_tokens, in->budget_blocks,
+                        in->budget_reqs, out->admit_idx, out->admit_cnt, out->offload_idx,
+                        out->offload_cnt, out->drop_idx, out->drop_cnt, out->batch_lat_us,
+                        out->prefill_us}))
+    return fail(c, ASC_E_INVAL, "asc_schedule_step: host and device pointers mixed");
+  const int32_t S = in->S;
+  int64_t Q = 0;
+  if (kind == 1) {
+    cudaError_t e = cudaMemcpy(&Q, in->seg_off + S, sizeof(int64_t), cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) return cuda_check(c, e, "asc_schedule_step: read seg_off[S]");
+  } else {
+    Q = in->seg_off[S];
+    for (int32_t s = 0; s < S; s++)
+      if (in->seg_off[s + 1] < in->seg_off[s]) return fail(c, ASC_E_INVAL, "asc_schedule_step: seg_off decreasing");
+  }
+  if (Q < 0) return fail(c, ASC_E_INVAL, "asc_schedule_step: seg_off[S] < 0");
+  if (Q >= INT32_MAX) return fail(c, ASC_E_RANGE, "asc_schedule_step: total entries >= 2^31");
+  asc_status st;
+  if (kind == 1) {
+    st = launch_schedule_step(c, in, out, Q);
+    if (st) return st;
+    return collect_errors(c, "asc_schedule_step");
+  }
+  const size_t Sn = (size_t)S, Qn = (size_t)Q;
+  size_t need = rup(8 * (Sn + 1)) + 2 * rup(8 * Sn) + rup(8 * Qn) + rup(4 * Qn) + rup(Qn) +
+                rup(4 * Sn) + rup(8 * Sn) + 4 * rup(4 * Sn) + 4 * rup(4 * Qn) + rup(8 * Sn) + 4096;
+  st = ensure_stage(c, need);
+  if (st) return st;
+  Stager sg{c};
+  sg.base = c->stage;
+  asc_step_in di = *in;
+  di.seg_off = sg.up(in->seg_off, Sn + 1);
+  di.now_us = sg.up(in->now_us, Sn);
+  di.deadline_us = sg.up(in->deadline_us, Qn);
+  di.eff_prompt = sg.up(in->eff_prompt, Qn);
+  di.flags = sg.up(in->flags, Qn);
+  di.dec_count = sg.up(in->dec_count, Sn);
+  di.dec_ctx_sum = sg.up(in->dec_ctx_sum, Sn);
+  di.tbt_slo_us = sg.up(in->tbt_slo_us, Sn);
+  di.budget_tokens = sg.up(in->budget_tokens, Sn);
+  di.budget_blocks = sg.up(in->budget_blocks, Sn);
+  di.budget_reqs = sg.up(in->budget_reqs, Sn);
+  asc_step_out dout;
+  dout.admit_idx = sg.out(out->admit_idx, Qn);
+  dout.admit_cnt = sg.out(out->admit_cnt, Sn);
+  dout.offload_idx = sg.out(out->offload_idx, Qn);
+  dout.offload_cnt = sg.out(out->offload_cnt, Sn);
+  dout.drop_idx = sg.out(out->drop_idx, Qn);
+  dout.drop_cnt = sg.out(out->drop_cnt, Sn);
+  dout.batch_lat_us = sg.out(out->batch_lat_us, Sn);
+  dout.prefill_us = sg.out(out->prefill_us, Qn);
+  st = launch_schedule_step(c, &di, &dout, Q);
+  if (st) return st;
+  st = collect_errors(c, "asc_schedule_step");
+  if (st) return st;
+  return cuda_check(c, sg.download(), "asc_schedule_step: download");
+}
+
+asc_status asc_simulate_batch(asc_ctx* c, const asc_traces* tr, asc_outcomes* out) {
+  if (!c || !tr || !out) return fail(c, ASC_E_INVAL, "asc_simulate_batch: NULL argument");
+  c->err.clear();
+  c->timed = false;
+  if (tr->T < 0) return fail(c, ASC_E_INVAL, "asc_simulate_batch: T < 0");
+  if (!tr->trace_off || !tr->arrival_us || !tr->prompt_len || !tr->output_len || !tr->ttft_slo_us ||
+      !tr->tbt_slo_us || !out->first_token_us || !out->done_us || !out->prefill_start_us ||
+      !out->status || !out->digest)
+    return fail(c, ASC_E_INVAL, "asc_simulate_batch: NULL array");
+  cudaSetDevice(c->device);
+  const int kind = ptr_kind(tr->trace_off);
+  if (!same_kind(kind, {tr->arrival_us, tr->prompt_len, tr->output_len, tr->ttft_slo_us,
+                        tr->tbt_slo_us, tr->req_ttft_slo_us, out->first_token_us, out->done_us,
+                        out->prefill_start_us, out->status, out->digest, out->decisions,
+                        out->evaluations}))
+    return fail(c, ASC_E_INVAL, "asc_simulate_batch: host and device pointers mixed");
+  const int32_t T = tr->T;
+  int64_t R = 0;
+  if (kind == 1) {
+    cudaError_t e = cudaMemcpy(&R, tr->trace_off + T, sizeof(int64_t), cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) return cuda_check(c, e, "asc_simulate_batch: read trace_off[T]");
+  } else {
+    R = tr->trace_off[T];
+    for (int32_t t = 0; t < T; t++)
+      if (tr->trace_off[t + 1] < tr->trace_off[t]) return fail(c, ASC_E_INVAL, "asc_simulate_batch: trace_off decreasing");
+  }
+  if (R < 0) return fail(c, ASC_E_INVAL, "asc_simulate_batch: trace_off[T] < 0");
+  if (R >= INT32_MAX) return fail(c, ASC_E_RANGE, "asc_simulate_batch: total requests >= 2^31");
+  asc_status st;
+  if (kind == 1) {
+    st = launch_simulate(c, tr, out, R);
+    if (st) return st;
+    return collect_errors(c, "asc_simulate_batch");
+  }
+  const size_t Tn = (size_t)T, Rn = (size_t)R;
+  size_t need = rup(8 * (Tn + 1)) + rup(8 * Rn) * 2 + rup(4 * Rn) * 2 + rup(8 * Tn) * 2 +
+                rup(8 * Rn) * 3 + rup(4 * Rn) + rup(8 * Tn) * 3 + 4096;
+  st = ensure_stage(c, need);
+  if (st) return st;
+  Stager sg{c};
+  sg.base = c->stage;
+  asc_traces dt = *tr;
+  dt.trace_off = sg.up(tr->trace_off, Tn + 1);
+  dt.arrival_us = sg.up(tr->arrival_us, Rn);
+  dt.prompt_len = sg.up(tr->prompt_len, Rn);
+  dt.output_len = sg.up(tr->output_len, Rn);
+  dt.ttft_slo_us = sg.up(tr->ttft_slo_us, Tn);
+  dt.tbt_slo_us = sg.up(tr->tbt_slo_us, Tn);
+  dt.req_ttft_slo_us = sg.up(tr->req_ttft_slo_us, Rn);
+  asc_outcomes doc;
+  doc.first_token_us = sg.out(out->first_token_us, Rn);
+  doc.done_us = sg.out(out->done_us, Rn);
+  doc.prefill_start_us = sg.out(out->prefill_start_us, Rn);
+  doc.status = sg.out(out->status, Rn);
+  doc.digest = sg.out(out->digest, Tn);
+  doc.decisions = sg.out(out->decisions, Tn);
+  doc.evaluations = sg.out(out->evaluations, Tn);
+  st = launch_simulate(c, &dt, &doc, R);
+  if (st) return st;
+  st = collect_errors(c, "asc_simulate_batch");
+  if (st) return st;
+  return cuda_check(c, sg.download(), "asc_simulate_batch: download");
+}
+
+asc_status asc_goodput(asc_ctx* c, const asc_traces* tr, const asc_outcomes* out, uint64_t* good,
+                       uint64_t* total) {
+  if (!c || !tr || !out || !good || !total) return fail(c, ASC_E_INVAL, "asc_goodput: NULL argument");
+  c->err.clear();
+  c->timed = false;
+  if (tr->T < 0) return fail(c, ASC_E_INVAL, "asc_goodput: T < 0");
+  cudaSetDevice(c->device);
+  const int kind = ptr_kind(tr->trace_off);
+  if (!same_kind(kind, {tr->arrival_us, tr->output_len, tr->ttft_slo_us, tr->tbt_slo_us,
+                        tr->req_ttft_slo_us, out->first_token_us, out->done_us, out->status,
+                        good, total}))
+    return fail(c, ASC_E_INVAL, "asc_goodput: host and device pointers mixed");
+  const int32_t T = tr->T;
+  asc_status st;
+  if (kind == 1) {
+    st = launch_goodput(c, tr, out, good, total);
+    if (st) return st;
+    return collect_errors(c, "asc_goodput");
+  }
+  const size_t Tn = (size_t)T, Rn = (size_t)tr->trace_off[T];
+  size_t need = rup(8 * (Tn + 1)) + rup(8 * Rn) * 4 + rup(4 * Rn) * 2 + rup(8 * Tn) * 4 + 4096;
+  st = ensure_stage(c, need);
+  if (st) return st;
+  Stager sg{c};
+  sg.base = c->stage;
+  asc_traces dt = *tr;
+  dt.trace_off = sg.up(tr->trace_off, Tn + 1);
+  dt.arrival_us = sg.up(tr->arrival_us, Rn);
+  dt.prompt_len = nullptr;
+  dt.output_len = sg.up(tr->output_len, Rn);
+  dt.ttft_slo_us = sg.up(tr->ttft_slo_us, Tn);
+  dt.tbt_slo_us = sg.up(tr->tbt_slo_us, Tn);
+  dt.req_ttft_slo_us = sg.up(tr->req_ttft_slo_us, Rn);
+  asc_outcomes doc{};
+  doc.first_token_us = sg.up(out->first_token_us, Rn);
+  doc.done_us = sg.up(out->done_us, Rn);
+  doc.status = sg.up(out->status, Rn);
+  uint64_t* dg = sg.out(good, Tn);
+  uint64_t* dtt = sg.out(total, Tn);
+  st = launch_goodput(c, &dt, &doc, dg, dtt);
+  if (st) return st;
+  st = collect_errors(c, "asc_goodput");
+  if (st) return st;
+  return cuda_check(c, sg.download(), "asc_goodput: download");
+}
+
+int64_t asc_last_kernel_launches(const asc_ctx* c) { return c ? c->last_kernel_launches : 0; }
+
+double asc_last_kernel_ms(const asc_ctx* c) {
+  if (!c || !c->timed) return -1.0;
+  float ms = -1.0f;
+  if (cudaEventElapsedTime(&ms, c->ev0, c->ev1) != cudaSuccess) { cudaGetLastError(); return -1.0; }
+  return (double)ms;
+}
+
+}  // extern "C"

@@ -1,0 +1,260 @@
+// asc_dev.cuh — device building blocks of the sm_100a hot path (no oracle code is shared).
+//
+//  * Model / lat_us: the performance model of PAPER.md Eq. 1-5 with the App. A GEMM
+//    terms (Tables 3-4, Eq. 6-7), evaluated from per-batch integer moments
+//    (B_p, Σp, Σp², Σp·⌈p/b⌉, B_d, Σl̂) so a batch of any size costs O(1) after a warp reduction.
+//    F and M are exact uint64 (< 2^53); the fp64 regression uses explicit round-to-nearest
+//    intrinsics in a fixed order (no FMA contraction) so the result is bitwise reproducible.
+//  * WarpTopK: per-warp streaming selection of the K = 32*KPL smallest (key, idx) pairs, held as a
+//    sorted list in registers (element e at lane e%32, register e/32), merged with bitonic
+//    networks over warp shuffles.  Algorithm 1 only ever admits a prefix of at most R <= K
+//    entries of the key order, so the K smallest entries are all it needs.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace asc {
+
+constexpr int64_t INF64 = INT64_MAX;
+constexpr int32_t INF32 = INT32_MAX;
+constexpr uint64_t TWO53 = 1ull << 53;
+constexpr uint32_t FULL = 0xffffffffu;
+
+// error bits raised by kernels (ctx->dev_err)
+constexpr int ERR_RANGE = 1;
+constexpr int ERR_INVARIANT = 2;
+constexpr int ERR_INVAL = 4;
+
+struct Model {
+  uint64_t n, s, L, d, b;
+  uint64_t W;    // weights per layer (elements): 4h^2 + 2hm (read once per non-empty batch, G8)
+  uint64_t FT;   // GEMM flops per token per layer: 4h^2 + 2hm (Tables 3-4 row sums)
+  uint64_t MT;   // GEMM activation elements per token per layer: 8h + 2m
+  double c0, c1, c2, c3, c4, FH, MH;
+};
+
+// Latency in integer microseconds of a batch given its integer moments (G17, G18).
+// Returns -1 (and the caller raises ERR_RANGE) when F or M reaches 2^53.
+__host__ __device__ inline int64_t lat_us(const Model& md, uint64_t Bp, uint64_t sp, uint64_t sp2,
+                                          uint64_t spc, uint64_t Bd, uint64_t sl) {
+  const uint64_t tok = sp + Bd;
+  const uint64_t G = (Bp + Bd) ? 1 : 0;
+  const uint64_t attnF = md.n * (2 * md.s * sp2 + 2 * md.s * sl);
+  const uint64_t attnM = md.n * (2 * md.s * sp + 3 * md.s * spc + 2 * md.s * sl + 2 * md.s * Bd);
+  const uint64_t F = md.L * (tok * md.FT + attnF);
+  const uint64_t M = md.L * (G * md.W + tok * md.MT + attnM) * md.d;
+  if (F >= TWO53 || M >= TWO53) return -1;
+#ifdef __CUDA_ARCH__
+  const double tM = __ddiv_rn(__ull2double_rn(M), md.MH);
+  const double tF = __ddiv_rn(__ull2double_rn(F), md.FH);
+  const double mx = (tM > tF) ? tM : tF;
+  double t = __dmul_rn(md.c0, __dadd_rn(tM, tF));
+  t = __dadd_rn(t, __dmul_rn(md.c1, mx));
+  t = __dadd_rn(t, __dmul_rn(md.c2, tM));
+  t = __dadd_rn(t, __dmul_rn(md.c3, tF));
+  t = __dadd_rn(t, md.c4);
+  if (!(t > 0.0)) t = 0.0;
+  const double us = ceil(__dmul_rn(t, 1e6));
+#else
+  volatile double tM = (double)M / md.MH;
+  volatile double tF = (double)F / md.FH;
+  const double mx = (tM > tF) ? tM : tF;
+  volatile double t = md.c0 * (tM + tF);
+  t = t + md.c1 * mx;
+  t = t + md.c2 * tM;
+  t = t + md.c3 * tF;
+  t = t + md.c4;
+  if (!(t > 0.0)) t = 0.0;
+  volatile double t6 = t * 1e6;
+  const double us = ceil(t6);
+#endif
+  const int64_t v = (int64_t)us;
+  return v < 1 ? 1 : v;
+}
+
+__host__ __device__ inline uint64_t ceil_div_u(uint64_t x, uint64_t y) { return (x + y - 1) / y; }
+
+// Standalone prefill latency of one prompt of p tokens (a1).
+__host__ __device__ inline int64_t prefill_lat(const Model& md, uint64_t p) {
+  return lat_us(md, 1, p, p * p, p * ceil_div_u(p, md.b), 0, 0);
+}
+
+__device__ __forceinline__ uint64_t mix64(uint64_t x) {
+  uint64_t z = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ull;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+  return z ^ (z >> 31);
+}
+
+__device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
+__device__ __forceinline__ uint32_t lanemask_lt() {
+  uint32_t m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+template <typename T>
+__device__ __forceinline__ T warp_sum(T v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
+  return v;
+}
+template <typename T>
+__device__ __forceinline__ T warp_min(T v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) { T w = __shfl_xor_sync(FULL, v, o); v = w < v ? w : v; }
+  return v;
+}
+template <typename T>
+__device__ __forceinline__ T warp_max(T v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) { T w = __shfl_xor_sync(FULL, v, o); v = w > v ? w : v; }
+  return v;
+}
+// inclusive scan across the warp
+template <typename T>
+__device__ __forceinline__ T warp_incl_scan(T v) {
+  const int l = lane_id();
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    T w = __shfl_up_sync(FULL, v, o);
+    if (l >= o) v += w;
+  }
+  return v;
+}
+
+// ------------------------------------------------------------------ (key, idx) ordering ------
+struct KI {
+  int64_t k;
+  int32_t i;
+};
+__device__ __forceinline__ bool ki_less(const KI& a, const KI& b) {
+  return a.k < b.k || (a.k == b.k && a.i < b.i);
+}
+__device__ __forceinline__ KI ki_inf() { return KI{INF64, INF32}; }
+__device__ __forceinline__ KI ki_shfl_xor(const KI& v, int m) {
+  return KI{__shfl_xor_sync(FULL, v.k, m), __shfl_xor_sync(FULL, v.i, m)};
+}
+__device__ __forceinline__ KI ki_shfl(const KI& v, int src) {
+  return KI{__shfl_sync(FULL, v.k, src), __shfl_sync(FULL, v.i, src)};
+}
+__device__ __forceinline__ KI ki_min(const KI& a, const KI& b) { return ki_less(b, a) ? b : a; }
+__device__ __forceinline__ KI ki_max(const KI& a, const KI& b) { return ki_less(b, a) ? a : b; }
+
+// Bitonic sort of 32 elements, one per lane, ascending by lane.
+__device__ __forceinline__ KI sort32(KI v) {
+  const int l = lane_id();
+#pragma unroll
+  for (int k = 2; k <= 32; k <<= 1) {
+#pragma unroll
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      const KI o = ki_shfl_xor(v, j);
+      const bool up = (l & k) == 0;
+      const bool lower = (l & j) == 0;
+      v = (lower == up) ? ki_min(v, o) : ki_max(v, o);
+    }
+  }
+  return v;
+}
+
+// Warp-held sorted list of the K = 32*KPL smallest elements seen.
+template <int KPL>
+struct WarpTopK {
+  KI a[KPL];
+
+  __device__ __forceinline__ void init() {
+#pragma unroll
+    for (int r = 0; r < KPL; r++) a[r] = ki_inf();
+  }
+  // a is bitonic after the min-with-reversed step; sort it ascending.
+  __device__ __forceinline__ void bitonic_merge() {
+    const int l = lane_id();
+#pragma unroll
+    for (int j = KPL / 2; j > 0; j >>= 1) {     // cross-register stages (stride j*32)
+#pragma unroll
+      for (int r = 0; r < KPL; r++) {
+        if ((r & j) == 0) {
+          const KI x = a[r], y = a[r | j];
+          a[r] = ki_min(x, y);
+          a[r | j] = ki_max(x, y);
+        }
+      }
+    }
+#pragma unroll
+    for (int j = 16; j > 0; j >>= 1) {          // in-register stages across lanes
+      const bool lower = (l & j) == 0;
+#pragma unroll
+      for (int r = 0; r < KPL; r++) {
+        const KI o = ki_shfl_xor(a[r], j);
+        a[r] = lower ? ki_min(a[r], o) : ki_max(a[r], o);
+      }
+    }
+  }
+  // merge a sorted 32-element warp vector b (one per lane, ascending) into the list
+  __device__ __forceinline__ void merge32(const KI& b) {
+    const KI br = ki_shfl(b, 31 - lane_id());
+    a[KPL - 1] = ki_min(a[KPL - 1], br);
+    bitonic_merge();
+  }
+  // merge another full sorted list (same layout)
+  __device__ __forceinline__ void merge_list(const KI (&b)[KPL]) {
+    const int src = 31 - lane_id();
+#pragma unroll
+    for (int r = 0; r < KPL; r++) a[r] = ki_min(a[r], ki_shfl(b[KPL - 1 - r], src));
+    bitonic_merge();
+  }
+  __device__ __forceinline__ KI kth() const {  // current K-th smallest (the threshold)
+    return ki_shfl(a[KPL - 1], 31);
+  }
+};
+
+// Streaming front-end: candidates below the threshold are appended to a 64-slot shared buffer and
+// merged 32 at a time, so a merge costs one sort32 + one bitonic merge per 32 survivors.
+template <int KPL>
+struct TopKStream {
+  WarpTopK<KPL> top;
+  KI thr;
+  int cnt;
+  KI* buf;  // 64 slots in shared memory (per warp)
+
+  __device__ __forceinline__ void init(KI* sbuf) {
+    top.init();
+    thr = ki_inf();
+    cnt = 0;
+    buf = sbuf;
+  }
+  __device__ __forceinline__ void flush32() {
+    __syncwarp();
+    KI y = buf[lane_id()];
+    __syncwarp();
+    KI rest = (lane_id() < cnt - 32) ? buf[32 + lane_id()] : ki_inf();
+    __syncwarp();
+    if (lane_id() < cnt - 32) buf[lane_id()] = rest;
+    cnt -= 32;
+    y = sort32(y);
+    top.merge32(y);
+    thr = top.kth();
+    __syncwarp();
+  }
+  // offer one element per lane (valid = participates)
+  __device__ __forceinline__ void push(const KI& x, bool valid) {
+    const bool c = valid && ki_less(x, thr);
+    const uint32_t m = __ballot_sync(FULL, c);
+    if (m == 0) return;
+    if (c) buf[cnt + __popc(m & lanemask_lt())] = x;
+    cnt += __popc(m);
+    if (cnt >= 32) flush32();
+  }
+  __device__ __forceinline__ void finish() {
+    if (cnt > 0) {
+      __syncwarp();
+      KI y = lane_id() < cnt ? buf[lane_id()] : ki_inf();
+      __syncwarp();
+      cnt = 0;
+      y = sort32(y);
+      top.merge32(y);
+      thr = top.kth();
+    }
+  }
+};
+
+}  // namespace asc

@@ -1,0 +1,55 @@
+// asc_internal.h — context, workspace and kernel-launch declarations behind include/asc.h.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <string>
+
+#include "../../include/asc.h"
+#include "asc_dev.cuh"
+
+struct asc_ctx {
+  asc_config cfg;          // as given (tp not yet applied)
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  asc::Model md;           // tp-divided model constants
+  int32_t pt_size = 0;     // prefill table covers eff_prompt in [0, pt_size)
+  int64_t* d_pf_tab = nullptr;  // prefill_us by eff_prompt (a1, cached per ctx)
+  int64_t w_hp = 0;        // worst-case HP batch latency (G24)
+  int* d_err = nullptr;    // device error bits (asc::ERR_*)
+  char* ws = nullptr;      // device workspace
+  size_t ws_cap = 0;
+  char* stage = nullptr;   // device staging for host-pointer calls
+  size_t stage_cap = 0;
+  std::string err;
+  int64_t last_kernel_launches = 0;  // kernels launched by the last call (bench evidence)
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;  // bracket the dominant kernel of the last call
+  bool timed = false;
+};
+
+namespace asc {
+
+// bump allocator over a device buffer
+struct Arena {
+  char* base;
+  size_t cap, off = 0;
+  template <typename T>
+  T* take(size_t n) {
+    off = (off + 255) & ~size_t(255);
+    T* p = reinterpret_cast<T*>(base + off);
+    off += n * sizeof(T);
+    return p;
+  }
+};
+
+struct StepArgs;  // defined in step.cu
+asc_status launch_schedule_step(asc_ctx* c, const asc_step_in* in, asc_step_out* out, int64_t Q);
+asc_status launch_simulate(asc_ctx* c, const asc_traces* tr, asc_outcomes* out, int64_t R);
+asc_status launch_goodput(asc_ctx* c, const asc_traces* tr, const asc_outcomes* out,
+                          uint64_t* good, uint64_t* total);
+asc_status ensure_ws(asc_ctx* c, size_t bytes);
+asc_status fail(asc_ctx* c, asc_status s, const std::string& msg);
+asc_status cuda_check(asc_ctx* c, cudaError_t e, const char* what);
+// read device error bits, reset them, map to a status
+asc_status collect_errors(asc_ctx* c, const char* where);
+
+}  // namespace asc

@@ -130,7 +130,7 @@ def check_textbook_rules(sim, goodput, rng, trials=40):
 def random_small_batch(rng, T, nmax, shape="sharegpt"):
     trs, tt, tb = [], [], []
     for t in range(T):
-        n = int(rng.integers(0, nmax + 1))
+        n = int(rng.integers(1, nmax + 1))
         j = int(rng.integers(4, 200))
         trs.append(TR.gen_trace(int(rng.integers(1, 1 << 30)), t, shape, j, n))
         scale = int(rng.integers(1, 17))

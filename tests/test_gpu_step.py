@@ -1,0 +1,147 @@
+"""GPU parity of asc_schedule_step (rows a1-a6) against the oracle, through the C ABI.
+
+Integer outputs (admission lists in priority order, offload/drop lists, counts, microsecond
+latencies) must be bit-exact; prefill latencies are compared exactly (the fp64 op order is fixed,
+DESIGN.md §Bit-exactness), which is stricter than north_star's 1e-9 relative bound.
+"""
+import numpy as np
+import pytest
+
+import helpers as H
+from gen import presets as P
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module")
+def asc():
+    from paper_2504_20828_b200 import asc as A
+    assert torch.cuda.is_available()
+    return A
+
+
+def to_dev(ins):
+    return {k: torch.from_numpy(np.ascontiguousarray(v)).cuda() for k, v in ins.items()}
+
+
+def run_gpu(asc, cfg, ins, host=False):
+    ctx = asc.Context(cfg, 0)
+    try:
+        if host:
+            out = ctx.schedule_step({k: np.ascontiguousarray(v) for k, v in ins.items()})
+        else:
+            out = ctx.schedule_step(to_dev(ins))
+            out = {k: (v.cpu().numpy() if v is not None else None) for k, v in out.items()}
+        launches = ctx.last_launches()
+    finally:
+        ctx.close()
+    assert launches >= 1
+    return out
+
+
+def compare(got, exp, seg_off):
+    S = len(seg_off) - 1
+    Q = int(seg_off[-1])
+    for k in ("admit_cnt", "offload_cnt", "drop_cnt", "batch_lat_us"):
+        assert np.array_equal(got[k][:S], exp[k][:S]), k
+    assert np.array_equal(got["prefill_us"][:Q], exp["prefill_us"][:Q])
+    g = H.segment_lists(got, seg_off)
+    e = H.segment_lists(exp, seg_off)
+    for s in range(S):
+        assert g[s] == e[s], f"segment {s}"
+
+
+@pytest.mark.parametrize("policy", ["EDF_LAXITY", "EDF_DEADLINE", "FCFS", "SJF", "LJF"])
+def test_w1_hand_worked_gpu(asc, policy):
+    cfg, ins, exp, rid = H.w1_step_inputs(policy)
+    out = run_gpu(asc, cfg, ins)
+    adm, off, drp = H.segment_lists(out, ins["seg_off"])[0]
+    assert [rid[i] for i in adm] == exp["admitted"]
+    assert [rid[i] for i in off] == exp["offloaded"]
+    assert out["batch_lat_us"][0] == exp["batch_lat"] * H.SEC
+
+
+def test_prefill_table_exhaustive(asc, oracle):
+    # a1 for every prompt length the LongBench preset can produce, and beyond the table
+    cfg = P.config(topo=P.topology(lp_token_budget=65536))
+    Q = 70000
+    ins = dict(seg_off=np.array([0, Q], np.int64), now_us=np.zeros(1, np.int64),
+               deadline_us=np.full(Q, 10 ** 12, np.int64),
+               eff_prompt=np.arange(1, Q + 1, dtype=np.int32), flags=np.zeros(Q, np.uint8),
+               dec_count=np.zeros(1, np.int32), dec_ctx_sum=np.zeros(1, np.int64),
+               tbt_slo_us=np.zeros(1, np.int64), budget_tokens=np.zeros(1, np.int32),
+               budget_blocks=np.zeros(1, np.int32), budget_reqs=np.zeros(1, np.int32))
+    got = run_gpu(asc, cfg, ins)
+    exp = oracle.schedule_step(cfg, **ins)
+    assert np.array_equal(got["prefill_us"][:Q], exp["prefill_us"])
+
+
+@pytest.mark.parametrize("policy", ["EDF_LAXITY", "EDF_DEADLINE", "FCFS", "SJF", "LJF"])
+@pytest.mark.parametrize("drop", [0, 1])
+def test_random_segments_shallow(asc, oracle, policy, drop):
+    rng = np.random.default_rng(hash((policy, drop)) % 2 ** 32)
+    cfg = P.config(flg=P.flags(policy=policy, drop=drop))
+    ins = H.random_step_inputs(rng, 300, 60, cfg)
+    compare(run_gpu(asc, cfg, ins), oracle.schedule_step(cfg, **ins), ins["seg_off"])
+
+
+@pytest.mark.parametrize("policy", ["EDF_LAXITY", "SJF", "FCFS", "LJF"])
+def test_random_segments_multi_task(asc, oracle, policy):
+    # segments spanning several 2048-entry warp tasks plus a ragged tail, and empty segments
+    rng = np.random.default_rng(7)
+    cfg = P.config(flg=P.flags(policy=policy, drop=1))
+    qs = [0, 1, 2047, 2048, 2049, 6000, 0, 13000, 31, 4097]
+    ins = H.random_step_inputs(rng, len(qs), 0, cfg, qs=qs)
+    compare(run_gpu(asc, cfg, ins), oracle.schedule_step(cfg, **ins), ins["seg_off"])
+
+
+def test_deep_segments_ample_budgets(asc, oracle):
+    rng = np.random.default_rng(9)
+    cfg = P.config()
+    ins = H.random_step_inputs(rng, 4, 0, cfg, budgets="config", qs=[100_000, 50_000, 3, 70_001])
+    compare(run_gpu(asc, cfg, ins), oracle.schedule_step(cfg, **ins), ins["seg_off"])
+
+
+def test_adversarial_key_order(asc, oracle):
+    # keys strictly decreasing with position: every entry beats the running threshold
+    cfg = P.config(flg=P.flags(policy="EDF_DEADLINE"))
+    Q = 9000
+    ins = dict(seg_off=np.array([0, Q], np.int64), now_us=np.array([10 ** 7], np.int64),
+               deadline_us=(2 * 10 ** 7 - np.arange(Q, dtype=np.int64) * 7),
+               eff_prompt=np.full(Q, 50, np.int32), flags=np.zeros(Q, np.uint8),
+               dec_count=np.zeros(1, np.int32), dec_ctx_sum=np.zeros(1, np.int64),
+               tbt_slo_us=np.zeros(1, np.int64), budget_tokens=np.array([8192], np.int32),
+               budget_blocks=np.array([25000], np.int32), budget_reqs=np.array([128], np.int32))
+    compare(run_gpu(asc, cfg, ins), oracle.schedule_step(cfg, **ins), ins["seg_off"])
+
+
+def test_host_pointer_path(asc, oracle):
+    rng = np.random.default_rng(3)
+    cfg = P.config(flg=P.flags(drop=1))
+    ins = H.random_step_inputs(rng, 50, 3000, cfg)
+    got = run_gpu(asc, cfg, ins, host=True)
+    compare(got, oracle.schedule_step(cfg, **ins), ins["seg_off"])
+
+
+def test_many_tiny_segments(asc, oracle):
+    rng = np.random.default_rng(4)
+    cfg = P.config()
+    ins = H.random_step_inputs(rng, 20000, 0, cfg, qs=np.full(20000, 32))
+    compare(run_gpu(asc, cfg, ins), oracle.schedule_step(cfg, **ins), ins["seg_off"])
+
+
+def test_errors(asc):
+    rng = np.random.default_rng(5)
+    cfg = P.config()
+    ins = H.random_step_inputs(rng, 3, 10, cfg)
+    bad = dict(ins, budget_reqs=np.array([129, 1, 1], np.int32))
+    with pytest.raises(asc.AscError) as e:
+        run_gpu(asc, cfg, bad)
+    assert e.value.code == 6
+    ins2 = H.random_step_inputs(rng, 2, 0, cfg, qs=[3, 3])
+    ins2["eff_prompt"][1] = 0
+    with pytest.raises(asc.AscError) as e:
+        run_gpu(asc, cfg, ins2)
+    assert e.value.code == 1
