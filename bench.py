@@ -267,13 +267,12 @@ def main():
     finished = int((st != 0).sum())
     good = int(res["good"][:batch.T].cpu().numpy().view(np.uint64).sum())
     total = int(res["total"][:batch.T].cpu().numpy().view(np.uint64).sum())
-    counters = torch.tensor([dec, evals, finished, good, total, batch.R], dtype=torch.int64, device=dev)
-    tmax = torch.tensor([ms_total], dtype=torch.float64, device=dev)
-    if world > 1:
-        torch.distributed.all_reduce(counters)
-        torch.distributed.all_reduce(tmax, op=torch.distributed.ReduceOp.MAX)
-    dec_all, evals_all, fin_all, good_all, total_all, R_all = [int(x) for x in counters.tolist()]
-    ms_step = float(tmax.item()) / a.steps
+    from paper_2504_20828_b200 import dist as D
+    tot = D.reduce_counters(dict(decisions=dec, evaluations=evals, finished=finished, good=good,
+                                 total=total, requests=batch.R), dev)
+    dec_all, evals_all, fin_all = tot["decisions"], tot["evaluations"], tot["finished"]
+    good_all, total_all = tot["good"], tot["total"]
+    ms_step = D.reduce_max(ms_total, dev) / a.steps
     value = dec_all / (ms_step * 1e-3)
     sim_ms = float(np.mean(sims))
     algo = 44 * batch.R + 12 * evals          # per launch on this rank
