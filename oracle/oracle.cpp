@@ -336,8 +336,12 @@ struct Sim {
     h.waiting.push_back(i);
     std::sort(h.waiting.begin(), h.waiting.end(), [&](int x, int y) { return fcfs_less(x, y); });
   }
+  // Digest: the record of one formation hashes as sum_i mix(v_i + (i+1) * G)
+  // (mod 2^64; position-keyed, so order-sensitive), chained per instance by h = mix(h ^ record).
   void record(Inst& in, const std::vector<uint64_t>& v) {
-    for (uint64_t x : v) in.hash = mix(in.hash ^ x);
+    uint64_t rec = 0;
+    for (size_t i = 0; i < v.size(); i++) rec += mix(v[i] + (uint64_t)(i + 1) * 0x9E3779B97F4A7C15ull);
+    in.hash = mix(in.hash ^ rec);
   }
   int64_t lat(const std::vector<int>& pre, const std::vector<int>& dec) {
     std::vector<int64_t> p, l;

@@ -107,8 +107,9 @@ asc_status asc_create(const asc_config* cfg, int device, void* cuda_stream, asc_
   CHK(t.n_lp >= 1, "topo.n_lp must be >= 1");
   CHK(t.n_hp >= 0, "topo.n_hp must be >= 0");
   CHK(t.n_lp + t.n_hp <= ASC_MAX_INSTANCES, "topo.n_lp + topo.n_hp exceeds ASC_MAX_INSTANCES");
-  CHK(t.block_tokens >= 1, "topo.block_tokens must be >= 1");
+  CHK(t.block_tokens >= 1 && t.block_tokens <= 512, "topo.block_tokens must be in [1, 512]");
   CHK(t.kv_blocks_lp >= 1 && (t.n_hp == 0 || t.kv_blocks_hp >= 1), "topo.kv_blocks must be >= 1");
+  CHK(t.kv_blocks_lp < (1 << 22) && t.kv_blocks_hp < (1 << 22), "topo.kv_blocks must be < 2^22");
   CHK(t.lp_max_batch >= 1 && t.lp_max_batch <= ASC_MAX_BATCH, "topo.lp_max_batch must be in [1, ASC_MAX_BATCH]");
   CHK(t.lp_token_budget >= 1 && t.lp_token_budget < (1 << 24), "topo.lp_token_budget must be in [1, 2^24)");
   CHK(t.hp_token_budget >= 1 && t.hp_token_budget < (1 << 24), "topo.hp_token_budget must be in [1, 2^24)");
@@ -139,6 +140,14 @@ asc_status asc_create(const asc_config* cfg, int device, void* cuda_stream, asc_
   c->md.W = 4 * h * h + 2 * h * m;
   c->md.FT = 4 * h * h + 2 * h * m;
   c->md.MT = 8 * h + 2 * m;
+  {
+    const uint64_t L = (uint64_t)a.L, d = (uint64_t)a.dtype_bytes, s2 = 2 * (uint64_t)a.s;
+    c->md.dF_bd = L * c->md.FT;
+    c->md.dF_sl = L * n * s2;
+    c->md.dM_0 = L * d * c->md.W;
+    c->md.dM_bd = L * d * (c->md.MT + n * s2);
+    c->md.dM_sl = L * d * n * s2;
+  }
   c->md.c0 = cfg->perf.c[0]; c->md.c1 = cfg->perf.c[1]; c->md.c2 = cfg->perf.c[2];
   c->md.c3 = cfg->perf.c[3]; c->md.c4 = cfg->perf.c[4];
   c->md.FH = cfg->perf.F_H;

@@ -30,8 +30,34 @@ struct Model {
   uint64_t W;    // weights per layer (elements): 4h^2 + 2hm (read once per non-empty batch, G8)
   uint64_t FT;   // GEMM flops per token per layer: 4h^2 + 2hm (Tables 3-4 row sums)
   uint64_t MT;   // GEMM activation elements per token per layer: 8h + 2m
+  // decode-only batches in closed form (exact integer identities of the expression below):
+  // F = dF_bd*B_d + dF_sl*Σl̂,  M = dM_0 + dM_bd*B_d + dM_sl*Σl̂
+  uint64_t dF_bd, dF_sl, dM_0, dM_bd, dM_sl;
   double c0, c1, c2, c3, c4, FH, MH;
 };
+
+// Eq. 4-5 + G17/G18 from exact integer F, M (< 2^53): fixed fp64 RN order, ceil to microseconds.
+__device__ __forceinline__ int64_t lat_from_FM(const Model& md, uint64_t F, uint64_t M) {
+  const double tM = __ddiv_rn(__ull2double_rn(M), md.MH);
+  const double tF = __ddiv_rn(__ull2double_rn(F), md.FH);
+  const double mx = (tM > tF) ? tM : tF;
+  double t = __dmul_rn(md.c0, __dadd_rn(tM, tF));
+  t = __dadd_rn(t, __dmul_rn(md.c1, mx));
+  t = __dadd_rn(t, __dmul_rn(md.c2, tM));
+  t = __dadd_rn(t, __dmul_rn(md.c3, tF));
+  t = __dadd_rn(t, md.c4);
+  if (!(t > 0.0)) t = 0.0;
+  const int64_t v = (int64_t)ceil(__dmul_rn(t, 1e6));
+  return v < 1 ? 1 : v;
+}
+
+// Decode-only batch of B_d requests with context sum sl (a2's TBT term, a6 for decode steps).
+__device__ __forceinline__ int64_t lat_decode(const Model& md, uint64_t Bd, uint64_t sl) {
+  const uint64_t F = md.dF_bd * Bd + md.dF_sl * sl;
+  const uint64_t M = md.dM_0 + md.dM_bd * Bd + md.dM_sl * sl;
+  if (F >= TWO53 || M >= TWO53) return -1;
+  return lat_from_FM(md, F, M);
+}
 
 // Latency in integer microseconds of a batch given its integer moments (G17, G18).
 // Returns -1 (and the caller raises ERR_RANGE) when F or M reaches 2^53.
@@ -45,16 +71,7 @@ __host__ __device__ inline int64_t lat_us(const Model& md, uint64_t Bp, uint64_t
   const uint64_t M = md.L * (G * md.W + tok * md.MT + attnM) * md.d;
   if (F >= TWO53 || M >= TWO53) return -1;
 #ifdef __CUDA_ARCH__
-  const double tM = __ddiv_rn(__ull2double_rn(M), md.MH);
-  const double tF = __ddiv_rn(__ull2double_rn(F), md.FH);
-  const double mx = (tM > tF) ? tM : tF;
-  double t = __dmul_rn(md.c0, __dadd_rn(tM, tF));
-  t = __dadd_rn(t, __dmul_rn(md.c1, mx));
-  t = __dadd_rn(t, __dmul_rn(md.c2, tM));
-  t = __dadd_rn(t, __dmul_rn(md.c3, tF));
-  t = __dadd_rn(t, md.c4);
-  if (!(t > 0.0)) t = 0.0;
-  const double us = ceil(__dmul_rn(t, 1e6));
+  return lat_from_FM(md, F, M);
 #else
   volatile double tM = (double)M / md.MH;
   volatile double tF = (double)F / md.FH;
@@ -66,10 +83,9 @@ __host__ __device__ inline int64_t lat_us(const Model& md, uint64_t Bp, uint64_t
   t = t + md.c4;
   if (!(t > 0.0)) t = 0.0;
   volatile double t6 = t * 1e6;
-  const double us = ceil(t6);
-#endif
-  const int64_t v = (int64_t)us;
+  const int64_t v = (int64_t)ceil(t6);
   return v < 1 ? 1 : v;
+#endif
 }
 
 __host__ __device__ inline uint64_t ceil_div_u(uint64_t x, uint64_t y) { return (x + y - 1) / y; }

@@ -2,15 +2,21 @@
 // rows a1-a6 inlined per formation) and asc_goodput (row a8).
 //
 // One warp owns one trace at a time (traces are handed out by an atomic counter so long traces
-// do not serialise a static partition).  All per-trace state stays resident in HBM/L2:
-//   per request  : deadline (int64), effective prompt (int32), flag word (uint32)
-//   per instance : waiting queue (id, key) with time-invariant keys, decode set
-//                  slots (id, context l̂, blocks held, tokens remaining), running-batch prefill list
-//   per trace    : drop / preemption / offload scratch lists and the in-flight offload ring
-// Instance scalars (busy, end, kv_free, ticket, history, digest) live in shared memory.  Every
-// queue operation is warp-parallel: ballot/popc stable compaction, warp scans, the bitonic top-K
-// of asc_dev.cuh for Algorithm 1's sort, warp reductions for the batch moments of Eq. 1-3.
-// The event order is the canonical A-E phase order of DESIGN.md §Event loop.
+// do not serialise a static partition).  Per-trace state stays resident on the GPU:
+//   per request  (HBM)  : deadline (int64), effective prompt (int32), flag word (uint32)
+//   per instance (HBM)  : waiting queue (key, id) with time-invariant keys, the
+//                         running batch's prefill ids
+//   per instance (SMEM) : scalars (end = INF when idle, kv_free, ticket, history, running Σl̂,
+//                         pending KV growth, digest) and the first 128 decode slots
+//                         {id, l̂, remaining, held | (l̂ mod bs)<<22 | pending<<31}
+//                         (LP decode sets never exceed 128 = P:371; HP slots beyond spill to HBM)
+//   per trace    (HBM)  : drop / eviction / offload scratch lists and the in-flight offload ring
+// A decode step — by far the most frequent decision — costs one pass over the decode slots in
+// shared memory (the completion pass also precomputes the next formation's block growth and
+// Σl̂, with no integer division), one closed-form decode cost + fp64 evaluation of Eq. 4-5, and
+// an 8-lane digest update.  Rare paths (admission with a non-empty queue, eviction, drops, HP
+// prefill, offload dispatch, prefill completions) are __noinline__ so the hot loop stays small.
+// The event order is the canonical A-E phase order of DESIGN.md §2.
 #include "asc_internal.h"
 
 using namespace asc;
@@ -18,17 +24,23 @@ using namespace asc;
 namespace {
 
 constexpr int KPL = 4;
-constexpr int SW = 4;  // warps (traces in flight) per CTA
-constexpr int MAXI = ASC_MAX_INSTANCES;
+constexpr int SW = 4;      // warps (traces in flight) per CTA
+constexpr int DCAP = 128;  // decode slots per instance kept in shared memory
+constexpr uint64_t GOLD = 0x9E3779B97F4A7C15ull;
 
 enum : uint32_t { F_EVER = 1u, F_ONHP = 2u, F_TICK = 4u, F_OFFL = 8u };
 constexpr uint32_t ST_SHIFT = 4, INST_SHIFT = 8, NPRE_SHIFT = 16;
+// decode slot .w: bits 0-21 blocks held (before pending growth), 22-30 l̂ mod bs, 31 pending
+constexpr int32_t HELD_MASK = (1 << 22) - 1;
+constexpr int R_SHIFT = 22;
+constexpr int32_t PEND = (int32_t)0x80000000;
 
 struct SInst {
-  int64_t end, hist_sum;
+  int64_t end;               // end of the running batch, INF64 when idle
+  int64_t hist_sum, ctx_sum;
   uint64_t hash;
-  int32_t kv_free, kv_total, wq_len, ds_len, bp_len, hist_cnt;
-  int32_t busy, batch_dec, ticket, tk_live, hp, pad;
+  int32_t kv_free, kv_total, wq_len, ds_len, bp_len, hist_cnt, need_sum;
+  int32_t batch_dec, ticket, tk_live, hp, papp;
 };
 
 struct SimP {
@@ -56,7 +68,7 @@ struct SimP {
   uint32_t* rq_fl;
   int64_t* wq_key;
   int32_t* wq_id;
-  int32_t *ds_id, *ds_ctx, *ds_held, *ds_rem;
+  int4* ds_g;  // decode-slot overflow (slot index >= DCAP)
   int32_t* bp_id;
   int32_t *scr_drop, *scr_pre, *scr_off;
   int64_t* fl_t;
@@ -65,10 +77,16 @@ struct SimP {
   int* next_trace;
 };
 
-struct Tr {  // per-trace registers (uniform across the warp)
+struct TS {  // mutable per-trace controller state (shared memory, one per warp)
+  int32_t rr_lp, rr_hp, fl_head, fl_tail;
+};
+
+struct Wp {  // per-warp trace context, passed by value (uniform across the warp)
+  SInst* SI;
+  int4* sd;
+  KI* buf;
+  TS* ts;
   int64_t base, n, tbt;
-  int64_t next, fl_head, fl_tail, decisions, evals;
-  int32_t rr_lp, rr_hp;
 };
 
 __device__ __forceinline__ int64_t pf_of(const SimP& P, int32_t p) {
@@ -79,7 +97,7 @@ __device__ __forceinline__ int64_t pf_of(const SimP& P, int32_t p) {
 }
 __device__ __forceinline__ int32_t blk_of(const SimP& P, int32_t eff) { return (eff + P.bs) / P.bs; }
 
-// time-invariant priority key of request gid with effective prompt eff
+// time-invariant priority key of request gid with effective prompt eff (DESIGN.md §2 Keys)
 __device__ __forceinline__ int64_t key_of(const SimP& P, int64_t gid, int32_t eff) {
   switch (P.policy) {
     case 0: return P.rq_dl[gid] - pf_of(P, eff);
@@ -90,24 +108,85 @@ __device__ __forceinline__ int64_t key_of(const SimP& P, int64_t gid, int32_t ef
   }
 }
 
-__device__ __forceinline__ int64_t ioff(const SimP& P, int k, const Tr& t) { return (int64_t)k * P.R + t.base; }
+__device__ __forceinline__ int64_t ioff(const SimP& P, int k, Wp w) { return (int64_t)k * P.R + w.base; }
+__device__ __forceinline__ int4* slotp(const SimP& P, Wp w, int k, int32_t j) {
+  return j < DCAP ? (w.sd + k * DCAP + j) : (P.ds_g + (int64_t)k * P.R + w.base + j);
+}
+__device__ __forceinline__ void set_state(const SimP& P, int64_t g, uint32_t st) {
+  const uint32_t f = P.rq_fl[g];
+  P.rq_fl[g] = (f & ~(3u << ST_SHIFT)) | (st << ST_SHIFT);
+}
 
-// ---------------------------------------------------------------------------- queue helpers ---
-__device__ void wq_append(const SimP& P, SInst& I, int k, const Tr& t, int32_t id) {
-  const int64_t o = ioff(P, k, t);
+// ------------------------------------------------------------------------------- digest ------
+// record = Σ_pos mix(v_pos + (pos+1)·G) over (T, k, B_p, admitted…, B_d, #off, off…, #drop,
+// drop…, #evicted, evicted…, lat) — positions as in the oracle; lanes hash in parallel.
+__device__ __noinline__ void digest_log(const SimP& P, Wp w, int k, int64_t T, int32_t nadm,
+                                        int64_t bd, int32_t noff, int32_t ndrop, int32_t npre,
+                                        int64_t lat) {
+  const int lane = lane_id();
+  const int64_t o = ioff(P, k, w);
+  uint64_t acc = 0;
+  if (lane < 8) {
+    uint64_t v, pos;
+    switch (lane) {
+      case 0: v = (uint64_t)T; pos = 0; break;
+      case 1: v = (uint64_t)k; pos = 1; break;
+      case 2: v = (uint64_t)nadm; pos = 2; break;
+      case 3: v = (uint64_t)bd; pos = 3 + nadm; break;
+      case 4: v = (uint64_t)noff; pos = 4 + nadm; break;
+      case 5: v = (uint64_t)ndrop; pos = 5 + nadm + noff; break;
+      case 6: v = (uint64_t)npre; pos = 6 + nadm + noff + ndrop; break;
+      default: v = (uint64_t)lat; pos = 7 + nadm + noff + ndrop + npre; break;
+    }
+    acc = mix64(v + (pos + 1) * GOLD);
+  }
+  for (int32_t j = lane; j < nadm; j += 32) acc += mix64((uint64_t)P.bp_id[o + j] + (uint64_t)(3 + j + 1) * GOLD);
+  for (int32_t j = lane; j < noff; j += 32)
+    acc += mix64((uint64_t)P.scr_off[w.base + j] + (uint64_t)(5 + nadm + j + 1) * GOLD);
+  for (int32_t j = lane; j < ndrop; j += 32)
+    acc += mix64((uint64_t)P.scr_drop[w.base + j] + (uint64_t)(6 + nadm + noff + j + 1) * GOLD);
+  for (int32_t j = lane; j < npre; j += 32)
+    acc += mix64((uint64_t)P.scr_pre[w.base + j] + (uint64_t)(7 + nadm + noff + ndrop + j + 1) * GOLD);
+  acc = warp_sum(acc);
+  const uint64_t h = mix64(w.SI[k].hash ^ acc);
+  __syncwarp();
+  w.SI[k].hash = h;  // uniform value, every lane stores the same word
+  __syncwarp();
+}
+
+// the pure-decode record (T, k, 0, B_d, 0, 0, 0, lat): 8 lanes, 3 shuffle steps
+__device__ __forceinline__ uint64_t digest_decode(uint64_t h, int k, int64_t T, int64_t bd, int64_t lat) {
+  const int lane = lane_id();
+  const uint64_t v = lane == 0 ? (uint64_t)T : lane == 1 ? (uint64_t)k : lane == 3 ? (uint64_t)bd
+                   : lane == 7 ? (uint64_t)lat : 0ull;
+  uint64_t acc = mix64(v + (uint64_t)(lane + 1) * GOLD);
+  acc += __shfl_xor_sync(FULL, acc, 4);
+  acc += __shfl_xor_sync(FULL, acc, 2);
+  acc += __shfl_xor_sync(FULL, acc, 1);
+  acc = __shfl_sync(FULL, acc, 0);
+  return mix64(h ^ acc);
+}
+
+// ------------------------------------------------------------------------ queue helpers -------
+__device__ __forceinline__ void wq_append(const SimP& P, Wp w, int k, int32_t id) {
+  SInst& I = w.SI[k];
+  const int64_t o = ioff(P, k, w);
   const int32_t len = I.wq_len;
+  const int64_t key = key_of(P, w.base + id, P.rq_eff[w.base + id]);
+  __syncwarp();
   if (lane_id() == 0) {
     P.wq_id[o + len] = id;
-    P.wq_key[o + len] = key_of(P, t.base + id, P.rq_eff[t.base + id]);
-    I.wq_len = len + 1;
+    P.wq_key[o + len] = key;
   }
+  I.wq_len = len + 1;
   __syncwarp();
 }
 
 // HP waiting queues are kept in ascending id order = FCFS by (arrival, id) (G26)
-__device__ void wq_insert_sorted(const SimP& P, SInst& I, int k, const Tr& t, int32_t id) {
+__device__ __noinline__ void wq_insert_sorted(const SimP& P, Wp w, int k, int32_t id) {
+  SInst& I = w.SI[k];
   const int lane = lane_id();
-  const int64_t o = ioff(P, k, t);
+  const int64_t o = ioff(P, k, w);
   const int32_t len = I.wq_len;
   int32_t pos = 0;
   for (int32_t c = 0; c < len; c += 32) {
@@ -124,25 +203,22 @@ __device__ void wq_insert_sorted(const SimP& P, SInst& I, int k, const Tr& t, in
     if (v) { P.wq_id[o + j + 1] = xi; P.wq_key[o + j + 1] = xk; }
     __syncwarp();
   }
+  const int64_t key = key_of(P, w.base + id, P.rq_eff[w.base + id]);
   if (lane == 0) {
     P.wq_id[o + pos] = id;
-    P.wq_key[o + pos] = key_of(P, t.base + id, P.rq_eff[t.base + id]);
-    I.wq_len = len + 1;
+    P.wq_key[o + pos] = key;
   }
   __syncwarp();
-}
-
-__device__ __forceinline__ void set_state(const SimP& P, int64_t gid, uint32_t st) {
-  uint32_t f = P.rq_fl[gid];
-  P.rq_fl[gid] = (f & ~(3u << ST_SHIFT)) | (st << ST_SHIFT);
+  I.wq_len = len + 1;
+  __syncwarp();
 }
 
 // Drop rule (G34): waiting, never prefilled, strictly past the deadline.  Stable
 // compaction of the queue; dropped ids (queue order = ascending id) go to scr_drop.
-__device__ int32_t drop_step(const SimP& P, SInst& I, int k, const Tr& t, int64_t T) {
-  if (!P.drop || I.wq_len == 0) return 0;
+__device__ __noinline__ int32_t drop_step(const SimP& P, Wp w, int k, int64_t T) {
+  SInst& I = w.SI[k];
   const int lane = lane_id();
-  const int64_t o = ioff(P, k, t);
+  const int64_t o = ioff(P, k, w);
   const int32_t len = I.wq_len;
   int32_t out = 0, nd = 0, tkd = 0;
   for (int32_t c = 0; c < len; c += 32) {
@@ -154,15 +230,14 @@ __device__ int32_t drop_step(const SimP& P, SInst& I, int k, const Tr& t, int64_
     if (v) {
       id = P.wq_id[o + j];
       key = P.wq_key[o + j];
-      const int64_t g = t.base + id;
+      const int64_t g = w.base + id;
       dr = !(P.rq_fl[g] & F_EVER) && T > P.rq_dl[g];
     }
     const uint32_t mk = __ballot_sync(FULL, v && !dr), md = __ballot_sync(FULL, dr);
-    __syncwarp();
     if (v && !dr) { const int32_t q = out + __popc(mk & lanemask_lt()); P.wq_id[o + q] = id; P.wq_key[o + q] = key; }
     if (dr) {
-      const int64_t g = t.base + id;
-      P.scr_drop[t.base + nd + __popc(md & lanemask_lt())] = id;
+      const int64_t g = w.base + id;
+      P.scr_drop[w.base + nd + __popc(md & lanemask_lt())] = id;
       set_state(P, g, 2u);
       if (I.hp && (P.rq_fl[g] & F_TICK)) tkd++;
     }
@@ -171,78 +246,71 @@ __device__ int32_t drop_step(const SimP& P, SInst& I, int k, const Tr& t, int64_
     __syncwarp();
   }
   tkd = warp_sum(tkd);
-  if (lane == 0) { I.wq_len = out; I.tk_live -= tkd; }
+  const int32_t tk = I.tk_live - tkd;
+  __syncwarp();
+  I.wq_len = out;
+  I.tk_live = tk;
   __syncwarp();
   return nd;
 }
 
-// Decode preparation (§5.4): grow each decode's KV by the blocks its next token
-// needs; while short of blocks, evict the latest-arrived decode (LIFO, G31) by recomputation:
-// its generated tokens join its prompt and it re-enters this instance's queue.
-__device__ int32_t decode_prep(const SimP& P, SInst& I, int k, const Tr& t) {
+// --------------------------------------------------------------------------- decode prep -----
+// §5.4; grow each decode's KV by the blocks its next token needs (precomputed by the
+// completion pass as pending bits); while short of blocks, evict the latest-arrived decode (LIFO,
+// G31) by recomputation: generated tokens join its prompt, it re-enters the queue.
+__device__ __noinline__ int32_t evict(const SimP& P, Wp w, int k) {
+  SInst& I = w.SI[k];
   const int lane = lane_id();
-  const int64_t o = ioff(P, k, t);
   int32_t np = 0;
-  while (true) {
+  while (I.need_sum > I.kv_free) {
     const int32_t len = I.ds_len;
-    int64_t need = 0;
     int32_t best = -1, bslot = -1;
     for (int32_t c = 0; c < len; c += 32) {
       const int32_t j = c + lane;
       if (j < len) {
-        const int32_t ctx = P.ds_ctx[o + j];
-        need += (ctx + P.bs - 1) / P.bs - P.ds_held[o + j];
-        const int32_t id = P.ds_id[o + j];
+        const int32_t id = slotp(P, w, k, j)->x;
         if (id > best) { best = id; bslot = j; }
       }
     }
-    need = warp_sum(need);
-    if (need <= I.kv_free) break;
     const int32_t vid = warp_max(best);
     const uint32_t who = __ballot_sync(FULL, best == vid);
     const int32_t vslot = __shfl_sync(FULL, bslot, __ffs(who) - 1);
-    const int32_t held = P.ds_held[o + vslot], ctx = P.ds_ctx[o + vslot];
-    const int64_t g = t.base + vid;
+    const int4 s = *slotp(P, w, k, vslot);
+    const int4 last = *slotp(P, w, k, len - 1);
+    const int64_t g = w.base + vid;
+    const int32_t kvf = I.kv_free + (s.w & HELD_MASK);  // blocks held before this step's growth
+    const int32_t need = I.need_sum - (int32_t)((uint32_t)s.w >> 31);
+    const int64_t cs = I.ctx_sum - s.y;
     __syncwarp();
     if (lane == 0) {
-      I.kv_free += held;
-      P.rq_eff[g] = ctx;
+      P.rq_eff[g] = s.y;  // eff_prompt = prompt + generated = lhat
       P.rq_fl[g] += (1u << NPRE_SHIFT);
-      P.scr_pre[t.base + np] = vid;
-      const int32_t last = len - 1;
-      P.ds_id[o + vslot] = P.ds_id[o + last];
-      P.ds_ctx[o + vslot] = P.ds_ctx[o + last];
-      P.ds_held[o + vslot] = P.ds_held[o + last];
-      P.ds_rem[o + vslot] = P.ds_rem[o + last];
-      I.ds_len = last;
+      P.scr_pre[w.base + np] = vid;
+      *slotp(P, w, k, vslot) = last;
     }
+    I.kv_free = kvf;
+    I.need_sum = need;
+    I.ctx_sum = cs;
+    I.ds_len = len - 1;
     __syncwarp();
     np++;
-    if (I.hp) wq_insert_sorted(P, I, k, t, vid); else wq_append(P, I, k, t, vid);
+    if (I.hp) wq_insert_sorted(P, w, k, vid); else wq_append(P, w, k, vid);
   }
-  const int32_t len = I.ds_len;
-  int64_t grow = 0;
-  for (int32_t c = 0; c < len; c += 32) {
-    const int32_t j = c + lane;
-    if (j < len) {
-      const int32_t need = (P.ds_ctx[o + j] + P.bs - 1) / P.bs;
-      const int32_t gr = need - P.ds_held[o + j];
-      if (gr) P.ds_held[o + j] = need;
-      grow += gr;
-    }
-  }
-  grow = warp_sum(grow);
-  __syncwarp();
-  if (lane == 0) I.kv_free -= (int32_t)grow;
-  __syncwarp();
   return np;
 }
 
-__device__ __forceinline__ int64_t ds_ctx_sum(const SimP& P, const SInst& I, int k, const Tr& t) {
-  const int64_t o = ioff(P, k, t);
-  int64_t s = 0;
-  for (int32_t j = lane_id(); j < I.ds_len; j += 32) s += P.ds_ctx[o + j];
-  return warp_sum(s);
+// returns the number of evictions; leaves the growth applied (papp = 1)
+__device__ __forceinline__ int32_t decode_prep(const SimP& P, Wp w, int k) {
+  SInst& I = w.SI[k];
+  if (I.papp) return 0;  // growth for the last decode step already applied
+  int32_t np = 0;
+  if (I.need_sum > I.kv_free) np = evict(P, w, k);
+  const int32_t kvf = I.kv_free - I.need_sum;  // pending growth of the surviving decodes
+  __syncwarp();
+  I.kv_free = kvf;
+  I.papp = 1;
+  __syncwarp();
+  return np;
 }
 
 // mark request admitted at T on instance k
@@ -253,54 +321,44 @@ __device__ __forceinline__ void admit_req(const SimP& P, int64_t g, int k, int64
   if (P.pstart[g] < 0) P.pstart[g] = T;
 }
 
-__device__ void digest_log(const SimP& P, SInst& I, int k, const Tr& t, int64_t T, int32_t nadm,
-                           int64_t bd, int32_t noff, int32_t ndrop, int32_t npre, int64_t lat) {
-  if (lane_id() == 0) {
-    const int64_t o = ioff(P, k, t);
-    uint64_t h = I.hash;
-    h = mix64(h ^ (uint64_t)T);
-    h = mix64(h ^ (uint64_t)k);
-    h = mix64(h ^ (uint64_t)nadm);
-    for (int32_t j = 0; j < nadm; j++) h = mix64(h ^ (uint64_t)P.bp_id[o + j]);
-    h = mix64(h ^ (uint64_t)bd);
-    h = mix64(h ^ (uint64_t)noff);
-    for (int32_t j = 0; j < noff; j++) h = mix64(h ^ (uint64_t)P.scr_off[t.base + j]);
-    h = mix64(h ^ (uint64_t)ndrop);
-    for (int32_t j = 0; j < ndrop; j++) h = mix64(h ^ (uint64_t)P.scr_drop[t.base + j]);
-    h = mix64(h ^ (uint64_t)npre);
-    for (int32_t j = 0; j < npre; j++) h = mix64(h ^ (uint64_t)P.scr_pre[t.base + j]);
-    h = mix64(h ^ (uint64_t)lat);
-    I.hash = h;
-  }
+__device__ __forceinline__ void set_batch(const SimP& P, SInst& I, int64_t T, int64_t l,
+                                          int32_t bdec, int32_t nadm) {
+  if (l < 0) atomicOr(P.err, ERR_RANGE);
+  __syncwarp();
+  I.end = T + l;
+  I.batch_dec = bdec;
+  I.bp_len = nadm;
   __syncwarp();
 }
 
-// --------------------------------------------------------------------------- LP formation ---
-__device__ void form_lp(const SimP& P, SInst* SI, int k, Tr& t, int64_t T, KI* sbuf) {
-  SInst& I = SI[k];
+// --------------------------------------------------------------- LP admission (non-empty queue)
+__device__ __noinline__ int lp_admit(const SimP& P, Wp w, int k, int64_t T, int32_t ndrop,
+                                     int32_t npre) {
+  SInst& I = w.SI[k];
   const int lane = lane_id();
-  const int64_t o = ioff(P, k, t);
-  const int32_t ndrop = drop_step(P, I, k, t, T);
-  const int32_t npre = decode_prep(P, I, k, t);
-  t.evals += I.wq_len;
+  const int64_t o = ioff(P, k, w);
   const int64_t Bd = I.ds_len;
-  const int64_t sl = Bd ? ds_ctx_sum(P, I, k, t) : 0;
+  const int64_t sl = I.ctx_sum;
   // budgets (G22)
   const int64_t N = P.lp_tok, M = I.kv_free, Rb = P.lp_max - Bd;
-  int64_t C = INF64;
+  int64_t C = INF64, ldec = 0;
   if (Bd) {
-    const int64_t d = lat_us(P.md, 0, 0, 0, 0, (uint64_t)Bd, (uint64_t)sl);
-    if (d < 0) atomicOr(P.err, ERR_RANGE);
-    C = t.tbt - d;
+    ldec = lat_decode(P.md, (uint64_t)Bd, (uint64_t)sl);
+    if (ldec < 0) atomicOr(P.err, ERR_RANGE);
+    C = w.tbt - ldec;
   }
-  // Algorithm 1: K smallest (key, id) of the waiting queue, sorted (line 3) ...
+  // Algorithm 1 line 3: the (key, id)-sorted prefix; only the first R <= 128 can be admitted
   const int32_t len = I.wq_len;
-  int32_t nadm = 0;
-  uint64_t sp = 0, sp2 = 0, spc = 0;
-  KI last = ki_inf();
-  if (len > 0) {
+  KI a[KPL];
+  if (len <= 32) {
+    KI x = ki_inf();
+    if (lane < len) x = KI{P.wq_key[o + lane], P.wq_id[o + lane]};
+    a[0] = sort32(x);
+#pragma unroll
+    for (int r = 1; r < KPL; r++) a[r] = ki_inf();
+  } else {
     TopKStream<KPL> st;
-    st.init(sbuf);
+    st.init(w.buf);
     for (int32_t c = 0; c < len; c += 32) {
       const int32_t j = c + lane;
       const bool v = j < len;
@@ -310,53 +368,63 @@ __device__ void form_lp(const SimP& P, SInst* SI, int k, Tr& t, int64_t T, KI* s
     }
     st.finish();
     __syncwarp();
-    // ... lines 5-13 as a strict prefix-sum scan over the sorted candidates
-    int64_t ct = 0, cb = 0, cc = 0;
-    bool go = true;
 #pragma unroll
-    for (int r = 0; r < KPL; r++) {
-      const KI e = st.top.a[r];
-      const bool valid = e.i != INF32;
-      const int64_t g = t.base + (valid ? e.i : 0);
-      const int32_t p = valid ? P.rq_eff[g] : 0;
-      const int64_t pf = valid ? pf_of(P, p) : 0;
-      const int64_t bl = valid ? blk_of(P, p) : 0;
-      const int64_t St = ct + warp_incl_scan((int64_t)p);
-      const int64_t Sb = cb + warp_incl_scan(bl);
-      const int64_t Sc = cc + warp_incl_scan(pf);
-      const int pos = r * 32 + lane;
-      const bool ok = go && valid && St < N && Sb < M && Sc < C && pos < Rb;
-      const uint32_t m = __ballot_sync(FULL, ok);
-      const int cnt = (m == FULL) ? 32 : (__ffs(~m) - 1);
-      const bool adm = go && lane < cnt;
-      if (adm) {
-        admit_req(P, g, k, T);
-        P.bp_id[o + pos] = e.i;
-        const uint64_t q = (uint64_t)p;
-        sp += q;
-        sp2 += q * q;
-        spc += q * ceil_div_u(q, P.md.b);
-      }
-      nadm += go ? cnt : 0;
-      if (cnt < 32) go = false;
-      ct = __shfl_sync(FULL, St, 31);
-      cb = __shfl_sync(FULL, Sb, 31);
-      cc = __shfl_sync(FULL, Sc, 31);
-    }
-    if (nadm > 0) last = ki_shfl(st.top.a[(nadm - 1) >> 5], (nadm - 1) & 31);
-    sp = warp_sum(sp);
-    sp2 = warp_sum(sp2);
-    spc = warp_sum(spc);
+    for (int r = 0; r < KPL; r++) a[r] = st.top.a[r];
   }
-  // admitted KV blocks: sum_j ceil((p_j + 1)/bs)
-  int64_t used = 0;
-  for (int32_t j = lane; j < nadm; j += 32) used += blk_of(P, P.rq_eff[t.base + P.bp_id[o + j]]);
+  // lines 5-13 as a strict prefix-sum scan over the sorted candidates
+  int32_t nadm = 0;
+  uint64_t sp = 0, sp2 = 0, spc = 0;
+  int64_t used = 0, ct = 0, cb = 0, cc = 0;
+  bool go = true;
+#pragma unroll
+  for (int r = 0; r < KPL; r++) {
+    if (!go) break;
+    const KI e = a[r];
+    const bool valid = e.i != INF32;
+    const int64_t g = w.base + (valid ? e.i : 0);
+    const int32_t p = valid ? P.rq_eff[g] : 0;
+    const int64_t pf = valid ? pf_of(P, p) : 0;
+    const int64_t bl = valid ? blk_of(P, p) : 0;
+    const int64_t St = ct + warp_incl_scan((int64_t)p);
+    const int64_t Sb = cb + warp_incl_scan(bl);
+    const int64_t Sc = cc + warp_incl_scan(pf);
+    const int pos = r * 32 + lane;
+    const bool ok = valid && St < N && Sb < M && Sc < C && pos < Rb;
+    const uint32_t m = __ballot_sync(FULL, ok);
+    const int cnt = (m == FULL) ? 32 : (__ffs(~m) - 1);
+    if (lane < cnt) {
+      admit_req(P, g, k, T);
+      P.bp_id[o + pos] = e.i;
+      const uint64_t q = (uint64_t)p;
+      sp += q;
+      sp2 += q * q;
+      spc += q * ceil_div_u(q, P.md.b);
+      used += bl;
+    }
+    nadm += cnt;
+    if (cnt < 32) go = false;
+    ct = __shfl_sync(FULL, St, 31);
+    cb = __shfl_sync(FULL, Sb, 31);
+    cc = __shfl_sync(FULL, Sc, 31);
+  }
+  KI last = ki_inf();
+  if (nadm > 0) {
+    const int r = (nadm - 1) >> 5;
+    KI lr = a[0];
+#pragma unroll
+    for (int q = 1; q < KPL; q++) if (q == r) lr = a[q];
+    last = ki_shfl(lr, (nadm - 1) & 31);
+  }
+  sp = warp_sum(sp);
+  sp2 = warp_sum(sp2);
+  spc = warp_sum(spc);
   used = warp_sum(used);
   // offload (§5.3, G24) + queue compaction in one pass; the admitted set is exactly the entries
   // at or before `last` in (key, id) order
   int32_t noff = 0;
-  if (len > 0 && (nadm > 0 || P.offl)) {
-    int32_t out = 0;
+  int32_t out = len;
+  if (nadm > 0 || P.offl) {
+    out = 0;
     for (int32_t c = 0; c < len; c += 32) {
       const int32_t j = c + lane;
       const bool v = j < len;
@@ -366,7 +434,7 @@ __device__ void form_lp(const SimP& P, SInst* SI, int k, Tr& t, int64_t T, KI* s
         x = KI{P.wq_key[o + j], P.wq_id[o + j]};
         adm = nadm > 0 && !ki_less(last, x);
         if (!adm && P.offl) {
-          const int64_t g = t.base + x.i;
+          const int64_t g = w.base + x.i;
           const uint32_t f = P.rq_fl[g];
           off = !(f & (F_EVER | F_ONHP)) &&
                 P.rq_dl[g] - T <= pf_of(P, P.rq_eff[g]) + P.W + P.margin;
@@ -374,62 +442,100 @@ __device__ void form_lp(const SimP& P, SInst* SI, int k, Tr& t, int64_t T, KI* s
       }
       const bool keep = v && !adm && !off;
       const uint32_t mk = __ballot_sync(FULL, keep), mo = __ballot_sync(FULL, off);
-      __syncwarp();
       if (keep) { const int32_t q = out + __popc(mk & lanemask_lt()); P.wq_id[o + q] = x.i; P.wq_key[o + q] = x.k; }
-      if (off) P.scr_off[t.base + noff + __popc(mo & lanemask_lt())] = x.i;
+      if (off) P.scr_off[w.base + noff + __popc(mo & lanemask_lt())] = x.i;
       out += __popc(mk);
       noff += __popc(mo);
       __syncwarp();
     }
-    if (lane == 0) I.wq_len = out;
-    __syncwarp();
   }
-  if (lane == 0) I.kv_free -= (int32_t)used;
+  const int32_t kvf = I.kv_free - (int32_t)used;
+  __syncwarp();
+  I.wq_len = out;
+  I.kv_free = kvf;
   __syncwarp();
   // dispatch offloads round-robin over the HPs, ascending id
   for (int32_t j = 0; j < noff; j++) {
-    const int32_t id = P.scr_off[t.base + j];
-    const int64_t g = t.base + id;
-    if (lane == 0) P.rq_fl[g] |= (F_ONHP | F_OFFL);
+    const int32_t id = P.scr_off[w.base + j];
+    const int64_t g = w.base + id;
+    const int32_t rr = w.ts->rr_hp;
+    const int h = P.n_lp + rr;
+    const int32_t tail = w.ts->fl_tail;
     __syncwarp();
-    const int h = P.n_lp + t.rr_hp;
-    t.rr_hp = (t.rr_hp + 1) % P.n_hp;
-    if (P.delay == 0) {
-      wq_insert_sorted(P, SI[h], h, t, id);
-    } else {
-      if (lane == 0) {
-        P.fl_t[t.base + t.fl_tail] = T + P.delay;
-        P.fl_req[t.base + t.fl_tail] = id;
-        P.fl_hp[t.base + t.fl_tail] = h;
+    if (lane == 0) {
+      P.rq_fl[g] |= (F_ONHP | F_OFFL);
+      w.ts->rr_hp = (rr + 1) % P.n_hp;
+      if (P.delay != 0) {
+        P.fl_t[w.base + tail] = T + P.delay;
+        P.fl_req[w.base + tail] = id;
+        P.fl_hp[w.base + tail] = h;
+        w.ts->fl_tail = tail + 1;
       }
-      __syncwarp();
-      t.fl_tail++;
     }
+    __syncwarp();
+    if (P.delay == 0) wq_insert_sorted(P, w, h, id);
   }
   // batch (§5.4): decodes piggybacked with the admitted prefills
   const bool nonempty = nadm > 0 || Bd > 0;
   int64_t l = 0;
   if (nonempty) {
-    l = lat_us(P.md, (uint64_t)nadm, sp, sp2, spc, (uint64_t)Bd, (uint64_t)sl);
-    if (l < 0) atomicOr(P.err, ERR_RANGE);
-    if (lane == 0) {
-      I.end = T + l;
-      I.busy = 1;
-      I.batch_dec = Bd > 0;
-      I.bp_len = nadm;
-    }
-    __syncwarp();
-    t.decisions++;
+    l = nadm ? lat_us(P.md, (uint64_t)nadm, sp, sp2, spc, (uint64_t)Bd, (uint64_t)sl) : ldec;
+    set_batch(P, I, T, l, Bd > 0, nadm);
   }
-  if (nonempty || noff || ndrop || npre) digest_log(P, I, k, t, T, nadm, nonempty ? Bd : 0, noff, ndrop, npre, l);
+  if (nonempty || noff || ndrop || npre)
+    digest_log(P, w, k, T, nadm, nonempty ? Bd : 0, noff, ndrop, npre, l);
+  return nonempty ? 1 : 0;
+}
+
+// one decode-only batch of the whole decode set (LP with an empty queue, or HP) — the hot path
+__device__ __forceinline__ void decode_batch(const SimP& P, SInst& I, int k, int64_t T) {
+  const int32_t bd = I.ds_len;
+  const int64_t l = lat_decode(P.md, (uint64_t)bd, (uint64_t)I.ctx_sum);
+  if (l < 0) atomicOr(P.err, ERR_RANGE);
+  const uint64_t h = digest_decode(I.hash, k, T, bd, l);
+  __syncwarp();
+  I.hash = h;  // uniform values: every lane stores the same words
+  I.end = T + l;
+  I.batch_dec = 1;
+  I.bp_len = 0;
+  __syncwarp();
+}
+
+// returns (waiting-queue entries evaluated << 1) | (1 if a batch was formed)
+__device__ __forceinline__ int64_t form_lp(const SimP& P, Wp w, int k, int64_t T) {
+  SInst& I = w.SI[k];
+  if (I.wq_len == 0) {
+    if (I.ds_len == 0) return 0;  // parked
+    const int32_t np = decode_prep(P, w, k);
+    if (np == 0) {  // no eviction: the common case, a pure decode step
+      decode_batch(P, I, k, T);
+      return 1;
+    }
+    const int64_t ev = (int64_t)I.wq_len << 1;  // the queue now holds the evicted decodes
+    return ev | lp_admit(P, w, k, T, 0, np);
+  }
+  const int32_t ndrop = P.drop ? drop_step(P, w, k, T) : 0;
+  const int32_t npre = I.ds_len ? decode_prep(P, w, k) : 0;
+  const int64_t ev = (int64_t)I.wq_len << 1;
+  if (I.wq_len == 0) {
+    const int64_t Bd = I.ds_len;
+    int64_t l = 0;
+    if (Bd) {
+      l = lat_decode(P.md, (uint64_t)Bd, (uint64_t)I.ctx_sum);
+      set_batch(P, I, T, l, 1, 0);
+    }
+    digest_log(P, w, k, T, 0, Bd, 0, ndrop, 0, l);  // ndrop > 0 here
+    return ev | (Bd ? 1 : 0);
+  }
+  return ev | lp_admit(P, w, k, T, ndrop, npre);
 }
 
 // --------------------------------------------------------------------------- HP formation ---
 // FCFS prefill-first under the (elastic) token limit (G27-G28).
-__device__ int32_t hp_prefill(const SimP& P, SInst& I, int k, const Tr& t, int64_t T,
-                              uint64_t& sp, uint64_t& sp2, uint64_t& spc) {
+__device__ __noinline__ int32_t hp_prefill(const SimP& P, Wp w, int k, int64_t T, uint64_t* mom) {
+  SInst& I = w.SI[k];
   const int lane = lane_id();
-  const int64_t o = ioff(P, k, t);
+  const int64_t o = ioff(P, k, w);
   int64_t limit = P.hp_tok;
   if (P.elastic) {
     const int64_t mean = I.hist_cnt ? I.hist_sum / I.hist_cnt : (int64_t)P.hist_def;
@@ -438,14 +544,14 @@ __device__ int32_t hp_prefill(const SimP& P, SInst& I, int k, const Tr& t, int64
   }
   const int32_t len = I.wq_len;
   const int64_t kvf = I.kv_free;
-  int64_t ct = 0, cb = 0;
+  int64_t ct = 0, cb = 0, used = 0;
   int32_t nadm = 0;
-  sp = sp2 = spc = 0;
+  uint64_t sp = 0, sp2 = 0, spc = 0;
   for (int32_t c = 0; c < len; c += 32) {
     const int32_t j = c + lane;
     const bool v = j < len;
     int32_t id = 0, p = 0;
-    if (v) { id = P.wq_id[o + j]; p = P.rq_eff[t.base + id]; }
+    if (v) { id = P.wq_id[o + j]; p = P.rq_eff[w.base + id]; }
     const int64_t bl = v ? blk_of(P, p) : 0;
     const int64_t St = ct + warp_incl_scan((int64_t)p);
     const int64_t Sb = cb + warp_incl_scan(bl);
@@ -453,24 +559,23 @@ __device__ int32_t hp_prefill(const SimP& P, SInst& I, int k, const Tr& t, int64
     const uint32_t m = __ballot_sync(FULL, ok);
     const int cnt = (m == FULL) ? 32 : (__ffs(~m) - 1);
     if (lane < cnt) {
-      admit_req(P, t.base + id, k, T);
+      admit_req(P, w.base + id, k, T);
       P.bp_id[o + j] = id;
       const uint64_t q = (uint64_t)p;
       sp += q;
       sp2 += q * q;
       spc += q * ceil_div_u(q, P.md.b);
+      used += bl;
     }
     nadm += cnt;
     if (cnt < 32) break;
     ct = __shfl_sync(FULL, St, 31);
     cb = __shfl_sync(FULL, Sb, 31);
   }
-  sp = warp_sum(sp);
-  sp2 = warp_sum(sp2);
-  spc = warp_sum(spc);
   if (nadm == 0) return 0;
-  int64_t used = 0;
-  for (int32_t j = lane; j < nadm; j += 32) used += blk_of(P, P.rq_eff[t.base + P.bp_id[o + j]]);
+  mom[0] = warp_sum(sp);
+  mom[1] = warp_sum(sp2);
+  mom[2] = warp_sum(spc);
   used = warp_sum(used);
   // remove the admitted prefix
   for (int32_t c = 0; c < len - nadm; c += 32) {
@@ -483,261 +588,357 @@ __device__ int32_t hp_prefill(const SimP& P, SInst& I, int k, const Tr& t, int64
     if (v) { P.wq_id[o + j] = xi; P.wq_key[o + j] = xk; }
     __syncwarp();
   }
-  if (lane == 0) { I.wq_len = len - nadm; I.kv_free -= (int32_t)used; }
+  const int32_t kvn = I.kv_free - (int32_t)used;
+  __syncwarp();
+  I.wq_len = len - nadm;
+  I.kv_free = kvn;
   __syncwarp();
   return nadm;
 }
 
-__device__ void form_hp(const SimP& P, SInst* SI, int k, Tr& t, int64_t T) {
-  SInst& I = SI[k];
-  const int lane = lane_id();
-  const int32_t ndrop = drop_step(P, I, k, t, T);
-  t.evals += I.wq_len;
-  uint64_t sp = 0, sp2 = 0, spc = 0;
+__device__ __noinline__ int64_t form_hp_general(const SimP& P, Wp w, int k, int64_t T) {
+  SInst& I = w.SI[k];
+  const int32_t ndrop = (P.drop && I.wq_len) ? drop_step(P, w, k, T) : 0;
+  const int64_t ev = (int64_t)I.wq_len << 1;
+  uint64_t mom[3] = {0, 0, 0};
   int32_t nadm = 0, npre = 0;
-  int64_t bd = 0, sl = 0;
+  int64_t bd = 0;
   bool batch = false;
-  if (I.wq_len > 0) { nadm = hp_prefill(P, I, k, t, T, sp, sp2, spc); batch = nadm > 0; }
+  if (I.wq_len > 0) { nadm = hp_prefill(P, w, k, T, mom); batch = nadm > 0; }  // prefill first
   if (!batch && I.ds_len > 0) {
-    npre = decode_prep(P, I, k, t);
+    npre = decode_prep(P, w, k);
     if (I.ds_len > 0) {
       batch = true;
       bd = I.ds_len;
-      sl = ds_ctx_sum(P, I, k, t);
-    } else if (I.wq_len > 0) {
-      nadm = hp_prefill(P, I, k, t, T, sp, sp2, spc);
+    } else if (I.wq_len > 0) {  // every decode was evicted (G43)
+      nadm = hp_prefill(P, w, k, T, mom);
       batch = nadm > 0;
     }
   }
   int64_t l = 0;
   if (batch) {
-    l = bd ? lat_us(P.md, 0, 0, 0, 0, (uint64_t)bd, (uint64_t)sl)
-           : lat_us(P.md, (uint64_t)nadm, sp, sp2, spc, 0, 0);
-    if (l < 0) atomicOr(P.err, ERR_RANGE);
-    if (lane == 0) {
-      I.end = T + l;
-      I.busy = 1;
-      I.batch_dec = bd > 0;
-      I.bp_len = bd ? 0 : nadm;
-    }
-    __syncwarp();
-    t.decisions++;
+    l = bd ? lat_decode(P.md, (uint64_t)bd, (uint64_t)I.ctx_sum)
+           : lat_us(P.md, (uint64_t)nadm, mom[0], mom[1], mom[2], 0, 0);
+    set_batch(P, I, T, l, bd > 0, bd ? 0 : nadm);
   }
-  if (batch || ndrop || npre) digest_log(P, I, k, t, T, bd ? 0 : nadm, bd, 0, ndrop, npre, l);
+  if (batch || ndrop || npre) digest_log(P, w, k, T, bd ? 0 : nadm, bd, 0, ndrop, npre, l);
+  return ev | (batch ? 1 : 0);
+}
+
+__device__ __forceinline__ int64_t form_hp(const SimP& P, Wp w, int k, int64_t T) {
+  SInst& I = w.SI[k];
+  if (I.wq_len == 0) {
+    if (I.ds_len == 0) return 0;  // parked
+    if (I.papp || I.need_sum <= I.kv_free) {  // decode-only batch without eviction: hot path
+      decode_prep(P, w, k);
+      decode_batch(P, I, k, T);
+      return 1;
+    }
+  }
+  return form_hp_general(P, w, k, T);
 }
 
 // ------------------------------------------------------------------ phase A: batch completion --
-__device__ void finish_req(const SimP& P, int64_t g, int64_t T) {
+__device__ __forceinline__ void finish_req(const SimP& P, int64_t g, int64_t T) {
   P.done[g] = T;
   set_state(P, g, 1u);
 }
 
-__device__ void complete(const SimP& P, SInst& I, int k, const Tr& t, int64_t T) {
+// per finished request: blocks freed, HP history, resident-ticket release (G29)
+__device__ __noinline__ void finish_sums(const SimP& P, Wp w, int k, int64_t freed, int64_t hsum,
+                                         int32_t hcnt, int32_t tkd, int64_t cfin) {
+  freed = warp_sum(freed);
+  hsum = warp_sum(hsum);
+  hcnt = warp_sum(hcnt);
+  tkd = warp_sum(tkd);
+  cfin = warp_sum(cfin);
+  SInst& I = w.SI[k];
+  const int32_t kvf = I.kv_free + (int32_t)freed, hc = I.hist_cnt + hcnt, tk = I.tk_live - tkd;
+  const int64_t hs = I.hist_sum + hsum, cs = I.ctx_sum - cfin;
+  __syncwarp();
+  I.kv_free = kvf;
+  I.hist_sum = hs;
+  I.hist_cnt = hc;
+  I.tk_live = tk;
+  I.ctx_sum = cs;
+  __syncwarp();
+}
+
+// prefill completions: first token, then completion or entry into the decode set
+__device__ __noinline__ void complete_prefills(const SimP& P, Wp w, int k, int64_t T) {
+  SInst& I = w.SI[k];
   const int lane = lane_id();
-  const int64_t o = ioff(P, k, t);
-  int64_t freed = 0, hsum = 0;
-  int32_t hcnt = 0, tkd = 0;
-  int32_t dlen = I.ds_len;
-  if (I.batch_dec) {
-    int32_t out = 0;
-    for (int32_t c = 0; c < dlen; c += 32) {
-      const int32_t j = c + lane;
-      const bool v = j < dlen;
-      int32_t id = 0, ctx = 0, held = 0, rem = 0;
-      bool fin = false;
-      if (v) {
-        id = P.ds_id[o + j]; ctx = P.ds_ctx[o + j] + 1; held = P.ds_held[o + j]; rem = P.ds_rem[o + j] - 1;
-        fin = rem == 0;
-        if (fin) {
-          const int64_t g = t.base + id;
-          finish_req(P, g, T);
-          freed += held;
-          if (I.hp) { hsum += P.ol[g]; hcnt++; if (P.rq_fl[g] & F_TICK) tkd++; }
-        }
-      }
-      const uint32_t mk = __ballot_sync(FULL, v && !fin);
-      __syncwarp();
-      if (v && !fin) {
-        const int32_t q = out + __popc(mk & lanemask_lt());
-        P.ds_id[o + q] = id; P.ds_ctx[o + q] = ctx; P.ds_held[o + q] = held; P.ds_rem[o + q] = rem;
-      }
-      out += __popc(mk);
-      __syncwarp();
-    }
-    dlen = out;
-  }
+  const int64_t o = ioff(P, k, w);
   const int32_t blen = I.bp_len;
+  int32_t dlen = I.ds_len;
+  int64_t freed = 0, hsum = 0, cadd = 0;
+  int32_t hcnt = 0, tkd = 0;
   for (int32_t c = 0; c < blen; c += 32) {
     const int32_t j = c + lane;
     const bool v = j < blen;
     bool stay = false;
-    int32_t id = 0, ctx = 0, held = 0, rem = 0;
+    int4 s = make_int4(0, 0, 0, 0);
     if (v) {
-      id = P.bp_id[o + j];
-      const int64_t g = t.base + id;
+      const int32_t id = P.bp_id[o + j];
+      const int64_t g = w.base + id;
       const int32_t eff = P.rq_eff[g], p = P.pl[g], out_len = P.ol[g];
       const int32_t gen = eff - p + 1;  // tokens generated after this prefill
       if (P.first[g] < 0) P.first[g] = T;
-      held = blk_of(P, eff);
+      const int32_t held = blk_of(P, eff);
       if (gen == out_len) {
         finish_req(P, g, T);
         freed += held;
         if (I.hp) { hsum += out_len; hcnt++; if (P.rq_fl[g] & F_TICK) tkd++; }
       } else {
         stay = true;
-        ctx = p + gen;
-        rem = out_len - gen;
+        const int32_t ctx = p + gen;
+        s = make_int4(id, ctx, out_len - gen, held | ((ctx % P.bs) << R_SHIFT));
+        cadd += ctx;
       }
     }
     const uint32_t ms = __ballot_sync(FULL, stay);
-    if (stay) {
-      const int32_t q = dlen + __popc(ms & lanemask_lt());
-      P.ds_id[o + q] = id; P.ds_ctx[o + q] = ctx; P.ds_held[o + q] = held; P.ds_rem[o + q] = rem;
-    }
+    if (stay) *slotp(P, w, k, dlen + __popc(ms & lanemask_lt())) = s;
     dlen += __popc(ms);
   }
   freed = warp_sum(freed);
   hsum = warp_sum(hsum);
   hcnt = warp_sum(hcnt);
   tkd = warp_sum(tkd);
+  cadd = warp_sum(cadd);
+  const int32_t kvf = I.kv_free + (int32_t)freed, hc = I.hist_cnt + hcnt, tk = I.tk_live - tkd;
+  const int64_t hs = I.hist_sum + hsum, cs = I.ctx_sum + cadd;
   __syncwarp();
-  if (lane == 0) {
-    I.ds_len = dlen;
-    I.kv_free += (int32_t)freed;
-    I.hist_sum += hsum;
-    I.hist_cnt += hcnt;
-    I.tk_live -= tkd;
-    I.bp_len = 0;
-    I.batch_dec = 0;
-    I.busy = 0;
+  I.ds_len = dlen;
+  I.kv_free = kvf;
+  I.hist_sum = hs;
+  I.hist_cnt = hc;
+  I.tk_live = tk;
+  I.ctx_sum = cs;
+  __syncwarp();
+}
+
+// The decode step just executed: one pass over the slots — l̂+1, remaining−1, completions, and
+// the block the next formation will need (pending bit: l̂ mod bs was 0 before the step).
+__device__ __forceinline__ void complete(const SimP& P, Wp w, int k, int64_t T) {
+  SInst& I = w.SI[k];
+  const int lane = lane_id();
+  if (I.batch_dec) {
+    const int32_t dlen = I.ds_len;
+    const int32_t bs = P.bs;
+    int32_t out = 0, need = 0;
+    bool anyfin = false;
+    int64_t freed = 0, hsum = 0, cfin = 0;
+    int32_t hcnt = 0, tkd = 0;
+    for (int32_t c = 0; c < dlen; c += 32) {
+      const int32_t j = c + lane;
+      const bool v = j < dlen;
+      int4 s = make_int4(0, 0, 1, 0);
+      if (v) s = *slotp(P, w, k, j);
+      const int32_t held = (s.w & HELD_MASK) + (int32_t)((uint32_t)s.w >> 31);  // growth applied
+      const int32_t r = (s.w >> R_SHIFT) & 0x1ff;
+      const bool pend = r == 0;
+      const int32_t r2 = r + 1 == bs ? 0 : r + 1;
+      s.y += 1;
+      s.z -= 1;
+      s.w = held | (r2 << R_SHIFT) | (pend ? PEND : 0);
+      const bool fin = v && s.z == 0;
+      const uint32_t mf = __ballot_sync(FULL, fin);
+      const uint32_t mk = __ballot_sync(FULL, v && !fin);
+      need += __popc(__ballot_sync(FULL, v && !fin && pend));
+      // stable compaction (positions == j until the first completion); every lane has read its
+      // slot before the ballots above, so in-place writes are safe
+      if (v && !fin) *slotp(P, w, k, out + __popc(mk & lanemask_lt())) = s;
+      if (mf) {
+        anyfin = true;
+        if (fin) {
+          const int64_t g = w.base + s.x;
+          finish_req(P, g, T);
+          freed += held;
+          cfin += s.y;
+          if (I.hp) { hsum += P.ol[g]; hcnt++; if (P.rq_fl[g] & F_TICK) tkd++; }
+        }
+      }
+      out += __popc(mk);
+    }
+    const int64_t cs = I.ctx_sum + dlen;  // every decode gained one token of context
+    __syncwarp();
+    I.ctx_sum = cs;
+    I.ds_len = out;
+    I.need_sum = need;
+    I.papp = 0;
+    __syncwarp();
+    if (anyfin) finish_sums(P, w, k, freed, hsum, hcnt, tkd, cfin);
   }
+  if (I.bp_len) complete_prefills(P, w, k, T);
+  __syncwarp();
+  I.bp_len = 0;
+  I.batch_dec = 0;
+  I.end = INF64;
   __syncwarp();
 }
 
 // --------------------------------------------------------------------- controller routing ---
-__device__ void route(const SimP& P, SInst* SI, Tr& t, int32_t id) {
+__device__ __forceinline__ void route(const SimP& P, Wp w, int32_t id) {
   if (P.tickets) {
     for (int h = P.n_lp; h < P.K; h++) {
-      if (SI[h].ticket) {
-        if (lane_id() == 0) {
-          SI[h].ticket = 0;
-          SI[h].tk_live += 1;
-          P.rq_fl[t.base + id] |= (F_TICK | F_ONHP);
-        }
+      if (w.SI[h].ticket) {
+        const int32_t tk = w.SI[h].tk_live + 1;
         __syncwarp();
-        wq_append(P, SI[h], h, t, id);  // the newest arrival has the largest id: stays sorted
+        if (lane_id() == 0) P.rq_fl[w.base + id] |= (F_TICK | F_ONHP);
+        w.SI[h].ticket = 0;
+        w.SI[h].tk_live = tk;
+        __syncwarp();
+        wq_append(P, w, h, id);  // the newest arrival has the largest id: stays sorted
         return;
       }
     }
   }
-  wq_append(P, SI[t.rr_lp], t.rr_lp, t, id);
-  t.rr_lp = (t.rr_lp + 1) % P.n_lp;
+  const int32_t rr = w.ts->rr_lp;
+  wq_append(P, w, rr, id);
+  w.ts->rr_lp = (rr + 1) == P.n_lp ? 0 : rr + 1;
+  __syncwarp();
 }
 
-__global__ void __launch_bounds__(SW * 32) sim_kernel(SimP P) {
-  __shared__ SInst s_inst[SW][MAXI];
-  __shared__ KI s_buf[SW][64];
-  __shared__ int s_trace[SW];
-  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  SInst* SI = s_inst[w];
+__device__ __noinline__ void deliver(const SimP& P, Wp w, int64_t T) {
+  while (w.ts->fl_head < w.ts->fl_tail && P.fl_t[w.base + w.ts->fl_head] == T) {
+    const int32_t head = w.ts->fl_head;
+    const int32_t id = P.fl_req[w.base + head];
+    const int h = P.fl_hp[w.base + head];
+    wq_insert_sorted(P, w, h, id);
+    w.ts->fl_head = head + 1;
+    __syncwarp();
+  }
+}
+
+__device__ __noinline__ void init_trace(const SimP& P, Wp w, int trace) {
+  const int lane = lane_id();
+  if (lane == 0) { w.ts->rr_lp = w.ts->rr_hp = w.ts->fl_head = w.ts->fl_tail = 0; }
+  const int64_t ttft = P.ttft[trace];
+  for (int64_t i = lane; i < w.n; i += 32) {
+    const int64_t g = w.base + i;
+    P.rq_dl[g] = P.arr[g] + (P.rttft ? P.rttft[g] : ttft);
+    P.rq_eff[g] = P.pl[g];
+    P.rq_fl[g] = 0xffu << INST_SHIFT;
+    P.first[g] = -1;
+    P.done[g] = -1;
+    P.pstart[g] = -1;
+  }
+  if (lane < P.K) {
+    SInst& I = w.SI[lane];
+    I.hp = lane >= P.n_lp;
+    I.kv_total = I.kv_free = I.hp ? P.kv_hp : P.kv_lp;
+    I.end = INF64; I.hist_sum = 0; I.ctx_sum = 0; I.hash = 0;
+    I.wq_len = I.ds_len = I.bp_len = I.hist_cnt = I.need_sum = 0;
+    I.batch_dec = I.tk_live = 0;
+    I.papp = 1;
+    I.ticket = (I.hp && P.tickets) ? 1 : 0;  // issued at t = 0 (G29)
+  }
+  __syncwarp();
+}
+
+__device__ __noinline__ void finish_trace(const SimP& P, Wp w, int trace, int64_t decisions,
+                                          int64_t evals) {
+  const int lane = lane_id();
+  bool stuck = false;
+  if (lane < P.K) stuck = w.SI[lane].wq_len > 0 || w.SI[lane].ds_len > 0;
+  if (__any_sync(FULL, stuck) && lane == 0) atomicOr(P.err, ERR_INVARIANT);
+  for (int64_t i = lane; i < w.n; i += 32) {
+    const int64_t g = w.base + i;
+    const uint32_t f = P.rq_fl[g];
+    uint32_t st = (f >> ST_SHIFT) & 3u;
+    st |= (f & F_OFFL) ? 4u : 0u;
+    st |= (f & F_TICK) ? 8u : 0u;
+    st |= ((f >> INST_SHIFT) & 0xffu) << 4;
+    st |= ((f >> NPRE_SHIFT) & 0xffffu) << 12;
+    P.status[g] = st;
+  }
+  if (lane == 0) {
+    uint64_t d = 0;
+    for (int k = 0; k < P.K; k++) d = mix64(d ^ w.SI[k].hash);
+    P.digest[trace] = d;
+    if (P.decisions) P.decisions[trace] = decisions;
+    if (P.evals) P.evals[trace] = evals;
+  }
+  __syncwarp();
+}
+
+__global__ void __launch_bounds__(SW * 32, 8) sim_kernel(const __grid_constant__ SimP P) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int wi = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const size_t per_warp = 64 * sizeof(KI) + (size_t)P.K * DCAP * sizeof(int4) +
+                          (size_t)P.K * sizeof(SInst) + sizeof(TS);
+  unsigned char* mine = smem + wi * ((per_warp + 15) & ~size_t(15));
+  Wp w;
+  w.buf = reinterpret_cast<KI*>(mine);
+  w.sd = reinterpret_cast<int4*>(mine + 64 * sizeof(KI));
+  w.SI = reinterpret_cast<SInst*>(mine + 64 * sizeof(KI) + (size_t)P.K * DCAP * sizeof(int4));
+  w.ts = reinterpret_cast<TS*>(mine + 64 * sizeof(KI) + (size_t)P.K * DCAP * sizeof(int4) +
+                               (size_t)P.K * sizeof(SInst));
+  const int K = P.K, n_lp = P.n_lp;
   while (true) {
-    if (lane == 0) s_trace[w] = atomicAdd(P.next_trace, 1);
-    __syncwarp();
-    const int trace = s_trace[w];
-    __syncwarp();
+    int trace = 0;
+    if (lane == 0) trace = atomicAdd(P.next_trace, 1);
+    trace = __shfl_sync(FULL, trace, 0);
     if (trace >= P.T) break;
-    Tr t;
-    t.base = P.off[trace];
-    t.n = P.off[trace + 1] - t.base;
-    t.tbt = P.tbt[trace];
-    t.next = t.fl_head = t.fl_tail = t.decisions = t.evals = 0;
-    t.rr_lp = t.rr_hp = 0;
-    const int64_t ttft = P.ttft[trace];
-    for (int64_t i = lane; i < t.n; i += 32) {
-      const int64_t g = t.base + i;
-      P.rq_dl[g] = P.arr[g] + (P.rttft ? P.rttft[g] : ttft);
-      P.rq_eff[g] = P.pl[g];
-      P.rq_fl[g] = 0xffu << INST_SHIFT;
-      P.first[g] = -1;
-      P.done[g] = -1;
-      P.pstart[g] = -1;
-    }
-    if (lane < P.K) {
-      SInst& I = SI[lane];
-      I.hp = lane >= P.n_lp;
-      I.kv_total = I.kv_free = I.hp ? P.kv_hp : P.kv_lp;
-      I.end = 0; I.hist_sum = 0; I.hash = 0;
-      I.wq_len = I.ds_len = I.bp_len = I.hist_cnt = 0;
-      I.busy = I.batch_dec = I.tk_live = 0;
-      I.ticket = (I.hp && P.tickets) ? 1 : 0;  // issued at t = 0 (G29)
-    }
-    __syncwarp();
+    w.base = P.off[trace];
+    w.n = P.off[trace + 1] - w.base;
+    w.tbt = P.tbt[trace];
+    init_trace(P, w, trace);
+    int64_t next = 0, next_arr = w.n > 0 ? P.arr[w.base] : INF64, decisions = 0, evals = 0;
     while (true) {
-      int64_t T = INF64;
-      if (t.next < t.n) T = P.arr[t.base + t.next];
-      int64_t te = INF64;
-      if (lane < P.K && SI[lane].busy) te = SI[lane].end;
-      te = warp_min(te);
-      T = te < T ? te : T;
-      if (t.fl_head < t.fl_tail) {
-        const int64_t tf = P.fl_t[t.base + t.fl_head];
+      int64_t T = next_arr;
+      for (int k = 0; k < K; k++) {
+        const int64_t e = w.SI[k].end;
+        T = e < T ? e : T;
+      }
+      const bool flight = w.ts->fl_head < w.ts->fl_tail;
+      if (flight) {
+        const int64_t tf = P.fl_t[w.base + w.ts->fl_head];
         T = tf < T ? tf : T;
       }
-      if (T == INF64) {
-        const bool stuck = lane < P.K && (SI[lane].wq_len > 0 || SI[lane].ds_len > 0);
-        if (__any_sync(FULL, stuck) && lane == 0) atomicOr(P.err, ERR_INVARIANT);
-        break;
-      }
+      if (T == INF64) break;
       // A. completions in instance order
-      for (int k = 0; k < P.K; k++)
-        if (SI[k].busy && SI[k].end == T) complete(P, SI[k], k, t, T);
+      for (int k = 0; k < K; k++)
+        if (w.SI[k].end == T) complete(P, w, k, T);
       // B. offload deliveries (FIFO = time order)
-      while (t.fl_head < t.fl_tail && P.fl_t[t.base + t.fl_head] == T) {
-        const int32_t id = P.fl_req[t.base + t.fl_head];
-        const int h = P.fl_hp[t.base + t.fl_head];
-        wq_insert_sorted(P, SI[h], h, t, id);
-        t.fl_head++;
-      }
+      if (flight) deliver(P, w, T);
       // C. arrivals, ascending id
-      while (t.next < t.n && P.arr[t.base + t.next] == T) {
-        route(P, SI, t, (int32_t)t.next);
-        t.next++;
+      while (next_arr == T) {
+        route(P, w, (int32_t)next);
+        next++;
+        next_arr = next < w.n ? P.arr[w.base + next] : INF64;
       }
       // D. formations of idle instances, LPs before HPs
-      for (int k = 0; k < P.K; k++) {
-        if (SI[k].busy) continue;
-        if (SI[k].hp) form_hp(P, SI, k, t, T);
-        else form_lp(P, SI, k, t, T, s_buf[w]);
+      for (int k = 0; k < n_lp; k++) {
+        if (w.SI[k].end == INF64) {
+          const int64_t r = form_lp(P, w, k, T);
+          decisions += r & 1;
+          evals += r >> 1;
+        }
+      }
+      for (int k = n_lp; k < K; k++) {
+        if (w.SI[k].end == INF64) {
+          const int64_t r = form_hp(P, w, k, T);
+          decisions += r & 1;
+          evals += r >> 1;
+        }
       }
       // E. tickets (G29)
       if (P.tickets) {
-        if (lane >= P.n_lp && lane < P.K) {
-          SInst& I = SI[lane];
+        if (lane >= n_lp && lane < K) {
+          SInst& I = w.SI[lane];
           if (!I.ticket && I.wq_len == 0 && I.tk_live == 0) I.ticket = 1;
         }
         __syncwarp();
       }
     }
-    // outputs
-    for (int64_t i = lane; i < t.n; i += 32) {
-      const int64_t g = t.base + i;
-      const uint32_t f = P.rq_fl[g];
-      uint32_t st = (f >> ST_SHIFT) & 3u;
-      st |= (f & F_OFFL) ? 4u : 0u;
-      st |= (f & F_TICK) ? 8u : 0u;
-      st |= ((f >> INST_SHIFT) & 0xffu) << 4;
-      st |= ((f >> NPRE_SHIFT) & 0xffffu) << 12;
-      P.status[g] = st;
-    }
-    if (lane == 0) {
-      uint64_t d = 0;
-      for (int k = 0; k < P.K; k++) d = mix64(d ^ SI[k].hash);
-      P.digest[trace] = d;
-      if (P.decisions) P.decisions[trace] = t.decisions;
-      if (P.evals) P.evals[trace] = t.evals;
-    }
-    __syncwarp();
+    finish_trace(P, w, trace, decisions, evals);
   }
+}
+
+size_t sim_smem_per_warp(int K) {
+  const size_t per_warp = 64 * sizeof(KI) + (size_t)K * DCAP * sizeof(int4) + (size_t)K * sizeof(SInst) + sizeof(TS);
+  return (per_warp + 15) & ~size_t(15);
 }
 
 // liveness / layout validation (ASC_E_CONFIG / ASC_E_INVAL before simulating)
@@ -822,10 +1023,7 @@ asc_status launch_simulate(asc_ctx* c, const asc_traces* tr, asc_outcomes* out, 
   P.rq_fl = ar.take<uint32_t>(R);
   P.wq_key = ar.take<int64_t>((size_t)K * R);
   P.wq_id = ar.take<int32_t>((size_t)K * R);
-  P.ds_id = ar.take<int32_t>((size_t)K * R);
-  P.ds_ctx = ar.take<int32_t>((size_t)K * R);
-  P.ds_held = ar.take<int32_t>((size_t)K * R);
-  P.ds_rem = ar.take<int32_t>((size_t)K * R);
+  P.ds_g = ar.take<int4>((size_t)K * R);
   P.bp_id = ar.take<int32_t>((size_t)K * R);
   P.scr_drop = ar.take<int32_t>(R);
   P.scr_pre = ar.take<int32_t>(R);
@@ -852,11 +1050,16 @@ asc_status launch_simulate(asc_ctx* c, const asc_traces* tr, asc_outcomes* out, 
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
   int64_t blocks = ((int64_t)T + SW - 1) / SW;
-  const int64_t cap = (int64_t)sms * 16;
+  const int64_t cap = (int64_t)sms * 8;
   if (blocks > cap) blocks = cap;
+  const size_t smem = SW * sim_smem_per_warp(K);
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(sim_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return cuda_check(c, e, "simulate smem attribute");
+  }
   if (blocks > 0) {
     cudaEventRecord(c->ev0, sm);
-    sim_kernel<<<(unsigned)blocks, SW * 32, 0, sm>>>(P);
+    sim_kernel<<<(unsigned)blocks, SW * 32, smem, sm>>>(P);
     cudaEventRecord(c->ev1, sm);
     c->timed = true;
     launches++;
