@@ -69,11 +69,14 @@ asc_status collect_errors(asc_ctx* c, const char* where) {
 }  // namespace asc
 
 // prefill latency table for eff_prompt in [0, n) and the worst-case HP batch latency W_hp
-__global__ void build_tables(Model md, int64_t* tab, int32_t n, int32_t hp_tok, int64_t* w_hp, int* err) {
+__global__ void build_tables(Model md, int64_t* tab, int32_t* tab32, int32_t n, int32_t hp_tok,
+                             int64_t* w_hp, int* err) {
   for (int32_t p = blockIdx.x * blockDim.x + threadIdx.x; p < n; p += gridDim.x * blockDim.x) {
     const int64_t v = p == 0 ? 0 : prefill_lat(md, (uint64_t)p);
     if (v < 0) atomicOr(err, ERR_RANGE);
     tab[p] = v < 0 ? INT32_MAX : v;
+    if (v > INT32_MAX) atomicOr((int*)(w_hp + 1), 1);  // int32 copy unusable
+    tab32[p] = (int32_t)(v < 0 ? INT32_MAX : (v > INT32_MAX ? INT32_MAX : v));
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     const int64_t v = prefill_lat(md, (uint64_t)hp_tok);
@@ -157,7 +160,8 @@ asc_status asc_create(const asc_config* cfg, int device, void* cuda_stream, asc_
   int64_t* d_w = nullptr;
   if (cudaMalloc(&c->d_err, sizeof(int)) != cudaSuccess ||
       cudaMalloc(&c->d_pf_tab, sizeof(int64_t) * c->pt_size) != cudaSuccess ||
-      cudaMalloc(&d_w, sizeof(int64_t)) != cudaSuccess) {
+      cudaMalloc(&c->d_pf_tab32_mem, sizeof(int32_t) * c->pt_size) != cudaSuccess ||
+      cudaMalloc(&d_w, 2 * sizeof(int64_t)) != cudaSuccess) {
     cudaGetLastError();
     asc_destroy(c);
     if (d_w) cudaFree(d_w);
@@ -166,10 +170,14 @@ asc_status asc_create(const asc_config* cfg, int device, void* cuda_stream, asc_
   cudaEventCreate(&c->ev0);
   cudaEventCreate(&c->ev1);
   cudaMemsetAsync(c->d_err, 0, sizeof(int), c->stream);
-  build_tables<<<(c->pt_size + 255) / 256, 256, 0, c->stream>>>(c->md, c->d_pf_tab, c->pt_size,
-                                                                 t.hp_token_budget, d_w, c->d_err);
-  e = cudaMemcpyAsync(&c->w_hp, d_w, sizeof(int64_t), cudaMemcpyDeviceToHost, c->stream);
+  cudaMemsetAsync(d_w, 0, 2 * sizeof(int64_t), c->stream);
+  build_tables<<<(c->pt_size + 255) / 256, 256, 0, c->stream>>>(
+      c->md, c->d_pf_tab, c->d_pf_tab32_mem, c->pt_size, t.hp_token_budget, d_w, c->d_err);
+  int64_t hw[2] = {0, 0};
+  e = cudaMemcpyAsync(hw, d_w, 2 * sizeof(int64_t), cudaMemcpyDeviceToHost, c->stream);
   asc_status st = e != cudaSuccess ? cuda_check(c, e, "asc_create") : collect_errors(c, "asc_create tables");
+  c->w_hp = hw[0];
+  c->d_pf_tab32 = hw[1] ? nullptr : c->d_pf_tab32_mem;
   cudaFree(d_w);
   if (st) {
     g_create_err = c->err;
@@ -184,6 +192,7 @@ void asc_destroy(asc_ctx* ctx) {
   if (!ctx) return;
   if (ctx->d_err) cudaFree(ctx->d_err);
   if (ctx->d_pf_tab) cudaFree(ctx->d_pf_tab);
+  if (ctx->d_pf_tab32_mem) cudaFree(ctx->d_pf_tab32_mem);
   if (ctx->ws) cudaFree(ctx->ws);
   if (ctx->stage) cudaFree(ctx->stage);
   if (ctx->ev0) cudaEventDestroy(ctx->ev0);

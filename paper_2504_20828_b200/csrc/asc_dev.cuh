@@ -156,6 +156,18 @@ __device__ __forceinline__ KI ki_shfl(const KI& v, int src) {
 __device__ __forceinline__ KI ki_min(const KI& a, const KI& b) { return ki_less(b, a) ? b : a; }
 __device__ __forceinline__ KI ki_max(const KI& a, const KI& b) { return ki_less(b, a) ? a : b; }
 
+// Compare-exchange helpers: one (key, idx) comparison per exchange.
+__device__ __forceinline__ KI ki_keep(const KI& v, const KI& o, bool keep_min) {
+  const bool o_less = ki_less(o, v);
+  return (o_less == keep_min) ? o : v;
+}
+__device__ __forceinline__ void ki_cas(KI& lo, KI& hi) {
+  const bool sw = ki_less(hi, lo);
+  const KI t = lo;
+  lo = sw ? hi : lo;
+  hi = sw ? t : hi;
+}
+
 // Bitonic sort of 32 elements, one per lane, ascending by lane.
 __device__ __forceinline__ KI sort32(KI v) {
   const int l = lane_id();
@@ -166,7 +178,7 @@ __device__ __forceinline__ KI sort32(KI v) {
       const KI o = ki_shfl_xor(v, j);
       const bool up = (l & k) == 0;
       const bool lower = (l & j) == 0;
-      v = (lower == up) ? ki_min(v, o) : ki_max(v, o);
+      v = ki_keep(v, o, lower == up);
     }
   }
   return v;
@@ -188,11 +200,7 @@ struct WarpTopK {
     for (int j = KPL / 2; j > 0; j >>= 1) {     // cross-register stages (stride j*32)
 #pragma unroll
       for (int r = 0; r < KPL; r++) {
-        if ((r & j) == 0) {
-          const KI x = a[r], y = a[r | j];
-          a[r] = ki_min(x, y);
-          a[r | j] = ki_max(x, y);
-        }
+        if ((r & j) == 0) ki_cas(a[r], a[r | j]);
       }
     }
 #pragma unroll
@@ -201,7 +209,7 @@ struct WarpTopK {
 #pragma unroll
       for (int r = 0; r < KPL; r++) {
         const KI o = ki_shfl_xor(a[r], j);
-        a[r] = lower ? ki_min(a[r], o) : ki_max(a[r], o);
+        a[r] = ki_keep(a[r], o, lower);
       }
     }
   }
@@ -221,34 +229,57 @@ struct WarpTopK {
   __device__ __forceinline__ KI kth() const {  // current K-th smallest (the threshold)
     return ki_shfl(a[KPL - 1], 31);
   }
+  // element at sorted position pos (0 <= pos < 32*KPL), broadcast to every lane
+  __device__ __forceinline__ KI at(int pos) const {
+    const int r = pos >> 5;
+    KI x = a[0];
+#pragma unroll
+    for (int q = 1; q < KPL; q++) if (q == r) x = a[q];
+    return ki_shfl(x, pos & 31);
+  }
 };
 
-// Streaming front-end: candidates below the threshold are appended to a 64-slot shared buffer and
-// merged 32 at a time, so a merge costs one sort32 + one bitonic merge per 32 survivors.
+// Streaming front-end: candidates below the threshold are appended to a shared buffer (64 slots for
+// push(); 160 for append() x4 + drain()) and
+// merged 32 at a time, so a merge costs one sort32 + one bitonic merge per 32 survivors.  The
+// threshold is the element at sorted position kpos (the last position the consumer can use:
+// Algorithm 1 admits at most min(R, N-1, M-1, C-1) entries); kpos < 0 disables selection.
 template <int KPL>
 struct TopKStream {
   WarpTopK<KPL> top;
   KI thr;
-  int cnt;
-  KI* buf;  // 64 slots in shared memory (per warp)
+  int cnt, kpos;
+  bool any;  // has a merge happened (list non-empty)?
+  KI* buf;   // 64 slots in shared memory (per warp)
 
-  __device__ __forceinline__ void init(KI* sbuf) {
+  __device__ __forceinline__ void init(KI* sbuf, int kpos_ = 32 * KPL - 1) {
     top.init();
     thr = ki_inf();
     cnt = 0;
+    kpos = kpos_;
+    any = false;
     buf = sbuf;
   }
   __device__ __forceinline__ void flush32() {
     __syncwarp();
     KI y = buf[lane_id()];
     __syncwarp();
-    KI rest = (lane_id() < cnt - 32) ? buf[32 + lane_id()] : ki_inf();
-    __syncwarp();
-    if (lane_id() < cnt - 32) buf[lane_id()] = rest;
+    for (int c0 = 32; c0 < cnt; c0 += 32) {  // shift the remaining candidates down by 32
+      const int j = c0 + lane_id();
+      KI rest = j < cnt ? buf[j] : ki_inf();
+      __syncwarp();
+      if (j < cnt) buf[j - 32] = rest;
+      __syncwarp();
+    }
     cnt -= 32;
     y = sort32(y);
-    top.merge32(y);
-    thr = top.kth();
+    if (any) {
+      top.merge32(y);
+    } else {
+      top.a[0] = y;  // first batch: the list was empty
+      any = true;
+    }
+    thr = top.at(kpos);
     __syncwarp();
   }
   // offer one element per lane (valid = participates)
@@ -260,15 +291,141 @@ struct TopKStream {
     cnt += __popc(m);
     if (cnt >= 32) flush32();
   }
+  // append without merging (the buffer must hold cnt + 32): call drain() once per few pushes so
+  // the merge network is instantiated at a single code location
+  // c: this lane offers x (the caller already tested it against thr)
+  __device__ __forceinline__ void append(const KI& x, bool c) {
+    const uint32_t m = __ballot_sync(FULL, c);
+    if (c) buf[cnt + __popc(m & lanemask_lt())] = x;
+    cnt += __popc(m);
+  }
+  __device__ __forceinline__ void drain() {
+    while (cnt >= 32) flush32();
+  }
   __device__ __forceinline__ void finish() {
+    drain();
     if (cnt > 0) {
       __syncwarp();
       KI y = lane_id() < cnt ? buf[lane_id()] : ki_inf();
       __syncwarp();
       cnt = 0;
       y = sort32(y);
-      top.merge32(y);
-      thr = top.kth();
+      if (any) top.merge32(y); else top.a[0] = y;
+      any = true;
+      thr = top.at(kpos);
+    }
+  }
+};
+
+// ------------------------------------------------------------- packed (key, idx) variant -------
+// A (key, idx) pair whose key fits 32 bits relative to a base packs into one uint64 whose unsigned
+// order is the (key, idx) order: ((key32 + 2^31) << 32) | idx32.  Compare-exchanges then cost one
+// 64-bit compare and two shuffles instead of three.
+constexpr uint64_t PK_INF = ~0ull;
+
+__device__ __forceinline__ uint64_t pk_keep(uint64_t v, uint64_t o, bool keep_min) {
+  return ((o < v) == keep_min) ? o : v;
+}
+
+__device__ __forceinline__ uint64_t sort32_pk(uint64_t v) {
+  const int l = lane_id();
+#pragma unroll
+  for (int k = 2; k <= 32; k <<= 1) {
+#pragma unroll
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      const uint64_t o = __shfl_xor_sync(FULL, v, j);
+      v = pk_keep(v, o, ((l & j) == 0) == ((l & k) == 0));
+    }
+  }
+  return v;
+}
+
+template <int KPL>
+struct TopKPk {
+  uint64_t a[KPL];
+  uint64_t thr;
+  int cnt, kpos;
+  bool any;
+  uint64_t* buf;  // 160 slots in shared memory (per warp)
+
+  __device__ __forceinline__ void init(uint64_t* sbuf, int kpos_) {
+#pragma unroll
+    for (int r = 0; r < KPL; r++) a[r] = PK_INF;
+    thr = PK_INF;
+    cnt = 0;
+    kpos = kpos_;
+    any = false;
+    buf = sbuf;
+  }
+  __device__ __forceinline__ void bitonic_merge() {
+    const int l = lane_id();
+#pragma unroll
+    for (int j = KPL / 2; j > 0; j >>= 1) {
+#pragma unroll
+      for (int r = 0; r < KPL; r++) {
+        if ((r & j) == 0) {
+          const uint64_t x = a[r], y = a[r | j];
+          a[r] = x < y ? x : y;
+          a[r | j] = x < y ? y : x;
+        }
+      }
+    }
+#pragma unroll
+    for (int j = 16; j > 0; j >>= 1) {
+      const bool lower = (l & j) == 0;
+#pragma unroll
+      for (int r = 0; r < KPL; r++) a[r] = pk_keep(a[r], __shfl_xor_sync(FULL, a[r], j), lower);
+    }
+  }
+  __device__ __forceinline__ uint64_t at(int pos) const {
+    const int r = pos >> 5;
+    uint64_t x = a[0];
+#pragma unroll
+    for (int q = 1; q < KPL; q++) if (q == r) x = a[q];
+    return __shfl_sync(FULL, x, pos & 31);
+  }
+  __device__ __forceinline__ void merge_sorted32(uint64_t y) {
+    if (any) {
+      const uint64_t br = __shfl_sync(FULL, y, 31 - lane_id());
+      a[KPL - 1] = a[KPL - 1] < br ? a[KPL - 1] : br;
+      bitonic_merge();
+    } else {
+      a[0] = y;
+      any = true;
+    }
+    thr = at(kpos);
+  }
+  __device__ __forceinline__ void flush32() {
+    __syncwarp();
+    uint64_t y = buf[lane_id()];
+    __syncwarp();
+    for (int c0 = 32; c0 < cnt; c0 += 32) {
+      const int j = c0 + lane_id();
+      const uint64_t rest = j < cnt ? buf[j] : PK_INF;
+      __syncwarp();
+      if (j < cnt) buf[j - 32] = rest;
+      __syncwarp();
+    }
+    cnt -= 32;
+    merge_sorted32(sort32_pk(y));
+    __syncwarp();
+  }
+  __device__ __forceinline__ void append(uint64_t x, bool c) {
+    const uint32_t m = __ballot_sync(FULL, c);
+    if (c) buf[cnt + __popc(m & lanemask_lt())] = x;
+    cnt += __popc(m);
+  }
+  __device__ __forceinline__ void drain() {
+    while (cnt >= 32) flush32();
+  }
+  __device__ __forceinline__ void finish() {
+    drain();
+    if (cnt > 0) {
+      __syncwarp();
+      uint64_t y = lane_id() < cnt ? buf[lane_id()] : PK_INF;
+      __syncwarp();
+      cnt = 0;
+      merge_sorted32(sort32_pk(y));
     }
   }
 };

@@ -14,6 +14,8 @@ struct asc_ctx {
   asc::Model md;           // tp-divided model constants
   int32_t pt_size = 0;     // prefill table covers eff_prompt in [0, pt_size)
   int64_t* d_pf_tab = nullptr;  // prefill_us by eff_prompt (a1, cached per ctx)
+  int32_t* d_pf_tab32 = nullptr;  // int32 copy for lookups (nullptr if some entry > INT32_MAX)
+  int32_t* d_pf_tab32_mem = nullptr;
   int64_t w_hp = 0;        // worst-case HP batch latency (G24)
   int* d_err = nullptr;    // device error bits (asc::ERR_*)
   char* ws = nullptr;      // device workspace

@@ -1,14 +1,16 @@
 // step.cu — asc_schedule_step: the stateless LP decision over S segments.
 //
-// Design (DESIGN.md §Kernels/step):
-//   plan   : per segment, #warp-tasks = max(1, ceil(Q_s / 2048)); exclusive scans give each
-//            segment its first task and (for segments of > 1 task) its first candidate slot.
-//   k1     : one warp per task streams its <= 2048 entries once (coalesced 8+4+1 B per entry),
-//            evaluates a1 (prefill latency via the ctx's device table), the key (a2), the drop and
-//            offload predicates (a5, as ballot bitmasks) and keeps the 128 smallest (key, pos)
-//            in a register-resident bitonic list (a3).  Single-task segments are finished in
-//            place: Algorithm 1 prefix scan (a4), batch latency (a6), admitted bits removed from
-//            the offload mask, ballot/popc compaction of offload and drop indices (a5).
+// Design (DESIGN.md §6):
+//   plan   : per segment, #warp-tasks = max(1, ceil(Q_s / 16384)); exclusive scans give each
+//            segment its first task and (for segments of > 1 task) its first candidate slot, and
+//            a task -> segment map.
+//   k1     : one warp per task streams its <= 16384 entries once: each lane owns 4 consecutive
+//            entries per 128-entry group (128-bit loads of deadline/eff_prompt, 32-bit flags),
+//            evaluates a1 (prefill latency via the ctx's device table), the key (a2, branch-free),
+//            the drop and offload predicates (a5, as ballot bitmasks) and keeps the smallest
+//            (key, pos) entries Algorithm 1 could admit in a register-resident bitonic list (a3).
+//            Single-task segments finish in place: Algorithm 1 prefix scan (a4), batch latency
+//            (a6), admitted bits removed from the offload mask, popc/scan compaction (a5).
 //   k2     : one CTA per multi-task segment merges the per-task lists (bitonic, warp shuffles
 //            + shared-memory tree), runs Algorithm 1, clears admitted bits, scans task counts.
 //   k3     : one warp per multi-task task expands its masks into id-ascending output indices.
@@ -20,11 +22,13 @@ using namespace asc;
 
 namespace {
 
-constexpr int KPL = 4;  // K = 128 = ASC_MAX_BATCH
-constexpr int ITERS = 64;
-constexpr int CH = 32 * ITERS;  // entries per warp task
-constexpr int UNR = 4;
-constexpr int WARPS = 8;
+constexpr int KPL = 4;             // K = 128 = ASC_MAX_BATCH
+constexpr int CH = 16384;          // entries per warp task
+constexpr int GE = 128;            // entries per warp iteration (4 per lane)
+constexpr int NG = CH / GE + 1;    // groups per task (+1: the task base is rounded down to 4)
+constexpr int MW = 4 * NG;         // mask words per task per mask (word 4g+u, bit l <-> 4l+u)
+constexpr int WARPS = 8;   // k2/k3 CTA size
+constexpr int K1W = 4;     // k1 CTA size (warps); 3 CTAs/SM -> 12 warps
 constexpr int SCAN_ITEMS = 4;
 constexpr int SCAN_THREADS = 1024;
 constexpr int SCAN_TILE = SCAN_ITEMS * SCAN_THREADS;
@@ -32,8 +36,9 @@ constexpr int SCAN_TILE = SCAN_ITEMS * SCAN_THREADS;
 struct StepP {
   Model md;
   const int64_t* pf_tab;
-  int32_t pt, bs, policy, drop, offl;
-  int64_t W, margin;
+  const int32_t* pf_tab32;  // int32 copy when every entry fits (else nullptr)
+  int32_t pt, bs, drop, offl, kdl, kpf;
+  int64_t W, margin, Q;
   int32_t S;
   const int64_t* seg_off;
   const int64_t* now;
@@ -49,7 +54,8 @@ struct StepP {
   int32_t* pfout;
   int64_t* task_off;   // [S+1]
   int64_t* mtask_off;  // [S+1]
-  int64_t* scan_tmp;   // block totals
+  int32_t* task_seg;   // [#tasks]
+  int64_t* scan_tmp;   // tile totals
   KI* cand;
   uint32_t *moff, *mdrop;
   int32_t *coff, *cdrop;
@@ -57,20 +63,10 @@ struct StepP {
 };
 
 __device__ __forceinline__ int64_t pf_of(const StepP& P, int32_t p) {
-  if (p < P.pt) return __ldg(P.pf_tab + p);
+  if (p < P.pt) return P.pf_tab32 ? (int64_t)__ldg(P.pf_tab32 + p) : __ldg(P.pf_tab + p);
   const int64_t v = prefill_lat(P.md, (uint64_t)p);
   if (v < 0) { atomicOr(P.err, ERR_RANGE); return INT32_MAX; }
   return v;
-}
-
-__device__ __forceinline__ int64_t key_of(int policy, int64_t dl, int64_t pf) {
-  switch (policy) {
-    case 0: return dl - pf;          // EDF_LAXITY
-    case 1: return dl;               // EDF_DEADLINE
-    case 2: return pf;               // SJF
-    case 3: return -pf;              // LJF
-    default: return 0;               // FCFS: position order (entries are in arrival order)
-  }
 }
 
 // ---------------------------------------------------------------- planning (two scans) ------
@@ -129,27 +125,26 @@ __global__ void scan_totals(int64_t* tmp, int64_t nt) {  // one warp, exclusive 
   }
 }
 
-__global__ void scan_add(int64_t* a, int64_t* b, int64_t n, const int64_t* tmp) {
+__global__ void scan_add(StepP P, int64_t n, const int64_t* tmp) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= n) return;
   const int64_t t = i / SCAN_TILE;
-  a[i] += tmp[2 * t];
-  b[i] += tmp[2 * t + 1];
+  P.task_off[i] += tmp[2 * t];
+  P.mtask_off[i] += tmp[2 * t + 1];
 }
 
-__device__ __forceinline__ int64_t find_seg(const int64_t* task_off, int32_t S, int64_t task) {
-  int64_t lo = 0, hi = S;  // largest s with task_off[s] <= task
-  while (hi - lo > 1) {
-    const int64_t mid = (lo + hi) >> 1;
-    if (__ldg(task_off + mid) <= task) lo = mid; else hi = mid;
+__global__ void fill_task_seg(StepP P) {
+  for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < P.S;
+       s += (int64_t)gridDim.x * blockDim.x) {
+    for (int64_t t = P.task_off[s]; t < P.task_off[s + 1]; t++) P.task_seg[t] = (int32_t)s;
   }
-  return lo;
 }
 
 // ----------------------------------------------------------- Algorithm 1 over a sorted list --
-// a[] holds the <= 128 smallest live entries in (key, pos) order.  Writes admitted positions,
-// the batch latency, and returns k; `adm[r]` tells each lane which of its elements were admitted.
-__device__ int finalize_segment(const StepP& P, int64_t s, const KI (&a)[KPL], bool (&adm)[KPL]) {
+// a[] holds the smallest live entries in (key, pos) order.  Writes admitted positions and the
+// batch latency, returns k; `adm[r]` tells each lane which of its elements were admitted.
+__device__ __forceinline__ int finalize_segment(const StepP& P, int64_t s, const KI (&a)[KPL],
+                                                 bool (&adm)[KPL]) {
   const int lane = lane_id();
   const int64_t lo = P.seg_off[s];
   const int64_t N = P.bN[s], M = P.bM[s];
@@ -158,7 +153,7 @@ __device__ int finalize_segment(const StepP& P, int64_t s, const KI (&a)[KPL], b
   const int64_t Bd = P.dcnt[s], sl = P.dctx[s];
   int64_t C = INF64;
   if (Bd > 0) {
-    const int64_t d = lat_us(P.md, 0, 0, 0, 0, (uint64_t)Bd, (uint64_t)sl);
+    const int64_t d = lat_decode(P.md, (uint64_t)Bd, (uint64_t)sl);
     if (d < 0) atomicOr(P.err, ERR_RANGE);
     C = P.tbt[s] - d;
   }
@@ -168,6 +163,12 @@ __device__ int finalize_segment(const StepP& P, int64_t s, const KI (&a)[KPL], b
   bool go = true;
 #pragma unroll
   for (int r = 0; r < KPL; r++) {
+    adm[r] = false;
+    p[r] = 0;
+  }
+#pragma unroll
+  for (int r = 0; r < KPL; r++) {
+    if (!go) break;
     const bool valid = a[r].i != INF32;
     p[r] = valid ? __ldg(P.eff + a[r].i) : 0;
     const int64_t pf = valid ? pf_of(P, p[r]) : 0;
@@ -176,11 +177,11 @@ __device__ int finalize_segment(const StepP& P, int64_t s, const KI (&a)[KPL], b
     const int64_t Sb = cb + warp_incl_scan(bl);
     const int64_t Sc = cc + warp_incl_scan(pf);
     const int pos = r * 32 + lane;
-    const bool ok = go && valid && St < N && Sb < M && Sc < C && pos < R;
+    const bool ok = valid && St < N && Sb < M && Sc < C && pos < R;
     const uint32_t m = __ballot_sync(FULL, ok);
     const int cnt = (m == FULL) ? 32 : (__ffs(~m) - 1);
-    adm[r] = go && lane < cnt;
-    k += go ? cnt : 0;
+    adm[r] = lane < cnt;
+    k += cnt;
     if (cnt < 32) go = false;
     ct = __shfl_sync(FULL, St, 31);
     cb = __shfl_sync(FULL, Sb, 31);
@@ -197,14 +198,17 @@ __device__ int finalize_segment(const StepP& P, int64_t s, const KI (&a)[KPL], b
       P.admit_idx[lo + r * 32 + lane] = a[r].i;
     }
   }
-  sp = warp_sum(sp);
-  sp2 = warp_sum(sp2);
-  spc = warp_sum(spc);
+  if (k > 0) {
+    sp = warp_sum(sp);
+    sp2 = warp_sum(sp2);
+    spc = warp_sum(spc);
+  }
   if (lane == 0) {
     P.admit_cnt[s] = k;
     int64_t l = 0;
     if (k > 0 || Bd > 0) {
-      l = lat_us(P.md, (uint64_t)k, sp, sp2, spc, (uint64_t)Bd, (uint64_t)sl);
+      l = k ? lat_us(P.md, (uint64_t)k, sp, sp2, spc, (uint64_t)Bd, (uint64_t)sl)
+            : lat_decode(P.md, (uint64_t)Bd, (uint64_t)sl);
       if (l < 0) atomicOr(P.err, ERR_RANGE);
     }
     P.blat[s] = l;
@@ -212,97 +216,338 @@ __device__ int finalize_segment(const StepP& P, int64_t s, const KI (&a)[KPL], b
   return k;
 }
 
-// expand ballot words into output indices (id-ascending), starting at out + base
-__device__ __forceinline__ int64_t expand_words(const uint32_t* words, int nw, int64_t first_e,
-                                                int32_t* out, int64_t base) {
+// expand nibble-layout mask words (word 4g+u, bit l <-> entry b4 + 128g + 4l + u) into
+// id-ascending output indices starting at out[base]; returns the new base
+__device__ __forceinline__ int64_t expand_groups(const uint32_t* words, int ng, int64_t b4,
+                                                 int32_t* out, int64_t base) {
   const int lane = lane_id();
-  for (int w = 0; w < nw; w++) {
-    const uint32_t m = words[w];
-    if (m == 0) continue;
-    if ((m >> lane) & 1u) out[base + __popc(m & lanemask_lt())] = (int32_t)(first_e + w * 32 + lane);
-    base += __popc(m);
+  for (int g = 0; g < ng; g++) {
+    const uint32_t w0 = words[4 * g], w1 = words[4 * g + 1], w2 = words[4 * g + 2], w3 = words[4 * g + 3];
+    if ((w0 | w1 | w2 | w3) == 0) continue;
+    const uint32_t nib = ((w0 >> lane) & 1u) | (((w1 >> lane) & 1u) << 1) |
+                         (((w2 >> lane) & 1u) << 2) | (((w3 >> lane) & 1u) << 3);
+    const int c = __popc(nib);
+    const int incl = warp_incl_scan(c);
+    int64_t pos = base + incl - c;
+    const int32_t e0 = (int32_t)(b4 + g * GE + 4 * lane);
+#pragma unroll
+    for (int u = 0; u < 4; u++)
+      if ((nib >> u) & 1u) out[pos++] = e0 + u;
+    base += __shfl_sync(FULL, incl, 31);
   }
   return base;
 }
 
-__global__ void __launch_bounds__(WARPS * 32) k1_tasks(StepP P) {
-  __shared__ KI sbuf[WARPS][64];
-  __shared__ uint32_t s_off[WARPS][ITERS], s_drop[WARPS][ITERS];
+__device__ __forceinline__ void clear_admitted(uint32_t* words, int64_t loc) {
+  const int64_t g = loc >> 7, r = loc & 127;
+  atomicAnd(&words[4 * g + (r & 3)], ~(1u << (r >> 2)));
+}
+
+struct Grp {  // one lane's 4 consecutive entries
+  int64_t dl[4];
+  int32_t p[4];
+  uint32_t f4;
+};
+
+template <bool VEC>
+__device__ __forceinline__ void load_grp(const StepP& P, int64_t e0, Grp& g) {
+  if (VEC && e0 + 4 <= P.Q) {
+    const longlong2 d01 = __ldcs(reinterpret_cast<const longlong2*>(P.dl + e0));
+    const longlong2 d23 = __ldcs(reinterpret_cast<const longlong2*>(P.dl + e0 + 2));
+    const int4 pv = __ldcs(reinterpret_cast<const int4*>(P.eff + e0));
+    g.f4 = __ldcs(reinterpret_cast<const unsigned int*>(P.fl + e0));
+    g.dl[0] = d01.x; g.dl[1] = d01.y; g.dl[2] = d23.x; g.dl[3] = d23.y;
+    g.p[0] = pv.x; g.p[1] = pv.y; g.p[2] = pv.z; g.p[3] = pv.w;
+  } else {
+    g.f4 = 0;
+#pragma unroll
+    for (int u = 0; u < 4; u++) {
+      const bool in = e0 + u >= 0 && e0 + u < P.Q;
+      g.dl[u] = in ? P.dl[e0 + u] : 0;
+      g.p[u] = in ? P.eff[e0 + u] : 1;
+      g.f4 |= (in ? (uint32_t)P.fl[e0 + u] : 0u) << (8 * u);
+    }
+  }
+}
+
+// ---- cp.async staging: each lane copies its own 4 entries of a 128-entry group into a per-warp
+// shared-memory ring (deadline 32 B, eff 16 B, flags 4 B per lane); no registers are held for
+// data in flight and no cross-lane synchronisation is needed (a lane reads only what it copied).
+constexpr int NST = 4;  // pipeline stages per warp
+struct Stage {
+  longlong2 dl[2 * 32];  // lane l: dl[2l], dl[2l+1]
+  int4 eff[32];
+  uint32_t fl[32];
+};
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* g) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(g));
+}
+__device__ __forceinline__ void cp_async4(void* smem, const void* g) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(sa), "l"(g));
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+// issue the copies of the group at e0 (this lane's first entry); tail groups crossing Q are read
+// directly at consume time instead
+__device__ __forceinline__ void stage_issue(const StepP& P, Stage& st, int64_t e0) {
+  const int l = lane_id();
+  if (e0 + 4 <= P.Q) {
+    cp_async16(&st.dl[2 * l], P.dl + e0);
+    cp_async16(&st.dl[2 * l + 1], P.dl + e0 + 2);
+    cp_async16(&st.eff[l], P.eff + e0);
+    cp_async4(&st.fl[l], P.fl + e0);
+  }
+}
+
+__device__ __forceinline__ void stage_read(const StepP& P, const Stage& st, int64_t e0, Grp& g) {
+  const int l = lane_id();
+  if (e0 + 4 <= P.Q) {
+    const longlong2 d01 = st.dl[2 * l], d23 = st.dl[2 * l + 1];
+    const int4 pv = st.eff[l];
+    g.f4 = st.fl[l];
+    g.dl[0] = d01.x; g.dl[1] = d01.y; g.dl[2] = d23.x; g.dl[3] = d23.y;
+    g.p[0] = pv.x; g.p[1] = pv.y; g.p[2] = pv.z; g.p[3] = pv.w;
+  } else {
+    load_grp<false>(P, e0, g);
+  }
+}
+
+__device__ __noinline__ int64_t pf_slow(const StepP& P, int32_t p) {
+  const int64_t v = prefill_lat(P.md, (uint64_t)p);
+  if (v < 0) { atomicOr(P.err, ERR_RANGE); return INT32_MAX; }
+  return v;
+}
+
+constexpr size_t K1_SMEM = sizeof(Stage) * K1W * NST + sizeof(KI) * K1W * 160 + 2 * 4 * K1W * MW;
+
+struct TaskCtx {  // per-task constants (uniform across the warp)
+  int64_t s, lo, b, e_end, b4, now, othr;
+  int32_t ng, vlo, vhi, kpos;
+};
+
+// Generic exact path: 64-bit keys and deadlines.  Used for a task whose deadlines or prefill
+// latencies fall outside the 32-bit window of the fast path (or with an int64 latency table).
+template <bool DROP, bool OFFL>
+__device__ __noinline__ void task_generic(const StepP& P, const TaskCtx& t, KI* sbuf, uint32_t* m_off,
+                                          uint32_t* m_drop, KI* out_a) {
+  const int lane = lane_id();
+  TopKStream<KPL> st;
+  st.init(sbuf, t.kpos);
+  const bool select = t.kpos >= 0;
+  bool bad = false;
+  for (int g = 0; g < t.ng; g++) {
+    const int64_t e0 = t.b4 + (int64_t)g * GE + 4 * lane;
+    Grp cur;
+    load_grp<false>(P, e0, cur);
+    const int32_t r0 = g * GE + 4 * lane;
+    KI x[4];
+    bool cnd[4];
+    uint32_t mo_w = 0, md_w = 0;
+#pragma unroll
+    for (int u = 0; u < 4; u++) {
+      const bool v = r0 + u >= t.vlo && r0 + u < t.vhi;
+      const uint32_t f = (cur.f4 >> (8 * u)) & 0xffu;
+      const int32_t pu = cur.p[u];
+      bad |= v && pu < 1;
+      int64_t pf = 0;
+      if (v) {
+        if (pu >= 1 && pu < P.pt) pf = P.pf_tab32 ? (int64_t)__ldg(P.pf_tab32 + pu) : __ldg(P.pf_tab + pu);
+        else pf = pf_slow(P, pu < 1 ? 1 : pu);
+      }
+      if (P.pfout && v) {
+        bad |= pf > INT32_MAX;
+        __stcs(P.pfout + e0 + u, (int32_t)pf);
+      }
+      const bool dropped = DROP && v && !(f & 1u) && t.now > cur.dl[u];
+      const bool off = OFFL && v && !dropped && !(f & 3u) && cur.dl[u] - pf <= t.othr;
+      const uint32_t md = __ballot_sync(FULL, dropped), mo = __ballot_sync(FULL, off);
+      md_w = lane == u ? md : md_w;
+      mo_w = lane == u ? mo : mo_w;
+      const int64_t spf = P.kpf > 0 ? pf : (P.kpf < 0 ? -pf : 0);
+      x[u] = KI{(P.kdl ? cur.dl[u] : 0) + spf, (int32_t)(e0 + u)};
+      cnd[u] = select && v && !dropped && ki_less(x[u], st.thr);
+    }
+    if (lane < 4) {
+      if (DROP) m_drop[4 * g + lane] = md_w;
+      if (OFFL) m_off[4 * g + lane] = mo_w;
+    }
+    if (__any_sync(FULL, cnd[0] | cnd[1] | cnd[2] | cnd[3])) {
+#pragma unroll
+      for (int u = 0; u < 4; u++) st.append(x[u], cnd[u]);
+      st.drain();
+    }
+  }
+  if (__any_sync(FULL, bad) && lane == 0) atomicOr(P.err, ERR_INVAL);
+  if (select) st.finish();
+#pragma unroll
+  for (int r = 0; r < KPL; r++) out_a[r] = st.top.a[r];
+  __syncwarp();
+}
+
+constexpr int64_t WIN = int64_t(1) << 30;  // fast-path window: |deadline - now| < 2^30 us, pf < 2^30
+
+// TAB: 0 = int64 latency table (generic path only), 1 = int32 table (fast path)
+template <bool VEC, int TAB, bool DROP, bool OFFL>
+__global__ void __launch_bounds__(K1W * 32, 3) k1_tasks(const __grid_constant__ StepP P) {
+  extern __shared__ __align__(16) unsigned char k1_smem[];  // K1_SMEM bytes (dynamic)
+  auto& s_stage = *reinterpret_cast<Stage(*)[K1W][NST]>(k1_smem);
+  auto& sbuf = *reinterpret_cast<KI(*)[K1W][160]>(k1_smem + sizeof(Stage) * K1W * NST);
+  auto& s_off = *reinterpret_cast<uint32_t(*)[K1W][MW]>(k1_smem + sizeof(Stage) * K1W * NST +
+                                                         sizeof(KI) * K1W * 160);
+  auto& s_drop = *reinterpret_cast<uint32_t(*)[K1W][MW]>(k1_smem + sizeof(Stage) * K1W * NST +
+                                                          sizeof(KI) * K1W * 160 + 4 * K1W * MW);
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t ntasks = P.task_off[P.S];
-  for (int64_t task = blockIdx.x * (int64_t)WARPS + w; task < ntasks;
-       task += (int64_t)gridDim.x * WARPS) {
-    const int64_t s = find_seg(P.task_off, P.S, task);
+  for (int64_t task = blockIdx.x * (int64_t)K1W + w; task < ntasks;
+       task += (int64_t)gridDim.x * K1W) {
+    TaskCtx t;
+    t.s = P.task_seg[task];
+    const int64_t s = t.s;
     const int64_t c = task - P.task_off[s];
     const int64_t nt = P.task_off[s + 1] - P.task_off[s];
-    const int64_t lo = P.seg_off[s], hi = P.seg_off[s + 1];
-    const int64_t b = lo + c * CH;
-    const int64_t e_end = min(hi, b + CH);
-    const int64_t now = P.now[s];
-    TopKStream<KPL> st;
-    st.init(sbuf[w]);
-    int nw = 0;
-    for (int j0 = 0; j0 < ITERS && b + j0 * 32 < e_end; j0 += UNR) {
-      int64_t dl[UNR];
-      int32_t p[UNR];
-      uint32_t f[UNR];
+    t.lo = P.seg_off[s];
+    const int64_t hi = P.seg_off[s + 1];
+    t.b = t.lo + c * CH;
+    t.e_end = min(hi, t.b + CH);
+    t.b4 = t.b & ~int64_t(3);
+    t.ng = (int)((t.e_end - t.b4 + GE - 1) / GE);
+    t.vlo = (int32_t)(t.b - t.b4);
+    t.vhi = (int32_t)(t.e_end - t.b4);
+    t.now = P.now[s];
+    t.othr = t.now + P.W + P.margin;  // offload iff deadline - prefill_us <= othr
+    // Algorithm 1 can admit at most min(R, N-1, M-1) entries (strict budgets, costs >= 1): only
+    // that many smallest keys are needed, so the running threshold sits at that position
+    int64_t kneed = P.bR[s];
+    kneed = kneed < 32 * KPL ? kneed : 32 * KPL;
+    kneed = kneed < (int64_t)P.bN[s] - 1 ? kneed : (int64_t)P.bN[s] - 1;
+    kneed = kneed < (int64_t)P.bM[s] - 1 ? kneed : (int64_t)P.bM[s] - 1;
+    t.kpos = kneed > 0 ? (int)kneed - 1 : -1;
+    const bool select = kneed > 0;
+    const int64_t b4 = t.b4, lo = t.lo;
+    const int ng = t.ng;
+    KI top[KPL];
+    bool fast_ok = (TAB == 1);
+    if (TAB == 1) {
+      // ---- fast path: 32-bit arithmetic relative to `now`, packed (key, local idx) ----------
+      const int32_t othr32 = (int32_t)max(min(P.W + P.margin, (int64_t)INT32_MAX), (int64_t)INT32_MIN);
+      const int64_t kbase = P.kdl ? t.now : 0;  // key = kbase + key32
+      TopKPk<KPL> st;
+      st.init(reinterpret_cast<uint64_t*>(sbuf[w]), t.kpos);
+      bool bad = false, inwin = true;
 #pragma unroll
-      for (int u = 0; u < UNR; u++) {
-        const int64_t e = b + (j0 + u) * 32 + lane;
-        if (e < e_end) {
-          dl[u] = __ldcs(P.dl + e);
-          p[u] = __ldcs(P.eff + e);
-          f[u] = __ldcs(P.fl + e);
+      for (int q = 0; q < NST - 1; q++) {
+        if (VEC && q < ng) stage_issue(P, s_stage[w][q], b4 + (int64_t)q * GE + 4 * lane);
+        cp_commit();
+      }
+      for (int g = 0; g < ng; g++) {
+        const int64_t e0 = b4 + (int64_t)g * GE + 4 * lane;
+        if (VEC && g + NST - 1 < ng) stage_issue(P, s_stage[w][(g + NST - 1) % NST], e0 + (NST - 1) * GE);
+        cp_commit();
+        Grp cur;
+        if (VEC) {
+          cp_wait<NST - 1>();
+          stage_read(P, s_stage[w][g % NST], e0, cur);
         } else {
-          dl[u] = 0; p[u] = 1; f[u] = 0;
+          load_grp<false>(P, e0, cur);
         }
-      }
+        const int32_t r0 = g * GE + 4 * lane;
+        const uint32_t l0 = (uint32_t)(e0 - lo);  // local index of this lane's first entry
+        uint64_t x[4];
+        bool cnd[4];
+        uint32_t mo_w = 0, md_w = 0;
 #pragma unroll
-      for (int u = 0; u < UNR; u++) {
-        const int64_t e = b + (j0 + u) * 32 + lane;
-        const bool v = e < e_end;
-        if (v && p[u] < 1) atomicOr(P.err, ERR_INVAL);
-        const int64_t pf = v ? pf_of(P, p[u] < 1 ? 1 : p[u]) : 0;
-        if (v && P.pfout) {
-          if (pf > INT32_MAX) atomicOr(P.err, ERR_RANGE);
-          __stcs(P.pfout + e, (int32_t)pf);
+        for (int u = 0; u < 4; u++) {
+          const bool v = r0 + u >= t.vlo && r0 + u < t.vhi;
+          const uint32_t f = (cur.f4 >> (8 * u)) & 0xffu;
+          const int32_t pu = cur.p[u];
+          const int64_t d = cur.dl[u] - t.now;
+          int32_t pf = 0;
+          if (v) {
+            if (pu >= 1 && pu < P.pt) {
+              pf = __ldg(P.pf_tab32 + pu);
+            } else {
+              bad |= pu < 1;
+              const int64_t q = pf_slow(P, pu < 1 ? 1 : pu);
+              inwin &= q < WIN;
+              pf = (int32_t)min(q, (int64_t)INT32_MAX);
+            }
+            inwin &= (uint64_t)(d + WIN) < (uint64_t)(2 * WIN) && pf < (int32_t)WIN;
+          }
+          if (P.pfout && v) __stcs(P.pfout + e0 + u, pf);
+          const int32_t d32 = (int32_t)d;
+          const bool dropped = DROP && v && !(f & 1u) && d32 < 0;
+          const bool off = OFFL && v && !dropped && !(f & 3u) && d32 - pf <= othr32;
+          if (DROP) {
+            const uint32_t md = __ballot_sync(FULL, dropped);
+            md_w = lane == u ? md : md_w;
+          }
+          if (OFFL) {
+            const uint32_t mo = __ballot_sync(FULL, off);
+            mo_w = lane == u ? mo : mo_w;
+          }
+          const int32_t key32 = (P.kdl ? d32 : 0) + (P.kpf > 0 ? pf : (P.kpf < 0 ? -pf : 0));
+          x[u] = ((uint64_t)((uint32_t)key32 ^ 0x80000000u) << 32) | (uint64_t)(l0 + u);
+          cnd[u] = select && v && !dropped && x[u] < st.thr;
         }
-        const bool dropped = v && P.drop && !(f[u] & 1u) && now > dl[u];
-        const bool off = v && P.offl && !dropped && !(f[u] & 3u) &&
-                         dl[u] - now <= pf + P.W + P.margin;
-        const uint32_t md = __ballot_sync(FULL, dropped), mo = __ballot_sync(FULL, off);
-        if (lane == 0) { s_drop[w][j0 + u] = md; s_off[w][j0 + u] = mo; }
-        st.push(KI{key_of(P.policy, dl[u], pf), (int32_t)e}, v && !dropped);
+        if (lane < 4) {  // lanes 0-3 hold the 4 ballot words of this group
+          if (DROP) s_drop[w][4 * g + lane] = md_w;
+          if (OFFL) s_off[w][4 * g + lane] = mo_w;
+        }
+        if (__any_sync(FULL, cnd[0] | cnd[1] | cnd[2] | cnd[3])) {
+#pragma unroll
+          for (int u = 0; u < 4; u++) st.append(x[u], cnd[u]);
+          st.drain();
+        }
       }
-      nw = j0 + UNR;
+      cp_wait<0>();
+      __syncwarp();
+      if (__any_sync(FULL, bad) && lane == 0) atomicOr(P.err, ERR_INVAL);
+      fast_ok = __all_sync(FULL, inwin);
+      if (fast_ok) {
+        if (select) st.finish();
+#pragma unroll
+        for (int r = 0; r < KPL; r++) {
+          const uint64_t x = st.a[r];
+          top[r] = x == PK_INF ? ki_inf()
+                               : KI{kbase + (int64_t)(int32_t)((uint32_t)(x >> 32) ^ 0x80000000u),
+                                    (int32_t)(lo + (int64_t)(uint32_t)x)};
+        }
+      }
     }
-    st.finish();
+    if (!fast_ok) {
+      KI tmp[KPL];
+      task_generic<DROP, OFFL>(P, t, sbuf[w], s_off[w], s_drop[w], tmp);
+#pragma unroll
+      for (int r = 0; r < KPL; r++) top[r] = tmp[r];
+    }
     __syncwarp();
     if (nt == 1) {
       bool adm[KPL];
-      finalize_segment(P, s, st.top.a, adm);
+      finalize_segment(P, s, top, adm);
       // an admitted request is not offloaded (only unscheduled requests)
 #pragma unroll
-      for (int r = 0; r < KPL; r++) {
-        if (adm[r]) {
-          const int64_t loc = st.top.a[r].i - b;
-          atomicAnd(&s_off[w][loc >> 5], ~(1u << (loc & 31)));
-        }
-      }
+      for (int r = 0; r < KPL; r++)
+        if (OFFL && adm[r]) clear_admitted(s_off[w], top[r].i - b4);
       __syncwarp();
-      const int64_t no = expand_words(s_off[w], nw, b, P.off_idx, lo);
-      const int64_t nd = expand_words(s_drop[w], nw, b, P.drop_idx, lo);
+      const int64_t no = OFFL ? expand_groups(s_off[w], ng, b4, P.off_idx, lo) : lo;
+      const int64_t nd = DROP ? expand_groups(s_drop[w], ng, b4, P.drop_idx, lo) : lo;
       if (lane == 0) { P.off_cnt[s] = (int32_t)(no - lo); P.drop_cnt[s] = (int32_t)(nd - lo); }
     } else {
       const int64_t mt = P.mtask_off[s] + c;
       KI* cd = P.cand + mt * (32 * KPL);
 #pragma unroll
-      for (int r = 0; r < KPL; r++) cd[r * 32 + lane] = st.top.a[r];
+      for (int r = 0; r < KPL; r++) cd[r * 32 + lane] = top[r];
       int32_t co = 0, cdp = 0;
-      for (int j = lane; j < ITERS; j += 32) {
-        const uint32_t mo = j < nw ? s_off[w][j] : 0u, mdp = j < nw ? s_drop[w][j] : 0u;
-        P.moff[mt * ITERS + j] = mo;
-        P.mdrop[mt * ITERS + j] = mdp;
+      for (int j = lane; j < MW; j += 32) {
+        const uint32_t mo = (OFFL && j < 4 * ng) ? s_off[w][j] : 0u;
+        const uint32_t mdp = (DROP && j < 4 * ng) ? s_drop[w][j] : 0u;
+        P.moff[mt * MW + j] = mo;
+        P.mdrop[mt * MW + j] = mdp;
         co += __popc(mo);
         cdp += __popc(mdp);
       }
@@ -314,7 +559,7 @@ __global__ void __launch_bounds__(WARPS * 32) k1_tasks(StepP P) {
   }
 }
 
-__global__ void __launch_bounds__(WARPS * 32) k2_segments(StepP P) {
+__global__ void __launch_bounds__(WARPS * 32) k2_segments(const __grid_constant__ StepP P) {
   __shared__ KI lists[WARPS][32 * KPL];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   for (int64_t s = blockIdx.x; s < P.S; s += gridDim.x) {
@@ -351,10 +596,12 @@ __global__ void __launch_bounds__(WARPS * 32) k2_segments(StepP P) {
 #pragma unroll
       for (int r = 0; r < KPL; r++) {
         if (adm[r]) {
-          const int64_t loc = A.a[r].i - lo;
-          const int64_t t = loc / CH, j = (loc % CH) >> 5;
-          const uint32_t bit = 1u << (loc & 31);
-          const uint32_t old = atomicAnd(&P.moff[(m0 + t) * ITERS + j], ~bit);
+          const int64_t e = A.a[r].i;
+          const int64_t t = (e - lo) / CH;
+          const int64_t b4 = (lo + t * CH) & ~int64_t(3);
+          const int64_t loc = e - b4, g = loc >> 7, rr = loc & 127;
+          const uint32_t bit = 1u << (rr >> 2);
+          const uint32_t old = atomicAnd(&P.moff[(m0 + t) * MW + 4 * g + (rr & 3)], ~bit);
           if (old & bit) atomicSub(&P.coff[m0 + t], 1);
         }
       }
@@ -376,20 +623,52 @@ __global__ void __launch_bounds__(WARPS * 32) k2_segments(StepP P) {
   }
 }
 
-__global__ void __launch_bounds__(WARPS * 32) k3_expand(StepP P) {
+__global__ void __launch_bounds__(WARPS * 32) k3_expand(const __grid_constant__ StepP P) {
   const int w = threadIdx.x >> 5;
   const int64_t ntasks = P.task_off[P.S];
   for (int64_t task = blockIdx.x * (int64_t)WARPS + w; task < ntasks;
        task += (int64_t)gridDim.x * WARPS) {
-    const int64_t s = find_seg(P.task_off, P.S, task);
+    const int64_t s = P.task_seg[task];
     const int64_t nt = P.task_off[s + 1] - P.task_off[s];
     if (nt <= 1) continue;
     const int64_t c = task - P.task_off[s];
     const int64_t mt = P.mtask_off[s] + c;
-    const int64_t lo = P.seg_off[s];
+    const int64_t lo = P.seg_off[s], hi = P.seg_off[s + 1];
     const int64_t b = lo + c * CH;
-    expand_words(P.moff + mt * ITERS, ITERS, b, P.off_idx, lo + P.coff[mt]);
-    expand_words(P.mdrop + mt * ITERS, ITERS, b, P.drop_idx, lo + P.cdrop[mt]);
+    const int64_t e_end = min(hi, b + CH);
+    const int64_t b4 = b & ~int64_t(3);
+    const int ng = (int)((e_end - b4 + GE - 1) / GE);
+    expand_groups(P.moff + mt * MW, ng, b4, P.off_idx, lo + P.coff[mt]);
+    expand_groups(P.mdrop + mt * MW, ng, b4, P.drop_idx, lo + P.cdrop[mt]);
+  }
+}
+
+template <bool VEC, int TAB, bool DROP, bool OFFL>
+void launch_k1_t(unsigned grid, size_t, cudaStream_t sm, const StepP& P) {
+  cudaFuncSetAttribute(k1_tasks<VEC, TAB, DROP, OFFL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)K1_SMEM);
+  k1_tasks<VEC, TAB, DROP, OFFL><<<grid, K1W * 32, K1_SMEM, sm>>>(P);
+}
+
+template <int TAB, bool DROP, bool OFFL>
+void launch_k1_v(bool vec, unsigned grid, size_t dsm, cudaStream_t sm, const StepP& P) {
+  if (vec) launch_k1_t<true, TAB, DROP, OFFL>(grid, dsm, sm, P);
+  else launch_k1_t<false, TAB, DROP, OFFL>(grid, dsm, sm, P);
+}
+
+template <int TAB>
+void launch_k1_d(int variant, unsigned grid, size_t dsm, cudaStream_t sm, const StepP& P) {
+  const bool vec = variant & 1, drop = variant & 8, offl = variant & 16;
+  if (drop && offl) launch_k1_v<TAB, true, true>(vec, grid, dsm, sm, P);
+  else if (drop) launch_k1_v<TAB, true, false>(vec, grid, dsm, sm, P);
+  else if (offl) launch_k1_v<TAB, false, true>(vec, grid, dsm, sm, P);
+  else launch_k1_v<TAB, false, false>(vec, grid, dsm, sm, P);
+}
+
+void launch_k1(int variant, unsigned grid, size_t dsm, cudaStream_t sm, const StepP& P) {
+  switch ((variant >> 1) & 3) {
+    case 1: launch_k1_d<1>(variant, grid, dsm, sm, P); break;
+    default: launch_k1_d<0>(variant, grid, dsm, sm, P); break;
   }
 }
 
@@ -400,23 +679,33 @@ namespace asc {
 asc_status launch_schedule_step(asc_ctx* c, const asc_step_in* in, asc_step_out* out, int64_t Q) {
   const int32_t S = in->S;
   const int64_t max_mt = 2 * (Q / CH) + 2;
+  const int64_t ntask_max = (int64_t)S + Q / CH + 1;
   const int64_t ntile = (S + 1 + SCAN_TILE - 1) / SCAN_TILE;
   size_t need = 0;
-  need += 2 * (size_t)(S + 1) * 8 + 2 * (size_t)ntile * 8 + 4096;
-  need += (size_t)max_mt * (32 * KPL) * sizeof(KI) + (size_t)max_mt * ITERS * 8 + (size_t)max_mt * 8 + 8192;
+  need += 2 * (size_t)(S + 1) * 8 + 2 * (size_t)ntile * 8 + (size_t)ntask_max * 4 + 8192;
+  need += (size_t)max_mt * (32 * KPL) * sizeof(KI) + (size_t)max_mt * MW * 8 + (size_t)max_mt * 8 + 8192;
   asc_status st = ensure_ws(c, need);
   if (st) return st;
   Arena ar{c->ws, c->ws_cap};
   StepP P;
   P.md = c->md;
   P.pf_tab = c->d_pf_tab;
+  P.pf_tab32 = c->d_pf_tab32;
   P.pt = c->pt_size;
   P.bs = c->cfg.topo.block_tokens;
-  P.policy = c->cfg.flags.policy;
   P.drop = c->cfg.flags.drop;
   P.offl = (c->cfg.flags.offload && c->cfg.topo.n_hp >= 1) ? 1 : 0;
+  // value function as key = kdl*deadline + kpf*prefill_us (FCFS: 0 = position order)
+  switch (c->cfg.flags.policy) {
+    case ASC_POLICY_EDF_LAXITY: P.kdl = 1; P.kpf = -1; break;
+    case ASC_POLICY_EDF_DEADLINE: P.kdl = 1; P.kpf = 0; break;
+    case ASC_POLICY_SJF: P.kdl = 0; P.kpf = 1; break;
+    case ASC_POLICY_LJF: P.kdl = 0; P.kpf = -1; break;
+    default: P.kdl = 0; P.kpf = 0; break;
+  }
   P.W = c->w_hp;
   P.margin = c->cfg.flags.offload_margin_us;
+  P.Q = Q;
   P.S = S;
   P.seg_off = in->seg_off; P.now = in->now_us; P.dl = in->deadline_us; P.eff = in->eff_prompt;
   P.fl = in->flags; P.dcnt = in->dec_count; P.dctx = in->dec_ctx_sum; P.tbt = in->tbt_slo_us;
@@ -427,33 +716,43 @@ asc_status launch_schedule_step(asc_ctx* c, const asc_step_in* in, asc_step_out*
   P.task_off = ar.take<int64_t>(S + 1);
   P.mtask_off = ar.take<int64_t>(S + 1);
   P.scan_tmp = ar.take<int64_t>(2 * ntile);
+  P.task_seg = ar.take<int32_t>(ntask_max);
   P.cand = ar.take<KI>(max_mt * 32 * KPL);
-  P.moff = ar.take<uint32_t>(max_mt * ITERS);
-  P.mdrop = ar.take<uint32_t>(max_mt * ITERS);
+  P.moff = ar.take<uint32_t>(max_mt * MW);
+  P.mdrop = ar.take<uint32_t>(max_mt * MW);
   P.coff = ar.take<int32_t>(max_mt);
   P.cdrop = ar.take<int32_t>(max_mt);
   P.err = c->d_err;
   cudaStream_t sm = c->stream;
   int64_t launches = 0;
+  int dev_sms = 148;
+  cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, c->device);
   plan_counts<<<(S + 1 + 255) / 256, 256, 0, sm>>>(P);
   scan_tiles<<<ntile, SCAN_THREADS, 0, sm>>>(P.task_off, P.mtask_off, S + 1, P.scan_tmp);
   scan_totals<<<1, 32, 0, sm>>>(P.scan_tmp, ntile);
-  scan_add<<<(S + 1 + 255) / 256, 256, 0, sm>>>(P.task_off, P.mtask_off, S + 1, P.scan_tmp);
-  launches += 4;
-  int dev_sms = 148;
-  cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, c->device);
-  const int64_t ntask_max = (int64_t)S + Q / CH + 1;
-  int64_t g1 = (ntask_max + WARPS - 1) / WARPS;
-  g1 = g1 < (int64_t)dev_sms * 8 ? g1 : (int64_t)dev_sms * 8;
+  scan_add<<<(S + 1 + 255) / 256, 256, 0, sm>>>(P, S + 1, P.scan_tmp);
+  const int64_t gf = (S + 255) / 256;
+  fill_task_seg<<<(unsigned)(gf < 4 * dev_sms ? (gf > 0 ? gf : 1) : 4 * dev_sms), 256, 0, sm>>>(P);
+  launches += 5;
+  int64_t g1 = (ntask_max + K1W - 1) / K1W;
+  g1 = g1 < (int64_t)dev_sms * 3 ? g1 : (int64_t)dev_sms * 3;
+  const bool vec = ((uintptr_t)in->deadline_us % 16 == 0) && ((uintptr_t)in->eff_prompt % 16 == 0) &&
+                   ((uintptr_t)in->flags % 4 == 0);
+  const unsigned gk = (unsigned)(g1 > 0 ? g1 : 1);
+  const int tab = P.pf_tab32 ? 1 : 0;
+  const size_t dsm = 0;
+  const int variant = (vec ? 1 : 0) | (tab << 1) | (P.drop ? 8 : 0) | (P.offl ? 16 : 0);
   cudaEventRecord(c->ev0, sm);
-  k1_tasks<<<(unsigned)(g1 > 0 ? g1 : 1), WARPS * 32, 0, sm>>>(P);
+  launch_k1(variant, gk, dsm, sm, P);
   cudaEventRecord(c->ev1, sm);
   c->timed = true;
   launches += 1;
   if (Q > CH) {
     int64_t g2 = S < (int64_t)dev_sms * 4 ? S : (int64_t)dev_sms * 4;
     k2_segments<<<(unsigned)(g2 > 0 ? g2 : 1), WARPS * 32, 0, sm>>>(P);
-    k3_expand<<<(unsigned)(g1 > 0 ? g1 : 1), WARPS * 32, 0, sm>>>(P);
+    int64_t g3 = (ntask_max + WARPS - 1) / WARPS;
+    g3 = g3 < (int64_t)dev_sms * 8 ? g3 : (int64_t)dev_sms * 8;
+    k3_expand<<<(unsigned)(g3 > 0 ? g3 : 1), WARPS * 32, 0, sm>>>(P);
     launches += 2;
   }
   c->last_kernel_launches = launches;

@@ -145,3 +145,15 @@ def test_errors(asc):
     with pytest.raises(asc.AscError) as e:
         run_gpu(asc, cfg, ins2)
     assert e.value.code == 1
+
+
+def test_generic_path_wide_deadlines(asc, oracle):
+    # deadlines hours away from `now` leave the 32-bit fast-path window: the exact 64-bit path
+    # must take over for those tasks (mixed with in-window segments)
+    rng = np.random.default_rng(21)
+    for pol in ("EDF_LAXITY", "SJF"):
+        cfg = P.config(flg=P.flags(policy=pol, drop=1))
+        ins = H.random_step_inputs(rng, 6, 0, cfg, qs=[300, 5000, 40000, 7, 0, 20000])
+        ins["deadline_us"][:300] += 10 ** 12
+        ins["deadline_us"][5300:5400] -= 5 * 10 ** 10
+        compare(run_gpu(asc, cfg, ins), oracle.schedule_step(cfg, **ins), ins["seg_off"])
