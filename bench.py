@@ -178,6 +178,7 @@ def step_microbench(asc, torch, dev, stream, warmup, steps, hbm_peak):
     S, Qs = 4096, 10_000
     ins = H.random_step_inputs(rng, S, 0, cfg, qs=np.full(S, Qs))
     dins = {k: torch.from_numpy(np.ascontiguousarray(v)).to(dev) for k, v in ins.items()}
+    dins["Q"] = S * Qs
     ctx = asc.Context(cfg, dev.index, stream)
     Q = S * Qs
     out = None
@@ -315,7 +316,7 @@ def e2e(asc, torch, ctx, batch, world, steps, dev):
     def pinned(x):
         t = torch.from_numpy(np.ascontiguousarray(x)).pin_memory()
         return t.numpy()
-    tr = {k: pinned(v) for k, v in asc.batch_arrays(batch).items()}
+    tr = {k: (pinned(v) if k != "R" else v) for k, v in asc.batch_arrays(batch).items()}
     R, T = batch.R, batch.T
     out = {k: pinned(np.zeros(max(n, 1), dt)) for k, (n, dt) in dict(
         first_token_us=(R, np.int64), done_us=(R, np.int64), prefill_start_us=(R, np.int64),

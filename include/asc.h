@@ -120,6 +120,8 @@ int32_t asc_abi_version(void);
  * ------------------------------------------------------------------------------------------- */
 typedef struct {
   int32_t S;
+  int64_t Q;                     /* total entries = seg_off[S]; -1: the library reads it (one
+                                    device->host copy of 8 bytes for device arrays) */
   const int64_t* seg_off;        /* [S+1] */
   const int64_t* now_us;         /* [S] */
   const int64_t* deadline_us;    /* [Q] arrival + TTFT SLO */
@@ -165,6 +167,7 @@ asc_status asc_schedule_step(asc_ctx* ctx, const asc_step_in* in, asc_step_out* 
  * ------------------------------------------------------------------------------------------- */
 typedef struct {
   int32_t T;
+  int64_t R;                       /* total requests = trace_off[T]; -1: the library reads it */
   const int64_t* trace_off;        /* [T+1] */
   const int64_t* arrival_us;       /* [R] */
   const int32_t* prompt_len;       /* [R] */

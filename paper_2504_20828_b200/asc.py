@@ -57,7 +57,7 @@ _P = C.c_void_p
 
 
 class asc_step_in(C.Structure):
-    _fields_ = [("S", C.c_int32)] + [(k, _P) for k in (
+    _fields_ = [("S", C.c_int32), ("Q", C.c_int64)] + [(k, _P) for k in (
         "seg_off", "now_us", "deadline_us", "eff_prompt", "flags", "dec_count", "dec_ctx_sum",
         "tbt_slo_us", "budget_tokens", "budget_blocks", "budget_reqs")]
 
@@ -68,7 +68,7 @@ class asc_step_out(C.Structure):
 
 
 class asc_traces(C.Structure):
-    _fields_ = [("T", C.c_int32)] + [(k, _P) for k in (
+    _fields_ = [("T", C.c_int32), ("R", C.c_int64)] + [(k, _P) for k in (
         "trace_off", "arrival_us", "prompt_len", "output_len", "ttft_slo_us", "tbt_slo_us",
         "req_ttft_slo_us")]
 
@@ -161,9 +161,10 @@ def asc_last_kernel_ms(ctx):
 
 def asc_schedule_step(ctx, seg_off, now_us, deadline_us, eff_prompt, flags, dec_count, dec_ctx_sum,
                       tbt_slo_us, budget_tokens, budget_blocks, budget_reqs, admit_idx, admit_cnt,
-                      offload_idx, offload_cnt, drop_idx, drop_cnt, batch_lat_us, prefill_us=None):
+                      offload_idx, offload_cnt, drop_idx, drop_cnt, batch_lat_us, prefill_us=None,
+                      Q=-1):
     S = len(seg_off) - 1
-    i = asc_step_in(S, *[_ptr(x) for x in (seg_off, now_us, deadline_us, eff_prompt, flags,
+    i = asc_step_in(S, Q, *[_ptr(x) for x in (seg_off, now_us, deadline_us, eff_prompt, flags,
                                            dec_count, dec_ctx_sum, tbt_slo_us, budget_tokens,
                                            budget_blocks, budget_reqs)])
     o = asc_step_out(*[_ptr(x) for x in (admit_idx, admit_cnt, offload_idx, offload_cnt, drop_idx,
@@ -173,9 +174,9 @@ def asc_schedule_step(ctx, seg_off, now_us, deadline_us, eff_prompt, flags, dec_
 
 def asc_simulate_batch(ctx, trace_off, arrival_us, prompt_len, output_len, ttft_slo_us, tbt_slo_us,
                        first_token_us, done_us, prefill_start_us, status, digest, decisions=None,
-                       evaluations=None, req_ttft_slo_us=None):
+                       evaluations=None, req_ttft_slo_us=None, R=-1):
     T = len(trace_off) - 1
-    tr = asc_traces(T, *[_ptr(x) for x in (trace_off, arrival_us, prompt_len, output_len,
+    tr = asc_traces(T, R, *[_ptr(x) for x in (trace_off, arrival_us, prompt_len, output_len,
                                            ttft_slo_us, tbt_slo_us, req_ttft_slo_us)])
     oc = asc_outcomes(*[_ptr(x) for x in (first_token_us, done_us, prefill_start_us, status,
                                           digest, decisions, evaluations)])
@@ -183,9 +184,9 @@ def asc_simulate_batch(ctx, trace_off, arrival_us, prompt_len, output_len, ttft_
 
 
 def asc_goodput(ctx, trace_off, arrival_us, output_len, ttft_slo_us, tbt_slo_us, first_token_us,
-                done_us, status, good, total, req_ttft_slo_us=None):
+                done_us, status, good, total, req_ttft_slo_us=None, R=-1):
     T = len(trace_off) - 1
-    tr = asc_traces(T, _ptr(trace_off), _ptr(arrival_us), None, _ptr(output_len), _ptr(ttft_slo_us),
+    tr = asc_traces(T, R, _ptr(trace_off), _ptr(arrival_us), None, _ptr(output_len), _ptr(ttft_slo_us),
                     _ptr(tbt_slo_us), _ptr(req_ttft_slo_us))
     oc = asc_outcomes(_ptr(first_token_us), _ptr(done_us), None, _ptr(status), None, None, None)
     _check(ctx, lib().asc_goodput(ctx, C.byref(tr), C.byref(oc), _ptr(good), _ptr(total)),
@@ -222,7 +223,7 @@ class Context:
         """ins: dict of arrays (all torch CUDA or all numpy).  Returns dict of outputs."""
         dev = not isinstance(ins["seg_off"], np.ndarray)
         S = len(ins["seg_off"]) - 1
-        Q = int(ins["seg_off"][-1])
+        Q = int(ins["Q"]) if "Q" in ins else int(ins["seg_off"][-1])
         out = _alloc(dev, self.device, dict(admit_idx=(Q, "i4"), admit_cnt=(S, "i4"),
                                             offload_idx=(Q, "i4"), offload_cnt=(S, "i4"),
                                             drop_idx=(Q, "i4"), drop_cnt=(S, "i4"),
@@ -235,14 +236,14 @@ class Context:
                           ins["tbt_slo_us"], ins["budget_tokens"], ins["budget_blocks"],
                           ins["budget_reqs"], out["admit_idx"], out["admit_cnt"],
                           out["offload_idx"], out["offload_cnt"], out["drop_idx"],
-                          out["drop_cnt"], out["batch_lat_us"], out["prefill_us"])
+                          out["drop_cnt"], out["batch_lat_us"], out["prefill_us"], Q=Q)
         return out
 
     def simulate_batch(self, tr, req_ttft_slo_us=None, out=None):
         """tr: dict trace_off, arrival_us, prompt_len, output_len, ttft_slo_us, tbt_slo_us."""
         dev = not isinstance(tr["trace_off"], np.ndarray)
         T = len(tr["trace_off"]) - 1
-        R = int(tr["trace_off"][-1])
+        R = int(tr["R"]) if "R" in tr else int(tr["trace_off"][-1])
         if out is None:
             out = _alloc(dev, self.device, dict(first_token_us=(R, "i8"), done_us=(R, "i8"),
                                                 prefill_start_us=(R, "i8"), status=(R, "u4"),
@@ -252,7 +253,7 @@ class Context:
                            tr["output_len"], tr["ttft_slo_us"], tr["tbt_slo_us"],
                            out["first_token_us"], out["done_us"], out["prefill_start_us"],
                            out["status"], out["digest"], out["decisions"], out["evaluations"],
-                           req_ttft_slo_us)
+                           req_ttft_slo_us, R=R)
         return out
 
     def goodput(self, tr, out, req_ttft_slo_us=None, res=None):
@@ -262,7 +263,7 @@ class Context:
             res = _alloc(dev, self.device, dict(good=(T, "u8"), total=(T, "u8")))
         asc_goodput(self.h, tr["trace_off"], tr["arrival_us"], tr["output_len"], tr["ttft_slo_us"],
                     tr["tbt_slo_us"], out["first_token_us"], out["done_us"], out["status"],
-                    res["good"], res["total"], req_ttft_slo_us)
+                    res["good"], res["total"], req_ttft_slo_us, R=int(tr["R"]) if "R" in tr else -1)
         return res["good"], res["total"]
 
 
@@ -281,7 +282,11 @@ def batch_arrays(batch, device=None):
              output_len=batch.output_len, ttft_slo_us=batch.ttft_slo_us, tbt_slo_us=batch.tbt_slo_us)
     # zero-length arrays would marshal as NULL: pad to one (never read) element
     d = {k: np.ascontiguousarray(v if len(v) else np.zeros(1, v.dtype)) for k, v in d.items()}
+    R = int(batch.trace_off[-1])
     if device is None:
+        d["R"] = R
         return d
     import torch
-    return {k: torch.from_numpy(v).to(device) for k, v in d.items()}
+    d = {k: torch.from_numpy(v).to(device) for k, v in d.items()}
+    d["R"] = R  # host-known total so the library needs no device->host read
+    return d

@@ -50,13 +50,12 @@ static asc_status ensure_stage(asc_ctx* c, size_t bytes) {
 }
 
 asc_status collect_errors(asc_ctx* c, const char* where) {
+  cudaMemcpyAsync(c->h_err, c->d_err, sizeof(int), cudaMemcpyDeviceToHost, c->stream);
+  cudaMemsetAsync(c->d_err, 0, sizeof(int), c->stream);
   cudaError_t e = cudaStreamSynchronize(c->stream);
   if (e != cudaSuccess) return cuda_check(c, e, where);
-  int bits = 0;
-  e = cudaMemcpy(&bits, c->d_err, sizeof(int), cudaMemcpyDeviceToHost);
-  if (e != cudaSuccess) return cuda_check(c, e, where);
+  const int bits = *c->h_err;
   if (!bits) return ASC_OK;
-  cudaMemset(c->d_err, 0, sizeof(int));
   std::string w(where);
   if (bits & 8) return fail(c, ASC_E_CONFIG, w + ": request violates liveness validation (prompt_len, output_len >= 1; prompt+output <= lp_token_budget; ceil((prompt+output)/block_tokens) < kv_blocks)");
   if (bits & ERR_INVAL) return fail(c, ASC_E_INVAL, w + ": invalid input (eff_prompt < 1, seg_off decreasing, or arrivals not sorted within a trace)");
@@ -159,6 +158,7 @@ asc_status asc_create(const asc_config* cfg, int device, void* cuda_stream, asc_
   c->pt_size = pt + 1;
   int64_t* d_w = nullptr;
   if (cudaMalloc(&c->d_err, sizeof(int)) != cudaSuccess ||
+      cudaMallocHost(&c->h_err, sizeof(int)) != cudaSuccess ||
       cudaMalloc(&c->d_pf_tab, sizeof(int64_t) * c->pt_size) != cudaSuccess ||
       cudaMalloc(&c->d_pf_tab32_mem, sizeof(int32_t) * c->pt_size) != cudaSuccess ||
       cudaMalloc(&d_w, 2 * sizeof(int64_t)) != cudaSuccess) {
@@ -191,6 +191,7 @@ asc_status asc_create(const asc_config* cfg, int device, void* cuda_stream, asc_
 void asc_destroy(asc_ctx* ctx) {
   if (!ctx) return;
   if (ctx->d_err) cudaFree(ctx->d_err);
+  if (ctx->h_err) cudaFreeHost(ctx->h_err);
   if (ctx->d_pf_tab) cudaFree(ctx->d_pf_tab);
   if (ctx->d_pf_tab32_mem) cudaFree(ctx->d_pf_tab32_mem);
   if (ctx->ws) cudaFree(ctx->ws);
@@ -275,11 +276,14 @@ asc_status asc_schedule_step(asc_ctx* c, const asc_step_in* in, asc_step_out* ou
                         out->prefill_us}))
     return fail(c, ASC_E_INVAL, "asc_schedule_step: host and device pointers mixed");
   const int32_t S = in->S;
-  int64_t Q = 0;
+  int64_t Q = in->Q;
   if (kind == 1) {
-    cudaError_t e = cudaMemcpy(&Q, in->seg_off + S, sizeof(int64_t), cudaMemcpyDeviceToHost);
-    if (e != cudaSuccess) return cuda_check(c, e, "asc_schedule_step: read seg_off[S]");
+    if (Q < 0) {
+      cudaError_t e = cudaMemcpy(&Q, in->seg_off + S, sizeof(int64_t), cudaMemcpyDeviceToHost);
+      if (e != cudaSuccess) return cuda_check(c, e, "asc_schedule_step: read seg_off[S]");
+    }
   } else {
+    if (Q >= 0 && Q != in->seg_off[S]) return fail(c, ASC_E_INVAL, "asc_schedule_step: Q != seg_off[S]");
     Q = in->seg_off[S];
     for (int32_t s = 0; s < S; s++)
       if (in->seg_off[s + 1] < in->seg_off[s]) return fail(c, ASC_E_INVAL, "asc_schedule_step: seg_off decreasing");
@@ -344,11 +348,14 @@ asc_status asc_simulate_batch(asc_ctx* c, const asc_traces* tr, asc_outcomes* ou
                         out->evaluations}))
     return fail(c, ASC_E_INVAL, "asc_simulate_batch: host and device pointers mixed");
   const int32_t T = tr->T;
-  int64_t R = 0;
+  int64_t R = tr->R;
   if (kind == 1) {
-    cudaError_t e = cudaMemcpy(&R, tr->trace_off + T, sizeof(int64_t), cudaMemcpyDeviceToHost);
-    if (e != cudaSuccess) return cuda_check(c, e, "asc_simulate_batch: read trace_off[T]");
+    if (R < 0) {
+      cudaError_t e = cudaMemcpy(&R, tr->trace_off + T, sizeof(int64_t), cudaMemcpyDeviceToHost);
+      if (e != cudaSuccess) return cuda_check(c, e, "asc_simulate_batch: read trace_off[T]");
+    }
   } else {
+    if (R >= 0 && R != tr->trace_off[T]) return fail(c, ASC_E_INVAL, "asc_simulate_batch: R != trace_off[T]");
     R = tr->trace_off[T];
     for (int32_t t = 0; t < T; t++)
       if (tr->trace_off[t + 1] < tr->trace_off[t]) return fail(c, ASC_E_INVAL, "asc_simulate_batch: trace_off decreasing");

@@ -18,6 +18,7 @@ struct asc_ctx {
   int32_t* d_pf_tab32_mem = nullptr;
   int64_t w_hp = 0;        // worst-case HP batch latency (G24)
   int* d_err = nullptr;    // device error bits (asc::ERR_*)
+  int* h_err = nullptr;    // pinned host copy of the error bits (one sync per call)
   char* ws = nullptr;      // device workspace
   size_t ws_cap = 0;
   char* stage = nullptr;   // device staging for host-pointer calls

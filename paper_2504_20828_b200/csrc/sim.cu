@@ -943,6 +943,7 @@ size_t sim_smem_per_warp(int K) {
 
 // liveness / layout validation (ASC_E_CONFIG / ASC_E_INVAL before simulating)
 __global__ void validate_traces(SimP P, int64_t R) {
+  if (blockIdx.x == 0 && threadIdx.x == 0 && P.off[P.T] != R) atomicOr(P.err, ERR_INVAL);
   for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < R;
        g += (int64_t)gridDim.x * blockDim.x) {
     const int32_t p = P.pl[g], o = P.ol[g];

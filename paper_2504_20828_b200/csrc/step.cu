@@ -35,6 +35,7 @@ constexpr int SCAN_TILE = SCAN_ITEMS * SCAN_THREADS;
 
 struct StepP {
   Model md;
+  int64_t ntask_max, max_mt;  // workspace capacities (guards against an inconsistent Q)
   const int64_t* pf_tab;
   const int32_t* pf_tab32;  // int32 copy when every entry fits (else nullptr)
   int32_t pt, bs, drop, offl, kdl, kpf;
@@ -73,7 +74,12 @@ __device__ __forceinline__ int64_t pf_of(const StepP& P, int32_t p) {
 __global__ void plan_counts(StepP P) {
   const int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (s > P.S) return;
-  if (s == P.S) { P.task_off[s] = 0; P.mtask_off[s] = 0; return; }
+  if (s == P.S) {
+    if (P.seg_off[P.S] != P.Q) atomicOr(P.err, ERR_INVAL);
+    P.task_off[s] = 0;
+    P.mtask_off[s] = 0;
+    return;
+  }
   const int64_t len = P.seg_off[s + 1] - P.seg_off[s];
   if (len < 0) atomicOr(P.err, ERR_INVAL);
   const int64_t nt = len <= CH ? 1 : (len + CH - 1) / CH;
@@ -136,7 +142,55 @@ __global__ void scan_add(StepP P, int64_t n, const int64_t* tmp) {
 __global__ void fill_task_seg(StepP P) {
   for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < P.S;
        s += (int64_t)gridDim.x * blockDim.x) {
-    for (int64_t t = P.task_off[s]; t < P.task_off[s + 1]; t++) P.task_seg[t] = (int32_t)s;
+    for (int64_t t = P.task_off[s]; t < P.task_off[s + 1] && t < P.ntask_max; t++)
+      P.task_seg[t] = (int32_t)s;
+  }
+}
+
+// single-CTA planner for S < SCAN_TILE: counts, both exclusive scans and the task map in one launch
+__global__ void __launch_bounds__(SCAN_THREADS) plan_small(StepP P) {
+  __shared__ int64_t sa[SCAN_THREADS / 32], sb[SCAN_THREADS / 32];
+  const int64_t n = (int64_t)P.S + 1;
+  const int64_t base = threadIdx.x * SCAN_ITEMS;
+  int64_t va[SCAN_ITEMS], vb[SCAN_ITEMS], ta = 0, tb = 0;
+#pragma unroll
+  for (int i = 0; i < SCAN_ITEMS; i++) {
+    const int64_t s = base + i;
+    int64_t nt = 0;
+    if (s < P.S) {
+      const int64_t len = P.seg_off[s + 1] - P.seg_off[s];
+      if (len < 0) atomicOr(P.err, ERR_INVAL);
+      nt = len <= CH ? 1 : (len + CH - 1) / CH;
+    } else if (s == P.S && P.seg_off[P.S] != P.Q) {
+      atomicOr(P.err, ERR_INVAL);
+    }
+    va[i] = nt;
+    vb[i] = nt > 1 ? nt : 0;
+    ta += va[i];
+    tb += vb[i];
+  }
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  const int64_t ia = warp_incl_scan(ta), ib = warp_incl_scan(tb);
+  if (l == 31) { sa[w] = ia; sb[w] = ib; }
+  __syncthreads();
+  if (w == 0) {
+    const int64_t x = sa[l], y = sb[l];
+    const int64_t xi = warp_incl_scan(x), yi = warp_incl_scan(y);
+    sa[l] = xi - x;
+    sb[l] = yi - y;
+  }
+  __syncthreads();
+  int64_t ea = sa[w] + ia - ta, eb = sb[w] + ib - tb;
+#pragma unroll
+  for (int i = 0; i < SCAN_ITEMS; i++) {
+    const int64_t s = base + i;
+    if (s < n) {
+      P.task_off[s] = ea;
+      P.mtask_off[s] = eb;
+      for (int64_t t = ea; t < ea + va[i] && t < P.ntask_max; t++) P.task_seg[t] = (int32_t)s;
+    }
+    ea += va[i];
+    eb += vb[i];
   }
 }
 
@@ -402,7 +456,7 @@ __global__ void __launch_bounds__(K1W * 32, 3) k1_tasks(const __grid_constant__ 
   auto& s_drop = *reinterpret_cast<uint32_t(*)[K1W][MW]>(k1_smem + sizeof(Stage) * K1W * NST +
                                                           sizeof(KI) * K1W * 160 + 4 * K1W * MW);
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t ntasks = P.task_off[P.S];
+  const int64_t ntasks = min(P.task_off[P.S], P.ntask_max);
   for (int64_t task = blockIdx.x * (int64_t)K1W + w; task < ntasks;
        task += (int64_t)gridDim.x * K1W) {
     TaskCtx t;
@@ -438,7 +492,12 @@ __global__ void __launch_bounds__(K1W * 32, 3) k1_tasks(const __grid_constant__ 
       const int64_t kbase = P.kdl ? t.now : 0;  // key = kbase + key32
       TopKPk<KPL> st;
       st.init(reinterpret_cast<uint64_t*>(sbuf[w]), t.kpos);
-      bool bad = false, inwin = true;
+      bool inwin = true;  // any entry outside the 32-bit window (or the table) -> generic path
+      const uint32_t vspan = (uint32_t)(t.vhi - t.vlo);
+      const uint32_t tab_hi = (uint32_t)(P.pt - 1);
+      const int32_t* __restrict__ tab32 = P.pf_tab32;
+      const bool has_pfout = P.pfout != nullptr;
+      const int kdl = P.kdl, kpf = P.kpf;
 #pragma unroll
       for (int q = 0; q < NST - 1; q++) {
         if (VEC && q < ng) stage_issue(P, s_stage[w][q], b4 + (int64_t)q * GE + 4 * lane);
@@ -461,24 +520,15 @@ __global__ void __launch_bounds__(K1W * 32, 3) k1_tasks(const __grid_constant__ 
         bool cnd[4];
         uint32_t mo_w = 0, md_w = 0;
 #pragma unroll
-        for (int u = 0; u < 4; u++) {
-          const bool v = r0 + u >= t.vlo && r0 + u < t.vhi;
+        for (int u = 0; u < 4; u++) {  // branch-free: every lane runs the same instructions
+          const bool v = (uint32_t)(r0 + u - t.vlo) < vspan;
           const uint32_t f = (cur.f4 >> (8 * u)) & 0xffu;
           const int32_t pu = cur.p[u];
+          const bool inrange = (uint32_t)(pu - 1) < tab_hi;  // 1 <= pu < pt
+          const int32_t pf = __ldg(tab32 + (inrange ? pu : 1));
           const int64_t d = cur.dl[u] - t.now;
-          int32_t pf = 0;
-          if (v) {
-            if (pu >= 1 && pu < P.pt) {
-              pf = __ldg(P.pf_tab32 + pu);
-            } else {
-              bad |= pu < 1;
-              const int64_t q = pf_slow(P, pu < 1 ? 1 : pu);
-              inwin &= q < WIN;
-              pf = (int32_t)min(q, (int64_t)INT32_MAX);
-            }
-            inwin &= (uint64_t)(d + WIN) < (uint64_t)(2 * WIN) && pf < (int32_t)WIN;
-          }
-          if (P.pfout && v) __stcs(P.pfout + e0 + u, pf);
+          inwin &= !v || (inrange && (uint64_t)(d + WIN) < (uint64_t)(2 * WIN) && pf < (int32_t)WIN);
+          if (has_pfout && v) __stcs(P.pfout + e0 + u, pf);
           const int32_t d32 = (int32_t)d;
           const bool dropped = DROP && v && !(f & 1u) && d32 < 0;
           const bool off = OFFL && v && !dropped && !(f & 3u) && d32 - pf <= othr32;
@@ -490,7 +540,7 @@ __global__ void __launch_bounds__(K1W * 32, 3) k1_tasks(const __grid_constant__ 
             const uint32_t mo = __ballot_sync(FULL, off);
             mo_w = lane == u ? mo : mo_w;
           }
-          const int32_t key32 = (P.kdl ? d32 : 0) + (P.kpf > 0 ? pf : (P.kpf < 0 ? -pf : 0));
+          const int32_t key32 = (kdl ? d32 : 0) + (kpf > 0 ? pf : (kpf < 0 ? -pf : 0));
           x[u] = ((uint64_t)((uint32_t)key32 ^ 0x80000000u) << 32) | (uint64_t)(l0 + u);
           cnd[u] = select && v && !dropped && x[u] < st.thr;
         }
@@ -506,7 +556,6 @@ __global__ void __launch_bounds__(K1W * 32, 3) k1_tasks(const __grid_constant__ 
       }
       cp_wait<0>();
       __syncwarp();
-      if (__any_sync(FULL, bad) && lane == 0) atomicOr(P.err, ERR_INVAL);
       fast_ok = __all_sync(FULL, inwin);
       if (fast_ok) {
         if (select) st.finish();
@@ -539,6 +588,7 @@ __global__ void __launch_bounds__(K1W * 32, 3) k1_tasks(const __grid_constant__ 
       if (lane == 0) { P.off_cnt[s] = (int32_t)(no - lo); P.drop_cnt[s] = (int32_t)(nd - lo); }
     } else {
       const int64_t mt = P.mtask_off[s] + c;
+      if (mt >= P.max_mt) continue;
       KI* cd = P.cand + mt * (32 * KPL);
 #pragma unroll
       for (int r = 0; r < KPL; r++) cd[r * 32 + lane] = top[r];
@@ -566,6 +616,7 @@ __global__ void __launch_bounds__(WARPS * 32) k2_segments(const __grid_constant_
     const int64_t nt = P.task_off[s + 1] - P.task_off[s];
     if (nt <= 1) continue;
     const int64_t m0 = P.mtask_off[s];
+    if (m0 + nt > P.max_mt) continue;
     const int64_t lo = P.seg_off[s];
     WarpTopK<KPL> A;
     A.init();
@@ -625,7 +676,7 @@ __global__ void __launch_bounds__(WARPS * 32) k2_segments(const __grid_constant_
 
 __global__ void __launch_bounds__(WARPS * 32) k3_expand(const __grid_constant__ StepP P) {
   const int w = threadIdx.x >> 5;
-  const int64_t ntasks = P.task_off[P.S];
+  const int64_t ntasks = min(P.task_off[P.S], P.ntask_max);
   for (int64_t task = blockIdx.x * (int64_t)WARPS + w; task < ntasks;
        task += (int64_t)gridDim.x * WARPS) {
     const int64_t s = P.task_seg[task];
@@ -633,6 +684,7 @@ __global__ void __launch_bounds__(WARPS * 32) k3_expand(const __grid_constant__ 
     if (nt <= 1) continue;
     const int64_t c = task - P.task_off[s];
     const int64_t mt = P.mtask_off[s] + c;
+    if (mt >= P.max_mt) continue;
     const int64_t lo = P.seg_off[s], hi = P.seg_off[s + 1];
     const int64_t b = lo + c * CH;
     const int64_t e_end = min(hi, b + CH);
@@ -689,6 +741,8 @@ asc_status launch_schedule_step(asc_ctx* c, const asc_step_in* in, asc_step_out*
   Arena ar{c->ws, c->ws_cap};
   StepP P;
   P.md = c->md;
+  P.ntask_max = ntask_max;
+  P.max_mt = max_mt;
   P.pf_tab = c->d_pf_tab;
   P.pf_tab32 = c->d_pf_tab32;
   P.pt = c->pt_size;
@@ -727,13 +781,18 @@ asc_status launch_schedule_step(asc_ctx* c, const asc_step_in* in, asc_step_out*
   int64_t launches = 0;
   int dev_sms = 148;
   cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, c->device);
-  plan_counts<<<(S + 1 + 255) / 256, 256, 0, sm>>>(P);
-  scan_tiles<<<ntile, SCAN_THREADS, 0, sm>>>(P.task_off, P.mtask_off, S + 1, P.scan_tmp);
-  scan_totals<<<1, 32, 0, sm>>>(P.scan_tmp, ntile);
-  scan_add<<<(S + 1 + 255) / 256, 256, 0, sm>>>(P, S + 1, P.scan_tmp);
-  const int64_t gf = (S + 255) / 256;
-  fill_task_seg<<<(unsigned)(gf < 4 * dev_sms ? (gf > 0 ? gf : 1) : 4 * dev_sms), 256, 0, sm>>>(P);
-  launches += 5;
+  if (S + 1 <= SCAN_TILE) {
+    plan_small<<<1, SCAN_THREADS, 0, sm>>>(P);
+    launches += 1;
+  } else {
+    plan_counts<<<(S + 1 + 255) / 256, 256, 0, sm>>>(P);
+    scan_tiles<<<ntile, SCAN_THREADS, 0, sm>>>(P.task_off, P.mtask_off, S + 1, P.scan_tmp);
+    scan_totals<<<1, 32, 0, sm>>>(P.scan_tmp, ntile);
+    scan_add<<<(S + 1 + 255) / 256, 256, 0, sm>>>(P, S + 1, P.scan_tmp);
+    const int64_t gf = (S + 255) / 256;
+    fill_task_seg<<<(unsigned)(gf < 4 * dev_sms ? (gf > 0 ? gf : 1) : 4 * dev_sms), 256, 0, sm>>>(P);
+    launches += 5;
+  }
   int64_t g1 = (ntask_max + K1W - 1) / K1W;
   g1 = g1 < (int64_t)dev_sms * 3 ? g1 : (int64_t)dev_sms * 3;
   const bool vec = ((uintptr_t)in->deadline_us % 16 == 0) && ((uintptr_t)in->eff_prompt % 16 == 0) &&

@@ -12,6 +12,7 @@ for S, Q in ((4096, 10000), (64, 1000000), (1000000, 32)):
     cfg = P.config()
     ins = H.random_step_inputs(rng, S, 0, cfg, qs=np.full(S, Q))
     d = {k: torch.from_numpy(np.ascontiguousarray(v)).cuda() for k, v in ins.items()}
+    d["Q"] = S * Q
     ctx = asc.Context(cfg, 0)
     for _ in range(3):
         out = ctx.schedule_step(d, want_prefill=False)
