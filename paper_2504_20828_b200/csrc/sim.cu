@@ -810,6 +810,95 @@ __device__ __noinline__ void deliver(const SimP& P, Wp w, int64_t T) {
   }
 }
 
+// ---------------------------------------------------------------------- phase F: decode runs --
+// Between external events (the next arrival; for an HP also any LP formation that could offload
+// and any in-flight delivery) an instance whose queue is empty and whose running batch is a pure
+// decode batch evolves on its own: its next steps are decode-only batches of the same B_d
+// requests until the first completion (event min(rem) - 1) or the first step whose block growth
+// would not fit (eviction).  Those steps are evaluated 32 at a time, one per lane: block growth
+// from a histogram of l̂ mod bs, Σl̂ in closed form, latencies in parallel (Eq. 4-5), start times by
+// a prefix sum, and the per-instance digest chain applied in order.  Exactly the same formations,
+// times and digest as stepping them one by one through the event loop.
+__device__ __noinline__ int64_t run_decode(const SimP& P, Wp w, int k, int64_t T_limit) {
+  SInst& I = w.SI[k];
+  const int lane = lane_id();
+  const int32_t Bd = I.ds_len;
+  const int32_t bs = P.bs;
+  if (Bd == 0 || bs > 256 || !I.papp) return 0;
+  int32_t* hist = reinterpret_cast<int32_t*>(w.buf);  // 256 ints of per-warp scratch
+  for (int i = lane; i < bs; i += 32) hist[i] = 0;
+  __syncwarp();
+  int32_t mrem = INT32_MAX;
+  for (int32_t c = 0; c < Bd; c += 32) {
+    const int32_t j = c + lane;
+    if (j < Bd) {
+      const int4 s = *slotp(P, w, k, j);
+      mrem = min(mrem, s.z);
+      atomicAdd(&hist[(s.w >> R_SHIFT) & 0x1ff], 1);
+    }
+  }
+  mrem = warp_min(mrem);
+  __syncwarp();
+  const int64_t Jmax = (int64_t)mrem - 1;  // events before the first completion
+  if (Jmax <= 0) return 0;
+  const int64_t E = I.end, S0 = I.ctx_sum;
+  const int32_t kvf0 = I.kv_free;
+  uint64_t h = I.hash;
+  const uint64_t cpart = mix64((uint64_t)k + 2 * GOLD) + mix64(3 * GOLD) + mix64((uint64_t)Bd + 4 * GOLD) +
+                         mix64(5 * GOLD) + mix64(6 * GOLD) + mix64(7 * GOLD);
+  int64_t J = 0, tcarry = 0, ncarry = 0;
+  while (true) {
+    const int64_t c = J + lane;
+    const int32_t cm = (int32_t)(c % bs);
+    const int64_t need = hist[cm == 0 ? 0 : bs - cm];  // slots with (r0 + c) mod bs == 0
+    const int64_t cum = ncarry + warp_incl_scan(need);
+    const int64_t lc = lat_decode(P.md, (uint64_t)Bd, (uint64_t)(S0 + (c + 1) * Bd));
+    const int64_t incl = warp_incl_scan(lc < 0 ? (int64_t)0 : lc);
+    const int64_t tc = E + tcarry + incl - (lc < 0 ? 0 : lc);  // start (formation) time of event c
+    const bool ok = c < Jmax && tc < T_limit && cum <= kvf0 && lc > 0;
+    const uint32_t m = __ballot_sync(FULL, ok);
+    const int n = (m == FULL) ? 32 : (__ffs(~m) - 1);
+    const uint64_t rec = cpart + mix64((uint64_t)tc + GOLD) + mix64((uint64_t)lc + 8 * GOLD);
+    for (int j = 0; j < n; j++) h = mix64(h ^ __shfl_sync(FULL, rec, j));
+    if (n > 0) {
+      ncarry = __shfl_sync(FULL, cum, n - 1);
+      tcarry = __shfl_sync(FULL, incl, n - 1) + tcarry;
+    }
+    J += n;
+    if (n < 32) break;
+  }
+  if (J == 0) return 0;
+  // apply the J events to every decode slot: l̂ += J, remaining -= J, blocks and residue
+  for (int32_t c = 0; c < Bd; c += 32) {
+    const int32_t j = c + lane;
+    if (j < Bd) {
+      int4 s = *slotp(P, w, k, j);
+      const int32_t r0 = (s.w >> R_SHIFT) & 0x1ff;
+      const int32_t pend0 = (int32_t)((uint32_t)s.w >> 31);
+      const int64_t first = r0 == 0 ? 0 : bs - r0;  // first event index c with (r0 + c) % bs == 0
+      const int64_t last = J - 2;                   // growth applied through event J-2 ...
+      const int32_t grown = last >= first ? (int32_t)(1 + (last - first) / bs) : 0;
+      const int32_t held = (s.w & HELD_MASK) + pend0 + grown;
+      const int32_t rJ = (int32_t)((r0 + J) % bs);
+      const bool pend = ((r0 + J - 1) % bs) == 0;  // ... and left pending by event J-1
+      s.y += (int32_t)J;
+      s.z -= (int32_t)J;
+      s.w = held | (rJ << R_SHIFT) | (pend ? PEND : 0);
+      *slotp(P, w, k, j) = s;
+    }
+  }
+  const int32_t kvf = kvf0 - (int32_t)ncarry;
+  const int64_t cs = S0 + J * Bd, end = E + tcarry;
+  __syncwarp();
+  I.kv_free = kvf;
+  I.ctx_sum = cs;
+  I.end = end;
+  I.hash = h;
+  I.papp = 1;
+  __syncwarp();
+  return J;
+}
+
 __device__ __noinline__ void init_trace(const SimP& P, Wp w, int trace) {
   const int lane = lane_id();
   if (lane == 0) { w.ts->rr_lp = w.ts->rr_hp = w.ts->fl_head = w.ts->fl_tail = 0; }
@@ -930,6 +1019,20 @@ __global__ void __launch_bounds__(SW * 32, 8) sim_kernel(const __grid_constant__
           if (!I.ticket && I.wq_len == 0 && I.tk_live == 0) I.ticket = 1;
         }
         __syncwarp();
+      }
+      // F. decode runs of independent instances up to their next possible interaction
+      int64_t tl_hp = next_arr;
+      if (w.ts->fl_head < w.ts->fl_tail) {
+        const int64_t tf = P.fl_t[w.base + w.ts->fl_head];
+        tl_hp = tf < tl_hp ? tf : tl_hp;
+      }
+      for (int k = 0; k < n_lp; k++)
+        if (w.SI[k].wq_len > 0 && w.SI[k].end < tl_hp) tl_hp = w.SI[k].end;  // may offload
+      for (int k = 0; k < K; k++) {
+        const SInst& I = w.SI[k];
+        const int64_t lim = k < n_lp ? next_arr : tl_hp;
+        if (I.end < lim && I.batch_dec && I.bp_len == 0 && I.wq_len == 0)
+          decisions += run_decode(P, w, k, lim);
       }
     }
     finish_trace(P, w, trace, decisions, evals);
