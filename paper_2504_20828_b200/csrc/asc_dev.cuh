@@ -37,7 +37,9 @@ struct Model {
 };
 
 // Eq. 4-5 + G17/G18 from exact integer F, M (< 2^53): fixed fp64 RN order, ceil to microseconds.
-__device__ __forceinline__ int64_t lat_from_FM(const Model& md, uint64_t F, uint64_t M) {
+// Out of line: the two correctly rounded divisions expand to a long sequence, and one copy keeps
+// the event-loop kernel inside the instruction cache.
+static __device__ __noinline__ int64_t lat_from_FM(const Model& md, uint64_t F, uint64_t M) {
   const double tM = __ddiv_rn(__ull2double_rn(M), md.MH);
   const double tF = __ddiv_rn(__ull2double_rn(F), md.FH);
   const double mx = (tM > tF) ? tM : tF;

@@ -331,6 +331,26 @@ __device__ __forceinline__ void set_batch(const SimP& P, SInst& I, int64_t T, in
   __syncwarp();
 }
 
+// Deep queues (> 32 entries): streaming top-K of the queue (asc_dev.cuh), out of line so the big
+// merge networks stay out of the instruction cache of the common path.
+__device__ __noinline__ void select_deep(const SimP& P, Wp w, int64_t o, int32_t len, int64_t kneed,
+                                         KI* out) {
+  const int lane = lane_id();
+  TopKStream<KPL> st;
+  st.init(w.buf, kneed > 0 ? (int)kneed - 1 : 32 * KPL - 1);
+  for (int32_t c = 0; c < len; c += 32) {
+    const int32_t j = c + lane;
+    const bool v = j < len;
+    KI x = ki_inf();
+    if (v) x = KI{P.wq_key[o + j], P.wq_id[o + j]};
+    st.push(x, v);
+  }
+  st.finish();
+  __syncwarp();
+#pragma unroll
+  for (int r = 0; r < KPL; r++) out[r] = st.top.a[r];
+}
+
 // --------------------------------------------------------------- LP admission (non-empty queue)
 __device__ __noinline__ int lp_admit(const SimP& P, Wp w, int k, int64_t T, int32_t ndrop,
                                      int32_t npre) {
@@ -347,8 +367,12 @@ __device__ __noinline__ int lp_admit(const SimP& P, Wp w, int k, int64_t T, int3
     if (ldec < 0) atomicOr(P.err, ERR_RANGE);
     C = w.tbt - ldec;
   }
-  // Algorithm 1 line 3: the (key, id)-sorted prefix; only the first R <= 128 can be admitted
+  // Algorithm 1 line 3: the (key, id)-sorted prefix; only the first min(R, N-1, M-1) <= 128 can
+  // be admitted (strict budgets, costs >= 1)
   const int32_t len = I.wq_len;
+  int64_t kneed = Rb < 32 * KPL ? Rb : 32 * KPL;
+  kneed = kneed < N - 1 ? kneed : N - 1;
+  kneed = kneed < M - 1 ? kneed : M - 1;
   KI a[KPL];
   if (len <= 32) {
     KI x = ki_inf();
@@ -357,19 +381,7 @@ __device__ __noinline__ int lp_admit(const SimP& P, Wp w, int k, int64_t T, int3
 #pragma unroll
     for (int r = 1; r < KPL; r++) a[r] = ki_inf();
   } else {
-    TopKStream<KPL> st;
-    st.init(w.buf);
-    for (int32_t c = 0; c < len; c += 32) {
-      const int32_t j = c + lane;
-      const bool v = j < len;
-      KI x = ki_inf();
-      if (v) x = KI{P.wq_key[o + j], P.wq_id[o + j]};
-      st.push(x, v);
-    }
-    st.finish();
-    __syncwarp();
-#pragma unroll
-    for (int r = 0; r < KPL; r++) a[r] = st.top.a[r];
+    select_deep(P, w, o, len, kneed, a);
   }
   // lines 5-13 as a strict prefix-sum scan over the sorted candidates
   int32_t nadm = 0;
