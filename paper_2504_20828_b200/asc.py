@@ -11,7 +11,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libasc.so")
+LIB_PATH = os.environ.get("ASC_LIB", os.path.join(_HERE, "libasc.so"))
 _LIB = None
 
 ASC_MAX_BATCH = 128

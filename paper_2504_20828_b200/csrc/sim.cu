@@ -963,7 +963,10 @@ __device__ __noinline__ void finish_trace(const SimP& P, Wp w, int trace, int64_
   __syncwarp();
 }
 
-__global__ void __launch_bounds__(SW * 32, 8) sim_kernel(const __grid_constant__ SimP P) {
+#ifndef ASC_SIM_MINB
+#define ASC_SIM_MINB 8  // CTAs per SM the register budget must allow (8 -> 64 registers/thread)
+#endif
+__global__ void __launch_bounds__(SW * 32, ASC_SIM_MINB) sim_kernel(const __grid_constant__ SimP P) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int wi = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const size_t per_warp = 64 * sizeof(KI) + (size_t)P.K * DCAP * sizeof(int4) +
