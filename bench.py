@@ -41,7 +41,7 @@ def args_():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="asc", choices=["asc", "reference"])
     ap.add_argument("--workload", default="config3")
-    ap.add_argument("--n", type=int, default=None, help="requests per trace override")
+    ap.add_argument("--requests", type=int, default=None, help="requests per trace override")
     ap.add_argument("--traces", type=int, default=None, help="max traces (testing)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-step-bench", action="store_true")
@@ -139,7 +139,7 @@ def reference_arm(a):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    cfg, b, desc = load(a.workload, 0, 1, a.n, a.traces)
+    cfg, b, desc = load(a.workload, 0, 1, a.requests, a.traces)
     from oracle import oracle as O
     cores = os.cpu_count() or 1
     per_step = min(b.T, max(4, cores))
@@ -227,7 +227,7 @@ def main():
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=dev)
     hbm_peak, peak_src = peaks()
-    cfg, batch, desc = load(a.workload, rank, world, a.n, a.traces)
+    cfg, batch, desc = load(a.workload, rank, world, a.requests, a.traces)
     stream = torch.cuda.Stream(device=dev)
     ctx = asc.Context(cfg, local, stream)
     tr = asc.batch_arrays(batch, dev)

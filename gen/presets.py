@@ -73,7 +73,7 @@ def workload(name, n=None, max_traces=None, base_seed=1):
         shape = "sharegpt"
     elif name == "config4":    # 1 trace, LongBench-shaped, deep queues
         cfg = config(topo=topology(lp_token_budget=65536))
-        pts = [(0, 24, 16, 16)]   # QPS 3 (frozen)
+        pts = [(0, 96, 16, 16)]   # QPS 12 = ~2x the oracle-measured 2L1H saturation (frozen)
         n = n or 1_000_000
         shape = "longbench"
     elif name == "config5":    # 64 QPS x 64 scales x 16 seeds = 65536 traces x 100k

@@ -153,8 +153,21 @@ def test_per_request_slo_and_host_path(asc, oracle):
 
 
 def test_longbench_prefix(asc, oracle):
+    # config 4 (QPS 12, ~2x saturation): queues grow past 32 entries -> deep-queue selection
     cfg, b = P.workload("config4", n=3000)
-    assert_parity(oracle, cfg, b, gpu_sim(asc, cfg, b))
+    got = gpu_sim(asc, cfg, b)
+    assert int(got["evaluations"][0]) > 10 * int(got["decisions"][0])  # deep queues exercised
+    assert_parity(oracle, cfg, b, got)
+
+
+@pytest.mark.parametrize("policy", ["EDF_LAXITY", "SJF", "FCFS", "LJF", "EDF_DEADLINE"])
+def test_overloaded_deep_queues(asc, oracle, policy):
+    # heavy overload (QPS 48 on LongBench lengths, drops on/off): queues of hundreds of entries
+    for drop in (0, 1):
+        cfg, _ = P.workload("config4", n=10)
+        cfg["flags"] = P.flags(policy=policy, drop=drop)
+        b = TR.grid_batch([(7, 384, 16, 16), (8, 384, 8, 16)], 1500, "longbench", 2_500_000, 150_000)
+        assert_parity(oracle, cfg, b, gpu_sim(asc, cfg, b))
 
 
 def test_config3_full_scale_sampled(asc, oracle):
