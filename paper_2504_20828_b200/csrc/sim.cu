@@ -388,10 +388,11 @@ __device__ __noinline__ int lp_admit(const SimP& P, Wp w, int k, int64_t T, int3
   uint64_t sp = 0, sp2 = 0, spc = 0;
   int64_t used = 0, ct = 0, cb = 0, cc = 0;
   bool go = true;
-#pragma unroll
+#pragma unroll 1
   for (int r = 0; r < KPL; r++) {
     if (!go) break;
-    const KI e = a[r];
+    KI e = a[0];
+    for (int q = 1; q < KPL; q++) if (q == r) e = a[q];
     const bool valid = e.i != INF32;
     const int64_t g = w.base + (valid ? e.i : 0);
     const int32_t p = valid ? P.rq_eff[g] : 0;
@@ -871,6 +872,7 @@ __device__ __noinline__ int64_t run_decode(const SimP& P, Wp w, int k, int64_t T
     const uint32_t m = __ballot_sync(FULL, ok);
     const int n = (m == FULL) ? 32 : (__ffs(~m) - 1);
     const uint64_t rec = cpart + mix64((uint64_t)tc + GOLD) + mix64((uint64_t)lc + 8 * GOLD);
+#pragma unroll 1
     for (int j = 0; j < n; j++) h = mix64(h ^ __shfl_sync(FULL, rec, j));
     if (n > 0) {
       ncarry = __shfl_sync(FULL, cum, n - 1);

@@ -28,7 +28,7 @@ constexpr int GE = 128;            // entries per warp iteration (4 per lane)
 constexpr int NG = CH / GE + 1;    // groups per task (+1: the task base is rounded down to 4)
 constexpr int MW = 4 * NG;         // mask words per task per mask (word 4g+u, bit l <-> 4l+u)
 constexpr int WARPS = 8;   // k2/k3 CTA size
-constexpr int K1W = 4;     // k1 CTA size (warps); 3 CTAs/SM -> 12 warps
+constexpr int K1W = 4;     // k1 CTA size (warps); 4 CTAs/SM -> 16 warps, 128 registers
 constexpr int SCAN_ITEMS = 4;
 constexpr int SCAN_THREADS = 1024;
 constexpr int SCAN_TILE = SCAN_ITEMS * SCAN_THREADS;
@@ -327,7 +327,13 @@ __device__ __forceinline__ void load_grp(const StepP& P, int64_t e0, Grp& g) {
 // ---- cp.async staging: each lane copies its own 4 entries of a 128-entry group into a per-warp
 // shared-memory ring (deadline 32 B, eff 16 B, flags 4 B per lane); no registers are held for
 // data in flight and no cross-lane synchronisation is needed (a lane reads only what it copied).
-constexpr int NST = 4;  // pipeline stages per warp
+#ifndef ASC_K1_NST
+#define ASC_K1_NST 2
+#endif
+#ifndef ASC_K1_MINB
+#define ASC_K1_MINB 4
+#endif
+constexpr int NST = ASC_K1_NST;  // pipeline stages per warp
 struct Stage {
   longlong2 dl[2 * 32];  // lane l: dl[2l], dl[2l+1]
   int4 eff[32];
@@ -447,7 +453,7 @@ constexpr int64_t WIN = int64_t(1) << 30;  // fast-path window: |deadline - now|
 
 // TAB: 0 = int64 latency table (generic path only), 1 = int32 table (fast path)
 template <bool VEC, int TAB, bool DROP, bool OFFL>
-__global__ void __launch_bounds__(K1W * 32, 3) k1_tasks(const __grid_constant__ StepP P) {
+__global__ void __launch_bounds__(K1W * 32, ASC_K1_MINB) k1_tasks(const __grid_constant__ StepP P) {
   extern __shared__ __align__(16) unsigned char k1_smem[];  // K1_SMEM bytes (dynamic)
   auto& s_stage = *reinterpret_cast<Stage(*)[K1W][NST]>(k1_smem);
   auto& sbuf = *reinterpret_cast<KI(*)[K1W][160]>(k1_smem + sizeof(Stage) * K1W * NST);
@@ -794,7 +800,7 @@ asc_status launch_schedule_step(asc_ctx* c, const asc_step_in* in, asc_step_out*
     launches += 5;
   }
   int64_t g1 = (ntask_max + K1W - 1) / K1W;
-  g1 = g1 < (int64_t)dev_sms * 3 ? g1 : (int64_t)dev_sms * 3;
+  g1 = g1 < (int64_t)dev_sms * ASC_K1_MINB ? g1 : (int64_t)dev_sms * ASC_K1_MINB;
   const bool vec = ((uintptr_t)in->deadline_us % 16 == 0) && ((uintptr_t)in->eff_prompt % 16 == 0) &&
                    ((uintptr_t)in->flags % 4 == 0);
   const unsigned gk = (unsigned)(g1 > 0 ? g1 : 1);
