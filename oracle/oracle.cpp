@@ -306,6 +306,7 @@ struct Inst {
   int tk_live = 0;            // resident ticketed requests (at most one, G29)
   int64_t hist_sum = 0, hist_cnt = 0;
   uint64_t hash = 0;
+  uint64_t nrec = 0;  // recorded formations (digest position)
 };
 
 struct Sim {
@@ -336,12 +337,14 @@ struct Sim {
     h.waiting.push_back(i);
     std::sort(h.waiting.begin(), h.waiting.end(), [&](int x, int y) { return fcfs_less(x, y); });
   }
-  // Digest: the record of one formation hashes as sum_i mix(v_i + (i+1) * G)
-  // (mod 2^64; position-keyed, so order-sensitive), chained per instance by h = mix(h ^ record).
+  // Digest: the record of one formation hashes as rec = sum_i mix(v_i + (i+1) * G)
+  // (mod 2^64; position-keyed, so order-sensitive); the instance digest is the sum over its
+  // recorded formations f = 0, 1, ... of mix(rec_f + (f+1) * G2) (formation-index keyed).
   void record(Inst& in, const std::vector<uint64_t>& v) {
     uint64_t rec = 0;
     for (size_t i = 0; i < v.size(); i++) rec += mix(v[i] + (uint64_t)(i + 1) * 0x9E3779B97F4A7C15ull);
-    in.hash = mix(in.hash ^ rec);
+    in.nrec += 1;
+    in.hash += mix(rec + (uint64_t)in.nrec * 0xD1B54A32D192ED03ull);
   }
   int64_t lat(const std::vector<int>& pre, const std::vector<int>& dec) {
     std::vector<int64_t> p, l;

@@ -27,6 +27,7 @@ constexpr int KPL = 4;
 constexpr int SW = 4;      // warps (traces in flight) per CTA
 constexpr int DCAP = 128;  // decode slots per instance kept in shared memory
 constexpr uint64_t GOLD = 0x9E3779B97F4A7C15ull;
+constexpr uint64_t GOLD2 = 0xD1B54A32D192ED03ull;  // formation-index key of the instance digest
 
 enum : uint32_t { F_EVER = 1u, F_ONHP = 2u, F_TICK = 4u, F_OFFL = 8u };
 constexpr uint32_t ST_SHIFT = 4, INST_SHIFT = 8, NPRE_SHIFT = 16;
@@ -38,7 +39,7 @@ constexpr int32_t PEND = (int32_t)0x80000000;
 struct SInst {
   int64_t end;               // end of the running batch, INF64 when idle
   int64_t hist_sum, ctx_sum;
-  uint64_t hash;
+  uint64_t hash, nrec;       // instance digest and number of recorded formations
   int32_t kv_free, kv_total, wq_len, ds_len, bp_len, hist_cnt, need_sum;
   int32_t batch_dec, ticket, tk_live, hp, papp;
 };
@@ -148,14 +149,18 @@ __device__ __noinline__ void digest_log(const SimP& P, Wp w, int k, int64_t T, i
   for (int32_t j = lane; j < npre; j += 32)
     acc += mix64((uint64_t)P.scr_pre[w.base + j] + (uint64_t)(7 + nadm + noff + ndrop + j + 1) * GOLD);
   acc = warp_sum(acc);
-  const uint64_t h = mix64(w.SI[k].hash ^ acc);
+  const uint64_t nr = w.SI[k].nrec + 1;
+  const uint64_t h = w.SI[k].hash + mix64(acc + nr * GOLD2);
   __syncwarp();
-  w.SI[k].hash = h;  // uniform value, every lane stores the same word
+  w.SI[k].hash = h;  // uniform values, every lane stores the same words
+  w.SI[k].nrec = nr;
   __syncwarp();
 }
 
-// the pure-decode record (T, k, 0, B_d, 0, 0, 0, lat): 8 lanes, 3 shuffle steps
-__device__ __forceinline__ uint64_t digest_decode(uint64_t h, int k, int64_t T, int64_t bd, int64_t lat) {
+// the pure-decode record (T, k, 0, B_d, 0, 0, 0, lat): 8 lanes, 3 shuffle steps; nr = its
+// formation index (1-based) on the instance
+__device__ __forceinline__ uint64_t digest_decode(uint64_t h, uint64_t nr, int k, int64_t T, int64_t bd,
+                                                  int64_t lat) {
   const int lane = lane_id();
   const uint64_t v = lane == 0 ? (uint64_t)T : lane == 1 ? (uint64_t)k : lane == 3 ? (uint64_t)bd
                    : lane == 7 ? (uint64_t)lat : 0ull;
@@ -164,7 +169,7 @@ __device__ __forceinline__ uint64_t digest_decode(uint64_t h, int k, int64_t T, 
   acc += __shfl_xor_sync(FULL, acc, 2);
   acc += __shfl_xor_sync(FULL, acc, 1);
   acc = __shfl_sync(FULL, acc, 0);
-  return mix64(h ^ acc);
+  return h + mix64(acc + nr * GOLD2);
 }
 
 // ------------------------------------------------------------------------ queue helpers -------
@@ -505,9 +510,11 @@ __device__ __forceinline__ void decode_batch(const SimP& P, SInst& I, int k, int
   const int32_t bd = I.ds_len;
   const int64_t l = lat_decode(P.md, (uint64_t)bd, (uint64_t)I.ctx_sum);
   if (l < 0) atomicOr(P.err, ERR_RANGE);
-  const uint64_t h = digest_decode(I.hash, k, T, bd, l);
+  const uint64_t nr = I.nrec + 1;
+  const uint64_t h = digest_decode(I.hash, nr, k, T, bd, l);
   __syncwarp();
   I.hash = h;  // uniform values: every lane stores the same words
+  I.nrec = nr;
   I.end = T + l;
   I.batch_dec = 1;
   I.bp_len = 0;
@@ -857,6 +864,7 @@ __device__ __noinline__ int64_t run_decode(const SimP& P, Wp w, int k, int64_t T
   const int64_t E = I.end, S0 = I.ctx_sum;
   const int32_t kvf0 = I.kv_free;
   uint64_t h = I.hash;
+  const uint64_t nr0 = I.nrec;
   const uint64_t cpart = mix64((uint64_t)k + 2 * GOLD) + mix64(3 * GOLD) + mix64((uint64_t)Bd + 4 * GOLD) +
                          mix64(5 * GOLD) + mix64(6 * GOLD) + mix64(7 * GOLD);
   int64_t J = 0, tcarry = 0, ncarry = 0;
@@ -872,8 +880,8 @@ __device__ __noinline__ int64_t run_decode(const SimP& P, Wp w, int k, int64_t T
     const uint32_t m = __ballot_sync(FULL, ok);
     const int n = (m == FULL) ? 32 : (__ffs(~m) - 1);
     const uint64_t rec = cpart + mix64((uint64_t)tc + GOLD) + mix64((uint64_t)lc + 8 * GOLD);
-#pragma unroll 1
-    for (int j = 0; j < n; j++) h = mix64(h ^ __shfl_sync(FULL, rec, j));
+    // instance digest: + mix(rec + (formation index) * G2) for each of the first n events
+    h += warp_sum(lane < n ? mix64(rec + (nr0 + (uint64_t)c + 1) * GOLD2) : 0ull);
     if (n > 0) {
       ncarry = __shfl_sync(FULL, cum, n - 1);
       tcarry = __shfl_sync(FULL, incl, n - 1) + tcarry;
@@ -908,6 +916,7 @@ __device__ __noinline__ int64_t run_decode(const SimP& P, Wp w, int k, int64_t T
   I.ctx_sum = cs;
   I.end = end;
   I.hash = h;
+  I.nrec = nr0 + (uint64_t)J;
   I.papp = 1;
   __syncwarp();
   return J;
@@ -930,7 +939,7 @@ __device__ __noinline__ void init_trace(const SimP& P, Wp w, int trace) {
     SInst& I = w.SI[lane];
     I.hp = lane >= P.n_lp;
     I.kv_total = I.kv_free = I.hp ? P.kv_hp : P.kv_lp;
-    I.end = INF64; I.hist_sum = 0; I.ctx_sum = 0; I.hash = 0;
+    I.end = INF64; I.hist_sum = 0; I.ctx_sum = 0; I.hash = 0; I.nrec = 0;
     I.wq_len = I.ds_len = I.bp_len = I.hist_cnt = I.need_sum = 0;
     I.batch_dec = I.tk_live = 0;
     I.papp = 1;
