@@ -842,84 +842,171 @@ __device__ __noinline__ void deliver(const SimP& P, Wp w, int64_t T) {
 __device__ __noinline__ int64_t run_decode(const SimP& P, Wp w, int k, int64_t T_limit) {
   SInst& I = w.SI[k];
   const int lane = lane_id();
-  const int32_t Bd = I.ds_len;
   const int32_t bs = P.bs;
-  if (Bd == 0 || bs > 256 || !I.papp) return 0;
-  int32_t* hist = reinterpret_cast<int32_t*>(w.buf);  // 256 ints of per-warp scratch
-  for (int i = lane; i < bs; i += 32) hist[i] = 0;
+  if (I.ds_len == 0 || bs > 128 || !I.papp) return 0;
+  const bool hp = I.hp;
+  // two histograms of l̂ mod bs (current slots / survivors of the next completion), plus the
+  // histogram of the slots that would finish at the next completion event
+  int32_t* hA = reinterpret_cast<int32_t*>(w.buf);  // w.buf holds 256 ints: two histograms
+  int32_t* hB = hA + 128;
+  int32_t Bd = I.ds_len;
+  int64_t E = I.end, S = I.ctx_sum;
+  int32_t kvf = I.kv_free;
+  uint64_t h = I.hash, nr = I.nrec;
+  int64_t total = 0;
+  int64_t hsum_all = 0;
+  int32_t hcnt_all = 0, tkd_all = 0;
+  // pass A: histogram + minimum remaining tokens of the current slots
+  for (int i = lane; i < 128; i += 32) hA[i] = 0;
   __syncwarp();
   int32_t mrem = INT32_MAX;
   for (int32_t c = 0; c < Bd; c += 32) {
     const int32_t j = c + lane;
     if (j < Bd) {
-      const int4 s = *slotp(P, w, k, j);
-      mrem = min(mrem, s.z);
-      atomicAdd(&hist[(s.w >> R_SHIFT) & 0x1ff], 1);
+      const int4 sl = *slotp(P, w, k, j);
+      mrem = min(mrem, sl.z);
+      atomicAdd(&hA[(sl.w >> R_SHIFT) & 0x1ff], 1);
     }
   }
   mrem = warp_min(mrem);
   __syncwarp();
-  const int64_t Jmax = (int64_t)mrem - 1;  // events before the first completion
-  if (Jmax <= 0) return 0;
-  const int64_t E = I.end, S0 = I.ctx_sum;
-  const int32_t kvf0 = I.kv_free;
-  uint64_t h = I.hash;
-  const uint64_t nr0 = I.nrec;
-  const uint64_t cpart = mix64((uint64_t)k + 2 * GOLD) + mix64(3 * GOLD) + mix64((uint64_t)Bd + 4 * GOLD) +
-                         mix64(5 * GOLD) + mix64(6 * GOLD) + mix64(7 * GOLD);
-  int64_t J = 0, tcarry = 0, ncarry = 0;
   while (true) {
-    const int64_t c = J + lane;
-    const int32_t cm = (int32_t)(c % bs);
-    const int64_t need = hist[cm == 0 ? 0 : bs - cm];  // slots with (r0 + c) mod bs == 0
-    const int64_t cum = ncarry + warp_incl_scan(need);
-    const int64_t lc = lat_decode(P.md, (uint64_t)Bd, (uint64_t)(S0 + (c + 1) * Bd));
-    const int64_t incl = warp_incl_scan(lc < 0 ? (int64_t)0 : lc);
-    const int64_t tc = E + tcarry + incl - (lc < 0 ? 0 : lc);  // start (formation) time of event c
-    const bool ok = c < Jmax && tc < T_limit && cum <= kvf0 && lc > 0;
-    const uint32_t m = __ballot_sync(FULL, ok);
-    const int n = (m == FULL) ? 32 : (__ffs(~m) - 1);
-    const uint64_t rec = cpart + mix64((uint64_t)tc + GOLD) + mix64((uint64_t)lc + 8 * GOLD);
-    // instance digest: + mix(rec + (formation index) * G2) for each of the first n events
-    h += warp_sum(lane < n ? mix64(rec + (nr0 + (uint64_t)c + 1) * GOLD2) : 0ull);
-    if (n > 0) {
-      ncarry = __shfl_sync(FULL, cum, n - 1);
-      tcarry = __shfl_sync(FULL, incl, n - 1) + tcarry;
+    const uint64_t cpart = mix64((uint64_t)k + 2 * GOLD) + mix64(3 * GOLD) + mix64((uint64_t)Bd + 4 * GOLD) +
+                           mix64(5 * GOLD) + mix64(6 * GOLD) + mix64(7 * GOLD);
+    const int32_t Jmax = mrem - 1;  // decode-only events before the next completion
+    int32_t J = 0;
+    int64_t tcarry = 0, ncarry = 0;
+    // ---- lane-parallel segment: events c = 0 .. Jmax-1 (no completion among them)
+    while (J < Jmax) {
+      const int32_t c = J + lane;
+      const int32_t cm = c % bs;
+      const int64_t need = hA[cm == 0 ? 0 : bs - cm];  // slots with (r0 + c) mod bs == 0
+      const int64_t cum = ncarry + warp_incl_scan(need);
+      const int64_t lc = lat_decode(P.md, (uint64_t)Bd, (uint64_t)(S + (int64_t)(c + 1) * Bd));
+      const int64_t incl = warp_incl_scan(lc < 0 ? (int64_t)0 : lc);
+      const int64_t tc = E + tcarry + incl - (lc < 0 ? 0 : lc);  // formation time of event c
+      const bool ok = c < Jmax && tc < T_limit && cum <= kvf && lc > 0;
+      const uint32_t m = __ballot_sync(FULL, ok);
+      const int n = (m == FULL) ? 32 : (__ffs(~m) - 1);
+      const uint64_t rec = cpart + mix64((uint64_t)tc + GOLD) + mix64((uint64_t)lc + 8 * GOLD);
+      h += warp_sum(lane < n ? mix64(rec + (nr + (uint64_t)c + 1) * GOLD2) : 0ull);
+      if (n > 0) {
+        ncarry = __shfl_sync(FULL, cum, n - 1);
+        tcarry = __shfl_sync(FULL, incl, n - 1) + tcarry;
+      }
+      J += n;
+      if (n < 32) break;
     }
-    J += n;
-    if (n < 32) break;
-  }
-  if (J == 0) return 0;
-  // apply the J events to every decode slot: l̂ += J, remaining -= J, blocks and residue
-  for (int32_t c = 0; c < Bd; c += 32) {
-    const int32_t j = c + lane;
-    if (j < Bd) {
-      int4 s = *slotp(P, w, k, j);
-      const int32_t r0 = (s.w >> R_SHIFT) & 0x1ff;
-      const int32_t pend0 = (int32_t)((uint32_t)s.w >> 31);
-      const int64_t first = r0 == 0 ? 0 : bs - r0;  // first event index c with (r0 + c) % bs == 0
-      const int64_t last = J - 2;                   // growth applied through event J-2 ...
-      const int32_t grown = last >= first ? (int32_t)(1 + (last - first) / bs) : 0;
-      const int32_t held = (s.w & HELD_MASK) + pend0 + grown;
-      const int32_t rJ = (int32_t)((r0 + J) % bs);
-      const bool pend = ((r0 + J - 1) % bs) == 0;  // ... and left pending by event J-1
-      s.y += (int32_t)J;
-      s.z -= (int32_t)J;
-      s.w = held | (rJ << R_SHIFT) | (pend ? PEND : 0);
-      *slotp(P, w, k, j) = s;
+    const int64_t Et = E + tcarry;  // time of event J (a completion event iff J == Jmax)
+    // ---- can event J (the completion) be processed here?  Conservative KV check from the
+    // histogram (finishing slots included): the main loop handles it if eviction might be needed
+    const int32_t cJ = J % bs;
+    const int64_t needJ = hA[cJ == 0 ? 0 : bs - cJ];
+    const bool doC = J == Jmax && Et < T_limit && needJ <= kvf - ncarry;
+    const int32_t nstep = J + (doC ? 1 : 0);
+    if (nstep == 0) break;
+    // ---- pass B: apply the J decode steps (and the completion event J when doC)
+    for (int i = lane; i < 128; i += 32) hB[i] = 0;
+    __syncwarp();
+    int32_t out = 0, mrem2 = INT32_MAX, need2 = 0;
+    int64_t freed = 0, hsum = 0, csum = 0;
+    int32_t hcnt = 0, tkd = 0;
+    for (int32_t c0 = 0; c0 < Bd; c0 += 32) {
+      const int32_t j = c0 + lane;
+      const bool v = j < Bd;
+      int4 sl = make_int4(0, 0, 1 << 30, 0);
+      if (v) sl = *slotp(P, w, k, j);
+      const int32_t r0 = (sl.w >> R_SHIFT) & 0x1ff;
+      const int32_t pend0 = (int32_t)((uint32_t)sl.w >> 31);
+      // growth applied at formations 0 .. nstep-1 uses the pending bits of completions 0 .. nstep-1
+      // held after nstep completions = held_base + pend0 + #{c in [0, nstep-2] : (r0 + c) % bs == 0}
+      const int32_t first = r0 == 0 ? 0 : bs - r0;
+      const int32_t last = nstep - 2;
+      const int32_t grown = last >= first ? 1 + (last - first) / bs : 0;
+      const int32_t held = (sl.w & HELD_MASK) + pend0 + grown;
+      const int32_t rN = (r0 + nstep) % bs;
+      const bool pend = nstep > 0 && ((r0 + nstep - 1) % bs) == 0;
+      sl.y += nstep;
+      sl.z -= nstep;
+      sl.w = held | (rN << R_SHIFT) | (pend ? PEND : 0);
+      const bool fin = v && doC && sl.z == 0;
+      const bool keep = v && !fin;
+      const uint32_t mk = __ballot_sync(FULL, keep);
+      if (keep) {
+        *slotp(P, w, k, out + __popc(mk & lanemask_lt())) = sl;
+        mrem2 = min(mrem2, sl.z);
+        atomicAdd(&hB[rN], 1);
+        need2 += pend ? 1 : 0;
+        csum += sl.y;
+      }
+      if (fin) {  // completion at Et: done, KV freed, HP history / ticket bookkeeping
+        const int64_t g = w.base + sl.x;
+        finish_req(P, g, Et);
+        freed += held;  // held_base after nstep completions = blocks held when it finishes
+        if (hp) { hsum += P.ol[g]; hcnt++; if (P.rq_fl[g] & F_TICK) tkd++; }
+      }
+      out += __popc(mk);
     }
+    mrem2 = warp_min(mrem2);
+    need2 = warp_sum(need2);
+    csum = warp_sum(csum);
+    if (doC) {
+      freed = warp_sum(freed);
+      hsum = warp_sum(hsum);
+      hcnt = warp_sum(hcnt);
+      tkd = warp_sum(tkd);
+    }
+    __syncwarp();
+    total += J;
+    kvf -= (int32_t)ncarry;
+    nr += (uint64_t)J;
+    if (!doC) {  // the run ends before event J: event J (at Et) is left to the event loop
+      E = Et;
+      S = csum;
+      break;
+    }
+    // ---- the formation at Et after the completion: a decode-only batch of the survivors
+    kvf += (int32_t)freed;
+    hsum_all += hsum;
+    hcnt_all += hcnt;
+    tkd_all += tkd;
+    Bd = out;
+    S = csum;
+    if (Bd == 0) {  // everything finished: the instance parks
+      E = INF64;
+      break;
+    }
+    kvf -= need2;  // growth for the survivors' next token (fits: needJ <= kvf - ncarry above)
+    const int64_t l = lat_decode(P.md, (uint64_t)Bd, (uint64_t)S);
+    if (l < 0) atomicOr(P.err, ERR_RANGE);
+    nr += 1;
+    h = digest_decode(h, nr, k, Et, Bd, l);
+    total += 1;
+    E = Et + l;
+    // the survivors become the current slots (their pending bits were just applied: papp = 1)
+    int32_t* t = hA; hA = hB; hB = t;
+    mrem = mrem2;
+    if (E >= T_limit) break;
   }
-  const int32_t kvf = kvf0 - (int32_t)ncarry;
-  const int64_t cs = S0 + J * Bd, end = E + tcarry;
+  if (total == 0) return 0;
+  const int64_t hs = I.hist_sum + hsum_all;
+  const int32_t hc = I.hist_cnt + hcnt_all, tk = I.tk_live - tkd_all;
+  const bool issue = hp && P.tickets && !I.ticket && I.wq_len == 0 && tk == 0;  // phase E
   __syncwarp();
   I.kv_free = kvf;
-  I.ctx_sum = cs;
-  I.end = end;
+  I.ctx_sum = S;
+  I.end = E;
   I.hash = h;
-  I.nrec = nr0 + (uint64_t)J;
+  I.nrec = nr;
+  I.ds_len = Bd;
   I.papp = 1;
+  I.hist_sum = hs;
+  I.hist_cnt = hc;
+  I.tk_live = tk;
+  if (Bd == 0) { I.batch_dec = 0; I.bp_len = 0; }
+  if (issue) I.ticket = 1;
   __syncwarp();
-  return J;
+  return total;
 }
 
 __device__ __noinline__ void init_trace(const SimP& P, Wp w, int trace) {
