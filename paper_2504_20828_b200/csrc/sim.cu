@@ -42,6 +42,7 @@ struct SInst {
   uint64_t hash, nrec;       // instance digest and number of recorded formations
   int32_t kv_free, kv_total, wq_len, ds_len, bp_len, hist_cnt, need_sum;
   int32_t batch_dec, ticket, tk_live, hp, papp;
+  int32_t wq_head;           // the waiting queue occupies [wq_head, wq_head + wq_len) of the region
 };
 
 struct SimP {
@@ -71,7 +72,7 @@ struct SimP {
   int32_t* wq_id;
   int4* ds_g;  // decode-slot overflow (slot index >= DCAP)
   int32_t* bp_id;
-  int32_t *scr_drop, *scr_pre, *scr_off;
+  int32_t *scr_drop, *scr_pre, *scr_off, *scr_tmp;
   int64_t* fl_t;
   int32_t *fl_req, *fl_hp;
   int* err;
@@ -173,57 +174,130 @@ __device__ __forceinline__ uint64_t digest_decode(uint64_t h, uint64_t nr, int k
 }
 
 // ------------------------------------------------------------------------ queue helpers -------
-__device__ __forceinline__ void wq_append(const SimP& P, Wp w, int k, int32_t id) {
-  SInst& I = w.SI[k];
-  const int64_t o = ioff(P, k, w);
-  const int32_t len = I.wq_len;
-  const int64_t key = key_of(P, w.base + id, P.rq_eff[w.base + id]);
-  __syncwarp();
-  if (lane_id() == 0) {
-    P.wq_id[o + len] = id;
-    P.wq_key[o + len] = key;
-  }
-  I.wq_len = len + 1;
-  __syncwarp();
+// Every waiting queue lives in [head, head + len) of its instance region (capacity = trace size)
+// and is kept sorted: LP queues by the time-invariant (key, id) of the value function (so Algorithm
+// 1 reads a prefix), HP queues by id = FCFS by (arrival, id) (G26).  Admission removes a
+// prefix by moving the head.
+__device__ __forceinline__ int64_t qoff(const SimP& P, const SInst& I, int k, Wp w) {
+  return ioff(P, k, w) + I.wq_head;
 }
 
-// HP waiting queues are kept in ascending id order = FCFS by (arrival, id) (G26)
-__device__ __noinline__ void wq_insert_sorted(const SimP& P, Wp w, int k, int32_t id) {
+// make room for one more entry at the tail (compacts the queue to the region start if needed)
+__device__ __noinline__ void wq_compact(const SimP& P, Wp w, int k) {
   SInst& I = w.SI[k];
   const int lane = lane_id();
   const int64_t o = ioff(P, k, w);
-  const int32_t len = I.wq_len;
-  int32_t pos = 0;
+  const int32_t h = I.wq_head, len = I.wq_len;
   for (int32_t c = 0; c < len; c += 32) {
     const int32_t j = c + lane;
-    pos += __popc(__ballot_sync(FULL, j < len && P.wq_id[o + j] < id));
+    int32_t xi = 0;
+    int64_t xk = 0;
+    if (j < len) { xi = P.wq_id[o + h + j]; xk = P.wq_key[o + h + j]; }
+    __syncwarp();
+    if (j < len) { P.wq_id[o + j] = xi; P.wq_key[o + j] = xk; }
+    __syncwarp();
   }
-  for (int32_t c = len - 1; c >= pos; c -= 32) {
+  I.wq_head = 0;
+  __syncwarp();
+}
+
+// insert request id in order: LP by (key, id), HP by id.  The position is searched from the tail:
+// new arrivals carry the largest ids and, under the laxity key, keys near the largest.
+__device__ __noinline__ void wq_insert(const SimP& P, Wp w, int k, int32_t id) {
+  SInst& I = w.SI[k];
+  const int lane = lane_id();
+  if (I.wq_head + I.wq_len >= (int32_t)w.n) wq_compact(P, w, k);
+  const int64_t q = qoff(P, I, k, w);
+  const int32_t len = I.wq_len;
+  const int64_t key = key_of(P, w.base + id, P.rq_eff[w.base + id]);
+  const bool by_id = I.hp;
+  int32_t pos = len;  // number of entries ordered before the new one
+  for (int32_t c = len - 1; c >= 0; c -= 32) {
+    const int32_t j = c - lane;
+    bool after = false;  // entry j sorts after the new entry
+    if (j >= 0) {
+      const int32_t xi = P.wq_id[q + j];
+      const int64_t xk = P.wq_key[q + j];
+      after = by_id ? xi > id : (xk > key || (xk == key && xi > id));
+    }
+    const uint32_t m = __ballot_sync(FULL, after);
+    pos -= __popc(m);
+    if (m != FULL) break;  // entries are sorted: everything before this chunk sorts before
+  }
+  for (int32_t c = len - 1; c >= pos; c -= 32) {  // shift [pos, len) up by one
     const int32_t j = c - lane;
     int32_t xi = 0;
     int64_t xk = 0;
     const bool v = j >= pos;
-    if (v) { xi = P.wq_id[o + j]; xk = P.wq_key[o + j]; }
+    if (v) { xi = P.wq_id[q + j]; xk = P.wq_key[q + j]; }
     __syncwarp();
-    if (v) { P.wq_id[o + j + 1] = xi; P.wq_key[o + j + 1] = xk; }
+    if (v) { P.wq_id[q + j + 1] = xi; P.wq_key[q + j + 1] = xk; }
     __syncwarp();
   }
-  const int64_t key = key_of(P, w.base + id, P.rq_eff[w.base + id]);
   if (lane == 0) {
-    P.wq_id[o + pos] = id;
-    P.wq_key[o + pos] = key;
+    P.wq_id[q + pos] = id;
+    P.wq_key[q + pos] = key;
   }
   __syncwarp();
   I.wq_len = len + 1;
   __syncwarp();
 }
 
+// append (HP ticket: the newest arrival has the largest id, so the order is kept)
+__device__ __forceinline__ void wq_append(const SimP& P, Wp w, int k, int32_t id) {
+  SInst& I = w.SI[k];
+  if (I.wq_head + I.wq_len >= (int32_t)w.n) wq_compact(P, w, k);
+  const int64_t q = qoff(P, I, k, w);
+  const int32_t len = I.wq_len;
+  const int64_t key = key_of(P, w.base + id, P.rq_eff[w.base + id]);
+  __syncwarp();
+  if (lane_id() == 0) {
+    P.wq_id[q + len] = id;
+    P.wq_key[q + len] = key;
+  }
+  I.wq_len = len + 1;
+  __syncwarp();
+}
+
+// sort n request ids ascending (offload / drop lists come out in key order; the dispatch and the
+// digest use id order).  Rank by counting: ids are distinct.
+__device__ __noinline__ void sort_ids(const SimP& P, Wp w, int32_t* a, int32_t n) {
+  const int lane = lane_id();
+  if (n <= 1) return;
+  if (n <= 32) {
+    int32_t x = lane < n ? a[lane] : INT32_MAX;
+    const int l = lane;
+#pragma unroll
+    for (int kk = 2; kk <= 32; kk <<= 1)
+#pragma unroll
+      for (int j = kk >> 1; j > 0; j >>= 1) {
+        const int32_t o = __shfl_xor_sync(FULL, x, j);
+        const bool keep_min = ((l & j) == 0) == ((l & kk) == 0);
+        x = keep_min ? min(x, o) : max(x, o);
+      }
+    __syncwarp();
+    if (lane < n) a[lane] = x;
+    __syncwarp();
+    return;
+  }
+  int32_t* tmp = P.scr_tmp + w.base;
+  for (int32_t i = lane; i < n; i += 32) {
+    const int32_t x = a[i];
+    int32_t r = 0;
+    for (int32_t j = 0; j < n; j++) r += a[j] < x;
+    tmp[r] = x;
+  }
+  __syncwarp();
+  for (int32_t i = lane; i < n; i += 32) a[i] = tmp[i];
+  __syncwarp();
+}
+
 // Drop rule (G34): waiting, never prefilled, strictly past the deadline.  Stable
-// compaction of the queue; dropped ids (queue order = ascending id) go to scr_drop.
+// compaction of the queue (order kept); dropped ids go to scr_drop in ascending id order.
 __device__ __noinline__ int32_t drop_step(const SimP& P, Wp w, int k, int64_t T) {
   SInst& I = w.SI[k];
   const int lane = lane_id();
-  const int64_t o = ioff(P, k, w);
+  const int64_t q = qoff(P, I, k, w);
   const int32_t len = I.wq_len;
   int32_t out = 0, nd = 0, tkd = 0;
   for (int32_t c = 0; c < len; c += 32) {
@@ -233,13 +307,13 @@ __device__ __noinline__ int32_t drop_step(const SimP& P, Wp w, int k, int64_t T)
     int64_t key = 0;
     bool dr = false;
     if (v) {
-      id = P.wq_id[o + j];
-      key = P.wq_key[o + j];
+      id = P.wq_id[q + j];
+      key = P.wq_key[q + j];
       const int64_t g = w.base + id;
       dr = !(P.rq_fl[g] & F_EVER) && T > P.rq_dl[g];
     }
     const uint32_t mk = __ballot_sync(FULL, v && !dr), md = __ballot_sync(FULL, dr);
-    if (v && !dr) { const int32_t q = out + __popc(mk & lanemask_lt()); P.wq_id[o + q] = id; P.wq_key[o + q] = key; }
+    if (v && !dr) { const int32_t o2 = out + __popc(mk & lanemask_lt()); P.wq_id[q + o2] = id; P.wq_key[q + o2] = key; }
     if (dr) {
       const int64_t g = w.base + id;
       P.scr_drop[w.base + nd + __popc(md & lanemask_lt())] = id;
@@ -256,6 +330,7 @@ __device__ __noinline__ int32_t drop_step(const SimP& P, Wp w, int k, int64_t T)
   I.wq_len = out;
   I.tk_live = tk;
   __syncwarp();
+  if (!I.hp) sort_ids(P, w, P.scr_drop + w.base, nd);  // LP queue order is key order
   return nd;
 }
 
@@ -299,7 +374,7 @@ __device__ __noinline__ int32_t evict(const SimP& P, Wp w, int k) {
     I.ds_len = len - 1;
     __syncwarp();
     np++;
-    if (I.hp) wq_insert_sorted(P, w, k, vid); else wq_append(P, w, k, vid);
+    wq_insert(P, w, k, vid);
   }
   return np;
 }
@@ -336,32 +411,17 @@ __device__ __forceinline__ void set_batch(const SimP& P, SInst& I, int64_t T, in
   __syncwarp();
 }
 
-// Deep queues (> 32 entries): streaming top-K of the queue (asc_dev.cuh), out of line so the big
-// merge networks stay out of the instruction cache of the common path.
-__device__ __noinline__ void select_deep(const SimP& P, Wp w, int64_t o, int32_t len, int64_t kneed,
-                                         KI* out) {
-  const int lane = lane_id();
-  TopKStream<KPL> st;
-  st.init(w.buf, kneed > 0 ? (int)kneed - 1 : 32 * KPL - 1);
-  for (int32_t c = 0; c < len; c += 32) {
-    const int32_t j = c + lane;
-    const bool v = j < len;
-    KI x = ki_inf();
-    if (v) x = KI{P.wq_key[o + j], P.wq_id[o + j]};
-    st.push(x, v);
-  }
-  st.finish();
-  __syncwarp();
-#pragma unroll
-  for (int r = 0; r < KPL; r++) out[r] = st.top.a[r];
-}
-
 // --------------------------------------------------------------- LP admission (non-empty queue)
+// The queue is sorted by the time-invariant (key, id), i.e. already in Algorithm 1's
+// line-3 order: lines 5-13 read its prefix.  Offload (§5.3, G24) under EDF_LAXITY is the range
+// key <= T + W_hp + margin right after the admitted prefix (key = deadline - prefill_us makes the
+// offload test a key bound); other policies scan the whole queue.
 __device__ __noinline__ int lp_admit(const SimP& P, Wp w, int k, int64_t T, int32_t ndrop,
                                      int32_t npre) {
   SInst& I = w.SI[k];
   const int lane = lane_id();
-  const int64_t o = ioff(P, k, w);
+  const int64_t o = ioff(P, k, w);  // running-batch list base
+  const int64_t q = qoff(P, I, k, w);
   const int64_t Bd = I.ds_len;
   const int64_t sl = I.ctx_sum;
   // budgets (G22)
@@ -372,104 +432,120 @@ __device__ __noinline__ int lp_admit(const SimP& P, Wp w, int k, int64_t T, int3
     if (ldec < 0) atomicOr(P.err, ERR_RANGE);
     C = w.tbt - ldec;
   }
-  // Algorithm 1 line 3: the (key, id)-sorted prefix; only the first min(R, N-1, M-1) <= 128 can
-  // be admitted (strict budgets, costs >= 1)
   const int32_t len = I.wq_len;
-  int64_t kneed = Rb < 32 * KPL ? Rb : 32 * KPL;
-  kneed = kneed < N - 1 ? kneed : N - 1;
-  kneed = kneed < M - 1 ? kneed : M - 1;
-  KI a[KPL];
-  if (len <= 32) {
-    KI x = ki_inf();
-    if (lane < len) x = KI{P.wq_key[o + lane], P.wq_id[o + lane]};
-    a[0] = sort32(x);
-#pragma unroll
-    for (int r = 1; r < KPL; r++) a[r] = ki_inf();
-  } else {
-    select_deep(P, w, o, len, kneed, a);
-  }
-  // lines 5-13 as a strict prefix-sum scan over the sorted candidates
+  // Algorithm 1 lines 5-13 as a strict prefix-sum scan over the sorted prefix
   int32_t nadm = 0;
   uint64_t sp = 0, sp2 = 0, spc = 0;
   int64_t used = 0, ct = 0, cb = 0, cc = 0;
-  bool go = true;
 #pragma unroll 1
   for (int r = 0; r < KPL; r++) {
-    if (!go) break;
-    KI e = a[0];
-    for (int q = 1; q < KPL; q++) if (q == r) e = a[q];
-    const bool valid = e.i != INF32;
-    const int64_t g = w.base + (valid ? e.i : 0);
+    const int pos = r * 32 + lane;
+    const bool valid = pos < len;
+    const int32_t id = valid ? P.wq_id[q + pos] : 0;
+    const int64_t g = w.base + id;
     const int32_t p = valid ? P.rq_eff[g] : 0;
     const int64_t pf = valid ? pf_of(P, p) : 0;
     const int64_t bl = valid ? blk_of(P, p) : 0;
     const int64_t St = ct + warp_incl_scan((int64_t)p);
     const int64_t Sb = cb + warp_incl_scan(bl);
     const int64_t Sc = cc + warp_incl_scan(pf);
-    const int pos = r * 32 + lane;
     const bool ok = valid && St < N && Sb < M && Sc < C && pos < Rb;
     const uint32_t m = __ballot_sync(FULL, ok);
     const int cnt = (m == FULL) ? 32 : (__ffs(~m) - 1);
     if (lane < cnt) {
       admit_req(P, g, k, T);
-      P.bp_id[o + pos] = e.i;
-      const uint64_t q = (uint64_t)p;
-      sp += q;
-      sp2 += q * q;
-      spc += q * ceil_div_u(q, P.md.b);
+      P.bp_id[o + pos] = id;
+      const uint64_t u = (uint64_t)p;
+      sp += u;
+      sp2 += u * u;
+      spc += u * ceil_div_u(u, P.md.b);
       used += bl;
     }
     nadm += cnt;
-    if (cnt < 32) go = false;
+    if (cnt < 32) break;
     ct = __shfl_sync(FULL, St, 31);
     cb = __shfl_sync(FULL, Sb, 31);
     cc = __shfl_sync(FULL, Sc, 31);
-  }
-  KI last = ki_inf();
-  if (nadm > 0) {
-    const int r = (nadm - 1) >> 5;
-    KI lr = a[0];
-#pragma unroll
-    for (int q = 1; q < KPL; q++) if (q == r) lr = a[q];
-    last = ki_shfl(lr, (nadm - 1) & 31);
   }
   sp = warp_sum(sp);
   sp2 = warp_sum(sp2);
   spc = warp_sum(spc);
   used = warp_sum(used);
-  // offload (§5.3, G24) + queue compaction in one pass; the admitted set is exactly the entries
-  // at or before `last` in (key, id) order
+  // the admitted requests are the queue's prefix
+  const int64_t q2 = q + nadm;
+  int32_t head = I.wq_head + nadm, rem = len - nadm;
   int32_t noff = 0;
-  int32_t out = len;
-  if (nadm > 0 || P.offl) {
-    out = 0;
-    for (int32_t c = 0; c < len; c += 32) {
-      const int32_t j = c + lane;
-      const bool v = j < len;
-      KI x = ki_inf();
-      bool adm = false, off = false;
-      if (v) {
-        x = KI{P.wq_key[o + j], P.wq_id[o + j]};
-        adm = nadm > 0 && !ki_less(last, x);
-        if (!adm && P.offl) {
-          const int64_t g = w.base + x.i;
-          const uint32_t f = P.rq_fl[g];
-          off = !(f & (F_EVER | F_ONHP)) &&
+  if (P.offl && rem > 0) {
+    if (P.policy == ASC_POLICY_EDF_LAXITY) {
+      // offload range: the prefix with key <= othr; eligible entries leave, the rest (evicted,
+      // ever-prefilled requests) are packed in order at the end of the range
+      const int64_t othr = T + P.W + P.margin;
+      int32_t m = 0;
+      for (int32_t c = 0; c < rem; c += 32) {
+        const int32_t j = c + lane;
+        const uint32_t in = __ballot_sync(FULL, j < rem && P.wq_key[q2 + j] <= othr);
+        m += __popc(in);
+        if (in != FULL) break;
+      }
+      int32_t wpos = m;  // backward stable compaction of the kept entries inside [0, m)
+      for (int32_t c = m - 1; c >= 0; c -= 32) {
+        const int32_t j = c - lane;
+        const bool v = j >= 0;
+        int32_t id = 0;
+        int64_t key = 0;
+        bool off = false;
+        if (v) {
+          id = P.wq_id[q2 + j];
+          key = P.wq_key[q2 + j];
+          off = !(P.rq_fl[w.base + id] & (F_EVER | F_ONHP));
+        }
+        const uint32_t mk = __ballot_sync(FULL, v && !off), mo = __ballot_sync(FULL, off);
+        if (v && !off) {
+          const int32_t d = wpos - 1 - __popc(mk & lanemask_lt());
+          P.wq_id[q2 + d] = id;
+          P.wq_key[q2 + d] = key;
+        }
+        if (off) P.scr_off[w.base + noff + __popc(mo & lanemask_lt())] = id;
+        wpos -= __popc(mk);
+        noff += __popc(mo);
+        __syncwarp();
+      }
+      head += wpos;  // wpos = number of offloaded entries
+      rem -= wpos;
+    } else {
+      int32_t out = 0;
+      for (int32_t c = 0; c < rem; c += 32) {
+        const int32_t j = c + lane;
+        const bool v = j < rem;
+        int32_t id = 0;
+        int64_t key = 0;
+        bool off = false;
+        if (v) {
+          id = P.wq_id[q2 + j];
+          key = P.wq_key[q2 + j];
+          const int64_t g = w.base + id;
+          off = !(P.rq_fl[g] & (F_EVER | F_ONHP)) &&
                 P.rq_dl[g] - T <= pf_of(P, P.rq_eff[g]) + P.W + P.margin;
         }
+        const uint32_t mk = __ballot_sync(FULL, v && !off), mo = __ballot_sync(FULL, off);
+        if (v && !off) {
+          const int32_t d = out + __popc(mk & lanemask_lt());
+          P.wq_id[q2 + d] = id;
+          P.wq_key[q2 + d] = key;
+        }
+        if (off) P.scr_off[w.base + noff + __popc(mo & lanemask_lt())] = id;
+        out += __popc(mk);
+        noff += __popc(mo);
+        __syncwarp();
       }
-      const bool keep = v && !adm && !off;
-      const uint32_t mk = __ballot_sync(FULL, keep), mo = __ballot_sync(FULL, off);
-      if (keep) { const int32_t q = out + __popc(mk & lanemask_lt()); P.wq_id[o + q] = x.i; P.wq_key[o + q] = x.k; }
-      if (off) P.scr_off[w.base + noff + __popc(mo & lanemask_lt())] = x.i;
-      out += __popc(mk);
-      noff += __popc(mo);
-      __syncwarp();
+      rem = out;
     }
+    sort_ids(P, w, P.scr_off + w.base, noff);  // dispatch and digest in ascending id order
   }
   const int32_t kvf = I.kv_free - (int32_t)used;
   __syncwarp();
-  I.wq_len = out;
+  I.wq_head = rem > 0 ? head : 0;
+  I.wq_len = rem;
   I.kv_free = kvf;
   __syncwarp();
   // dispatch offloads round-robin over the HPs, ascending id
@@ -491,7 +567,7 @@ __device__ __noinline__ int lp_admit(const SimP& P, Wp w, int k, int64_t T, int3
       }
     }
     __syncwarp();
-    if (P.delay == 0) wq_insert_sorted(P, w, h, id);
+    if (P.delay == 0) wq_insert(P, w, h, id);
   }
   // batch (§5.4): decodes piggybacked with the admitted prefills
   const bool nonempty = nadm > 0 || Bd > 0;
@@ -556,6 +632,7 @@ __device__ __noinline__ int32_t hp_prefill(const SimP& P, Wp w, int k, int64_t T
   SInst& I = w.SI[k];
   const int lane = lane_id();
   const int64_t o = ioff(P, k, w);
+  const int64_t q = qoff(P, I, k, w);
   int64_t limit = P.hp_tok;
   if (P.elastic) {
     const int64_t mean = I.hist_cnt ? I.hist_sum / I.hist_cnt : (int64_t)P.hist_def;
@@ -571,7 +648,7 @@ __device__ __noinline__ int32_t hp_prefill(const SimP& P, Wp w, int k, int64_t T
     const int32_t j = c + lane;
     const bool v = j < len;
     int32_t id = 0, p = 0;
-    if (v) { id = P.wq_id[o + j]; p = P.rq_eff[w.base + id]; }
+    if (v) { id = P.wq_id[q + j]; p = P.rq_eff[w.base + id]; }
     const int64_t bl = v ? blk_of(P, p) : 0;
     const int64_t St = ct + warp_incl_scan((int64_t)p);
     const int64_t Sb = cb + warp_incl_scan(bl);
@@ -581,10 +658,10 @@ __device__ __noinline__ int32_t hp_prefill(const SimP& P, Wp w, int k, int64_t T
     if (lane < cnt) {
       admit_req(P, w.base + id, k, T);
       P.bp_id[o + j] = id;
-      const uint64_t q = (uint64_t)p;
-      sp += q;
-      sp2 += q * q;
-      spc += q * ceil_div_u(q, P.md.b);
+      const uint64_t u = (uint64_t)p;
+      sp += u;
+      sp2 += u * u;
+      spc += u * ceil_div_u(u, P.md.b);
       used += bl;
     }
     nadm += cnt;
@@ -597,19 +674,9 @@ __device__ __noinline__ int32_t hp_prefill(const SimP& P, Wp w, int k, int64_t T
   mom[1] = warp_sum(sp2);
   mom[2] = warp_sum(spc);
   used = warp_sum(used);
-  // remove the admitted prefix
-  for (int32_t c = 0; c < len - nadm; c += 32) {
-    const int32_t j = c + lane;
-    const bool v = j < len - nadm;
-    int32_t xi = 0;
-    int64_t xk = 0;
-    if (v) { xi = P.wq_id[o + nadm + j]; xk = P.wq_key[o + nadm + j]; }
-    __syncwarp();
-    if (v) { P.wq_id[o + j] = xi; P.wq_key[o + j] = xk; }
-    __syncwarp();
-  }
   const int32_t kvn = I.kv_free - (int32_t)used;
   __syncwarp();
+  I.wq_head = len > nadm ? I.wq_head + nadm : 0;  // the admitted prefix leaves the queue
   I.wq_len = len - nadm;
   I.kv_free = kvn;
   __syncwarp();
@@ -814,7 +881,7 @@ __device__ __forceinline__ void route(const SimP& P, Wp w, int32_t id) {
     }
   }
   const int32_t rr = w.ts->rr_lp;
-  wq_append(P, w, rr, id);
+  wq_insert(P, w, rr, id);
   w.ts->rr_lp = (rr + 1) == P.n_lp ? 0 : rr + 1;
   __syncwarp();
 }
@@ -824,7 +891,7 @@ __device__ __noinline__ void deliver(const SimP& P, Wp w, int64_t T) {
     const int32_t head = w.ts->fl_head;
     const int32_t id = P.fl_req[w.base + head];
     const int h = P.fl_hp[w.base + head];
-    wq_insert_sorted(P, w, h, id);
+    wq_insert(P, w, h, id);
     w.ts->fl_head = head + 1;
     __syncwarp();
   }
@@ -1026,7 +1093,7 @@ __device__ __noinline__ void init_trace(const SimP& P, Wp w, int trace) {
     SInst& I = w.SI[lane];
     I.hp = lane >= P.n_lp;
     I.kv_total = I.kv_free = I.hp ? P.kv_hp : P.kv_lp;
-    I.end = INF64; I.hist_sum = 0; I.ctx_sum = 0; I.hash = 0; I.nrec = 0;
+    I.end = INF64; I.hist_sum = 0; I.ctx_sum = 0; I.hash = 0; I.nrec = 0; I.wq_head = 0;
     I.wq_len = I.ds_len = I.bp_len = I.hist_cnt = I.need_sum = 0;
     I.batch_dec = I.tk_live = 0;
     I.papp = 1;
@@ -1213,7 +1280,7 @@ asc_status launch_simulate(asc_ctx* c, const asc_traces* tr, asc_outcomes* out, 
   const asc_config& cf = c->cfg;
   const int K = cf.topo.n_lp + cf.topo.n_hp;
   const int32_t T = tr->T;
-  size_t need = (size_t)R * (8 + 4 + 4) + (size_t)K * R * (8 + 4 + 16 + 4) + (size_t)R * 12 +
+  size_t need = (size_t)R * (8 + 4 + 4) + (size_t)K * R * (8 + 4 + 16 + 4) + (size_t)R * 16 +
                 (cf.flags.offload_delay_us ? (size_t)R * 16 : 0) + 64 * 1024;
   asc_status st = ensure_ws(c, need);
   if (st) return st;
@@ -1245,6 +1312,7 @@ asc_status launch_simulate(asc_ctx* c, const asc_traces* tr, asc_outcomes* out, 
   P.scr_drop = ar.take<int32_t>(R);
   P.scr_pre = ar.take<int32_t>(R);
   P.scr_off = ar.take<int32_t>(R);
+  P.scr_tmp = ar.take<int32_t>(R);
   if (cf.flags.offload_delay_us) {
     P.fl_t = ar.take<int64_t>(R);
     P.fl_req = ar.take<int32_t>(R);
