@@ -17,6 +17,7 @@
 // an 8-lane digest update.  Rare paths (admission with a non-empty queue, eviction, drops, HP
 // prefill, offload dispatch, prefill completions) are __noinline__ so the hot loop stays small.
 // The event order is the canonical A-E phase order of DESIGN.md §2.
+#include <mutex>
 #include "asc_internal.h"
 
 using namespace asc;
@@ -79,6 +80,12 @@ struct SimP {
   int* next_trace;
 };
 
+// The launch parameters live in the constant bank (one copy per device, written before each launch
+// under the per-device lock in launch_simulate): every out-of-line device function reads them as
+// constant operands, with no pointer to reload after stores.
+__constant__ SimP P;
+
+
 struct TS {  // mutable per-trace controller state (shared memory, one per warp)
   int32_t rr_lp, rr_hp, fl_head, fl_tail;
 };
@@ -91,30 +98,30 @@ struct Wp {  // per-warp trace context, passed by value (uniform across the warp
   int64_t base, n, tbt;
 };
 
-__device__ __forceinline__ int64_t pf_of(const SimP& P, int32_t p) {
+__device__ __forceinline__ int64_t pf_of(int32_t p) {
   if (p < P.pt) return __ldg(P.pf_tab + p);
   const int64_t v = prefill_lat(P.md, (uint64_t)p);
   if (v < 0) { atomicOr(P.err, ERR_RANGE); return INT32_MAX; }
   return v;
 }
-__device__ __forceinline__ int32_t blk_of(const SimP& P, int32_t eff) { return (eff + P.bs) / P.bs; }
+__device__ __forceinline__ int32_t blk_of(int32_t eff) { return (eff + P.bs) / P.bs; }
 
 // time-invariant priority key of request gid with effective prompt eff (DESIGN.md §2 Keys)
-__device__ __forceinline__ int64_t key_of(const SimP& P, int64_t gid, int32_t eff) {
+__device__ __forceinline__ int64_t key_of(int64_t gid, int32_t eff) {
   switch (P.policy) {
-    case 0: return P.rq_dl[gid] - pf_of(P, eff);
+    case 0: return P.rq_dl[gid] - pf_of(eff);
     case 1: return P.rq_dl[gid];
-    case 2: return pf_of(P, eff);
-    case 3: return -pf_of(P, eff);
+    case 2: return pf_of(eff);
+    case 3: return -pf_of(eff);
     default: return P.arr[gid];
   }
 }
 
-__device__ __forceinline__ int64_t ioff(const SimP& P, int k, Wp w) { return (int64_t)k * P.R + w.base; }
-__device__ __forceinline__ int4* slotp(const SimP& P, Wp w, int k, int32_t j) {
+__device__ __forceinline__ int64_t ioff(int k, Wp w) { return (int64_t)k * P.R + w.base; }
+__device__ __forceinline__ int4* slotp(Wp w, int k, int32_t j) {
   return j < DCAP ? (w.sd + k * DCAP + j) : (P.ds_g + (int64_t)k * P.R + w.base + j);
 }
-__device__ __forceinline__ void set_state(const SimP& P, int64_t g, uint32_t st) {
+__device__ __forceinline__ void set_state(int64_t g, uint32_t st) {
   const uint32_t f = P.rq_fl[g];
   P.rq_fl[g] = (f & ~(3u << ST_SHIFT)) | (st << ST_SHIFT);
 }
@@ -122,11 +129,11 @@ __device__ __forceinline__ void set_state(const SimP& P, int64_t g, uint32_t st)
 // ------------------------------------------------------------------------------- digest ------
 // record = Σ_pos mix(v_pos + (pos+1)·G) over (T, k, B_p, admitted…, B_d, #off, off…, #drop,
 // drop…, #evicted, evicted…, lat) — positions as in the oracle; lanes hash in parallel.
-__device__ __noinline__ void digest_log(const SimP& P, Wp w, int k, int64_t T, int32_t nadm,
+__device__ __noinline__ void digest_log(Wp w, int k, int64_t T, int32_t nadm,
                                         int64_t bd, int32_t noff, int32_t ndrop, int32_t npre,
                                         int64_t lat) {
   const int lane = lane_id();
-  const int64_t o = ioff(P, k, w);
+  const int64_t o = ioff(k, w);
   uint64_t acc = 0;
   if (lane < 8) {
     uint64_t v, pos;
@@ -178,15 +185,15 @@ __device__ __forceinline__ uint64_t digest_decode(uint64_t h, uint64_t nr, int k
 // and is kept sorted: LP queues by the time-invariant (key, id) of the value function (so Algorithm
 // 1 reads a prefix), HP queues by id = FCFS by (arrival, id) (G26).  Admission removes a
 // prefix by moving the head.
-__device__ __forceinline__ int64_t qoff(const SimP& P, const SInst& I, int k, Wp w) {
-  return ioff(P, k, w) + I.wq_head;
+__device__ __forceinline__ int64_t qoff(const SInst& I, int k, Wp w) {
+  return ioff(k, w) + I.wq_head;
 }
 
 // make room for one more entry at the tail (compacts the queue to the region start if needed)
-__device__ __noinline__ void wq_compact(const SimP& P, Wp w, int k) {
+__device__ __noinline__ void wq_compact(Wp w, int k) {
   SInst& I = w.SI[k];
   const int lane = lane_id();
-  const int64_t o = ioff(P, k, w);
+  const int64_t o = ioff(k, w);
   const int32_t h = I.wq_head, len = I.wq_len;
   for (int32_t c = 0; c < len; c += 32) {
     const int32_t j = c + lane;
@@ -203,13 +210,13 @@ __device__ __noinline__ void wq_compact(const SimP& P, Wp w, int k) {
 
 // insert request id in order: LP by (key, id), HP by id.  The position is searched from the tail:
 // new arrivals carry the largest ids and, under the laxity key, keys near the largest.
-__device__ __noinline__ void wq_insert(const SimP& P, Wp w, int k, int32_t id) {
+__device__ __noinline__ void wq_insert(Wp w, int k, int32_t id) {
   SInst& I = w.SI[k];
   const int lane = lane_id();
-  if (I.wq_head + I.wq_len >= (int32_t)w.n) wq_compact(P, w, k);
-  const int64_t q = qoff(P, I, k, w);
+  if (I.wq_head + I.wq_len >= (int32_t)w.n) wq_compact(w, k);
+  const int64_t q = qoff(I, k, w);
   const int32_t len = I.wq_len;
-  const int64_t key = key_of(P, w.base + id, P.rq_eff[w.base + id]);
+  const int64_t key = key_of(w.base + id, P.rq_eff[w.base + id]);
   const bool by_id = I.hp;
   int32_t pos = len;  // number of entries ordered before the new one
   for (int32_t c = len - 1; c >= 0; c -= 32) {
@@ -244,12 +251,12 @@ __device__ __noinline__ void wq_insert(const SimP& P, Wp w, int k, int32_t id) {
 }
 
 // append (HP ticket: the newest arrival has the largest id, so the order is kept)
-__device__ __forceinline__ void wq_append(const SimP& P, Wp w, int k, int32_t id) {
+__device__ __forceinline__ void wq_append(Wp w, int k, int32_t id) {
   SInst& I = w.SI[k];
-  if (I.wq_head + I.wq_len >= (int32_t)w.n) wq_compact(P, w, k);
-  const int64_t q = qoff(P, I, k, w);
+  if (I.wq_head + I.wq_len >= (int32_t)w.n) wq_compact(w, k);
+  const int64_t q = qoff(I, k, w);
   const int32_t len = I.wq_len;
-  const int64_t key = key_of(P, w.base + id, P.rq_eff[w.base + id]);
+  const int64_t key = key_of(w.base + id, P.rq_eff[w.base + id]);
   __syncwarp();
   if (lane_id() == 0) {
     P.wq_id[q + len] = id;
@@ -261,7 +268,7 @@ __device__ __forceinline__ void wq_append(const SimP& P, Wp w, int k, int32_t id
 
 // sort n request ids ascending (offload / drop lists come out in key order; the dispatch and the
 // digest use id order).  Rank by counting: ids are distinct.
-__device__ __noinline__ void sort_ids(const SimP& P, Wp w, int32_t* a, int32_t n) {
+__device__ __noinline__ void sort_ids(Wp w, int32_t* a, int32_t n) {
   const int lane = lane_id();
   if (n <= 1) return;
   if (n <= 32) {
@@ -294,10 +301,10 @@ __device__ __noinline__ void sort_ids(const SimP& P, Wp w, int32_t* a, int32_t n
 
 // Drop rule (G34): waiting, never prefilled, strictly past the deadline.  Stable
 // compaction of the queue (order kept); dropped ids go to scr_drop in ascending id order.
-__device__ __noinline__ int32_t drop_step(const SimP& P, Wp w, int k, int64_t T) {
+__device__ __noinline__ int32_t drop_step(Wp w, int k, int64_t T) {
   SInst& I = w.SI[k];
   const int lane = lane_id();
-  const int64_t q = qoff(P, I, k, w);
+  const int64_t q = qoff(I, k, w);
   const int32_t len = I.wq_len;
   int32_t out = 0, nd = 0, tkd = 0;
   for (int32_t c = 0; c < len; c += 32) {
@@ -317,7 +324,7 @@ __device__ __noinline__ int32_t drop_step(const SimP& P, Wp w, int k, int64_t T)
     if (dr) {
       const int64_t g = w.base + id;
       P.scr_drop[w.base + nd + __popc(md & lanemask_lt())] = id;
-      set_state(P, g, 2u);
+      set_state(g, 2u);
       if (I.hp && (P.rq_fl[g] & F_TICK)) tkd++;
     }
     out += __popc(mk);
@@ -330,7 +337,7 @@ __device__ __noinline__ int32_t drop_step(const SimP& P, Wp w, int k, int64_t T)
   I.wq_len = out;
   I.tk_live = tk;
   __syncwarp();
-  if (!I.hp) sort_ids(P, w, P.scr_drop + w.base, nd);  // LP queue order is key order
+  if (!I.hp) sort_ids(w, P.scr_drop + w.base, nd);  // LP queue order is key order
   return nd;
 }
 
@@ -338,7 +345,7 @@ __device__ __noinline__ int32_t drop_step(const SimP& P, Wp w, int k, int64_t T)
 // §5.4; grow each decode's KV by the blocks its next token needs (precomputed by the
 // completion pass as pending bits); while short of blocks, evict the latest-arrived decode (LIFO,
 // G31) by recomputation: generated tokens join its prompt, it re-enters the queue.
-__device__ __noinline__ int32_t evict(const SimP& P, Wp w, int k) {
+__device__ __noinline__ int32_t evict(Wp w, int k) {
   SInst& I = w.SI[k];
   const int lane = lane_id();
   int32_t np = 0;
@@ -348,15 +355,15 @@ __device__ __noinline__ int32_t evict(const SimP& P, Wp w, int k) {
     for (int32_t c = 0; c < len; c += 32) {
       const int32_t j = c + lane;
       if (j < len) {
-        const int32_t id = slotp(P, w, k, j)->x;
+        const int32_t id = slotp(w, k, j)->x;
         if (id > best) { best = id; bslot = j; }
       }
     }
     const int32_t vid = warp_max(best);
     const uint32_t who = __ballot_sync(FULL, best == vid);
     const int32_t vslot = __shfl_sync(FULL, bslot, __ffs(who) - 1);
-    const int4 s = *slotp(P, w, k, vslot);
-    const int4 last = *slotp(P, w, k, len - 1);
+    const int4 s = *slotp(w, k, vslot);
+    const int4 last = *slotp(w, k, len - 1);
     const int64_t g = w.base + vid;
     const int32_t kvf = I.kv_free + (s.w & HELD_MASK);  // blocks held before this step's growth
     const int32_t need = I.need_sum - (int32_t)((uint32_t)s.w >> 31);
@@ -366,7 +373,7 @@ __device__ __noinline__ int32_t evict(const SimP& P, Wp w, int k) {
       P.rq_eff[g] = s.y;  // eff_prompt = prompt + generated = lhat
       P.rq_fl[g] += (1u << NPRE_SHIFT);
       P.scr_pre[w.base + np] = vid;
-      *slotp(P, w, k, vslot) = last;
+      *slotp(w, k, vslot) = last;
     }
     I.kv_free = kvf;
     I.need_sum = need;
@@ -374,17 +381,17 @@ __device__ __noinline__ int32_t evict(const SimP& P, Wp w, int k) {
     I.ds_len = len - 1;
     __syncwarp();
     np++;
-    wq_insert(P, w, k, vid);
+    wq_insert(w, k, vid);
   }
   return np;
 }
 
 // returns the number of evictions; leaves the growth applied (papp = 1)
-__device__ __forceinline__ int32_t decode_prep(const SimP& P, Wp w, int k) {
+__device__ __forceinline__ int32_t decode_prep(Wp w, int k) {
   SInst& I = w.SI[k];
   if (I.papp) return 0;  // growth for the last decode step already applied
   int32_t np = 0;
-  if (I.need_sum > I.kv_free) np = evict(P, w, k);
+  if (I.need_sum > I.kv_free) np = evict(w, k);
   const int32_t kvf = I.kv_free - I.need_sum;  // pending growth of the surviving decodes
   __syncwarp();
   I.kv_free = kvf;
@@ -394,14 +401,14 @@ __device__ __forceinline__ int32_t decode_prep(const SimP& P, Wp w, int k) {
 }
 
 // mark request admitted at T on instance k
-__device__ __forceinline__ void admit_req(const SimP& P, int64_t g, int k, int64_t T) {
+__device__ __forceinline__ void admit_req(int64_t g, int k, int64_t T) {
   uint32_t f = P.rq_fl[g];
   f = (f & ~(0xffu << INST_SHIFT)) | ((uint32_t)k << INST_SHIFT) | F_EVER;
   P.rq_fl[g] = f;
   if (P.pstart[g] < 0) P.pstart[g] = T;
 }
 
-__device__ __forceinline__ void set_batch(const SimP& P, SInst& I, int64_t T, int64_t l,
+__device__ __forceinline__ void set_batch(SInst& I, int64_t T, int64_t l,
                                           int32_t bdec, int32_t nadm) {
   if (l < 0) atomicOr(P.err, ERR_RANGE);
   __syncwarp();
@@ -416,12 +423,12 @@ __device__ __forceinline__ void set_batch(const SimP& P, SInst& I, int64_t T, in
 // line-3 order: lines 5-13 read its prefix.  Offload (§5.3, G24) under EDF_LAXITY is the range
 // key <= T + W_hp + margin right after the admitted prefix (key = deadline - prefill_us makes the
 // offload test a key bound); other policies scan the whole queue.
-__device__ __noinline__ int lp_admit(const SimP& P, Wp w, int k, int64_t T, int32_t ndrop,
+__device__ __noinline__ int lp_admit(Wp w, int k, int64_t T, int32_t ndrop,
                                      int32_t npre) {
   SInst& I = w.SI[k];
   const int lane = lane_id();
-  const int64_t o = ioff(P, k, w);  // running-batch list base
-  const int64_t q = qoff(P, I, k, w);
+  const int64_t o = ioff(k, w);  // running-batch list base
+  const int64_t q = qoff(I, k, w);
   const int64_t Bd = I.ds_len;
   const int64_t sl = I.ctx_sum;
   // budgets (G22)
@@ -444,8 +451,8 @@ __device__ __noinline__ int lp_admit(const SimP& P, Wp w, int k, int64_t T, int3
     const int32_t id = valid ? P.wq_id[q + pos] : 0;
     const int64_t g = w.base + id;
     const int32_t p = valid ? P.rq_eff[g] : 0;
-    const int64_t pf = valid ? pf_of(P, p) : 0;
-    const int64_t bl = valid ? blk_of(P, p) : 0;
+    const int64_t pf = valid ? pf_of(p) : 0;
+    const int64_t bl = valid ? blk_of(p) : 0;
     const int64_t St = ct + warp_incl_scan((int64_t)p);
     const int64_t Sb = cb + warp_incl_scan(bl);
     const int64_t Sc = cc + warp_incl_scan(pf);
@@ -453,7 +460,7 @@ __device__ __noinline__ int lp_admit(const SimP& P, Wp w, int k, int64_t T, int3
     const uint32_t m = __ballot_sync(FULL, ok);
     const int cnt = (m == FULL) ? 32 : (__ffs(~m) - 1);
     if (lane < cnt) {
-      admit_req(P, g, k, T);
+      admit_req(g, k, T);
       P.bp_id[o + pos] = id;
       const uint64_t u = (uint64_t)p;
       sp += u;
@@ -525,7 +532,7 @@ __device__ __noinline__ int lp_admit(const SimP& P, Wp w, int k, int64_t T, int3
           key = P.wq_key[q2 + j];
           const int64_t g = w.base + id;
           off = !(P.rq_fl[g] & (F_EVER | F_ONHP)) &&
-                P.rq_dl[g] - T <= pf_of(P, P.rq_eff[g]) + P.W + P.margin;
+                P.rq_dl[g] - T <= pf_of(P.rq_eff[g]) + P.W + P.margin;
         }
         const uint32_t mk = __ballot_sync(FULL, v && !off), mo = __ballot_sync(FULL, off);
         if (v && !off) {
@@ -540,7 +547,7 @@ __device__ __noinline__ int lp_admit(const SimP& P, Wp w, int k, int64_t T, int3
       }
       rem = out;
     }
-    sort_ids(P, w, P.scr_off + w.base, noff);  // dispatch and digest in ascending id order
+    sort_ids(w, P.scr_off + w.base, noff);  // dispatch and digest in ascending id order
   }
   const int32_t kvf = I.kv_free - (int32_t)used;
   __syncwarp();
@@ -567,22 +574,22 @@ __device__ __noinline__ int lp_admit(const SimP& P, Wp w, int k, int64_t T, int3
       }
     }
     __syncwarp();
-    if (P.delay == 0) wq_insert(P, w, h, id);
+    if (P.delay == 0) wq_insert(w, h, id);
   }
   // batch (§5.4): decodes piggybacked with the admitted prefills
   const bool nonempty = nadm > 0 || Bd > 0;
   int64_t l = 0;
   if (nonempty) {
     l = nadm ? lat_us(P.md, (uint64_t)nadm, sp, sp2, spc, (uint64_t)Bd, (uint64_t)sl) : ldec;
-    set_batch(P, I, T, l, Bd > 0, nadm);
+    set_batch(I, T, l, Bd > 0, nadm);
   }
   if (nonempty || noff || ndrop || npre)
-    digest_log(P, w, k, T, nadm, nonempty ? Bd : 0, noff, ndrop, npre, l);
+    digest_log(w, k, T, nadm, nonempty ? Bd : 0, noff, ndrop, npre, l);
   return nonempty ? 1 : 0;
 }
 
 // one decode-only batch of the whole decode set (LP with an empty queue, or HP) — the hot path
-__device__ __forceinline__ void decode_batch(const SimP& P, SInst& I, int k, int64_t T) {
+__device__ __forceinline__ void decode_batch(SInst& I, int k, int64_t T) {
   const int32_t bd = I.ds_len;
   const int64_t l = lat_decode(P.md, (uint64_t)bd, (uint64_t)I.ctx_sum);
   if (l < 0) atomicOr(P.err, ERR_RANGE);
@@ -598,41 +605,41 @@ __device__ __forceinline__ void decode_batch(const SimP& P, SInst& I, int k, int
 }
 
 // returns (waiting-queue entries evaluated << 1) | (1 if a batch was formed)
-__device__ __forceinline__ int64_t form_lp(const SimP& P, Wp w, int k, int64_t T) {
+__device__ __forceinline__ int64_t form_lp(Wp w, int k, int64_t T) {
   SInst& I = w.SI[k];
   if (I.wq_len == 0) {
     if (I.ds_len == 0) return 0;  // parked
-    const int32_t np = decode_prep(P, w, k);
+    const int32_t np = decode_prep(w, k);
     if (np == 0) {  // no eviction: the common case, a pure decode step
-      decode_batch(P, I, k, T);
+      decode_batch(I, k, T);
       return 1;
     }
     const int64_t ev = (int64_t)I.wq_len << 1;  // the queue now holds the evicted decodes
-    return ev | lp_admit(P, w, k, T, 0, np);
+    return ev | lp_admit(w, k, T, 0, np);
   }
-  const int32_t ndrop = P.drop ? drop_step(P, w, k, T) : 0;
-  const int32_t npre = I.ds_len ? decode_prep(P, w, k) : 0;
+  const int32_t ndrop = P.drop ? drop_step(w, k, T) : 0;
+  const int32_t npre = I.ds_len ? decode_prep(w, k) : 0;
   const int64_t ev = (int64_t)I.wq_len << 1;
   if (I.wq_len == 0) {
     const int64_t Bd = I.ds_len;
     int64_t l = 0;
     if (Bd) {
       l = lat_decode(P.md, (uint64_t)Bd, (uint64_t)I.ctx_sum);
-      set_batch(P, I, T, l, 1, 0);
+      set_batch(I, T, l, 1, 0);
     }
-    digest_log(P, w, k, T, 0, Bd, 0, ndrop, 0, l);  // ndrop > 0 here
+    digest_log(w, k, T, 0, Bd, 0, ndrop, 0, l);  // ndrop > 0 here
     return ev | (Bd ? 1 : 0);
   }
-  return ev | lp_admit(P, w, k, T, ndrop, npre);
+  return ev | lp_admit(w, k, T, ndrop, npre);
 }
 
 // --------------------------------------------------------------------------- HP formation ---
 // FCFS prefill-first under the (elastic) token limit (G27-G28).
-__device__ __noinline__ int32_t hp_prefill(const SimP& P, Wp w, int k, int64_t T, uint64_t* mom) {
+__device__ __noinline__ int32_t hp_prefill(Wp w, int k, int64_t T, uint64_t* mom) {
   SInst& I = w.SI[k];
   const int lane = lane_id();
-  const int64_t o = ioff(P, k, w);
-  const int64_t q = qoff(P, I, k, w);
+  const int64_t o = ioff(k, w);
+  const int64_t q = qoff(I, k, w);
   int64_t limit = P.hp_tok;
   if (P.elastic) {
     const int64_t mean = I.hist_cnt ? I.hist_sum / I.hist_cnt : (int64_t)P.hist_def;
@@ -649,14 +656,14 @@ __device__ __noinline__ int32_t hp_prefill(const SimP& P, Wp w, int k, int64_t T
     const bool v = j < len;
     int32_t id = 0, p = 0;
     if (v) { id = P.wq_id[q + j]; p = P.rq_eff[w.base + id]; }
-    const int64_t bl = v ? blk_of(P, p) : 0;
+    const int64_t bl = v ? blk_of(p) : 0;
     const int64_t St = ct + warp_incl_scan((int64_t)p);
     const int64_t Sb = cb + warp_incl_scan(bl);
     const bool ok = v && ((j == 0) ? (bl <= kvf) : (St <= limit && Sb <= kvf));
     const uint32_t m = __ballot_sync(FULL, ok);
     const int cnt = (m == FULL) ? 32 : (__ffs(~m) - 1);
     if (lane < cnt) {
-      admit_req(P, w.base + id, k, T);
+      admit_req(w.base + id, k, T);
       P.bp_id[o + j] = id;
       const uint64_t u = (uint64_t)p;
       sp += u;
@@ -683,22 +690,22 @@ __device__ __noinline__ int32_t hp_prefill(const SimP& P, Wp w, int k, int64_t T
   return nadm;
 }
 
-__device__ __noinline__ int64_t form_hp_general(const SimP& P, Wp w, int k, int64_t T) {
+__device__ __noinline__ int64_t form_hp_general(Wp w, int k, int64_t T) {
   SInst& I = w.SI[k];
-  const int32_t ndrop = (P.drop && I.wq_len) ? drop_step(P, w, k, T) : 0;
+  const int32_t ndrop = (P.drop && I.wq_len) ? drop_step(w, k, T) : 0;
   const int64_t ev = (int64_t)I.wq_len << 1;
   uint64_t mom[3] = {0, 0, 0};
   int32_t nadm = 0, npre = 0;
   int64_t bd = 0;
   bool batch = false;
-  if (I.wq_len > 0) { nadm = hp_prefill(P, w, k, T, mom); batch = nadm > 0; }  // prefill first
+  if (I.wq_len > 0) { nadm = hp_prefill(w, k, T, mom); batch = nadm > 0; }  // prefill first
   if (!batch && I.ds_len > 0) {
-    npre = decode_prep(P, w, k);
+    npre = decode_prep(w, k);
     if (I.ds_len > 0) {
       batch = true;
       bd = I.ds_len;
     } else if (I.wq_len > 0) {  // every decode was evicted (G43)
-      nadm = hp_prefill(P, w, k, T, mom);
+      nadm = hp_prefill(w, k, T, mom);
       batch = nadm > 0;
     }
   }
@@ -706,33 +713,33 @@ __device__ __noinline__ int64_t form_hp_general(const SimP& P, Wp w, int k, int6
   if (batch) {
     l = bd ? lat_decode(P.md, (uint64_t)bd, (uint64_t)I.ctx_sum)
            : lat_us(P.md, (uint64_t)nadm, mom[0], mom[1], mom[2], 0, 0);
-    set_batch(P, I, T, l, bd > 0, bd ? 0 : nadm);
+    set_batch(I, T, l, bd > 0, bd ? 0 : nadm);
   }
-  if (batch || ndrop || npre) digest_log(P, w, k, T, bd ? 0 : nadm, bd, 0, ndrop, npre, l);
+  if (batch || ndrop || npre) digest_log(w, k, T, bd ? 0 : nadm, bd, 0, ndrop, npre, l);
   return ev | (batch ? 1 : 0);
 }
 
-__device__ __forceinline__ int64_t form_hp(const SimP& P, Wp w, int k, int64_t T) {
+__device__ __forceinline__ int64_t form_hp(Wp w, int k, int64_t T) {
   SInst& I = w.SI[k];
   if (I.wq_len == 0) {
     if (I.ds_len == 0) return 0;  // parked
     if (I.papp || I.need_sum <= I.kv_free) {  // decode-only batch without eviction: hot path
-      decode_prep(P, w, k);
-      decode_batch(P, I, k, T);
+      decode_prep(w, k);
+      decode_batch(I, k, T);
       return 1;
     }
   }
-  return form_hp_general(P, w, k, T);
+  return form_hp_general(w, k, T);
 }
 
 // ------------------------------------------------------------------ phase A: batch completion --
-__device__ __forceinline__ void finish_req(const SimP& P, int64_t g, int64_t T) {
+__device__ __forceinline__ void finish_req(int64_t g, int64_t T) {
   P.done[g] = T;
-  set_state(P, g, 1u);
+  set_state(g, 1u);
 }
 
 // per finished request: blocks freed, HP history, resident-ticket release (G29)
-__device__ __noinline__ void finish_sums(const SimP& P, Wp w, int k, int64_t freed, int64_t hsum,
+__device__ __noinline__ void finish_sums(Wp w, int k, int64_t freed, int64_t hsum,
                                          int32_t hcnt, int32_t tkd, int64_t cfin) {
   freed = warp_sum(freed);
   hsum = warp_sum(hsum);
@@ -752,10 +759,10 @@ __device__ __noinline__ void finish_sums(const SimP& P, Wp w, int k, int64_t fre
 }
 
 // prefill completions: first token, then completion or entry into the decode set
-__device__ __noinline__ void complete_prefills(const SimP& P, Wp w, int k, int64_t T) {
+__device__ __noinline__ void complete_prefills(Wp w, int k, int64_t T) {
   SInst& I = w.SI[k];
   const int lane = lane_id();
-  const int64_t o = ioff(P, k, w);
+  const int64_t o = ioff(k, w);
   const int32_t blen = I.bp_len;
   int32_t dlen = I.ds_len;
   int64_t freed = 0, hsum = 0, cadd = 0;
@@ -771,9 +778,9 @@ __device__ __noinline__ void complete_prefills(const SimP& P, Wp w, int k, int64
       const int32_t eff = P.rq_eff[g], p = P.pl[g], out_len = P.ol[g];
       const int32_t gen = eff - p + 1;  // tokens generated after this prefill
       if (P.first[g] < 0) P.first[g] = T;
-      const int32_t held = blk_of(P, eff);
+      const int32_t held = blk_of(eff);
       if (gen == out_len) {
-        finish_req(P, g, T);
+        finish_req(g, T);
         freed += held;
         if (I.hp) { hsum += out_len; hcnt++; if (P.rq_fl[g] & F_TICK) tkd++; }
       } else {
@@ -784,7 +791,7 @@ __device__ __noinline__ void complete_prefills(const SimP& P, Wp w, int k, int64
       }
     }
     const uint32_t ms = __ballot_sync(FULL, stay);
-    if (stay) *slotp(P, w, k, dlen + __popc(ms & lanemask_lt())) = s;
+    if (stay) *slotp(w, k, dlen + __popc(ms & lanemask_lt())) = s;
     dlen += __popc(ms);
   }
   freed = warp_sum(freed);
@@ -806,7 +813,7 @@ __device__ __noinline__ void complete_prefills(const SimP& P, Wp w, int k, int64
 
 // The decode step just executed: one pass over the slots — l̂+1, remaining−1, completions, and
 // the block the next formation will need (pending bit: l̂ mod bs was 0 before the step).
-__device__ __forceinline__ void complete(const SimP& P, Wp w, int k, int64_t T) {
+__device__ __forceinline__ void complete(Wp w, int k, int64_t T) {
   SInst& I = w.SI[k];
   const int lane = lane_id();
   if (I.batch_dec) {
@@ -820,7 +827,7 @@ __device__ __forceinline__ void complete(const SimP& P, Wp w, int k, int64_t T) 
       const int32_t j = c + lane;
       const bool v = j < dlen;
       int4 s = make_int4(0, 0, 1, 0);
-      if (v) s = *slotp(P, w, k, j);
+      if (v) s = *slotp(w, k, j);
       const int32_t held = (s.w & HELD_MASK) + (int32_t)((uint32_t)s.w >> 31);  // growth applied
       const int32_t r = (s.w >> R_SHIFT) & 0x1ff;
       const bool pend = r == 0;
@@ -834,12 +841,12 @@ __device__ __forceinline__ void complete(const SimP& P, Wp w, int k, int64_t T) 
       need += __popc(__ballot_sync(FULL, v && !fin && pend));
       // stable compaction (positions == j until the first completion); every lane has read its
       // slot before the ballots above, so in-place writes are safe
-      if (v && !fin) *slotp(P, w, k, out + __popc(mk & lanemask_lt())) = s;
+      if (v && !fin) *slotp(w, k, out + __popc(mk & lanemask_lt())) = s;
       if (mf) {
         anyfin = true;
         if (fin) {
           const int64_t g = w.base + s.x;
-          finish_req(P, g, T);
+          finish_req(g, T);
           freed += held;
           cfin += s.y;
           if (I.hp) { hsum += P.ol[g]; hcnt++; if (P.rq_fl[g] & F_TICK) tkd++; }
@@ -854,9 +861,9 @@ __device__ __forceinline__ void complete(const SimP& P, Wp w, int k, int64_t T) 
     I.need_sum = need;
     I.papp = 0;
     __syncwarp();
-    if (anyfin) finish_sums(P, w, k, freed, hsum, hcnt, tkd, cfin);
+    if (anyfin) finish_sums(w, k, freed, hsum, hcnt, tkd, cfin);
   }
-  if (I.bp_len) complete_prefills(P, w, k, T);
+  if (I.bp_len) complete_prefills(w, k, T);
   __syncwarp();
   I.bp_len = 0;
   I.batch_dec = 0;
@@ -865,7 +872,7 @@ __device__ __forceinline__ void complete(const SimP& P, Wp w, int k, int64_t T) 
 }
 
 // --------------------------------------------------------------------- controller routing ---
-__device__ __forceinline__ void route(const SimP& P, Wp w, int32_t id) {
+__device__ __forceinline__ void route(Wp w, int32_t id) {
   if (P.tickets) {
     for (int h = P.n_lp; h < P.K; h++) {
       if (w.SI[h].ticket) {
@@ -875,23 +882,23 @@ __device__ __forceinline__ void route(const SimP& P, Wp w, int32_t id) {
         w.SI[h].ticket = 0;
         w.SI[h].tk_live = tk;
         __syncwarp();
-        wq_append(P, w, h, id);  // the newest arrival has the largest id: stays sorted
+        wq_append(w, h, id);  // the newest arrival has the largest id: stays sorted
         return;
       }
     }
   }
   const int32_t rr = w.ts->rr_lp;
-  wq_insert(P, w, rr, id);
+  wq_insert(w, rr, id);
   w.ts->rr_lp = (rr + 1) == P.n_lp ? 0 : rr + 1;
   __syncwarp();
 }
 
-__device__ __noinline__ void deliver(const SimP& P, Wp w, int64_t T) {
+__device__ __noinline__ void deliver(Wp w, int64_t T) {
   while (w.ts->fl_head < w.ts->fl_tail && P.fl_t[w.base + w.ts->fl_head] == T) {
     const int32_t head = w.ts->fl_head;
     const int32_t id = P.fl_req[w.base + head];
     const int h = P.fl_hp[w.base + head];
-    wq_insert(P, w, h, id);
+    wq_insert(w, h, id);
     w.ts->fl_head = head + 1;
     __syncwarp();
   }
@@ -906,7 +913,7 @@ __device__ __noinline__ void deliver(const SimP& P, Wp w, int64_t T) {
 // from a histogram of l̂ mod bs, Σl̂ in closed form, latencies in parallel (Eq. 4-5), start times by
 // a prefix sum, and the per-instance digest chain applied in order.  Exactly the same formations,
 // times and digest as stepping them one by one through the event loop.
-__device__ __noinline__ int64_t run_decode(const SimP& P, Wp w, int k, int64_t T_limit) {
+__device__ __noinline__ int64_t run_decode(Wp w, int k, int64_t T_limit) {
   SInst& I = w.SI[k];
   const int lane = lane_id();
   const int32_t bs = P.bs;
@@ -930,7 +937,7 @@ __device__ __noinline__ int64_t run_decode(const SimP& P, Wp w, int k, int64_t T
   for (int32_t c = 0; c < Bd; c += 32) {
     const int32_t j = c + lane;
     if (j < Bd) {
-      const int4 sl = *slotp(P, w, k, j);
+      const int4 sl = *slotp(w, k, j);
       mrem = min(mrem, sl.z);
       atomicAdd(&hA[(sl.w >> R_SHIFT) & 0x1ff], 1);
     }
@@ -982,7 +989,7 @@ __device__ __noinline__ int64_t run_decode(const SimP& P, Wp w, int k, int64_t T
       const int32_t j = c0 + lane;
       const bool v = j < Bd;
       int4 sl = make_int4(0, 0, 1 << 30, 0);
-      if (v) sl = *slotp(P, w, k, j);
+      if (v) sl = *slotp(w, k, j);
       const int32_t r0 = (sl.w >> R_SHIFT) & 0x1ff;
       const int32_t pend0 = (int32_t)((uint32_t)sl.w >> 31);
       // growth applied at formations 0 .. nstep-1 uses the pending bits of completions 0 .. nstep-1
@@ -1000,7 +1007,7 @@ __device__ __noinline__ int64_t run_decode(const SimP& P, Wp w, int k, int64_t T
       const bool keep = v && !fin;
       const uint32_t mk = __ballot_sync(FULL, keep);
       if (keep) {
-        *slotp(P, w, k, out + __popc(mk & lanemask_lt())) = sl;
+        *slotp(w, k, out + __popc(mk & lanemask_lt())) = sl;
         mrem2 = min(mrem2, sl.z);
         atomicAdd(&hB[rN], 1);
         need2 += pend ? 1 : 0;
@@ -1008,7 +1015,7 @@ __device__ __noinline__ int64_t run_decode(const SimP& P, Wp w, int k, int64_t T
       }
       if (fin) {  // completion at Et: done, KV freed, HP history / ticket bookkeeping
         const int64_t g = w.base + sl.x;
-        finish_req(P, g, Et);
+        finish_req(g, Et);
         freed += held;  // held_base after nstep completions = blocks held when it finishes
         if (hp) { hsum += P.ol[g]; hcnt++; if (P.rq_fl[g] & F_TICK) tkd++; }
       }
@@ -1076,7 +1083,7 @@ __device__ __noinline__ int64_t run_decode(const SimP& P, Wp w, int k, int64_t T
   return total;
 }
 
-__device__ __noinline__ void init_trace(const SimP& P, Wp w, int trace) {
+__device__ __noinline__ void init_trace(Wp w, int trace) {
   const int lane = lane_id();
   if (lane == 0) { w.ts->rr_lp = w.ts->rr_hp = w.ts->fl_head = w.ts->fl_tail = 0; }
   const int64_t ttft = P.ttft[trace];
@@ -1102,7 +1109,7 @@ __device__ __noinline__ void init_trace(const SimP& P, Wp w, int trace) {
   __syncwarp();
 }
 
-__device__ __noinline__ void finish_trace(const SimP& P, Wp w, int trace, int64_t decisions,
+__device__ __noinline__ void finish_trace(Wp w, int trace, int64_t decisions,
                                           int64_t evals) {
   const int lane = lane_id();
   bool stuck = false;
@@ -1131,7 +1138,7 @@ __device__ __noinline__ void finish_trace(const SimP& P, Wp w, int trace, int64_
 #ifndef ASC_SIM_MINB
 #define ASC_SIM_MINB 8  // CTAs per SM the register budget must allow (8 -> 64 registers/thread)
 #endif
-__global__ void __launch_bounds__(SW * 32, ASC_SIM_MINB) sim_kernel(const __grid_constant__ SimP P) {
+__global__ void __launch_bounds__(SW * 32, ASC_SIM_MINB) sim_kernel() {
   extern __shared__ __align__(16) unsigned char smem[];
   const int wi = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const size_t per_warp = 64 * sizeof(KI) + (size_t)P.K * DCAP * sizeof(int4) +
@@ -1152,7 +1159,7 @@ __global__ void __launch_bounds__(SW * 32, ASC_SIM_MINB) sim_kernel(const __grid
     w.base = P.off[trace];
     w.n = P.off[trace + 1] - w.base;
     w.tbt = P.tbt[trace];
-    init_trace(P, w, trace);
+    init_trace(w, trace);
     int64_t next = 0, next_arr = w.n > 0 ? P.arr[w.base] : INF64, decisions = 0, evals = 0;
     while (true) {
       int64_t T = next_arr;
@@ -1168,26 +1175,26 @@ __global__ void __launch_bounds__(SW * 32, ASC_SIM_MINB) sim_kernel(const __grid
       if (T == INF64) break;
       // A. completions in instance order
       for (int k = 0; k < K; k++)
-        if (w.SI[k].end == T) complete(P, w, k, T);
+        if (w.SI[k].end == T) complete(w, k, T);
       // B. offload deliveries (FIFO = time order)
-      if (flight) deliver(P, w, T);
+      if (flight) deliver(w, T);
       // C. arrivals, ascending id
       while (next_arr == T) {
-        route(P, w, (int32_t)next);
+        route(w, (int32_t)next);
         next++;
         next_arr = next < w.n ? P.arr[w.base + next] : INF64;
       }
       // D. formations of idle instances, LPs before HPs
       for (int k = 0; k < n_lp; k++) {
         if (w.SI[k].end == INF64) {
-          const int64_t r = form_lp(P, w, k, T);
+          const int64_t r = form_lp(w, k, T);
           decisions += r & 1;
           evals += r >> 1;
         }
       }
       for (int k = n_lp; k < K; k++) {
         if (w.SI[k].end == INF64) {
-          const int64_t r = form_hp(P, w, k, T);
+          const int64_t r = form_hp(w, k, T);
           decisions += r & 1;
           evals += r >> 1;
         }
@@ -1212,10 +1219,10 @@ __global__ void __launch_bounds__(SW * 32, ASC_SIM_MINB) sim_kernel(const __grid
         const SInst& I = w.SI[k];
         const int64_t lim = k < n_lp ? next_arr : tl_hp;
         if (I.end < lim && I.batch_dec && I.bp_len == 0 && I.wq_len == 0)
-          decisions += run_decode(P, w, k, lim);
+          decisions += run_decode(w, k, lim);
       }
     }
-    finish_trace(P, w, trace, decisions, evals);
+    finish_trace(w, trace, decisions, evals);
   }
 }
 
@@ -1225,7 +1232,7 @@ size_t sim_smem_per_warp(int K) {
 }
 
 // liveness / layout validation (ASC_E_CONFIG / ASC_E_INVAL before simulating)
-__global__ void validate_traces(SimP P, int64_t R) {
+__global__ void validate_traces(int64_t R) {
   if (blockIdx.x == 0 && threadIdx.x == 0 && P.off[P.T] != R) atomicOr(P.err, ERR_INVAL);
   for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < R;
        g += (int64_t)gridDim.x * blockDim.x) {
@@ -1271,6 +1278,13 @@ __global__ void goodput_kernel(int32_t T, const int64_t* off, const int64_t* arr
     }
   }
 }
+
+cudaError_t upload_params(const SimP& h, cudaStream_t s) {
+  return cudaMemcpyToSymbolAsync(P, &h, sizeof(SimP), 0, cudaMemcpyHostToDevice, s);
+}
+
+// the constant-bank parameters are per device: simulate calls on one device are serialised
+std::mutex g_sim_mu[64];
 
 }  // namespace
 
@@ -1323,10 +1337,13 @@ asc_status launch_simulate(asc_ctx* c, const asc_traces* tr, asc_outcomes* out, 
   P.next_trace = ar.take<int>(1);
   P.err = c->d_err;
   cudaStream_t sm = c->stream;
+  std::lock_guard<std::mutex> lock(g_sim_mu[c->device & 63]);
+  cudaError_t ue = upload_params(P, sm);
+  if (ue != cudaSuccess) return cuda_check(c, ue, "simulate parameters");
   int64_t launches = 0;
   if (R > 0) {
     const int64_t gb = (R + 255) / 256;
-    validate_traces<<<(unsigned)(gb < 4096 ? gb : 4096), 256, 0, sm>>>(P, R);
+    validate_traces<<<(unsigned)(gb < 4096 ? gb : 4096), 256, 0, sm>>>(R);
     launches++;
     asc_status v = collect_errors(c, "simulate_batch validation");
     if (v) return v;
@@ -1344,13 +1361,15 @@ asc_status launch_simulate(asc_ctx* c, const asc_traces* tr, asc_outcomes* out, 
   }
   if (blocks > 0) {
     cudaEventRecord(c->ev0, sm);
-    sim_kernel<<<(unsigned)blocks, SW * 32, smem, sm>>>(P);
+    sim_kernel<<<(unsigned)blocks, SW * 32, smem, sm>>>();
     cudaEventRecord(c->ev1, sm);
     c->timed = true;
     launches++;
   }
   c->last_kernel_launches = launches;
-  return cuda_check(c, cudaGetLastError(), "simulate launch");
+  cudaError_t le = cudaGetLastError();
+  if (le == cudaSuccess) le = cudaStreamSynchronize(sm);  // the parameters stay in use until here
+  return cuda_check(c, le, "simulate launch");
 }
 
 asc_status launch_goodput(asc_ctx* c, const asc_traces* tr, const asc_outcomes* out,
