@@ -78,6 +78,7 @@ struct SimP {
   int32_t *fl_req, *fl_hp;
   int* err;
   int* next_trace;
+  int32_t pw, o_sd, o_si, o_ts;  // per-warp shared-memory layout (bytes)
 };
 
 // The launch parameters live in the constant bank (one copy per device, written before each launch
@@ -86,16 +87,26 @@ struct SimP {
 __constant__ SimP P;
 
 
-struct TS {  // mutable per-trace controller state (shared memory, one per warp)
+struct TS {  // per-trace controller state (shared memory, one per warp)
   int32_t rr_lp, rr_hp, fl_head, fl_tail;
+  int64_t base, n, tbt;  // the trace's first request, its size and its TBT SLO
 };
 
-struct Wp {  // per-warp trace context, passed by value (uniform across the warp)
-  SInst* SI;
-  int4* sd;
-  KI* buf;
-  TS* ts;
-  int64_t base, n, tbt;
+// Per-warp trace context.  Empty: every member is recomputed from the warp index and the
+// constant-bank layout, so nothing is passed in registers across the out-of-line calls and the
+// compiler sees shared-memory addresses (LDS/STS, not generic loads).
+struct Wp {
+  __device__ __forceinline__ unsigned char* mine() const {
+    extern __shared__ __align__(16) unsigned char smem[];
+    return smem + (threadIdx.x >> 5) * P.pw;
+  }
+  __device__ __forceinline__ KI* buf() const { return reinterpret_cast<KI*>(mine()); }
+  __device__ __forceinline__ int4* sd() const { return reinterpret_cast<int4*>(mine() + P.o_sd); }
+  __device__ __forceinline__ SInst* SI() const { return reinterpret_cast<SInst*>(mine() + P.o_si); }
+  __device__ __forceinline__ TS* ts() const { return reinterpret_cast<TS*>(mine() + P.o_ts); }
+  __device__ __forceinline__ int64_t base() const { return ts()->base; }
+  __device__ __forceinline__ int64_t n() const { return ts()->n; }
+  __device__ __forceinline__ int64_t tbt() const { return ts()->tbt; }
 };
 
 __device__ __forceinline__ int64_t pf_of(int32_t p) {
@@ -117,9 +128,9 @@ __device__ __forceinline__ int64_t key_of(int64_t gid, int32_t eff) {
   }
 }
 
-__device__ __forceinline__ int64_t ioff(int k, Wp w) { return (int64_t)k * P.R + w.base; }
+__device__ __forceinline__ int64_t ioff(int k, Wp w) { return (int64_t)k * P.R + w.base(); }
 __device__ __forceinline__ int4* slotp(Wp w, int k, int32_t j) {
-  return j < DCAP ? (w.sd + k * DCAP + j) : (P.ds_g + (int64_t)k * P.R + w.base + j);
+  return j < DCAP ? (w.sd() + k * DCAP + j) : (P.ds_g + (int64_t)k * P.R + w.base() + j);
 }
 __device__ __forceinline__ void set_state(int64_t g, uint32_t st) {
   const uint32_t f = P.rq_fl[g];
@@ -151,17 +162,17 @@ __device__ __noinline__ void digest_log(Wp w, int k, int64_t T, int32_t nadm,
   }
   for (int32_t j = lane; j < nadm; j += 32) acc += mix64((uint64_t)P.bp_id[o + j] + (uint64_t)(3 + j + 1) * GOLD);
   for (int32_t j = lane; j < noff; j += 32)
-    acc += mix64((uint64_t)P.scr_off[w.base + j] + (uint64_t)(5 + nadm + j + 1) * GOLD);
+    acc += mix64((uint64_t)P.scr_off[w.base() + j] + (uint64_t)(5 + nadm + j + 1) * GOLD);
   for (int32_t j = lane; j < ndrop; j += 32)
-    acc += mix64((uint64_t)P.scr_drop[w.base + j] + (uint64_t)(6 + nadm + noff + j + 1) * GOLD);
+    acc += mix64((uint64_t)P.scr_drop[w.base() + j] + (uint64_t)(6 + nadm + noff + j + 1) * GOLD);
   for (int32_t j = lane; j < npre; j += 32)
-    acc += mix64((uint64_t)P.scr_pre[w.base + j] + (uint64_t)(7 + nadm + noff + ndrop + j + 1) * GOLD);
+    acc += mix64((uint64_t)P.scr_pre[w.base() + j] + (uint64_t)(7 + nadm + noff + ndrop + j + 1) * GOLD);
   acc = warp_sum(acc);
-  const uint64_t nr = w.SI[k].nrec + 1;
-  const uint64_t h = w.SI[k].hash + mix64(acc + nr * GOLD2);
+  const uint64_t nr = w.SI()[k].nrec + 1;
+  const uint64_t h = w.SI()[k].hash + mix64(acc + nr * GOLD2);
   __syncwarp();
-  w.SI[k].hash = h;  // uniform values, every lane stores the same words
-  w.SI[k].nrec = nr;
+  w.SI()[k].hash = h;  // uniform values, every lane stores the same words
+  w.SI()[k].nrec = nr;
   __syncwarp();
 }
 
@@ -191,7 +202,7 @@ __device__ __forceinline__ int64_t qoff(const SInst& I, int k, Wp w) {
 
 // make room for one more entry at the tail (compacts the queue to the region start if needed)
 __device__ __noinline__ void wq_compact(Wp w, int k) {
-  SInst& I = w.SI[k];
+  SInst& I = w.SI()[k];
   const int lane = lane_id();
   const int64_t o = ioff(k, w);
   const int32_t h = I.wq_head, len = I.wq_len;
@@ -211,12 +222,12 @@ __device__ __noinline__ void wq_compact(Wp w, int k) {
 // insert request id in order: LP by (key, id), HP by id.  The position is searched from the tail:
 // new arrivals carry the largest ids and, under the laxity key, keys near the largest.
 __device__ __noinline__ void wq_insert(Wp w, int k, int32_t id) {
-  SInst& I = w.SI[k];
+  SInst& I = w.SI()[k];
   const int lane = lane_id();
-  if (I.wq_head + I.wq_len >= (int32_t)w.n) wq_compact(w, k);
+  if (I.wq_head + I.wq_len >= (int32_t)w.n()) wq_compact(w, k);
   const int64_t q = qoff(I, k, w);
   const int32_t len = I.wq_len;
-  const int64_t key = key_of(w.base + id, P.rq_eff[w.base + id]);
+  const int64_t key = key_of(w.base() + id, P.rq_eff[w.base() + id]);
   const bool by_id = I.hp;
   int32_t pos = len;  // number of entries ordered before the new one
   for (int32_t c = len - 1; c >= 0; c -= 32) {
@@ -252,11 +263,11 @@ __device__ __noinline__ void wq_insert(Wp w, int k, int32_t id) {
 
 // append (HP ticket: the newest arrival has the largest id, so the order is kept)
 __device__ __forceinline__ void wq_append(Wp w, int k, int32_t id) {
-  SInst& I = w.SI[k];
-  if (I.wq_head + I.wq_len >= (int32_t)w.n) wq_compact(w, k);
+  SInst& I = w.SI()[k];
+  if (I.wq_head + I.wq_len >= (int32_t)w.n()) wq_compact(w, k);
   const int64_t q = qoff(I, k, w);
   const int32_t len = I.wq_len;
-  const int64_t key = key_of(w.base + id, P.rq_eff[w.base + id]);
+  const int64_t key = key_of(w.base() + id, P.rq_eff[w.base() + id]);
   __syncwarp();
   if (lane_id() == 0) {
     P.wq_id[q + len] = id;
@@ -287,7 +298,7 @@ __device__ __noinline__ void sort_ids(Wp w, int32_t* a, int32_t n) {
     __syncwarp();
     return;
   }
-  int32_t* tmp = P.scr_tmp + w.base;
+  int32_t* tmp = P.scr_tmp + w.base();
   for (int32_t i = lane; i < n; i += 32) {
     const int32_t x = a[i];
     int32_t r = 0;
@@ -302,7 +313,7 @@ __device__ __noinline__ void sort_ids(Wp w, int32_t* a, int32_t n) {
 // Drop rule (G34): waiting, never prefilled, strictly past the deadline.  Stable
 // compaction of the queue (order kept); dropped ids go to scr_drop in ascending id order.
 __device__ __noinline__ int32_t drop_step(Wp w, int k, int64_t T) {
-  SInst& I = w.SI[k];
+  SInst& I = w.SI()[k];
   const int lane = lane_id();
   const int64_t q = qoff(I, k, w);
   const int32_t len = I.wq_len;
@@ -316,14 +327,14 @@ __device__ __noinline__ int32_t drop_step(Wp w, int k, int64_t T) {
     if (v) {
       id = P.wq_id[q + j];
       key = P.wq_key[q + j];
-      const int64_t g = w.base + id;
+      const int64_t g = w.base() + id;
       dr = !(P.rq_fl[g] & F_EVER) && T > P.rq_dl[g];
     }
     const uint32_t mk = __ballot_sync(FULL, v && !dr), md = __ballot_sync(FULL, dr);
     if (v && !dr) { const int32_t o2 = out + __popc(mk & lanemask_lt()); P.wq_id[q + o2] = id; P.wq_key[q + o2] = key; }
     if (dr) {
-      const int64_t g = w.base + id;
-      P.scr_drop[w.base + nd + __popc(md & lanemask_lt())] = id;
+      const int64_t g = w.base() + id;
+      P.scr_drop[w.base() + nd + __popc(md & lanemask_lt())] = id;
       set_state(g, 2u);
       if (I.hp && (P.rq_fl[g] & F_TICK)) tkd++;
     }
@@ -337,7 +348,7 @@ __device__ __noinline__ int32_t drop_step(Wp w, int k, int64_t T) {
   I.wq_len = out;
   I.tk_live = tk;
   __syncwarp();
-  if (!I.hp) sort_ids(w, P.scr_drop + w.base, nd);  // LP queue order is key order
+  if (!I.hp) sort_ids(w, P.scr_drop + w.base(), nd);  // LP queue order is key order
   return nd;
 }
 
@@ -346,7 +357,7 @@ __device__ __noinline__ int32_t drop_step(Wp w, int k, int64_t T) {
 // completion pass as pending bits); while short of blocks, evict the latest-arrived decode (LIFO,
 // G31) by recomputation: generated tokens join its prompt, it re-enters the queue.
 __device__ __noinline__ int32_t evict(Wp w, int k) {
-  SInst& I = w.SI[k];
+  SInst& I = w.SI()[k];
   const int lane = lane_id();
   int32_t np = 0;
   while (I.need_sum > I.kv_free) {
@@ -364,7 +375,7 @@ __device__ __noinline__ int32_t evict(Wp w, int k) {
     const int32_t vslot = __shfl_sync(FULL, bslot, __ffs(who) - 1);
     const int4 s = *slotp(w, k, vslot);
     const int4 last = *slotp(w, k, len - 1);
-    const int64_t g = w.base + vid;
+    const int64_t g = w.base() + vid;
     const int32_t kvf = I.kv_free + (s.w & HELD_MASK);  // blocks held before this step's growth
     const int32_t need = I.need_sum - (int32_t)((uint32_t)s.w >> 31);
     const int64_t cs = I.ctx_sum - s.y;
@@ -372,7 +383,7 @@ __device__ __noinline__ int32_t evict(Wp w, int k) {
     if (lane == 0) {
       P.rq_eff[g] = s.y;  // eff_prompt = prompt + generated = lhat
       P.rq_fl[g] += (1u << NPRE_SHIFT);
-      P.scr_pre[w.base + np] = vid;
+      P.scr_pre[w.base() + np] = vid;
       *slotp(w, k, vslot) = last;
     }
     I.kv_free = kvf;
@@ -388,7 +399,7 @@ __device__ __noinline__ int32_t evict(Wp w, int k) {
 
 // returns the number of evictions; leaves the growth applied (papp = 1)
 __device__ __forceinline__ int32_t decode_prep(Wp w, int k) {
-  SInst& I = w.SI[k];
+  SInst& I = w.SI()[k];
   if (I.papp) return 0;  // growth for the last decode step already applied
   int32_t np = 0;
   if (I.need_sum > I.kv_free) np = evict(w, k);
@@ -425,7 +436,7 @@ __device__ __forceinline__ void set_batch(SInst& I, int64_t T, int64_t l,
 // offload test a key bound); other policies scan the whole queue.
 __device__ __noinline__ int lp_admit(Wp w, int k, int64_t T, int32_t ndrop,
                                      int32_t npre) {
-  SInst& I = w.SI[k];
+  SInst& I = w.SI()[k];
   const int lane = lane_id();
   const int64_t o = ioff(k, w);  // running-batch list base
   const int64_t q = qoff(I, k, w);
@@ -437,7 +448,7 @@ __device__ __noinline__ int lp_admit(Wp w, int k, int64_t T, int32_t ndrop,
   if (Bd) {
     ldec = lat_decode(P.md, (uint64_t)Bd, (uint64_t)sl);
     if (ldec < 0) atomicOr(P.err, ERR_RANGE);
-    C = w.tbt - ldec;
+    C = w.tbt() - ldec;
   }
   const int32_t len = I.wq_len;
   // Algorithm 1 lines 5-13 as a strict prefix-sum scan over the sorted prefix
@@ -449,7 +460,7 @@ __device__ __noinline__ int lp_admit(Wp w, int k, int64_t T, int32_t ndrop,
     const int pos = r * 32 + lane;
     const bool valid = pos < len;
     const int32_t id = valid ? P.wq_id[q + pos] : 0;
-    const int64_t g = w.base + id;
+    const int64_t g = w.base() + id;
     const int32_t p = valid ? P.rq_eff[g] : 0;
     const int64_t pf = valid ? pf_of(p) : 0;
     const int64_t bl = valid ? blk_of(p) : 0;
@@ -504,7 +515,7 @@ __device__ __noinline__ int lp_admit(Wp w, int k, int64_t T, int32_t ndrop,
         if (v) {
           id = P.wq_id[q2 + j];
           key = P.wq_key[q2 + j];
-          off = !(P.rq_fl[w.base + id] & (F_EVER | F_ONHP));
+          off = !(P.rq_fl[w.base() + id] & (F_EVER | F_ONHP));
         }
         const uint32_t mk = __ballot_sync(FULL, v && !off), mo = __ballot_sync(FULL, off);
         if (v && !off) {
@@ -512,7 +523,7 @@ __device__ __noinline__ int lp_admit(Wp w, int k, int64_t T, int32_t ndrop,
           P.wq_id[q2 + d] = id;
           P.wq_key[q2 + d] = key;
         }
-        if (off) P.scr_off[w.base + noff + __popc(mo & lanemask_lt())] = id;
+        if (off) P.scr_off[w.base() + noff + __popc(mo & lanemask_lt())] = id;
         wpos -= __popc(mk);
         noff += __popc(mo);
         __syncwarp();
@@ -530,7 +541,7 @@ __device__ __noinline__ int lp_admit(Wp w, int k, int64_t T, int32_t ndrop,
         if (v) {
           id = P.wq_id[q2 + j];
           key = P.wq_key[q2 + j];
-          const int64_t g = w.base + id;
+          const int64_t g = w.base() + id;
           off = !(P.rq_fl[g] & (F_EVER | F_ONHP)) &&
                 P.rq_dl[g] - T <= pf_of(P.rq_eff[g]) + P.W + P.margin;
         }
@@ -540,14 +551,14 @@ __device__ __noinline__ int lp_admit(Wp w, int k, int64_t T, int32_t ndrop,
           P.wq_id[q2 + d] = id;
           P.wq_key[q2 + d] = key;
         }
-        if (off) P.scr_off[w.base + noff + __popc(mo & lanemask_lt())] = id;
+        if (off) P.scr_off[w.base() + noff + __popc(mo & lanemask_lt())] = id;
         out += __popc(mk);
         noff += __popc(mo);
         __syncwarp();
       }
       rem = out;
     }
-    sort_ids(w, P.scr_off + w.base, noff);  // dispatch and digest in ascending id order
+    sort_ids(w, P.scr_off + w.base(), noff);  // dispatch and digest in ascending id order
   }
   const int32_t kvf = I.kv_free - (int32_t)used;
   __syncwarp();
@@ -557,20 +568,20 @@ __device__ __noinline__ int lp_admit(Wp w, int k, int64_t T, int32_t ndrop,
   __syncwarp();
   // dispatch offloads round-robin over the HPs, ascending id
   for (int32_t j = 0; j < noff; j++) {
-    const int32_t id = P.scr_off[w.base + j];
-    const int64_t g = w.base + id;
-    const int32_t rr = w.ts->rr_hp;
+    const int32_t id = P.scr_off[w.base() + j];
+    const int64_t g = w.base() + id;
+    const int32_t rr = w.ts()->rr_hp;
     const int h = P.n_lp + rr;
-    const int32_t tail = w.ts->fl_tail;
+    const int32_t tail = w.ts()->fl_tail;
     __syncwarp();
     if (lane == 0) {
       P.rq_fl[g] |= (F_ONHP | F_OFFL);
-      w.ts->rr_hp = (rr + 1) % P.n_hp;
+      w.ts()->rr_hp = (rr + 1) % P.n_hp;
       if (P.delay != 0) {
-        P.fl_t[w.base + tail] = T + P.delay;
-        P.fl_req[w.base + tail] = id;
-        P.fl_hp[w.base + tail] = h;
-        w.ts->fl_tail = tail + 1;
+        P.fl_t[w.base() + tail] = T + P.delay;
+        P.fl_req[w.base() + tail] = id;
+        P.fl_hp[w.base() + tail] = h;
+        w.ts()->fl_tail = tail + 1;
       }
     }
     __syncwarp();
@@ -606,7 +617,7 @@ __device__ __forceinline__ void decode_batch(SInst& I, int k, int64_t T) {
 
 // returns (waiting-queue entries evaluated << 1) | (1 if a batch was formed)
 __device__ __forceinline__ int64_t form_lp(Wp w, int k, int64_t T) {
-  SInst& I = w.SI[k];
+  SInst& I = w.SI()[k];
   if (I.wq_len == 0) {
     if (I.ds_len == 0) return 0;  // parked
     const int32_t np = decode_prep(w, k);
@@ -636,7 +647,7 @@ __device__ __forceinline__ int64_t form_lp(Wp w, int k, int64_t T) {
 // --------------------------------------------------------------------------- HP formation ---
 // FCFS prefill-first under the (elastic) token limit (G27-G28).
 __device__ __noinline__ int32_t hp_prefill(Wp w, int k, int64_t T, uint64_t* mom) {
-  SInst& I = w.SI[k];
+  SInst& I = w.SI()[k];
   const int lane = lane_id();
   const int64_t o = ioff(k, w);
   const int64_t q = qoff(I, k, w);
@@ -655,7 +666,7 @@ __device__ __noinline__ int32_t hp_prefill(Wp w, int k, int64_t T, uint64_t* mom
     const int32_t j = c + lane;
     const bool v = j < len;
     int32_t id = 0, p = 0;
-    if (v) { id = P.wq_id[q + j]; p = P.rq_eff[w.base + id]; }
+    if (v) { id = P.wq_id[q + j]; p = P.rq_eff[w.base() + id]; }
     const int64_t bl = v ? blk_of(p) : 0;
     const int64_t St = ct + warp_incl_scan((int64_t)p);
     const int64_t Sb = cb + warp_incl_scan(bl);
@@ -663,7 +674,7 @@ __device__ __noinline__ int32_t hp_prefill(Wp w, int k, int64_t T, uint64_t* mom
     const uint32_t m = __ballot_sync(FULL, ok);
     const int cnt = (m == FULL) ? 32 : (__ffs(~m) - 1);
     if (lane < cnt) {
-      admit_req(w.base + id, k, T);
+      admit_req(w.base() + id, k, T);
       P.bp_id[o + j] = id;
       const uint64_t u = (uint64_t)p;
       sp += u;
@@ -691,7 +702,7 @@ __device__ __noinline__ int32_t hp_prefill(Wp w, int k, int64_t T, uint64_t* mom
 }
 
 __device__ __noinline__ int64_t form_hp_general(Wp w, int k, int64_t T) {
-  SInst& I = w.SI[k];
+  SInst& I = w.SI()[k];
   const int32_t ndrop = (P.drop && I.wq_len) ? drop_step(w, k, T) : 0;
   const int64_t ev = (int64_t)I.wq_len << 1;
   uint64_t mom[3] = {0, 0, 0};
@@ -720,7 +731,7 @@ __device__ __noinline__ int64_t form_hp_general(Wp w, int k, int64_t T) {
 }
 
 __device__ __forceinline__ int64_t form_hp(Wp w, int k, int64_t T) {
-  SInst& I = w.SI[k];
+  SInst& I = w.SI()[k];
   if (I.wq_len == 0) {
     if (I.ds_len == 0) return 0;  // parked
     if (I.papp || I.need_sum <= I.kv_free) {  // decode-only batch without eviction: hot path
@@ -746,7 +757,7 @@ __device__ __noinline__ void finish_sums(Wp w, int k, int64_t freed, int64_t hsu
   hcnt = warp_sum(hcnt);
   tkd = warp_sum(tkd);
   cfin = warp_sum(cfin);
-  SInst& I = w.SI[k];
+  SInst& I = w.SI()[k];
   const int32_t kvf = I.kv_free + (int32_t)freed, hc = I.hist_cnt + hcnt, tk = I.tk_live - tkd;
   const int64_t hs = I.hist_sum + hsum, cs = I.ctx_sum - cfin;
   __syncwarp();
@@ -760,7 +771,7 @@ __device__ __noinline__ void finish_sums(Wp w, int k, int64_t freed, int64_t hsu
 
 // prefill completions: first token, then completion or entry into the decode set
 __device__ __noinline__ void complete_prefills(Wp w, int k, int64_t T) {
-  SInst& I = w.SI[k];
+  SInst& I = w.SI()[k];
   const int lane = lane_id();
   const int64_t o = ioff(k, w);
   const int32_t blen = I.bp_len;
@@ -774,7 +785,7 @@ __device__ __noinline__ void complete_prefills(Wp w, int k, int64_t T) {
     int4 s = make_int4(0, 0, 0, 0);
     if (v) {
       const int32_t id = P.bp_id[o + j];
-      const int64_t g = w.base + id;
+      const int64_t g = w.base() + id;
       const int32_t eff = P.rq_eff[g], p = P.pl[g], out_len = P.ol[g];
       const int32_t gen = eff - p + 1;  // tokens generated after this prefill
       if (P.first[g] < 0) P.first[g] = T;
@@ -814,7 +825,7 @@ __device__ __noinline__ void complete_prefills(Wp w, int k, int64_t T) {
 // The decode step just executed: one pass over the slots — l̂+1, remaining−1, completions, and
 // the block the next formation will need (pending bit: l̂ mod bs was 0 before the step).
 __device__ __forceinline__ void complete(Wp w, int k, int64_t T) {
-  SInst& I = w.SI[k];
+  SInst& I = w.SI()[k];
   const int lane = lane_id();
   if (I.batch_dec) {
     const int32_t dlen = I.ds_len;
@@ -845,7 +856,7 @@ __device__ __forceinline__ void complete(Wp w, int k, int64_t T) {
       if (mf) {
         anyfin = true;
         if (fin) {
-          const int64_t g = w.base + s.x;
+          const int64_t g = w.base() + s.x;
           finish_req(g, T);
           freed += held;
           cfin += s.y;
@@ -875,31 +886,31 @@ __device__ __forceinline__ void complete(Wp w, int k, int64_t T) {
 __device__ __forceinline__ void route(Wp w, int32_t id) {
   if (P.tickets) {
     for (int h = P.n_lp; h < P.K; h++) {
-      if (w.SI[h].ticket) {
-        const int32_t tk = w.SI[h].tk_live + 1;
+      if (w.SI()[h].ticket) {
+        const int32_t tk = w.SI()[h].tk_live + 1;
         __syncwarp();
-        if (lane_id() == 0) P.rq_fl[w.base + id] |= (F_TICK | F_ONHP);
-        w.SI[h].ticket = 0;
-        w.SI[h].tk_live = tk;
+        if (lane_id() == 0) P.rq_fl[w.base() + id] |= (F_TICK | F_ONHP);
+        w.SI()[h].ticket = 0;
+        w.SI()[h].tk_live = tk;
         __syncwarp();
         wq_append(w, h, id);  // the newest arrival has the largest id: stays sorted
         return;
       }
     }
   }
-  const int32_t rr = w.ts->rr_lp;
+  const int32_t rr = w.ts()->rr_lp;
   wq_insert(w, rr, id);
-  w.ts->rr_lp = (rr + 1) == P.n_lp ? 0 : rr + 1;
+  w.ts()->rr_lp = (rr + 1) == P.n_lp ? 0 : rr + 1;
   __syncwarp();
 }
 
 __device__ __noinline__ void deliver(Wp w, int64_t T) {
-  while (w.ts->fl_head < w.ts->fl_tail && P.fl_t[w.base + w.ts->fl_head] == T) {
-    const int32_t head = w.ts->fl_head;
-    const int32_t id = P.fl_req[w.base + head];
-    const int h = P.fl_hp[w.base + head];
+  while (w.ts()->fl_head < w.ts()->fl_tail && P.fl_t[w.base() + w.ts()->fl_head] == T) {
+    const int32_t head = w.ts()->fl_head;
+    const int32_t id = P.fl_req[w.base() + head];
+    const int h = P.fl_hp[w.base() + head];
     wq_insert(w, h, id);
-    w.ts->fl_head = head + 1;
+    w.ts()->fl_head = head + 1;
     __syncwarp();
   }
 }
@@ -914,14 +925,14 @@ __device__ __noinline__ void deliver(Wp w, int64_t T) {
 // a prefix sum, and the per-instance digest chain applied in order.  Exactly the same formations,
 // times and digest as stepping them one by one through the event loop.
 __device__ __noinline__ int64_t run_decode(Wp w, int k, int64_t T_limit) {
-  SInst& I = w.SI[k];
+  SInst& I = w.SI()[k];
   const int lane = lane_id();
   const int32_t bs = P.bs;
   if (I.ds_len == 0 || bs > 128 || !I.papp) return 0;
   const bool hp = I.hp;
   // two histograms of l̂ mod bs (current slots / survivors of the next completion), plus the
   // histogram of the slots that would finish at the next completion event
-  int32_t* hA = reinterpret_cast<int32_t*>(w.buf);  // w.buf holds 256 ints: two histograms
+  int32_t* hA = reinterpret_cast<int32_t*>(w.buf());  // w.buf() holds 256 ints: two histograms
   int32_t* hB = hA + 128;
   int32_t Bd = I.ds_len;
   int64_t E = I.end, S = I.ctx_sum;
@@ -1014,7 +1025,7 @@ __device__ __noinline__ int64_t run_decode(Wp w, int k, int64_t T_limit) {
         csum += sl.y;
       }
       if (fin) {  // completion at Et: done, KV freed, HP history / ticket bookkeeping
-        const int64_t g = w.base + sl.x;
+        const int64_t g = w.base() + sl.x;
         finish_req(g, Et);
         freed += held;  // held_base after nstep completions = blocks held when it finishes
         if (hp) { hsum += P.ol[g]; hcnt++; if (P.rq_fl[g] & F_TICK) tkd++; }
@@ -1085,10 +1096,10 @@ __device__ __noinline__ int64_t run_decode(Wp w, int k, int64_t T_limit) {
 
 __device__ __noinline__ void init_trace(Wp w, int trace) {
   const int lane = lane_id();
-  if (lane == 0) { w.ts->rr_lp = w.ts->rr_hp = w.ts->fl_head = w.ts->fl_tail = 0; }
+  if (lane == 0) { w.ts()->rr_lp = w.ts()->rr_hp = w.ts()->fl_head = w.ts()->fl_tail = 0; }
   const int64_t ttft = P.ttft[trace];
-  for (int64_t i = lane; i < w.n; i += 32) {
-    const int64_t g = w.base + i;
+  for (int64_t i = lane; i < w.n(); i += 32) {
+    const int64_t g = w.base() + i;
     P.rq_dl[g] = P.arr[g] + (P.rttft ? P.rttft[g] : ttft);
     P.rq_eff[g] = P.pl[g];
     P.rq_fl[g] = 0xffu << INST_SHIFT;
@@ -1097,7 +1108,7 @@ __device__ __noinline__ void init_trace(Wp w, int trace) {
     P.pstart[g] = -1;
   }
   if (lane < P.K) {
-    SInst& I = w.SI[lane];
+    SInst& I = w.SI()[lane];
     I.hp = lane >= P.n_lp;
     I.kv_total = I.kv_free = I.hp ? P.kv_hp : P.kv_lp;
     I.end = INF64; I.hist_sum = 0; I.ctx_sum = 0; I.hash = 0; I.nrec = 0; I.wq_head = 0;
@@ -1113,10 +1124,10 @@ __device__ __noinline__ void finish_trace(Wp w, int trace, int64_t decisions,
                                           int64_t evals) {
   const int lane = lane_id();
   bool stuck = false;
-  if (lane < P.K) stuck = w.SI[lane].wq_len > 0 || w.SI[lane].ds_len > 0;
+  if (lane < P.K) stuck = w.SI()[lane].wq_len > 0 || w.SI()[lane].ds_len > 0;
   if (__any_sync(FULL, stuck) && lane == 0) atomicOr(P.err, ERR_INVARIANT);
-  for (int64_t i = lane; i < w.n; i += 32) {
-    const int64_t g = w.base + i;
+  for (int64_t i = lane; i < w.n(); i += 32) {
+    const int64_t g = w.base() + i;
     const uint32_t f = P.rq_fl[g];
     uint32_t st = (f >> ST_SHIFT) & 3u;
     st |= (f & F_OFFL) ? 4u : 0u;
@@ -1127,7 +1138,7 @@ __device__ __noinline__ void finish_trace(Wp w, int trace, int64_t decisions,
   }
   if (lane == 0) {
     uint64_t d = 0;
-    for (int k = 0; k < P.K; k++) d = mix64(d ^ w.SI[k].hash);
+    for (int k = 0; k < P.K; k++) d = mix64(d ^ w.SI()[k].hash);
     P.digest[trace] = d;
     if (P.decisions) P.decisions[trace] = decisions;
     if (P.evals) P.evals[trace] = evals;
@@ -1139,61 +1150,57 @@ __device__ __noinline__ void finish_trace(Wp w, int trace, int64_t decisions,
 #define ASC_SIM_MINB 8  // CTAs per SM the register budget must allow (8 -> 64 registers/thread)
 #endif
 __global__ void __launch_bounds__(SW * 32, ASC_SIM_MINB) sim_kernel() {
-  extern __shared__ __align__(16) unsigned char smem[];
-  const int wi = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const size_t per_warp = 64 * sizeof(KI) + (size_t)P.K * DCAP * sizeof(int4) +
-                          (size_t)P.K * sizeof(SInst) + sizeof(TS);
-  unsigned char* mine = smem + wi * ((per_warp + 15) & ~size_t(15));
+  const int lane = threadIdx.x & 31;
   Wp w;
-  w.buf = reinterpret_cast<KI*>(mine);
-  w.sd = reinterpret_cast<int4*>(mine + 64 * sizeof(KI));
-  w.SI = reinterpret_cast<SInst*>(mine + 64 * sizeof(KI) + (size_t)P.K * DCAP * sizeof(int4));
-  w.ts = reinterpret_cast<TS*>(mine + 64 * sizeof(KI) + (size_t)P.K * DCAP * sizeof(int4) +
-                               (size_t)P.K * sizeof(SInst));
   const int K = P.K, n_lp = P.n_lp;
   while (true) {
     int trace = 0;
     if (lane == 0) trace = atomicAdd(P.next_trace, 1);
     trace = __shfl_sync(FULL, trace, 0);
     if (trace >= P.T) break;
-    w.base = P.off[trace];
-    w.n = P.off[trace + 1] - w.base;
-    w.tbt = P.tbt[trace];
+    if (lane == 0) {
+      TS* t = w.ts();
+      const int64_t b = P.off[trace];
+      t->base = b;
+      t->n = P.off[trace + 1] - b;
+      t->tbt = P.tbt[trace];
+    }
+    __syncwarp();
     init_trace(w, trace);
-    int64_t next = 0, next_arr = w.n > 0 ? P.arr[w.base] : INF64, decisions = 0, evals = 0;
+    int64_t next = 0, next_arr = w.n() > 0 ? P.arr[w.base()] : INF64, decisions = 0, evals = 0;
     while (true) {
       int64_t T = next_arr;
       for (int k = 0; k < K; k++) {
-        const int64_t e = w.SI[k].end;
+        const int64_t e = w.SI()[k].end;
         T = e < T ? e : T;
       }
-      const bool flight = w.ts->fl_head < w.ts->fl_tail;
+      const bool flight = w.ts()->fl_head < w.ts()->fl_tail;
       if (flight) {
-        const int64_t tf = P.fl_t[w.base + w.ts->fl_head];
+        const int64_t tf = P.fl_t[w.base() + w.ts()->fl_head];
         T = tf < T ? tf : T;
       }
       if (T == INF64) break;
       // A. completions in instance order
       for (int k = 0; k < K; k++)
-        if (w.SI[k].end == T) complete(w, k, T);
+        if (w.SI()[k].end == T) complete(w, k, T);
       // B. offload deliveries (FIFO = time order)
       if (flight) deliver(w, T);
       // C. arrivals, ascending id
       while (next_arr == T) {
         route(w, (int32_t)next);
         next++;
-        next_arr = next < w.n ? P.arr[w.base + next] : INF64;
+        next_arr = next < w.n() ? P.arr[w.base() + next] : INF64;
       }
       // D. formations of idle instances, LPs before HPs
       for (int k = 0; k < n_lp; k++) {
-        if (w.SI[k].end == INF64) {
+        if (w.SI()[k].end == INF64) {
           const int64_t r = form_lp(w, k, T);
           decisions += r & 1;
           evals += r >> 1;
         }
       }
       for (int k = n_lp; k < K; k++) {
-        if (w.SI[k].end == INF64) {
+        if (w.SI()[k].end == INF64) {
           const int64_t r = form_hp(w, k, T);
           decisions += r & 1;
           evals += r >> 1;
@@ -1202,21 +1209,21 @@ __global__ void __launch_bounds__(SW * 32, ASC_SIM_MINB) sim_kernel() {
       // E. tickets (G29)
       if (P.tickets) {
         if (lane >= n_lp && lane < K) {
-          SInst& I = w.SI[lane];
+          SInst& I = w.SI()[lane];
           if (!I.ticket && I.wq_len == 0 && I.tk_live == 0) I.ticket = 1;
         }
         __syncwarp();
       }
       // F. decode runs of independent instances up to their next possible interaction
       int64_t tl_hp = next_arr;
-      if (w.ts->fl_head < w.ts->fl_tail) {
-        const int64_t tf = P.fl_t[w.base + w.ts->fl_head];
+      if (w.ts()->fl_head < w.ts()->fl_tail) {
+        const int64_t tf = P.fl_t[w.base() + w.ts()->fl_head];
         tl_hp = tf < tl_hp ? tf : tl_hp;
       }
       for (int k = 0; k < n_lp; k++)
-        if (w.SI[k].wq_len > 0 && w.SI[k].end < tl_hp) tl_hp = w.SI[k].end;  // may offload
+        if (w.SI()[k].wq_len > 0 && w.SI()[k].end < tl_hp) tl_hp = w.SI()[k].end;  // may offload
       for (int k = 0; k < K; k++) {
-        const SInst& I = w.SI[k];
+        const SInst& I = w.SI()[k];
         const int64_t lim = k < n_lp ? next_arr : tl_hp;
         if (I.end < lim && I.batch_dec && I.bp_len == 0 && I.wq_len == 0)
           decisions += run_decode(w, k, lim);
@@ -1226,9 +1233,12 @@ __global__ void __launch_bounds__(SW * 32, ASC_SIM_MINB) sim_kernel() {
   }
 }
 
-size_t sim_smem_per_warp(int K) {
-  const size_t per_warp = 64 * sizeof(KI) + (size_t)K * DCAP * sizeof(int4) + (size_t)K * sizeof(SInst) + sizeof(TS);
-  return (per_warp + 15) & ~size_t(15);
+// per-warp shared-memory layout: top-K buffer, decode slots, instance states, controller state
+size_t sim_smem_per_warp(int K, int32_t* o_sd = nullptr, int32_t* o_si = nullptr, int32_t* o_ts = nullptr) {
+  const size_t sd = 64 * sizeof(KI), si = sd + (size_t)K * DCAP * sizeof(int4);
+  const size_t ts = si + (size_t)K * sizeof(SInst);
+  if (o_sd) { *o_sd = (int32_t)sd; *o_si = (int32_t)si; *o_ts = (int32_t)ts; }
+  return (ts + sizeof(TS) + 15) & ~size_t(15);
 }
 
 // liveness / layout validation (ASC_E_CONFIG / ASC_E_INVAL before simulating)
@@ -1336,6 +1346,7 @@ asc_status launch_simulate(asc_ctx* c, const asc_traces* tr, asc_outcomes* out, 
   }
   P.next_trace = ar.take<int>(1);
   P.err = c->d_err;
+  P.pw = (int32_t)sim_smem_per_warp(K, &P.o_sd, &P.o_si, &P.o_ts);
   cudaStream_t sm = c->stream;
   std::lock_guard<std::mutex> lock(g_sim_mu[c->device & 63]);
   cudaError_t ue = upload_params(P, sm);
