@@ -27,7 +27,8 @@ def stale():
 def build(force=False, verbose=False):
     if not force and not stale():
         return LIB
-    cmd = [NVCC] + FLAGS + [os.path.join(CSRC, f) for f in SOURCES] + ["-o", LIB + ".tmp"]
+    extra = os.environ.get("ASC_NVCC_EXTRA", "").split()  # experiments only (e.g. -DASC_SIM_MINB=7)
+    cmd = [NVCC] + FLAGS + extra + [os.path.join(CSRC, f) for f in SOURCES] + ["-o", LIB + ".tmp"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)

@@ -1146,10 +1146,12 @@ __device__ __noinline__ void finish_trace(Wp w, int trace, int64_t decisions,
   __syncwarp();
 }
 
-#ifndef ASC_SIM_MINB
-#define ASC_SIM_MINB 8  // CTAs per SM the register budget must allow (8 -> 64 registers/thread)
-#endif
-__global__ void __launch_bounds__(SW * 32, ASC_SIM_MINB) sim_kernel() {
+// MINB = CTAs per SM the register budget must allow (8 -> 64 registers/thread ... 4 -> 128).  The
+// launch picks the largest budget that still keeps every trace of the call resident at once
+// (T <= SMs x MINB x SW): a trace is a serial chain, so registers beat extra resident warps
+// only while no trace waits for a slot.
+template <int MINB>
+__global__ void __launch_bounds__(SW * 32, MINB) sim_kernel() {
   const int lane = threadIdx.x & 31;
   Wp w;
   const int K = P.K, n_lp = P.n_lp;
@@ -1362,17 +1364,29 @@ asc_status launch_simulate(asc_ctx* c, const asc_traces* tr, asc_outcomes* out, 
   cudaMemsetAsync(P.next_trace, 0, sizeof(int), sm);
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
-  int64_t blocks = ((int64_t)T + SW - 1) / SW;
-  const int64_t cap = (int64_t)sms * 8;
-  if (blocks > cap) blocks = cap;
   const size_t smem = SW * sim_smem_per_warp(K);
+  // register budget: fewest resident CTAs per SM that still hold every trace (min 4), and never
+  // more than shared memory allows (1 KB per CTA is reserved by the runtime)
+  int smem_sm = 228 * 1024;
+  cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, c->device);
+  int minb = (int)(smem_sm / (smem + 1024));
+  minb = minb > 8 ? 8 : minb;
+  if (minb < 1) return fail(c, ASC_E_CONFIG, "simulate: per-CTA shared memory exceeds the SM");
+  for (int m = 4; m < minb; m++)
+    if ((int64_t)T <= (int64_t)sms * m * SW) { minb = m; break; }
+  if (minb < 4) minb = 4;  // (K so large that fewer than 4 CTAs fit: the launch itself reports it)
+  void (*kern)() = minb == 4 ? sim_kernel<4> : minb == 5 ? sim_kernel<5> : minb == 6 ? sim_kernel<6>
+                 : minb == 7 ? sim_kernel<7> : sim_kernel<8>;
+  int64_t blocks = ((int64_t)T + SW - 1) / SW;
+  const int64_t cap = (int64_t)sms * minb;
+  if (blocks > cap) blocks = cap;
   if (smem > 48 * 1024) {
-    cudaError_t e = cudaFuncSetAttribute(sim_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return cuda_check(c, e, "simulate smem attribute");
   }
   if (blocks > 0) {
     cudaEventRecord(c->ev0, sm);
-    sim_kernel<<<(unsigned)blocks, SW * 32, smem, sm>>>();
+    kern<<<(unsigned)blocks, SW * 32, smem, sm>>>();
     cudaEventRecord(c->ev1, sm);
     c->timed = true;
     launches++;
