@@ -28,7 +28,7 @@
 extern "C" {
 #endif
 
-#define ASC_ABI_VERSION 1
+#define ASC_ABI_VERSION 2
 #define ASC_MAX_BATCH 128      /* max request-count budget R / lp_max_batch */
 #define ASC_MAX_INSTANCES 16   /* n_lp + n_hp per trace */
 
@@ -83,7 +83,17 @@ typedef struct {
   int64_t offload_margin_us;     /* tunable threshold of P:336 (G24), default 0 */
   int64_t offload_delay_us;      /* LP->HP transfer delay, default 0 */
   int32_t hist_default_tokens;   /* decode-length history mean before any HP completion (G28) */
+  int32_t scheduler;             /* asc_scheduler: Ascendra, or a baseline on n_lp homogeneous
+                                    instances (requires n_hp = 0, DESIGN G46) */
 } asc_flags;
+
+/* Schedulers asc_simulate_batch can run.  ASC_SCHED_VLLM is the vLLM-like baseline the paper
+ * compares against ("prefill-prioritizing"): every instance orders its
+ * waiting queue by the policy key (FCFS = vLLM), runs a prefill-only batch of the longest prefix
+ * fitting lp_token_budget (<=), the free KV blocks and lp_max_batch whenever one fits (ongoing
+ * decodes stall), else one decode-only step of every running request (preemption by
+ * recomputation).  asc_schedule_step is Ascendra's LP decision and ignores this field. */
+typedef enum { ASC_SCHED_ASCENDRA = 0, ASC_SCHED_VLLM = 1 } asc_scheduler;
 
 typedef struct { asc_arch arch; asc_perf perf; asc_topology topo; asc_flags flags; } asc_config;
 

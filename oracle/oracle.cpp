@@ -566,6 +566,57 @@ struct Sim {
       log(in, T, k, adm, bd, {}, dropped, pre, l);
   }
 
+  // vLLM-like baseline ("prefill-prioritizing"; reading G46): every instance is
+  // homogeneous; at each formation the waiting queue is ordered by the policy key (FCFS = arrival:
+  // vLLM) and, if any request fits, a prefill-only batch of the longest prefix with
+  // sum(tokens) <= N, sum(blocks) <= free blocks and |D| + count <= batch cap is run while the
+  // decodes stall; otherwise every decode runs (decode-only), after preemption by recomputation
+  // if their growth does not fit.
+  std::vector<int> vllm_prefill(Inst& in, int k, int64_t T) {
+    std::sort(in.waiting.begin(), in.waiting.end(), [&](int x, int y) {
+      const int64_t kx = key(x), ky = key(y);
+      return kx != ky ? kx < ky : x < y;
+    });
+    std::vector<int> adm;
+    int64_t tok = 0, blocks = 0;
+    for (int i : in.waiting) {
+      const int64_t t = r[i].eff, b = blk(r[i].eff);
+      if (tok + t > sc->lp_tok || blocks + b > in.kv_free ||
+          (int64_t)in.D.size() + (int64_t)adm.size() + 1 > sc->lp_max_batch)
+        break;
+      adm.push_back(i);
+      tok += t;
+      blocks += b;
+    }
+    for (int i : adm) admit(in, k, i, T);
+    return adm;
+  }
+
+  void form_vllm(int k, int64_t T) {
+    Inst& in = I[k];
+    std::vector<int> dropped = drop_step(in, T);
+    evaluations += (int64_t)in.waiting.size();
+    std::vector<int> adm, pre;
+    int64_t l = 0, bd = 0;
+    if (!in.waiting.empty()) adm = vllm_prefill(in, k, T);  // prefill first: decodes stall
+    if (adm.empty() && !in.D.empty()) {
+      pre = decode_prep(in);
+      if (!in.D.empty()) bd = (int64_t)in.D.size();
+      else if (!in.waiting.empty()) adm = vllm_prefill(in, k, T);  // every decode was evicted
+    }
+    const bool batch = !adm.empty() || bd > 0;
+    if (batch) {
+      l = bd ? lat({}, in.D) : lat(adm, {});
+      in.busy = true;
+      in.end = T + l;
+      in.batch_pf = adm;
+      in.batch_dec = bd > 0;
+      decisions++;
+    }
+    if (batch || !dropped.empty() || !pre.empty())
+      log(in, T, k, adm, bd, {}, dropped, pre, l);
+  }
+
   void log(Inst& in, int64_t T, int k, const std::vector<int>& adm, int64_t bd,
            const std::vector<int>& off, const std::vector<int>& dropped,
            const std::vector<int>& pre, int64_t l) {
@@ -631,7 +682,9 @@ struct Sim {
       // D. formations of idle instances, LPs before HPs
       for (int k = 0; k < K; k++) {
         if (I[k].busy) continue;
-        if (I[k].hp) form_hp(k, T); else form_lp(k, T);
+        if (sc->scheduler == 1) form_vllm(k, T);
+        else if (I[k].hp) form_hp(k, T);
+        else form_lp(k, T);
         if (!err.empty()) return false;
       }
       // E. ticket issue (G29)
@@ -696,6 +749,8 @@ extern "C" int or_simulate_batch(const or_arch* a_in, const or_perf* pf, const o
       sc->lp_max_batch < 1 || sc->lp_tok < 1 || sc->hp_tok < 1) {
     set_err("sched: bad topology"); return 2;
   }
+  if (sc->scheduler < 0 || sc->scheduler > 1) { set_err("sched: unknown scheduler"); return 2; }
+  if (sc->scheduler != 0 && sc->n_hp != 0) { set_err("sched: baseline schedulers take n_hp = 0"); return 2; }
   or_arch a;
   apply_tp(a_in, &a);
   // Liveness validation: every effective prompt fits the LP token

@@ -27,6 +27,7 @@ typedef struct {
   int32_t n_lp, n_hp, bs, kv_lp, kv_hp, lp_max_batch, lp_tok, hp_tok;
   int32_t policy, offload, tickets, elastic, drop, hist_default;
   int64_t margin_us, delay_us;
+  int32_t scheduler;  /* 0 = Ascendra (LP/HP); 1 = vLLM-like baseline (G46) */
 } or_sched;
 
 /* Eq. 1-3 with App. A.2/A.3 GEMM terms: exact integer F (flops) and M (bytes) of a batch of

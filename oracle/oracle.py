@@ -26,7 +26,7 @@ class OrSched(C.Structure):
     _fields_ = ([(k, C.c_int32) for k in ("n_lp", "n_hp", "bs", "kv_lp", "kv_hp", "lp_max_batch",
                                           "lp_tok", "hp_tok", "policy", "offload", "tickets",
                                           "elastic", "drop", "hist_default")]
-                + [("margin_us", C.c_int64), ("delay_us", C.c_int64)])
+                + [("margin_us", C.c_int64), ("delay_us", C.c_int64), ("scheduler", C.c_int32)])
 
 
 def build():
@@ -62,7 +62,7 @@ def sched_s(cfg):
     return OrSched(t["n_lp"], t["n_hp"], t["block_tokens"], t["kv_blocks_lp"], t["kv_blocks_hp"],
                    t["lp_max_batch"], t["lp_token_budget"], t["hp_token_budget"], f["policy"],
                    f["offload"], f["tickets"], f["elastic"], f["drop"], f["hist_default_tokens"],
-                   f["offload_margin_us"], f["offload_delay_us"])
+                   f["offload_margin_us"], f["offload_delay_us"], f.get("scheduler", 0))
 
 
 def _p(a, dt):

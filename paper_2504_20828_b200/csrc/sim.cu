@@ -79,6 +79,7 @@ struct SimP {
   int* err;
   int* next_trace;
   int32_t pw, o_sd, o_si, o_ts;  // per-warp shared-memory layout (bytes)
+  int32_t mode;                  // asc_scheduler (0 Ascendra, 1 vLLM-like baseline)
 };
 
 // The launch parameters live in the constant bank (one copy per device, written before each launch
@@ -645,14 +646,20 @@ __device__ __forceinline__ int64_t form_lp(Wp w, int k, int64_t T) {
 }
 
 // --------------------------------------------------------------------------- HP formation ---
-// FCFS prefill-first under the (elastic) token limit (G27-G28).
+// FCFS prefill-first under the (elastic) token limit (G27-G28).  The
+// vLLM-like baseline (G46) is the same prefill-first rule on an LP-type instance: its queue is in
+// policy-key order, the limit is lp_token_budget and the batch cap applies.
 __device__ __noinline__ int32_t hp_prefill(Wp w, int k, int64_t T, uint64_t* mom) {
   SInst& I = w.SI()[k];
   const int lane = lane_id();
   const int64_t o = ioff(k, w);
   const int64_t q = qoff(I, k, w);
   int64_t limit = P.hp_tok;
-  if (P.elastic) {
+  int32_t rcap = INT32_MAX;  // request cap: HPs have none
+  if (!I.hp) {               // vLLM-like baseline instance (G46): N and the batch cap
+    limit = P.lp_tok;
+    rcap = P.lp_max - I.ds_len;
+  } else if (P.elastic) {
     const int64_t mean = I.hist_cnt ? I.hist_sum / I.hist_cnt : (int64_t)P.hist_def;
     const int64_t avail = (int64_t)I.kv_free * P.bs - mean * ((int64_t)I.ds_len + 1);
     if (10 * avail > (int64_t)I.kv_total * P.bs) limit = P.hp_tok + avail;
@@ -670,7 +677,7 @@ __device__ __noinline__ int32_t hp_prefill(Wp w, int k, int64_t T, uint64_t* mom
     const int64_t bl = v ? blk_of(p) : 0;
     const int64_t St = ct + warp_incl_scan((int64_t)p);
     const int64_t Sb = cb + warp_incl_scan(bl);
-    const bool ok = v && ((j == 0) ? (bl <= kvf) : (St <= limit && Sb <= kvf));
+    const bool ok = v && j < rcap && ((j == 0 && I.hp) ? (bl <= kvf) : (St <= limit && Sb <= kvf));
     const uint32_t m = __ballot_sync(FULL, ok);
     const int cnt = (m == FULL) ? 32 : (__ffs(~m) - 1);
     if (lane < cnt) {
@@ -1196,7 +1203,7 @@ __global__ void __launch_bounds__(SW * 32, MINB) sim_kernel() {
       // D. formations of idle instances, LPs before HPs
       for (int k = 0; k < n_lp; k++) {
         if (w.SI()[k].end == INF64) {
-          const int64_t r = form_lp(w, k, T);
+          const int64_t r = P.mode == 0 ? form_lp(w, k, T) : form_hp(w, k, T);
           decisions += r & 1;
           evals += r >> 1;
         }
@@ -1349,6 +1356,7 @@ asc_status launch_simulate(asc_ctx* c, const asc_traces* tr, asc_outcomes* out, 
   P.next_trace = ar.take<int>(1);
   P.err = c->d_err;
   P.pw = (int32_t)sim_smem_per_warp(K, &P.o_sd, &P.o_si, &P.o_ts);
+  P.mode = cf.flags.scheduler;
   cudaStream_t sm = c->stream;
   std::lock_guard<std::mutex> lock(g_sim_mu[c->device & 63]);
   cudaError_t ue = upload_params(P, sm);

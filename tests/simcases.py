@@ -9,6 +9,7 @@ import itertools
 import numpy as np
 
 import helpers as H
+from gen import presets as P
 from gen import traces as TR
 
 SEC = H.SEC
@@ -160,3 +161,35 @@ def check_invariants(batch, out, cfg):
         tk = ((s >> 3) & 1) == 1
         assert np.all(inst(s)[(ofl | tk) & comp] >= n_lp)
         assert not np.any(ofl & tk)
+
+
+# ------------------------------------------------------------------ baselines (row f1) --------
+def with_scheduler(cfg, name):
+    """Same config on homogeneous baseline instances (reading G46: n_hp = 0, no offload/tickets)."""
+    cfg = {k: dict(v) for k, v in cfg.items()}
+    cfg["flags"]["scheduler"] = P.SCHEDULER[name]
+    cfg["topo"]["n_hp"] = 0
+    cfg["flags"]["offload"] = 0
+    cfg["flags"]["tickets"] = 0
+    return cfg
+
+
+def check_vllm_fcfs_order(sim, rng, trials=4):
+    """FCFS baselines never start request j's prefill before request i's when i arrived
+    earlier on the same instance (checked without preemption: ample KV), round-robin routing."""
+    for _ in range(trials):
+        n_lp = int(rng.integers(1, 4))
+        cfg = with_scheduler(P.config(topo=P.topology(n_lp=n_lp, kv_blocks_lp=25000),
+                                      flg=P.flags(policy="FCFS")), "vllm")
+        b = random_small_batch(rng, 3, 300)
+        out = sim(cfg, b)
+        check_invariants(b, out, cfg)
+        for t in range(b.T):
+            lo, hi = int(b.trace_off[t]), int(b.trace_off[t + 1])
+            ins = inst(out["status"][lo:hi])
+            assert list(ins) == [i % n_lp for i in range(hi - lo)]
+            assert npre(out["status"][lo:hi]).sum() == 0
+            ps = out["prefill_start_us"][lo:hi]
+            for k in range(n_lp):
+                q = ps[ins == k]
+                assert np.all(np.diff(q) >= 0)

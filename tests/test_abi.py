@@ -24,7 +24,7 @@ def test_exports_every_declared_symbol():
     assert set(names) == set(asc.EXPORTS)
     for n in names:
         assert hasattr(L, n), n
-    assert L.asc_abi_version() == 1
+    assert L.asc_abi_version() == 2
 
 
 def test_struct_layout_matches_header():
@@ -33,6 +33,7 @@ def test_struct_layout_matches_header():
     assert C.sizeof(asc.asc_perf) == 56
     assert C.sizeof(asc.asc_topology) == 32
     assert C.sizeof(asc.asc_flags) == 32 and asc.asc_flags.offload_margin_us.offset == 8
+    assert asc.asc_flags.scheduler.offset == 28
     assert asc.asc_config.flags.offset == 128
 
 
@@ -43,6 +44,8 @@ def test_struct_layout_matches_header():
     (lambda c: c["topo"].update(n_lp=0), "n_lp"),
     (lambda c: c["perf"].update(M_H=0.0), "M_H"),
     (lambda c: c["flags"].update(policy=9), "policy"),
+    (lambda c: c["flags"].update(scheduler=5), "flags.scheduler must be"),
+    (lambda c: c["flags"].update(scheduler=1), "topo.n_hp must be 0"),
 ])
 def test_config_validation(mut, field):
     cfg = P.config()

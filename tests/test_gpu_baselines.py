@@ -1,0 +1,97 @@
+"""GPU parity of the baseline schedulers in asc_simulate_batch (DESIGN G46).
+
+Same bar as the Ascendra path: per-request times, status words, digests, decision and
+evaluation counts equal the oracle's bit for bit; the hand-stepped W6 trace and the textbook
+reductions pin the GPU path directly.
+"""
+import numpy as np
+import pytest
+
+import simcases as SC
+from gen import presets as P
+from gen import traces as TR
+from test_gpu_sim import assert_parity, gpu_sim
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module")
+def asc():
+    from paper_2504_20828_b200 import asc as A
+    assert torch.cuda.is_available()
+    return A
+
+
+def test_w6_gpu(asc):
+    SC.check_fixture(lambda cfg, b, rt=None: gpu_sim(asc, cfg, b, rt),
+                     lambda b, o: (o["good"], o["total"]), "w6_vllm_decode_stall.json")
+
+
+def test_vllm_reductions_gpu(asc):
+    rng = np.random.default_rng(5)
+    for n in (1, 40, 200):
+        cfg, b, end = SC.lindley_case(rng, n)
+        got = gpu_sim(asc, SC.with_scheduler(cfg, "vllm"), b)
+        assert [int(x) for x in got["first_token_us"]] == end
+    for p, o in [(1, 1), (17, 40), (300, 7)]:
+        cfg, b, first, done = SC.single_request_case(p, o)
+        r = gpu_sim(asc, SC.with_scheduler(cfg, "vllm"), b)
+        assert int(r["first_token_us"][0]) == first and int(r["done_us"][0]) == done
+
+
+def test_vllm_fcfs_order_gpu(asc):
+    SC.check_vllm_fcfs_order(lambda cfg, b, rt=None: gpu_sim(asc, cfg, b, rt),
+                             np.random.default_rng(6))
+
+
+@pytest.mark.parametrize("policy", ["FCFS", "EDF_LAXITY", "SJF", "LJF", "EDF_DEADLINE"])
+@pytest.mark.parametrize("drop", [0, 1])
+def test_vllm_random_batches(asc, oracle, policy, drop):
+    rng = np.random.default_rng(hash((policy, drop, 46)) % 2 ** 32)
+    cfg = SC.with_scheduler(P.config(topo=P.topology(n_lp=3, kv_blocks_lp=700),
+                                     flg=P.flags(policy=policy, drop=drop)), "vllm")
+    b = SC.random_small_batch(rng, 24, 400)
+    got = gpu_sim(asc, cfg, b)
+    SC.check_invariants(b, got, cfg)
+    assert_parity(oracle, cfg, b, got)
+
+
+@pytest.mark.parametrize("variant", ["tiny_kv", "cap16", "one_instance"])
+def test_vllm_pressure_variants(asc, oracle, variant):
+    rng = np.random.default_rng(47)
+    topo = dict(n_lp=3, kv_blocks_lp=900)
+    if variant == "tiny_kv":
+        topo.update(kv_blocks_lp=420)
+    elif variant == "cap16":
+        topo.update(lp_max_batch=16)
+    else:
+        topo.update(n_lp=1)
+    cfg = SC.with_scheduler(P.config(topo=P.topology(**topo), flg=P.flags(policy="FCFS")), "vllm")
+    b = SC.random_small_batch(rng, 16, 500)
+    assert_parity(oracle, cfg, b, gpu_sim(asc, cfg, b))
+
+
+def test_vllm_config3_subgrid(asc, oracle):
+    cfg, b = P.workload("config3", n=600)
+    cfg = SC.with_scheduler(cfg, "vllm")
+    cfg["topo"]["n_lp"] = 3  # the paper's three homogeneous instances
+    sub = b.subset(range(0, 4096, 16))
+    assert_parity(oracle, cfg, sub, gpu_sim(asc, cfg, sub))
+
+
+def test_vllm_longbench_prefix(asc, oracle):
+    cfg, b = P.workload("config4", n=3000)
+    cfg = SC.with_scheduler(cfg, "vllm")
+    cfg["topo"]["n_lp"] = 3
+    assert_parity(oracle, cfg, b, gpu_sim(asc, cfg, b))
+
+
+def test_vllm_config_errors(asc):
+    cfg, b = P.workload("config1", n=10)
+    bad = {k: dict(v) for k, v in cfg.items()}
+    bad["flags"]["scheduler"] = 1  # n_hp = 1
+    with pytest.raises(asc.AscError) as e:
+        asc.Context(bad, 0)
+    assert e.value.code == 2
