@@ -41,6 +41,7 @@ def args_():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="asc", choices=["asc", "reference"])
     ap.add_argument("--workload", default="config3")
+    ap.add_argument("--no-baselines", action="store_true", help="skip the vLLM-like baseline run")
     ap.add_argument("--requests", type=int, default=None, help="requests per trace override")
     ap.add_argument("--traces", type=int, default=None, help="max traces (testing)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -305,6 +306,8 @@ def main():
         line["step_microbench"] = step_microbench(asc, torch, dev, stream, 2, max(3, a.steps), hbm_peak)
     if not a.no_e2e:
         line["e2e"] = e2e(asc, torch, ctx, batch, world, min(a.steps, 2), dev)
+    if rank == 0 and not a.no_baselines:
+        line["baselines"] = baselines(asc, torch, dev, stream, cfg, batch, good_all / max(total_all, 1))
     if rank == 0 and world == 1 and not a.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(cfg, batch)
     ctx.close()
@@ -312,6 +315,30 @@ def main():
         print(json.dumps(line), flush=True)
     if world > 1:
         torch.distributed.destroy_process_group()
+
+
+def baselines(asc, torch, dev, stream, cfg, batch, ascendra_goodput):
+    """Row f1: the same traces under the vLLM-like baseline on the same number of homogeneous
+    instances, one timed asc_simulate_batch after a warm-up; goodput beside Ascendra's."""
+    res = {"ascendra_goodput": ascendra_goodput}
+    for name in ("vllm",):
+        c = {k: dict(v) for k, v in cfg.items()}
+        c["topo"]["n_lp"] = cfg["topo"]["n_lp"] + cfg["topo"]["n_hp"]
+        c["topo"]["n_hp"] = 0
+        c["flags"].update(scheduler=P.SCHEDULER[name], offload=0, tickets=0)
+        ctx = asc.Context(c, dev.index, stream)
+        tr = asc.batch_arrays(batch, dev)
+        out = ctx.simulate_batch(tr)
+        out = ctx.simulate_batch(tr, out=out)
+        ms = ctx.last_kernel_ms()
+        good, total = ctx.goodput(tr, out)
+        dec = int(out["decisions"][:batch.T].sum().item())
+        g = int(good[:batch.T].cpu().numpy().view(np.uint64).sum())
+        t = int(total[:batch.T].cpu().numpy().view(np.uint64).sum())
+        ctx.close()
+        res[name] = {"decisions_per_s": dec / (ms * 1e-3), "kernel_ms": ms, "goodput": g / max(t, 1),
+                     "instances": f"{c['topo']['n_lp']} homogeneous (P:575)"}
+    return res
 
 
 def e2e(asc, torch, ctx, batch, world, steps, dev):
