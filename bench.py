@@ -41,7 +41,7 @@ def args_():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="asc", choices=["asc", "reference"])
     ap.add_argument("--workload", default="config3")
-    ap.add_argument("--no-baselines", action="store_true", help="skip the vLLM-like baseline run")
+    ap.add_argument("--no-baselines", action="store_true", help="skip the baseline scheduler runs")
     ap.add_argument("--requests", type=int, default=None, help="requests per trace override")
     ap.add_argument("--traces", type=int, default=None, help="max traces (testing)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -318,10 +318,11 @@ def main():
 
 
 def baselines(asc, torch, dev, stream, cfg, batch, ascendra_goodput):
-    """Row f1: the same traces under the vLLM-like baseline on the same number of homogeneous
+    """Row f1: the same traces under the vLLM-like and Sarathi-like (chunk budget 512) baselines on
+    the same number of homogeneous
     instances, one timed asc_simulate_batch after a warm-up; goodput beside Ascendra's."""
     res = {"ascendra_goodput": ascendra_goodput}
-    for name in ("vllm",):
+    for name in ("vllm", "sarathi"):
         c = {k: dict(v) for k, v in cfg.items()}
         c["topo"]["n_lp"] = cfg["topo"]["n_lp"] + cfg["topo"]["n_hp"]
         c["topo"]["n_hp"] = 0

@@ -84,7 +84,9 @@ typedef struct {
   int64_t offload_delay_us;      /* LP->HP transfer delay, default 0 */
   int32_t hist_default_tokens;   /* decode-length history mean before any HP completion (G28) */
   int32_t scheduler;             /* asc_scheduler: Ascendra, or a baseline on n_lp homogeneous
-                                    instances (requires n_hp = 0, DESIGN G46) */
+                                    instances (requires n_hp = 0, DESIGN G46-G48) */
+  int32_t chunk_tokens;          /* ASC_SCHED_SARATHI: per-batch token budget, decodes + prefill
+                                    chunks (G47; in [1, 2^24)); ignored otherwise */
 } asc_flags;
 
 /* Schedulers asc_simulate_batch can run.  ASC_SCHED_VLLM is the vLLM-like baseline the paper
@@ -92,8 +94,12 @@ typedef struct {
  * waiting queue by the policy key (FCFS = vLLM), runs a prefill-only batch of the longest prefix
  * fitting lp_token_budget (<=), the free KV blocks and lp_max_batch whenever one fits (ongoing
  * decodes stall), else one decode-only step of every running request (preemption by
- * recomputation).  asc_schedule_step is Ascendra's LP decision and ignores this field. */
-typedef enum { ASC_SCHED_ASCENDRA = 0, ASC_SCHED_VLLM = 1 } asc_scheduler;
+ * recomputation).  ASC_SCHED_SARATHI is the Sarathi-like chunked-prefill baseline (
+ * S:392-400; App. A.4 cost): every decode runs each batch and the rest of
+ * chunk_tokens is filled with prefill chunks in queue order (a partially prefilled request is
+ * continued first), each request taking min(budget left, prompt left).  asc_schedule_step is
+ * Ascendra's LP decision and ignores this field. */
+typedef enum { ASC_SCHED_ASCENDRA = 0, ASC_SCHED_VLLM = 1, ASC_SCHED_SARATHI = 2 } asc_scheduler;
 
 typedef struct { asc_arch arch; asc_perf perf; asc_topology topo; asc_flags flags; } asc_config;
 

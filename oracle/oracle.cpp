@@ -69,6 +69,45 @@ extern "C" int or_cost(const or_arch* a, int32_t np, const int64_t* p, int32_t n
   return (*F >= TWO53 || *M >= TWO53) ? 1 : 0;
 }
 
+// App. A.4 hybrid batch with chunked prefill, readings G48.  M_m's garbled
+// "8 sum l_i h + 2 sum l_i m" activations are the chunk tokens c_i (the GEMM rows this batch
+// processes, as in Tables 3-4); "l_i / b" is ceil(l_i / b) (G9); the chunk's self-attention
+// (absent from A.4, whose terms vanish at l_i = 0) is Eq. 1 applied to the chunk, so
+// whole prompts (l = 0) cost exactly what or_cost charges.  Same per-layer / x L / x d rules.
+extern "C" int or_cost_chunked(const or_arch* a, int32_t nc, const int64_t* l, const int64_t* c,
+                               int32_t nd, const int64_t* lhat, uint64_t* F, uint64_t* M) {
+  const uint64_t h = a->h, n = a->n, s = a->s, m = a->m, b = a->b, L = a->L, d = a->d;
+  uint64_t t = 0;
+  for (int32_t i = 0; i < nc; i++) t += (uint64_t)c[i];
+  const uint64_t tok = t + (uint64_t)nd;
+  const uint64_t G = (nc + nd) > 0 ? 1 : 0;
+  const uint64_t gemm_F = 3 * tok * h * h + tok * h * h + tok * h * m + tok * h * m;
+  const uint64_t gemm_M = G * (3 * h * h + h * h + h * m + h * m) +
+                          (tok * h + 3 * tok * h) + (tok * h + tok * h) +
+                          (tok * h + tok * m) + (tok * m + tok * h);
+  uint64_t Mp = 0, Fp = 0;
+  for (int32_t i = 0; i < nc; i++) {
+    const uint64_t li = (uint64_t)l[i], ci = (uint64_t)c[i];
+    // cached context of the chunk: 2 l s (load k, v) + 3 c s per k/v block (q, o read/write)
+    Mp += 2 * li * s + 3 * ci * s * (uint64_t)ceil_div((int64_t)li, (int64_t)b);
+    Fp += 2 * s * li * ci;
+    // the chunk's own tokens (Eq. 1 on the chunk)
+    Mp += 2 * ci * s + 3 * ci * s * (uint64_t)ceil_div((int64_t)ci, (int64_t)b);
+    Fp += 2 * s * ci * ci;
+  }
+  uint64_t Md = 0, Fd = 0;
+  for (int32_t j = 0; j < nd; j++) {
+    const uint64_t lj = (uint64_t)lhat[j];
+    Md += 2 * lj * s + 2 * s;
+    Fd += 2 * lj * s;
+  }
+  const uint64_t M_layer = (Mp + Md) * n + gemm_M;
+  const uint64_t F_layer = (Fp + Fd) * n + gemm_F;
+  *F = L * F_layer;
+  *M = L * M_layer * d;
+  return (*F >= TWO53 || *M >= TWO53) ? 1 : 0;
+}
+
 // Eq. 4-5: t = C1 (tM + tF) + C2 max(tM, tF) + C3 tM + C4 tF + C5,
 // tM = M / M_H, tF = F / F_H.  Fixed left-to-right order; clamp negative to 0 (G17).
 extern "C" double or_latency_s(const or_perf* pf, uint64_t F, uint64_t M) {
@@ -286,6 +325,7 @@ struct Req {
   int64_t g = 0;       // tokens generated so far
   int64_t eff;         // effective prompt (prompt + generated after preemption)
   int64_t held = 0;    // KV blocks held
+  int64_t cdone = 0;   // prompt tokens already prefilled (Sarathi-like chunks, G47)
   bool ever = false, onhp = false, ticketed = false, offloaded = false;
   int state = UNFINISHED;
   int64_t first = -1, done = -1, pstart = -1;
@@ -377,6 +417,10 @@ struct Sim {
       in.D = keep;
     }
     for (int i : in.batch_pf) {
+      if (sc->scheduler == 2) {
+        if (r[i].cdone < r[i].eff) continue;  // partial chunk: stays at the head of the queue
+        in.waiting.erase(std::find(in.waiting.begin(), in.waiting.end(), i));
+      }
       r[i].g += 1;
       if (r[i].first < 0) r[i].first = T;  // TTFT: first token at the end of its prefill
       if (r[i].g == r[i].o) finish(in, i, T); else in.D.push_back(i);
@@ -435,6 +479,7 @@ struct Sim {
       r[v].held = 0;
       in.D.erase(std::find(in.D.begin(), in.D.end(), v));
       r[v].eff = r[v].p + r[v].g;  // append generated tokens to the prompt
+      r[v].cdone = 0;
       r[v].npre += 1;
       pre.push_back(v);
       if (in.hp) hp_insert(in, v); else in.waiting.push_back(v);
@@ -617,9 +662,80 @@ struct Sim {
       log(in, T, k, adm, bd, {}, dropped, pre, l);
   }
 
+  // Sarathi-like baseline ("chunked prefill, allowing a partial prefill request to be
+  // appended at the end of each decoding batch"; reading G47).  Each formation: drop
+  // step; decode preparation (growth, LIFO preemption); then every decode runs and the rest of
+  // the per-batch token budget (chunk_tokens - |D|) is filled in queue order — a partially
+  // prefilled request first, then by (key, id) — each request contributing
+  // c = min(budget left, prompt left), stopping at the first request whose blocks (prompt tokens
+  // prefilled so far, + 1 for the first output token on the last chunk) do not fit, or at the
+  // batch cap.  Chunked requests stay in the queue until their last chunk completes.
+  void form_sarathi(int k, int64_t T) {
+    Inst& in = I[k];
+    std::vector<int> dropped = drop_step(in, T);
+    std::vector<int> pre = decode_prep(in);
+    evaluations += (int64_t)in.waiting.size();
+    std::sort(in.waiting.begin(), in.waiting.end(), [&](int x, int y) {
+      const bool px = r[x].cdone > 0, py = r[y].cdone > 0;
+      if (px != py) return px;
+      const int64_t kx = key(x), ky = key(y);
+      return kx != ky ? kx < ky : x < y;
+    });
+    int64_t budget = (int64_t)sc->chunk_tokens - (int64_t)in.D.size();
+    int64_t kv = in.kv_free;
+    std::vector<int> ids;
+    std::vector<int64_t> ls, cs;
+    for (int i : in.waiting) {
+      if (budget <= 0 || (int64_t)in.D.size() + (int64_t)ids.size() + 1 > sc->lp_max_batch) break;
+      const int64_t rem = r[i].eff - r[i].cdone;
+      const int64_t c = std::min(budget, rem);
+      const int64_t target = c == rem ? blk(r[i].eff) : ceil_div(r[i].cdone + c, sc->bs);
+      const int64_t need = target - r[i].held;
+      if (need > kv) break;
+      ids.push_back(i);
+      ls.push_back(r[i].cdone);
+      cs.push_back(c);
+      budget -= c;
+      kv -= need;
+    }
+    for (size_t j = 0; j < ids.size(); j++) {
+      const int i = ids[j];
+      const int64_t c = cs[j], rem = r[i].eff - r[i].cdone;
+      const int64_t target = c == rem ? blk(r[i].eff) : ceil_div(r[i].cdone + c, sc->bs);
+      r[i].ever = true;
+      if (r[i].pstart < 0) r[i].pstart = T;
+      r[i].inst = k;
+      in.kv_free -= target - r[i].held;
+      r[i].held = target;
+      r[i].cdone += c;
+    }
+    const bool batch = !ids.empty() || !in.D.empty();
+    int64_t l = 0;
+    if (batch) {
+      std::vector<int64_t> lh;
+      for (int j : in.D) lh.push_back(r[j].p + r[j].g);
+      uint64_t F, M;
+      if (or_cost_chunked(a, (int32_t)ids.size(), ls.data(), cs.data(), (int32_t)lh.size(),
+                          lh.data(), &F, &M)) {
+        if (err.empty()) err = "range: batch cost reaches 2^53";
+        l = -1;
+      } else {
+        l = or_latency_us(pf, F, M);
+      }
+      in.busy = true;
+      in.end = T + l;
+      in.batch_pf = ids;
+      in.batch_dec = !in.D.empty();
+      decisions++;
+    }
+    if (batch || !dropped.empty() || !pre.empty())
+      log(in, T, k, ids, batch ? (int64_t)in.D.size() : 0, {}, dropped, pre, l, cs);
+  }
+
   void log(Inst& in, int64_t T, int k, const std::vector<int>& adm, int64_t bd,
            const std::vector<int>& off, const std::vector<int>& dropped,
-           const std::vector<int>& pre, int64_t l) {
+           const std::vector<int>& pre, int64_t l,
+           const std::vector<int64_t>& chunks = {}) {
     std::vector<uint64_t> v;
     v.push_back((uint64_t)T);
     v.push_back((uint64_t)k);
@@ -633,6 +749,7 @@ struct Sim {
     v.push_back((uint64_t)pre.size());
     for (int i : pre) v.push_back((uint64_t)i);
     v.push_back((uint64_t)l);
+    for (int64_t c : chunks) v.push_back((uint64_t)c);  // Sarathi-like: chunk sizes, in order
     record(in, v);
   }
 
@@ -640,7 +757,9 @@ struct Sim {
     for (auto& in : I) {
       int64_t held = 0;
       for (int j : in.D) held += r[j].held;
-      for (int i : in.batch_pf) held += r[i].held;
+      for (int i : in.batch_pf)  // (a Sarathi chunk is also in the queue: counted there)
+        if (std::find(in.waiting.begin(), in.waiting.end(), i) == in.waiting.end()) held += r[i].held;
+      for (int i : in.waiting) held += r[i].held;
       if (held + in.kv_free != in.kv_total || in.kv_free < 0) {
         err = "invariant: KV ledger at T=" + std::to_string(T);
         return false;
@@ -683,6 +802,7 @@ struct Sim {
       for (int k = 0; k < K; k++) {
         if (I[k].busy) continue;
         if (sc->scheduler == 1) form_vllm(k, T);
+        else if (sc->scheduler == 2) form_sarathi(k, T);
         else if (I[k].hp) form_hp(k, T);
         else form_lp(k, T);
         if (!err.empty()) return false;
@@ -749,7 +869,8 @@ extern "C" int or_simulate_batch(const or_arch* a_in, const or_perf* pf, const o
       sc->lp_max_batch < 1 || sc->lp_tok < 1 || sc->hp_tok < 1) {
     set_err("sched: bad topology"); return 2;
   }
-  if (sc->scheduler < 0 || sc->scheduler > 1) { set_err("sched: unknown scheduler"); return 2; }
+  if (sc->scheduler < 0 || sc->scheduler > 2) { set_err("sched: unknown scheduler"); return 2; }
+  if (sc->scheduler == 2 && sc->chunk_tokens < 1) { set_err("sched: chunk_tokens < 1"); return 2; }
   if (sc->scheduler != 0 && sc->n_hp != 0) { set_err("sched: baseline schedulers take n_hp = 0"); return 2; }
   or_arch a;
   apply_tp(a_in, &a);

@@ -27,7 +27,8 @@ typedef struct {
   int32_t n_lp, n_hp, bs, kv_lp, kv_hp, lp_max_batch, lp_tok, hp_tok;
   int32_t policy, offload, tickets, elastic, drop, hist_default;
   int64_t margin_us, delay_us;
-  int32_t scheduler;  /* 0 = Ascendra (LP/HP); 1 = vLLM-like baseline (G46) */
+  int32_t scheduler;  /* 0 Ascendra (LP/HP); 1 vLLM-like (G46); 2 Sarathi-like (G47) */
+  int32_t chunk_tokens;  /* Sarathi-like per-batch token budget (decodes + prefill chunks, G47) */
 } or_sched;
 
 /* Eq. 1-3 with App. A.2/A.3 GEMM terms: exact integer F (flops) and M (bytes) of a batch of
@@ -35,6 +36,13 @@ typedef struct {
  * result would reach 2^53 (not exactly representable in fp64). */
 int or_cost(const or_arch* a, int32_t np, const int64_t* p, int32_t nd, const int64_t* lhat,
             uint64_t* F, uint64_t* M);
+/* App. A.4 hybrid batch with chunked prefill, readings G48: nc chunks, chunk j has
+ * l[j] prompt tokens already prefilled and processes c[j] more; plus nd decodes.  GEMM terms
+ * count sum(c) + nd tokens; attention per head: chunk j costs M = 2 l s + 3 c s ceil(l/b) (its
+ * cached context) + 2 c s + 3 c s ceil(c/b) (intra-chunk) and F = 2 s l c + 2 s c^2.
+ * With every l = 0 this is or_cost of whole prompts c[].  Returns 0, or 1 at 2^53. */
+int or_cost_chunked(const or_arch* a, int32_t nc, const int64_t* l, const int64_t* c, int32_t nd,
+                    const int64_t* lhat, uint64_t* F, uint64_t* M);
 /* Eq. 4-5: predicted seconds, fp64, fixed operation order, clamp at 0. */
 double or_latency_s(const or_perf* pf, uint64_t F, uint64_t M);
 /* G18/G17: integer microseconds = max(1, ceil(t * 1e6)). */

@@ -26,7 +26,8 @@ class OrSched(C.Structure):
     _fields_ = ([(k, C.c_int32) for k in ("n_lp", "n_hp", "bs", "kv_lp", "kv_hp", "lp_max_batch",
                                           "lp_tok", "hp_tok", "policy", "offload", "tickets",
                                           "elastic", "drop", "hist_default")]
-                + [("margin_us", C.c_int64), ("delay_us", C.c_int64), ("scheduler", C.c_int32)])
+                + [("margin_us", C.c_int64), ("delay_us", C.c_int64), ("scheduler", C.c_int32),
+                   ("chunk_tokens", C.c_int32)])
 
 
 def build():
@@ -62,7 +63,8 @@ def sched_s(cfg):
     return OrSched(t["n_lp"], t["n_hp"], t["block_tokens"], t["kv_blocks_lp"], t["kv_blocks_hp"],
                    t["lp_max_batch"], t["lp_token_budget"], t["hp_token_budget"], f["policy"],
                    f["offload"], f["tickets"], f["elastic"], f["drop"], f["hist_default_tokens"],
-                   f["offload_margin_us"], f["offload_delay_us"], f.get("scheduler", 0))
+                   f["offload_margin_us"], f["offload_delay_us"], f.get("scheduler", 0),
+                   f.get("chunk_tokens", 512))
 
 
 def _p(a, dt):
@@ -86,6 +88,17 @@ def cost(arch, p, lhat=()):
     F, M = C.c_uint64(), C.c_uint64()
     a = arch_s(arch)
     rc = lib().or_cost(C.byref(a), len(pa), pp, len(la), lp, C.byref(F), C.byref(M))
+    return F.value, M.value, rc
+
+
+def cost_chunked(arch, l, c, lhat=()):
+    la_, lp_ = _p(l, np.int64)
+    ca, cp = _p(c, np.int64)
+    da, dp = _p(lhat, np.int64)
+    assert len(la_) == len(ca)
+    F, M = C.c_uint64(), C.c_uint64()
+    a = arch_s(arch)
+    rc = lib().or_cost_chunked(C.byref(a), len(ca), lp_, cp, len(da), dp, C.byref(F), C.byref(M))
     return F.value, M.value, rc
 
 

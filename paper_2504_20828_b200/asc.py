@@ -47,7 +47,7 @@ class asc_flags(C.Structure):
     _fields_ = [("policy", C.c_int32), ("offload", C.c_uint8), ("tickets", C.c_uint8),
                 ("elastic", C.c_uint8), ("drop", C.c_uint8), ("offload_margin_us", C.c_int64),
                 ("offload_delay_us", C.c_int64), ("hist_default_tokens", C.c_int32),
-                ("scheduler", C.c_int32)]
+                ("scheduler", C.c_int32), ("chunk_tokens", C.c_int32)]
 
 
 class asc_config(C.Structure):
@@ -117,7 +117,7 @@ def make_config(cfg):
                      t["lp_max_batch"], t["lp_token_budget"], t["hp_token_budget"]),
         asc_flags(f["policy"], f["offload"], f["tickets"], f["elastic"], f["drop"],
                   f["offload_margin_us"], f["offload_delay_us"], f["hist_default_tokens"],
-                  f.get("scheduler", 0)))
+                  f.get("scheduler", 0), f.get("chunk_tokens", 512)))
 
 
 def _ptr(x):

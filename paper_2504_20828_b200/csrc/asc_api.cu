@@ -118,7 +118,10 @@ asc_status asc_create(const asc_config* cfg, int device, void* cuda_stream, asc_
   CHK(f.policy >= 0 && f.policy <= 4, "flags.policy must be an asc_policy");
   CHK(f.offload_margin_us >= 0 && f.offload_delay_us >= 0, "flags.offload_margin_us/offload_delay_us must be >= 0");
   CHK(f.hist_default_tokens >= 0, "flags.hist_default_tokens must be >= 0");
-  CHK(f.scheduler == ASC_SCHED_ASCENDRA || f.scheduler == ASC_SCHED_VLLM, "flags.scheduler must be an asc_scheduler");
+  CHK(f.scheduler == ASC_SCHED_ASCENDRA || f.scheduler == ASC_SCHED_VLLM || f.scheduler == ASC_SCHED_SARATHI,
+      "flags.scheduler must be an asc_scheduler");
+  CHK(f.scheduler != ASC_SCHED_SARATHI || (f.chunk_tokens >= 1 && f.chunk_tokens < (1 << 24)),
+      "flags.chunk_tokens must be in [1, 2^24) for ASC_SCHED_SARATHI");
   CHK(f.scheduler == ASC_SCHED_ASCENDRA || t.n_hp == 0,
       "flags.scheduler: baseline schedulers run on homogeneous instances (topo.n_hp must be 0)");
 #undef CHK

@@ -92,6 +92,22 @@ __host__ __device__ inline int64_t lat_us(const Model& md, uint64_t Bp, uint64_t
 
 __host__ __device__ inline uint64_t ceil_div_u(uint64_t x, uint64_t y) { return (x + y - 1) / y; }
 
+// App. A.4 hybrid batch with chunked prefill (readings G48) from per-batch sums over its nch
+// chunks (chunk = l tokens already prefilled + c new): sc = Σc, aF = Σ(l·c + c²),
+// aM = Σ(2l + 3c⌈l/b⌉ + 2c + 3c⌈c/b⌉); plus B_d decodes with context sum sl.  Whole prompts
+// (l = 0) give exactly lat_us's F and M.
+__device__ __forceinline__ int64_t lat_chunked(const Model& md, uint64_t nch, uint64_t sc,
+                                               uint64_t aF, uint64_t aM, uint64_t Bd, uint64_t sl) {
+  const uint64_t tok = sc + Bd;
+  const uint64_t G = (nch + Bd) ? 1 : 0;
+  const uint64_t attnF = md.n * (2 * md.s * aF + 2 * md.s * sl);
+  const uint64_t attnM = md.n * (md.s * aM + 2 * md.s * sl + 2 * md.s * Bd);
+  const uint64_t F = md.L * (tok * md.FT + attnF);
+  const uint64_t M = md.L * (G * md.W + tok * md.MT + attnM) * md.d;
+  if (F >= TWO53 || M >= TWO53) return -1;
+  return lat_from_FM(md, F, M);
+}
+
 // Standalone prefill latency of one prompt of p tokens (a1).
 __host__ __device__ inline int64_t prefill_lat(const Model& md, uint64_t p) {
   return lat_us(md, 1, p, p * p, p * ceil_div_u(p, md.b), 0, 0);

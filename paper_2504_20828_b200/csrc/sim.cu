@@ -79,7 +79,9 @@ struct SimP {
   int* err;
   int* next_trace;
   int32_t pw, o_sd, o_si, o_ts;  // per-warp shared-memory layout (bytes)
-  int32_t mode;                  // asc_scheduler (0 Ascendra, 1 vLLM-like baseline)
+  int32_t mode;                  // asc_scheduler (0 Ascendra, 1 vLLM-like, 2 Sarathi-like)
+  int32_t chunk_tok;             // Sarathi-like per-batch token budget
+  int32_t* rq_cdone;             // Sarathi-like: prompt tokens prefilled (after the running chunk)
 };
 
 // The launch parameters live in the constant bank (one copy per device, written before each launch
@@ -143,7 +145,7 @@ __device__ __forceinline__ void set_state(int64_t g, uint32_t st) {
 // drop…, #evicted, evicted…, lat) — positions as in the oracle; lanes hash in parallel.
 __device__ __noinline__ void digest_log(Wp w, int k, int64_t T, int32_t nadm,
                                         int64_t bd, int32_t noff, int32_t ndrop, int32_t npre,
-                                        int64_t lat) {
+                                        int64_t lat, int32_t nch = 0) {
   const int lane = lane_id();
   const int64_t o = ioff(k, w);
   uint64_t acc = 0;
@@ -168,6 +170,8 @@ __device__ __noinline__ void digest_log(Wp w, int k, int64_t T, int32_t nadm,
     acc += mix64((uint64_t)P.scr_drop[w.base() + j] + (uint64_t)(6 + nadm + noff + j + 1) * GOLD);
   for (int32_t j = lane; j < npre; j += 32)
     acc += mix64((uint64_t)P.scr_pre[w.base() + j] + (uint64_t)(7 + nadm + noff + ndrop + j + 1) * GOLD);
+  for (int32_t j = lane; j < nch; j += 32)  // Sarathi-like chunk sizes (staged in scr_off)
+    acc += mix64((uint64_t)P.scr_off[w.base() + j] + (uint64_t)(8 + nadm + noff + ndrop + npre + j + 1) * GOLD);
   acc = warp_sum(acc);
   const uint64_t nr = w.SI()[k].nrec + 1;
   const uint64_t h = w.SI()[k].hash + mix64(acc + nr * GOLD2);
@@ -383,6 +387,7 @@ __device__ __noinline__ int32_t evict(Wp w, int k) {
     __syncwarp();
     if (lane == 0) {
       P.rq_eff[g] = s.y;  // eff_prompt = prompt + generated = lhat
+      if (P.rq_cdone) P.rq_cdone[g] = 0;
       P.rq_fl[g] += (1u << NPRE_SHIFT);
       P.scr_pre[w.base() + np] = vid;
       *slotp(w, k, vslot) = last;
@@ -750,6 +755,111 @@ __device__ __forceinline__ int64_t form_hp(Wp w, int k, int64_t T) {
   return form_hp_general(w, k, T);
 }
 
+// ------------------------------------------------------------- Sarathi-like baseline (G47) ---
+// Decodes first (growth, LIFO preemption), then the per-batch token budget chunk_tokens - B_d is
+// filled in queue order: the queue's prefix takes whole remaining prompts while their running sum
+// fits; the next request gets the leftover as a partial chunk and stays at the head of the queue
+// (key sentinel INT64_MIN: a partial prefill is always continued first).  Stops at the first
+// request whose blocks (⌈prefilled/bs⌉, or ⌈(eff+1)/bs⌉ on the last chunk) or batch slot do not fit.
+__device__ __noinline__ int64_t form_sarathi(Wp w, int k, int64_t T) {
+  SInst& I = w.SI()[k];
+  const int lane = lane_id();
+  const int32_t ndrop = (P.drop && I.wq_len) ? drop_step(w, k, T) : 0;
+  const int32_t npre = I.ds_len ? decode_prep(w, k) : 0;
+  const int64_t ev = (int64_t)I.wq_len << 1;
+  const int64_t o = ioff(k, w);
+  const int64_t q = qoff(I, k, w);
+  const int32_t Bd = I.ds_len, len = I.wq_len;
+  const int64_t budget = (int64_t)P.chunk_tok - Bd, kvf = I.kv_free;
+  const int32_t rcap = P.lp_max - Bd;
+  const uint64_t b = P.md.b;
+  int64_t crem = 0, cneed = 0;
+  int32_t nfull = 0, part = 0;
+  uint64_t sc = 0, aF = 0, aM = 0;
+  int64_t used = 0;
+  for (int32_t c0 = 0; c0 < len; c0 += 32) {
+    const int32_t j = c0 + lane;
+    const bool v = j < len;
+    int32_t id = 0, eff = 0, cd = 0;
+    if (v) {
+      id = P.wq_id[q + j];
+      eff = P.rq_eff[w.base() + id];
+      cd = P.rq_cdone[w.base() + id];
+    }
+    const int64_t rem = eff - cd, held = (cd + P.bs - 1) / P.bs;
+    const int64_t Srem = crem + warp_incl_scan(rem);
+    const int64_t Sneed = cneed + warp_incl_scan(v ? blk_of(eff) - held : (int64_t)0);
+    const bool okf = v && Srem <= budget && Sneed <= kvf && j < rcap;
+    const uint32_t m = __ballot_sync(FULL, okf);
+    const int cnt = (m == FULL) ? 32 : (__ffs(~m) - 1);
+    // the first request that is not taken whole may take the leftover budget as a partial chunk
+    const int64_t left = budget - (cnt ? __shfl_sync(FULL, Srem, (cnt - 1) & 31) : crem);
+    const int64_t kvl = kvf - (cnt ? __shfl_sync(FULL, Sneed, (cnt - 1) & 31) : cneed);
+    int64_t c = 0, need = 0;
+    bool take = false;
+    if (lane < cnt) {
+      c = rem;
+      need = blk_of(eff) - held;
+      take = true;
+    } else if (lane == cnt && v && rem > left && left > 0 && j < rcap) {
+      c = left;
+      need = (cd + c + P.bs - 1) / P.bs - held;
+      take = need <= kvl;
+    }
+    if (take) {
+      const int64_t g = w.base() + id;
+      admit_req(g, k, T);
+      P.rq_cdone[g] = cd + (int32_t)c;
+      P.bp_id[o + j] = id;
+      P.scr_off[w.base() + j] = (int32_t)c;
+      const uint64_t lc = (uint64_t)cd, cc = (uint64_t)c;
+      sc += cc;
+      aF += lc * cc + cc * cc;
+      aM += 2 * lc + 3 * cc * ceil_div_u(lc, b) + 2 * cc + 3 * cc * ceil_div_u(cc, b);
+      used += need;
+    }
+    nfull += cnt;
+    if (cnt < 32) {
+      part = __popc(__ballot_sync(FULL, take && lane == cnt));
+      break;
+    }
+    crem = __shfl_sync(FULL, Srem, 31);
+    cneed = __shfl_sync(FULL, Sneed, 31);
+  }
+  sc = warp_sum(sc);
+  aF = warp_sum(aF);
+  aM = warp_sum(aM);
+  used = warp_sum(used);
+  const int32_t nch = nfull + part;
+  __syncwarp();
+  if (part && lane == 0) P.wq_key[q + nfull] = INT64_MIN;  // the partial request leads the queue
+  I.wq_head = len > nfull ? I.wq_head + nfull : 0;            // whole prompts leave the queue
+  I.wq_len = len - nfull;
+  I.kv_free = (int32_t)(kvf - used);
+  __syncwarp();
+  const bool batch = nch > 0 || Bd > 0;
+  int64_t l = 0;
+  if (batch) {
+    l = lat_chunked(P.md, (uint64_t)nch, sc, aF, aM, (uint64_t)Bd, (uint64_t)I.ctx_sum);
+    set_batch(I, T, l, Bd > 0, nch);
+  }
+  if (batch || ndrop || npre) digest_log(w, k, T, nch, batch ? Bd : 0, 0, ndrop, npre, l, nch);
+  return ev | (batch ? 1 : 0);
+}
+
+__device__ __forceinline__ int64_t form_sar(Wp w, int k, int64_t T) {
+  SInst& I = w.SI()[k];
+  if (I.wq_len == 0) {
+    if (I.ds_len == 0) return 0;  // parked
+    if (I.papp || I.need_sum <= I.kv_free) {  // decode-only batch without eviction: hot path
+      decode_prep(w, k);
+      decode_batch(I, k, T);
+      return 1;
+    }
+  }
+  return form_sarathi(w, k, T);
+}
+
 // ------------------------------------------------------------------ phase A: batch completion --
 __device__ __forceinline__ void finish_req(int64_t g, int64_t T) {
   P.done[g] = T;
@@ -790,7 +900,9 @@ __device__ __noinline__ void complete_prefills(Wp w, int k, int64_t T) {
     const bool v = j < blen;
     bool stay = false;
     int4 s = make_int4(0, 0, 0, 0);
-    if (v) {
+    if (v && P.mode == 2 && P.rq_cdone[w.base() + P.bp_id[o + j]] != P.rq_eff[w.base() + P.bp_id[o + j]]) {
+      // Sarathi-like partial chunk: the request stays at the head of its queue
+    } else if (v) {
       const int32_t id = P.bp_id[o + j];
       const int64_t g = w.base() + id;
       const int32_t eff = P.rq_eff[g], p = P.pl[g], out_len = P.ol[g];
@@ -1109,6 +1221,7 @@ __device__ __noinline__ void init_trace(Wp w, int trace) {
     const int64_t g = w.base() + i;
     P.rq_dl[g] = P.arr[g] + (P.rttft ? P.rttft[g] : ttft);
     P.rq_eff[g] = P.pl[g];
+    if (P.rq_cdone) P.rq_cdone[g] = 0;
     P.rq_fl[g] = 0xffu << INST_SHIFT;
     P.first[g] = -1;
     P.done[g] = -1;
@@ -1203,7 +1316,8 @@ __global__ void __launch_bounds__(SW * 32, MINB) sim_kernel() {
       // D. formations of idle instances, LPs before HPs
       for (int k = 0; k < n_lp; k++) {
         if (w.SI()[k].end == INF64) {
-          const int64_t r = P.mode == 0 ? form_lp(w, k, T) : form_hp(w, k, T);
+          const int64_t r = P.mode == 0 ? form_lp(w, k, T) : P.mode == 1 ? form_hp(w, k, T)
+                                                                       : form_sar(w, k, T);
           decisions += r & 1;
           evals += r >> 1;
         }
@@ -1314,7 +1428,8 @@ asc_status launch_simulate(asc_ctx* c, const asc_traces* tr, asc_outcomes* out, 
   const int K = cf.topo.n_lp + cf.topo.n_hp;
   const int32_t T = tr->T;
   size_t need = (size_t)R * (8 + 4 + 4) + (size_t)K * R * (8 + 4 + 16 + 4) + (size_t)R * 16 +
-                (cf.flags.offload_delay_us ? (size_t)R * 16 : 0) + 64 * 1024;
+                (cf.flags.offload_delay_us ? (size_t)R * 16 : 0) +
+                (cf.flags.scheduler == 2 ? (size_t)R * 4 : 0) + 64 * 1024;
   asc_status st = ensure_ws(c, need);
   if (st) return st;
   Arena ar{c->ws, c->ws_cap};
@@ -1357,6 +1472,8 @@ asc_status launch_simulate(asc_ctx* c, const asc_traces* tr, asc_outcomes* out, 
   P.err = c->d_err;
   P.pw = (int32_t)sim_smem_per_warp(K, &P.o_sd, &P.o_si, &P.o_ts);
   P.mode = cf.flags.scheduler;
+  P.chunk_tok = cf.flags.chunk_tokens;
+  P.rq_cdone = P.mode == 2 ? ar.take<int32_t>(R) : nullptr;
   cudaStream_t sm = c->stream;
   std::lock_guard<std::mutex> lock(g_sim_mu[c->device & 63]);
   cudaError_t ue = upload_params(P, sm);

@@ -18,7 +18,8 @@ def golden(name):
 
 def tiny_cfg(n_lp=1, n_hp=1, block_tokens=4, kv_blocks=100, lp_max_batch=4, lp_token_budget=8,
              hp_token_budget=4, policy="EDF_LAXITY", offload=1, tickets=1, elastic=0, drop=0,
-             margin=0, delay=0, hist_default=256, kv_blocks_hp=None, scheduler="ascendra"):
+             margin=0, delay=0, hist_default=256, kv_blocks_hp=None, scheduler="ascendra",
+             chunk_tokens=512):
     return P.config(arch=P.TINY, perf=P.PERF_TINY,
                     topo=P.topology(n_lp=n_lp, n_hp=n_hp, block_tokens=block_tokens,
                                     kv_blocks_lp=kv_blocks,
@@ -27,7 +28,8 @@ def tiny_cfg(n_lp=1, n_hp=1, block_tokens=4, kv_blocks=100, lp_max_batch=4, lp_t
                                     hp_token_budget=hp_token_budget),
                     flg=P.flags(policy=policy, offload=offload, tickets=tickets, elastic=elastic,
                                 drop=drop, offload_margin_us=margin, offload_delay_us=delay,
-                                hist_default_tokens=hist_default, scheduler=scheduler))
+                                hist_default_tokens=hist_default, scheduler=scheduler,
+                                chunk_tokens=chunk_tokens))
 
 
 def fixture_sim(name):
@@ -38,7 +40,8 @@ def fixture_sim(name):
                    kv_blocks=t["kv_blocks"], lp_max_batch=t["lp_max_batch"],
                    lp_token_budget=t["lp_token_budget"], hp_token_budget=t["hp_token_budget"],
                    policy=f["policy"], offload=f["offload"], tickets=f["tickets"],
-                   elastic=f["elastic"], scheduler=f.get("scheduler", "ascendra"))
+                   elastic=f["elastic"], scheduler=f.get("scheduler", "ascendra"),
+                   chunk_tokens=f.get("chunk_tokens", 512))
     req = np.array(g["requests"], dtype=np.int64)
     batch = TR.make_batch([(req[:, 0] * SEC, req[:, 1], req[:, 2])], [g["ttft"] * SEC],
                           [g["tbt"] * SEC])

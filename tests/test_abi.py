@@ -32,8 +32,8 @@ def test_struct_layout_matches_header():
     assert C.sizeof(asc.asc_arch) == 36
     assert C.sizeof(asc.asc_perf) == 56
     assert C.sizeof(asc.asc_topology) == 32
-    assert C.sizeof(asc.asc_flags) == 32 and asc.asc_flags.offload_margin_us.offset == 8
-    assert asc.asc_flags.scheduler.offset == 28
+    assert C.sizeof(asc.asc_flags) == 40 and asc.asc_flags.offload_margin_us.offset == 8
+    assert asc.asc_flags.scheduler.offset == 28 and asc.asc_flags.chunk_tokens.offset == 32
     assert asc.asc_config.flags.offset == 128
 
 
@@ -46,6 +46,7 @@ def test_struct_layout_matches_header():
     (lambda c: c["flags"].update(policy=9), "policy"),
     (lambda c: c["flags"].update(scheduler=5), "flags.scheduler must be"),
     (lambda c: c["flags"].update(scheduler=1), "topo.n_hp must be 0"),
+    (lambda c: (c["flags"].update(scheduler=2, chunk_tokens=0), c["topo"].update(n_hp=0)), "chunk_tokens"),
 ])
 def test_config_validation(mut, field):
     cfg = P.config()

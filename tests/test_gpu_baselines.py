@@ -95,3 +95,67 @@ def test_vllm_config_errors(asc):
     with pytest.raises(asc.AscError) as e:
         asc.Context(bad, 0)
     assert e.value.code == 2
+
+
+# --------------------------------------------------------------- Sarathi-like (G47, G48) ------
+def test_w7_gpu(asc):
+    SC.check_fixture(lambda cfg, b, rt=None: gpu_sim(asc, cfg, b, rt),
+                     lambda b, o: (o["good"], o["total"]), "w7_sarathi_chunks.json")
+
+
+def test_sarathi_reductions_gpu(asc):
+    rng = np.random.default_rng(11)
+    for n in (1, 40):
+        cfg, b, end = SC.lindley_case(rng, n)
+        cfg = SC.with_scheduler(cfg, "sarathi")
+        cfg["flags"]["chunk_tokens"] = 64
+        got = gpu_sim(asc, cfg, b)
+        assert [int(x) for x in got["first_token_us"]] == end
+
+
+@pytest.mark.parametrize("policy", ["FCFS", "EDF_LAXITY", "SJF", "LJF", "EDF_DEADLINE"])
+@pytest.mark.parametrize("chunk", [64, 512, 2048])
+def test_sarathi_random_batches(asc, oracle, policy, chunk):
+    rng = np.random.default_rng(hash((policy, chunk, 47)) % 2 ** 32)
+    cfg = SC.with_scheduler(P.config(topo=P.topology(n_lp=3, kv_blocks_lp=700),
+                                     flg=P.flags(policy=policy, drop=int(chunk == 64),
+                                                 chunk_tokens=chunk)), "sarathi")
+    b = SC.random_small_batch(rng, 24, 400)
+    got = gpu_sim(asc, cfg, b)
+    SC.check_invariants(b, got, cfg)
+    assert_parity(oracle, cfg, b, got)
+
+
+@pytest.mark.parametrize("variant", ["tiny_kv", "cap16", "one_instance", "chunk1"])
+def test_sarathi_pressure_variants(asc, oracle, variant):
+    rng = np.random.default_rng(48)
+    topo = dict(n_lp=3, kv_blocks_lp=900)
+    chunk = 256
+    if variant == "tiny_kv":
+        topo.update(kv_blocks_lp=420)
+    elif variant == "cap16":
+        topo.update(lp_max_batch=16)
+    elif variant == "one_instance":
+        topo.update(n_lp=1)
+    else:
+        chunk = 1  # budget below the decode count: prefill waits for decodes to drain
+    cfg = SC.with_scheduler(P.config(topo=P.topology(**topo),
+                                     flg=P.flags(policy="FCFS", chunk_tokens=chunk)), "sarathi")
+    b = SC.random_small_batch(rng, 16, 300 if variant == "chunk1" else 500)
+    assert_parity(oracle, cfg, b, gpu_sim(asc, cfg, b))
+
+
+def test_sarathi_config3_subgrid(asc, oracle):
+    cfg, b = P.workload("config3", n=600)
+    cfg = SC.with_scheduler(cfg, "sarathi")
+    cfg["topo"]["n_lp"] = 3
+    sub = b.subset(range(0, 4096, 16))
+    assert_parity(oracle, cfg, sub, gpu_sim(asc, cfg, sub))
+
+
+def test_sarathi_longbench_prefix(asc, oracle):
+    cfg, b = P.workload("config4", n=3000)
+    cfg = SC.with_scheduler(cfg, "sarathi")
+    cfg["topo"]["n_lp"] = 3
+    cfg["flags"]["chunk_tokens"] = 2048
+    assert_parity(oracle, cfg, b, gpu_sim(asc, cfg, b))

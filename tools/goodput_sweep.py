@@ -1,5 +1,5 @@
-"""Goodput vs QPS: Ascendra (2 LP + 1 HP) against the vLLM-like baseline (3 homogeneous
-instances) on the same synthetic traces — the shape of the paper's Fig goodput_main
+"""Goodput vs QPS: Ascendra (2 LP + 1 HP) against the vLLM-like and Sarathi-like baselines (3
+homogeneous instances) on the same synthetic traces — the shape of the paper's Fig goodput_main
 (P:453-510), not its numbers (those need the A100 testbed and real datasets).  GPU only.
 usage: goodput_sweep.py [shape] [n] [seeds] [j,j,...]   (QPS = j / 8)"""
 import json, os, sys, time
@@ -24,6 +24,9 @@ v = {k: dict(x) for k, x in base.items()}
 v["topo"].update(n_lp=3, n_hp=0)
 v["flags"].update(scheduler=P.SCHEDULER["vllm"], offload=0, tickets=0, policy=P.POLICY["FCFS"])
 systems["vllm_3x"] = v
+sa = {k: dict(x) for k, x in v.items()}
+sa["flags"].update(scheduler=P.SCHEDULER["sarathi"], chunk_tokens=512)
+systems["sarathi_3x"] = sa
 res = {"shape": shape, "requests_per_trace": n, "seeds": seeds, "qps": [j / 8 for j in js], "goodput": {}}
 tr = asc.batch_arrays(b, "cuda:0")
 for name, cfg in systems.items():
