@@ -42,6 +42,7 @@ def args_():
     ap.add_argument("--impl", default="asc", choices=["asc", "reference"])
     ap.add_argument("--workload", default="config3")
     ap.add_argument("--no-baselines", action="store_true", help="skip the baseline scheduler runs")
+    ap.add_argument("--no-fit-bench", action="store_true", help="skip the perf-model fit microbench")
     ap.add_argument("--requests", type=int, default=None, help="requests per trace override")
     ap.add_argument("--traces", type=int, default=None, help="max traces (testing)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -306,6 +307,8 @@ def main():
         line["step_microbench"] = step_microbench(asc, torch, dev, stream, 2, max(3, a.steps), hbm_peak)
     if not a.no_e2e:
         line["e2e"] = e2e(asc, torch, ctx, batch, world, min(a.steps, 2), dev)
+    if rank == 0 and not a.no_fit_bench:
+        line["fit_microbench"] = fit_microbench(asc, torch, dev, stream, hbm_peak)
     if rank == 0 and not a.no_baselines:
         line["baselines"] = baselines(asc, torch, dev, stream, cfg, batch, good_all / max(total_all, 1))
     if rank == 0 and world == 1 and not a.no_cpu_baseline:
@@ -315,6 +318,43 @@ def main():
         print(json.dumps(line), flush=True)
     if world > 1:
         torch.distributed.destroy_process_group()
+
+
+def fit_microbench(asc, torch, dev, stream, hbm_peak, groups=1024, per=65536, steps=5):
+    """Row f2: asc_fit_perf over groups x per synthetic batch records (gen/records.py), device
+    resident; roofline on fit_partials (24 B per record: F, M, y) over its event-timed duration."""
+    from gen import records as RC
+    rec = RC.make_records(21, [per] * groups)
+    N = int(rec["off"][-1])
+    d = {k: torch.from_numpy(np.ascontiguousarray(v)).to(dev) for k, v in rec.items()}
+    d["N"] = N
+    ctx = asc.Context(P.config(), dev.index, stream)
+    for _ in range(2):
+        ctx.fit_perf(d, 1e-8, errors=False)
+    torch.cuda.synchronize()
+    k_ms, launches = [], 0
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(steps):
+        ctx.fit_perf(d, 1e-8, errors=False)
+        k_ms.append(ctx.last_kernel_ms())
+        launches += ctx.last_launches()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    call_ms = e0.elapsed_time(e1) / steps
+    coef, me, mx = ctx.fit_perf(d, 1e-8, errors=True)
+    ctx.close()
+    kms = float(np.mean(k_ms))
+    byts = 24 * N
+    ach = byts / (kms * 1e-3) / 1e9
+    return {"shape": f"{groups} groups x {per} records", "records": N,
+            "records_per_s": N / (call_ms * 1e-3), "ms_per_call": call_ms,
+            "gpu_launches_per_call": launches / steps,
+            "median_in_sample_rel_err": float(np.median(me.cpu().numpy())),
+            "roofline": {"bound": "hbm", "achieved": ach, "peak": hbm_peak, "unit": "GB/s",
+                         "frac": ach / hbm_peak, "traffic": ncu_traffic("fit_partials"),
+                         "kernel": "fit_partials (features + Gram partials, one HBM pass)",
+                         "algorithmic_bytes": byts, "kernel_ms": kms, "kernel_share": kms / call_ms}}
 
 
 def baselines(asc, torch, dev, stream, cfg, batch, ascendra_goodput):

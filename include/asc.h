@@ -221,6 +221,34 @@ int64_t asc_last_kernel_launches(const asc_ctx* ctx);
  * or -1 if none ran. */
 double asc_last_kernel_ms(const asc_ctx* ctx);
 
+/* ---------------------------------------------------------------------------------------------
+ * asc_fit_perf — batched calibration of the performance model.
+ * PAPER P:273-277 (Eq. 4-5: "perform a linear regression to find the corresponding parameters
+ * C1 ... C5") and P:279 (runtime logs of each batch periodically refit the model); solver and
+ * regularisation are readings (DESIGN G49).  For each of G independent groups of
+ * batch records (CSR rec_off, group g = records [rec_off[g], rec_off[g+1])): record i has the
+ * batch's exact flop count F[i] and byte count M[i] (as the cost model gives them) and its
+ * observed latency y[i] in seconds (> 0).  With tM = M / M_H, tF = F / F_H (the ctx's perf caps)
+ * and x = (tM + tF, max(tM, tF), tM, tF, 1), returns the ridge least-squares coefficients
+ *     coef[5g .. 5g+4] = argmin_c  sum_i (x_i . c - y_i)^2 + lambda |c|^2      (C1 .. C5)
+ * solved from the normal equations by Cholesky (lambda > 0 breaks the exact x1 = x3 + x4
+ * collinearity; compare predictions, not coefficients).  mean_err / max_err (each may be NULL):
+ * in-sample mean and max of |pred - y| / y, pred = the fitted Eq. 4-5 clamped at 0.
+ * Layout: SoA arrays, all device pointers or all host pointers (host arrays are staged).
+ * Errors: ASC_E_INVAL (NULL arrays, lambda < 0 or not finite, y <= 0), ASC_E_EMPTY (a group with
+ * fewer than 20 records), ASC_E_RANGE (system not positive definite).  Results are
+ * deterministic (fixed reduction order); they match a sequential CPU sum to rounding. */
+typedef struct {
+  int32_t G;                 /* independent fits */
+  int64_t N;                 /* total records = rec_off[G]; -1 = read it from rec_off */
+  const int64_t* rec_off;    /* [G+1] non-decreasing, rec_off[0] = 0 */
+  const uint64_t* F;         /* [N] flops of the batch */
+  const uint64_t* M;         /* [N] bytes of the batch */
+  const double* y;           /* [N] observed seconds */
+} asc_fit_in;
+asc_status asc_fit_perf(asc_ctx* ctx, const asc_fit_in* in, double lambda, double* coef,
+                        double* mean_err, double* max_err);
+
 #ifdef __cplusplus
 }
 #endif

@@ -123,6 +123,73 @@ extern "C" double or_latency_s(const or_perf* pf, uint64_t F, uint64_t M) {
   return t;
 }
 
+// Eq. 4-5 calibration (G49).  Plain: features per record, the 5x5
+// Gram matrix and X'y by sequential sums in record order, + lambda on the diagonal, Cholesky
+// A = L L', forward and back substitution.  In-sample error through or_latency_s itself.
+extern "C" int or_fit_perf(const or_perf* pf, int32_t G, const int64_t* off, const uint64_t* F,
+                           const uint64_t* M, const double* y, double lambda, double* coef,
+                           double* mean_err, double* max_err) {
+  for (int32_t g = 0; g < G; g++) {
+    const int64_t lo = off[g], hi = off[g + 1];
+    if (hi - lo < 20) { set_err("fit: a group has fewer than 20 records (S:154)"); return 2; }
+    double A[5][5] = {{0}}, b[5] = {0};
+    for (int64_t i = lo; i < hi; i++)
+      if (!(y[i] > 0.0 && y[i] < HUGE_VAL)) { set_err("fit: observed latency must be > 0"); return 1; }
+    for (int64_t i = lo; i < hi; i++) {
+      const double tM = (double)M[i] / pf->M_H;
+      const double tF = (double)F[i] / pf->F_H;
+      const double x[5] = {tM + tF, tM > tF ? tM : tF, tM, tF, 1.0};
+      for (int j = 0; j < 5; j++) {
+        for (int k = j; k < 5; k++) A[j][k] = A[j][k] + x[j] * x[k];
+        b[j] = b[j] + x[j] * y[i];
+      }
+    }
+    for (int j = 0; j < 5; j++) {
+      A[j][j] = A[j][j] + lambda;
+      for (int k = 0; k < j; k++) A[j][k] = A[k][j];
+    }
+    // Cholesky: L[j][j] = sqrt(A[j][j] - sum_k L[j][k]^2), L[i][j] = (A[i][j] - sum_k L[i][k] L[j][k]) / L[j][j]
+    double Lc[5][5] = {{0}};
+    for (int j = 0; j < 5; j++) {
+      double d = A[j][j];
+      for (int k = 0; k < j; k++) d = d - Lc[j][k] * Lc[j][k];
+      if (!(d > 0.0)) { set_err("fit: regularised normal equations not positive definite"); return 2; }
+      Lc[j][j] = std::sqrt(d);
+      for (int i = j + 1; i < 5; i++) {
+        double v = A[i][j];
+        for (int k = 0; k < j; k++) v = v - Lc[i][k] * Lc[j][k];
+        Lc[i][j] = v / Lc[j][j];
+      }
+    }
+    double z[5], c[5];
+    for (int i = 0; i < 5; i++) {  // L z = b
+      double v = b[i];
+      for (int k = 0; k < i; k++) v = v - Lc[i][k] * z[k];
+      z[i] = v / Lc[i][i];
+    }
+    for (int i = 4; i >= 0; i--) {  // L' c = z
+      double v = z[i];
+      for (int k = i + 1; k < 5; k++) v = v - Lc[k][i] * c[k];
+      c[i] = v / Lc[i][i];
+    }
+    for (int j = 0; j < 5; j++) coef[5 * g + j] = c[j];
+    if (mean_err || max_err) {
+      or_perf fitted = *pf;
+      for (int j = 0; j < 5; j++) fitted.c[j] = c[j];
+      double sum = 0.0, mx = 0.0;
+      for (int64_t i = lo; i < hi; i++) {
+        const double pred = or_latency_s(&fitted, F[i], M[i]);
+        const double e = std::fabs(pred - y[i]) / y[i];
+        sum = sum + e;
+        if (e > mx) mx = e;
+      }
+      if (mean_err) mean_err[g] = sum / (double)(hi - lo);
+      if (max_err) max_err[g] = mx;
+    }
+  }
+  return 0;
+}
+
 // G18: continuous seconds -> event time in integer microseconds, at least 1 (G17).
 extern "C" int64_t or_latency_us(const or_perf* pf, uint64_t F, uint64_t M) {
   const double t = or_latency_s(pf, F, M);

@@ -51,6 +51,18 @@ int64_t or_latency_us(const or_perf* pf, uint64_t F, uint64_t M);
 int64_t or_batch_us(const or_arch* a, const or_perf* pf, int32_t np, const int64_t* p,
                     int32_t nd, const int64_t* lhat);
 
+/* Eq. 4-5 calibration ("perform a linear regression to find ... C1 ... C5", P:279
+ * online refit; readings G49): for each of G groups of batch records (CSR off[],
+ * exact F flops and M bytes, observed seconds y) the ridge least-squares coefficients
+ *   c = argmin sum_i (x_i . c - y_i)^2 + lambda |c|^2,  x = (tM + tF, max(tM, tF), tM, tF, 1),
+ * tM = M / M_H, tF = F / F_H, from the normal equations by Cholesky; coef[5g..5g+4] = C1..C5.
+ * mean_err / max_err (may be NULL): in-sample mean and max of |pred - y| / y with pred the
+ * Eq. 4-5 prediction of the fitted model (clamped at 0, or_latency_s).  Returns 0; 2 when a
+ * group has fewer than 20 records or the regularised system is not positive definite. */
+int or_fit_perf(const or_perf* pf, int32_t G, const int64_t* off, const uint64_t* F,
+                const uint64_t* M, const double* y, double lambda, double* coef,
+                double* mean_err, double* max_err);
+
 /* Algorithm 1, literal: n requests with value val[] (higher = more urgent),
  * compute cost c[], memory cost mem[], token cost tok[]; budgets C, M, N plus the request-count
  * budget R (reading G22).  Writes the selected request indices in scan order; returns count. */

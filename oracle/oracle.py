@@ -102,6 +102,25 @@ def cost_chunked(arch, l, c, lhat=()):
     return F.value, M.value, rc
 
 
+def fit_perf(perf, off, F, M, y, lam=1e-8, errors=True):
+    """-> (coef [G, 5], mean_err [G], max_err [G]) of the ridge fit (or_fit_perf)."""
+    offa, offp = _p(off, np.int64)
+    Fa, Fp = _p(F, np.uint64)
+    Ma, Mp = _p(M, np.uint64)
+    ya, yp = _p(y, np.float64)
+    G = len(offa) - 1
+    coef = np.zeros((max(G, 1), 5))
+    me, mx = np.zeros(max(G, 1)), np.zeros(max(G, 1))
+    ps = perf_s(perf)
+    rc = lib().or_fit_perf(C.byref(ps), G, offp, Fp, Mp, yp, C.c_double(lam),
+                           coef.ctypes.data_as(C.c_void_p),
+                           me.ctypes.data_as(C.c_void_p) if errors else None,
+                           mx.ctypes.data_as(C.c_void_p) if errors else None)
+    if rc:
+        raise OracleError(rc, _err())
+    return coef[:G], me[:G], mx[:G]
+
+
 def latency_s(perf, F, M):
     ps = perf_s(perf)
     return lib().or_latency_s(C.byref(ps), C.c_uint64(F), C.c_uint64(M))

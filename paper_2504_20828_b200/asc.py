@@ -19,7 +19,7 @@ ASC_MAX_INSTANCES = 16
 STATUS = {0: "ASC_OK", 1: "ASC_E_INVAL", 2: "ASC_E_CONFIG", 3: "ASC_E_NOMEM", 4: "ASC_E_CUDA",
           5: "ASC_E_EMPTY", 6: "ASC_E_RANGE", 7: "ASC_E_INVARIANT"}
 EXPORTS = ("asc_create", "asc_destroy", "asc_last_error", "asc_abi_version", "asc_schedule_step",
-           "asc_simulate_batch", "asc_goodput", "asc_last_kernel_launches",
+           "asc_simulate_batch", "asc_goodput", "asc_fit_perf", "asc_last_kernel_launches",
            "asc_last_kernel_ms")
 
 
@@ -74,6 +74,10 @@ class asc_traces(C.Structure):
         "req_ttft_slo_us")]
 
 
+class asc_fit_in(C.Structure):
+    _fields_ = [("G", C.c_int32), ("N", C.c_int64)] + [(k, _P) for k in ("rec_off", "F", "M", "y")]
+
+
 class asc_outcomes(C.Structure):
     _fields_ = [(k, _P) for k in ("first_token_us", "done_us", "prefill_start_us", "status",
                                   "digest", "decisions", "evaluations")]
@@ -100,6 +104,9 @@ def lib():
         L.asc_goodput.argtypes = [C.c_void_p, C.POINTER(asc_traces), C.POINTER(asc_outcomes),
                                   C.c_void_p, C.c_void_p]
         L.asc_goodput.restype = C.c_int
+        L.asc_fit_perf.argtypes = [C.c_void_p, C.POINTER(asc_fit_in), C.c_double, C.c_void_p,
+                                   C.c_void_p, C.c_void_p]
+        L.asc_fit_perf.restype = C.c_int
         L.asc_last_kernel_launches.argtypes = [C.c_void_p]
         L.asc_last_kernel_launches.restype = C.c_int64
         L.asc_last_kernel_ms.argtypes = [C.c_void_p]
@@ -195,6 +202,12 @@ def asc_goodput(ctx, trace_off, arrival_us, output_len, ttft_slo_us, tbt_slo_us,
            "asc_goodput")
 
 
+def asc_fit_perf(ctx, rec_off, F, M, y, lam, coef, mean_err=None, max_err=None, N=-1):
+    fi = asc_fit_in(len(rec_off) - 1, N, _ptr(rec_off), _ptr(F), _ptr(M), _ptr(y))
+    _check(ctx, lib().asc_fit_perf(ctx, C.byref(fi), C.c_double(lam), _ptr(coef), _ptr(mean_err),
+                                   _ptr(max_err)), "asc_fit_perf")
+
+
 # ------------------------------------------------------------------ convenience (allocation) --
 class Context:
     """Owns a ctx; allocates outputs as torch CUDA tensors (device path) or numpy (host path)."""
@@ -267,6 +280,24 @@ class Context:
                     tr["tbt_slo_us"], out["first_token_us"], out["done_us"], out["status"],
                     res["good"], res["total"], req_ttft_slo_us, R=int(tr["R"]) if "R" in tr else -1)
         return res["good"], res["total"]
+
+
+    def fit_perf(self, rec, lam=1e-8, errors=True):
+        """rec: dict(off, F, M, y) numpy (host path) or torch CUDA tensors (device path)
+        -> (coef [G, 5], mean_err [G] or None, max_err [G] or None), same kind as the input."""
+        dev = not isinstance(rec["off"], np.ndarray)
+        G = len(rec["off"]) - 1
+        if dev:
+            import torch
+            mk = lambda n: torch.empty(max(n, 1), dtype=torch.float64, device=f"cuda:{self.device}")
+        else:
+            mk = lambda n: np.zeros(max(n, 1), np.float64)
+        coef = mk(5 * G)
+        me, mx = (mk(G), mk(G)) if errors else (None, None)
+        N = int(rec["N"]) if "N" in rec else -1
+        asc_fit_perf(self.h, rec["off"], rec["F"], rec["M"], rec["y"], lam, coef, me, mx, N=N)
+        coef = coef[:5 * G].reshape(G, 5)
+        return coef, (me[:G] if errors else None), (mx[:G] if errors else None)
 
 
 def _alloc(dev, device, spec):

@@ -58,9 +58,10 @@ asc_status collect_errors(asc_ctx* c, const char* where) {
   if (!bits) return ASC_OK;
   std::string w(where);
   if (bits & 8) return fail(c, ASC_E_CONFIG, w + ": request violates liveness validation (prompt_len, output_len >= 1; prompt+output <= lp_token_budget; ceil((prompt+output)/block_tokens) < kv_blocks)");
-  if (bits & ERR_INVAL) return fail(c, ASC_E_INVAL, w + ": invalid input (eff_prompt < 1, seg_off decreasing, or arrivals not sorted within a trace)");
+  if (bits & ERR_INVAL) return fail(c, ASC_E_INVAL, w + ": invalid input (eff_prompt < 1, seg_off decreasing, arrivals not sorted within a trace, or a fit record with y <= 0)");
   if (bits & ERR_RANGE) return fail(c, ASC_E_RANGE, w + ": range (F or M >= 2^53, or budget_reqs > ASC_MAX_BATCH)");
-  if (bits & 16) return fail(c, ASC_E_EMPTY, w + ": goodput over a trace with 0 requests");
+  if (bits & 16) return fail(c, ASC_E_EMPTY, w + ": goodput over a trace with 0 requests, or a fit group with fewer than 20 records");
+  if (bits & 32) return fail(c, ASC_E_RANGE, w + ": regularised normal equations not positive definite");
   if (bits & ERR_INVARIANT) return fail(c, ASC_E_INVARIANT, w + ": invariant violated (queue left non-empty with no pending event)");
   return fail(c, ASC_E_INVARIANT, w + ": unknown device error");
 }
@@ -448,6 +449,54 @@ asc_status asc_goodput(asc_ctx* c, const asc_traces* tr, const asc_outcomes* out
   st = collect_errors(c, "asc_goodput");
   if (st) return st;
   return cuda_check(c, sg.download(), "asc_goodput: download");
+}
+
+asc_status asc_fit_perf(asc_ctx* c, const asc_fit_in* in, double lambda, double* coef,
+                        double* mean_err, double* max_err) {
+  if (!c || !in || !coef) return fail(c, ASC_E_INVAL, "asc_fit_perf: NULL argument");
+  c->err.clear();
+  c->timed = false;
+  if (in->G < 0) return fail(c, ASC_E_INVAL, "asc_fit_perf: G < 0");
+  if (!(lambda >= 0.0 && lambda < HUGE_VAL)) return fail(c, ASC_E_INVAL, "asc_fit_perf: lambda must be finite and >= 0");
+  if (!in->rec_off || !in->F || !in->M || !in->y) return fail(c, ASC_E_INVAL, "asc_fit_perf: NULL array");
+  cudaSetDevice(c->device);
+  const int kind = ptr_kind(in->rec_off);
+  if (!same_kind(kind, {in->F, in->M, in->y, coef, mean_err, max_err}))
+    return fail(c, ASC_E_INVAL, "asc_fit_perf: host and device pointers mixed");
+  const int32_t G = in->G;
+  int64_t N = in->N;
+  if (kind == 1) {
+    if (N < 0) {
+      cudaError_t e = cudaMemcpy(&N, in->rec_off + G, sizeof(int64_t), cudaMemcpyDeviceToHost);
+      if (e != cudaSuccess) return cuda_check(c, e, "asc_fit_perf: read rec_off[G]");
+    }
+    if (N < 0) return fail(c, ASC_E_INVAL, "asc_fit_perf: rec_off[G] < 0");
+    asc_status st = launch_fit(c, in, N, lambda, coef, mean_err, max_err);
+    if (st) return st;
+    return collect_errors(c, "asc_fit_perf");
+  }
+  if (N < 0) N = in->rec_off[G];
+  if (N != in->rec_off[G] || N < 0) return fail(c, ASC_E_INVAL, "asc_fit_perf: N != rec_off[G]");
+  const size_t Gn = (size_t)G, Nn = (size_t)N;
+  size_t need = rup(8 * (Gn + 1)) + rup(8 * Nn) * 3 + rup(8 * Gn) * 7 + 4096;
+  asc_status st = ensure_stage(c, need);
+  if (st) return st;
+  Stager sg{c};
+  sg.base = c->stage;
+  asc_fit_in d = *in;
+  d.N = N;
+  d.rec_off = sg.up(in->rec_off, Gn + 1);
+  d.F = sg.up(in->F, Nn);
+  d.M = sg.up(in->M, Nn);
+  d.y = sg.up(in->y, Nn);
+  double* dc = sg.out(coef, 5 * Gn);
+  double* dme = sg.out(mean_err, Gn);
+  double* dmx = sg.out(max_err, Gn);
+  st = launch_fit(c, &d, N, lambda, dc, dme, dmx);
+  if (st) return st;
+  st = collect_errors(c, "asc_fit_perf");
+  if (st) return st;
+  return cuda_check(c, sg.download(), "asc_fit_perf: download");
 }
 
 int64_t asc_last_kernel_launches(const asc_ctx* c) { return c ? c->last_kernel_launches : 0; }

@@ -49,6 +49,8 @@ asc_status launch_schedule_step(asc_ctx* c, const asc_step_in* in, asc_step_out*
 asc_status launch_simulate(asc_ctx* c, const asc_traces* tr, asc_outcomes* out, int64_t R);
 asc_status launch_goodput(asc_ctx* c, const asc_traces* tr, const asc_outcomes* out,
                           uint64_t* good, uint64_t* total);
+asc_status launch_fit(asc_ctx* c, const asc_fit_in* in, int64_t N, double lambda, double* coef,
+                      double* mean_err, double* max_err);
 asc_status ensure_ws(asc_ctx* c, size_t bytes);
 asc_status fail(asc_ctx* c, asc_status s, const std::string& msg);
 asc_status cuda_check(asc_ctx* c, cudaError_t e, const char* what);

@@ -13,7 +13,7 @@ from gen import presets as P  # noqa: E402
 from paper_2504_20828_b200 import asc  # noqa: E402
 
 ap = argparse.ArgumentParser()
-ap.add_argument("what", choices=["sim", "step"])
+ap.add_argument("what", choices=["sim", "step", "fit"])
 ap.add_argument("--traces", type=int, default=512)
 ap.add_argument("--n", type=int, default=1000)
 ap.add_argument("--S", type=int, default=4096)
@@ -28,6 +28,14 @@ if a.what == "sim":
     for _ in range(a.reps):
         out = ctx.simulate_batch(tr)
         print("sim ms", ctx.last_kernel_ms(), "decisions", int(out["decisions"].sum()))
+elif a.what == "fit":
+    from gen import records as RC
+    rec = RC.make_records(21, [65536] * 1024)
+    d = {k: torch.from_numpy(np.ascontiguousarray(v)).cuda() for k, v in rec.items()}
+    ctx = asc.Context(P.config(), 0)
+    for _ in range(a.reps):
+        ctx.fit_perf(d, 1e-8, errors=False)
+        print("fit ms", ctx.last_kernel_ms())
 else:
     import helpers as H
     rng = np.random.default_rng(123)
