@@ -191,6 +191,10 @@ typedef struct {
   const int64_t* ttft_slo_us;      /* [T] (Table 2) */
   const int64_t* tbt_slo_us;       /* [T] */
   const int64_t* req_ttft_slo_us;  /* [R] optional */
+  const int32_t* n_lp;             /* [T] optional per-trace subgroup topology (row
+                                      f3): trace t runs on n_lp[t] LP + n_hp[t] HP instances; */
+  const int32_t* n_hp;             /* n_lp >= 1, n_hp >= 0, n_lp + n_hp <= the ctx's n_lp + n_hp
+                                      (ASC_E_CONFIG otherwise); NULL = the ctx's topology */
 } asc_traces;
 
 typedef struct {

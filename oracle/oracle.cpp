@@ -927,7 +927,8 @@ static int simulate_one(const or_arch* a, const or_perf* pf, const or_sched* sc,
 extern "C" int or_simulate_batch(const or_arch* a_in, const or_perf* pf, const or_sched* sc,
                                  int32_t T, const int64_t* off, const int64_t* arr,
                                  const int32_t* pl, const int32_t* ol, const int64_t* ttft,
-                                 const int64_t* tbt, const int64_t* req_ttft, int64_t* first,
+                                 const int64_t* tbt, const int64_t* req_ttft,
+                                 const int32_t* tr_nlp, const int32_t* tr_nhp, int64_t* first,
                                  int64_t* done, int64_t* pstart, uint32_t* status,
                                  uint64_t* digest, int64_t* decisions, int64_t* evaluations,
                                  int32_t nthreads, int32_t check) {
@@ -938,6 +939,14 @@ extern "C" int or_simulate_batch(const or_arch* a_in, const or_perf* pf, const o
   }
   if (sc->scheduler < 0 || sc->scheduler > 2) { set_err("sched: unknown scheduler"); return 2; }
   if (sc->scheduler == 2 && sc->chunk_tokens < 1) { set_err("sched: chunk_tokens < 1"); return 2; }
+  for (int32_t t = 0; t < T; t++) {
+    const int32_t nl = tr_nlp ? tr_nlp[t] : sc->n_lp, nh = tr_nhp ? tr_nhp[t] : sc->n_hp;
+    if (nl < 1 || nh < 0 || nl + nh > sc->n_lp + sc->n_hp || (sc->scheduler != 0 && nh != 0)) {
+      set_err("trace topology: need n_lp >= 1, n_hp >= 0, n_lp + n_hp <= the configured pool"
+              " (and n_hp = 0 for baselines)");
+      return 2;
+    }
+  }
   if (sc->scheduler != 0 && sc->n_hp != 0) { set_err("sched: baseline schedulers take n_hp = 0"); return 2; }
   or_arch a;
   apply_tp(a_in, &a);
@@ -961,7 +970,10 @@ extern "C" int or_simulate_batch(const or_arch* a_in, const or_perf* pf, const o
       if (t >= T) break;
       const int64_t lo = off[t], n = off[t + 1] - off[t];
       std::string e;
-      const int st = simulate_one(&a, pf, sc, n, arr + lo, pl + lo, ol + lo, ttft[t], tbt[t],
+      or_sched sct = *sc;  // the trace's subgroup topology (row f3)
+      if (tr_nlp) sct.n_lp = tr_nlp[t];
+      if (tr_nhp) sct.n_hp = tr_nhp[t];
+      const int st = simulate_one(&a, pf, &sct, n, arr + lo, pl + lo, ol + lo, ttft[t], tbt[t],
                                   req_ttft ? req_ttft + lo : nullptr, first + lo, done + lo,
                                   pstart + lo, status + lo, digest + t, decisions + t,
                                   evaluations + t, check != 0, e);

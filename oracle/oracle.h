@@ -51,6 +51,9 @@ int64_t or_latency_us(const or_perf* pf, uint64_t F, uint64_t M);
 int64_t or_batch_us(const or_arch* a, const or_perf* pf, int32_t np, const int64_t* p,
                     int32_t nd, const int64_t* lhat);
 
+/* or_simulate_batch: trace_n_lp / trace_n_hp (may be NULL) give trace t its own subgroup
+ * topology (row f3): n_lp >= 1, n_hp >= 0, n_lp + n_hp <= sc->n_lp + sc->n_hp. */
+
 /* Eq. 4-5 calibration ("perform a linear regression to find ... C1 ... C5", P:279
  * online refit; readings G49): for each of G groups of batch records (CSR off[],
  * exact F flops and M bytes, observed seconds y) the ridge least-squares coefficients
@@ -87,6 +90,7 @@ int or_simulate_batch(const or_arch* a, const or_perf* pf, const or_sched* sc, i
                       const int32_t* prompt_len, const int32_t* output_len,
                       const int64_t* ttft_slo_us, const int64_t* tbt_slo_us,
                       const int64_t* req_ttft_slo_us,
+                      const int32_t* trace_n_lp, const int32_t* trace_n_hp,
                       int64_t* first_token_us, int64_t* done_us, int64_t* prefill_start_us,
                       uint32_t* status, uint64_t* digest, int64_t* decisions,
                       int64_t* evaluations, int32_t nthreads, int32_t check_invariants);

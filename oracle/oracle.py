@@ -176,8 +176,10 @@ def schedule_step(cfg, seg_off, now_us, deadline_us, eff_prompt, flags, dec_coun
     return out
 
 
-def simulate_batch(cfg, batch, req_ttft_slo_us=None, nthreads=0, check_invariants=False):
-    """batch: gen.traces.TraceBatch.  Returns dict of per-request and per-trace outputs."""
+def simulate_batch(cfg, batch, req_ttft_slo_us=None, nthreads=0, check_invariants=False,
+                   n_lp=None, n_hp=None):
+    """batch: gen.traces.TraceBatch; n_lp / n_hp: optional per-trace subgroup topology (row f3).
+    Returns dict of per-request and per-trace outputs."""
     T, R = batch.T, batch.R
     ins = [_p(x, dt) for x, dt in ((batch.trace_off, np.int64), (batch.arrival_us, np.int64),
                                    (batch.prompt_len, np.int32), (batch.output_len, np.int32),
@@ -190,8 +192,10 @@ def simulate_batch(cfg, batch, req_ttft_slo_us=None, nthreads=0, check_invariant
                status=np.zeros(max(R, 1), np.uint32), digest=np.zeros(max(T, 1), np.uint64),
                decisions=np.zeros(max(T, 1), np.int64), evaluations=np.zeros(max(T, 1), np.int64))
     a, ps, sc = arch_s(cfg["arch"]), perf_s(cfg["perf"]), sched_s(cfg)
+    nl = _p(n_lp, np.int32) if n_lp is not None else None
+    nh = _p(n_hp, np.int32) if n_hp is not None else None
     rc = lib().or_simulate_batch(C.byref(a), C.byref(ps), C.byref(sc), T, *[x[1] for x in ins],
-                                 rt[1] if rt else None,
+                                 rt[1] if rt else None, nl[1] if nl else None, nh[1] if nh else None,
                                  *[out[k].ctypes.data_as(C.c_void_p) for k in
                                    ("first_token_us", "done_us", "prefill_start_us", "status",
                                     "digest", "decisions", "evaluations")],

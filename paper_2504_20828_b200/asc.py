@@ -71,7 +71,7 @@ class asc_step_out(C.Structure):
 class asc_traces(C.Structure):
     _fields_ = [("T", C.c_int32), ("R", C.c_int64)] + [(k, _P) for k in (
         "trace_off", "arrival_us", "prompt_len", "output_len", "ttft_slo_us", "tbt_slo_us",
-        "req_ttft_slo_us")]
+        "req_ttft_slo_us", "n_lp", "n_hp")]
 
 
 class asc_fit_in(C.Structure):
@@ -183,10 +183,10 @@ def asc_schedule_step(ctx, seg_off, now_us, deadline_us, eff_prompt, flags, dec_
 
 def asc_simulate_batch(ctx, trace_off, arrival_us, prompt_len, output_len, ttft_slo_us, tbt_slo_us,
                        first_token_us, done_us, prefill_start_us, status, digest, decisions=None,
-                       evaluations=None, req_ttft_slo_us=None, R=-1):
+                       evaluations=None, req_ttft_slo_us=None, R=-1, n_lp=None, n_hp=None):
     T = len(trace_off) - 1
     tr = asc_traces(T, R, *[_ptr(x) for x in (trace_off, arrival_us, prompt_len, output_len,
-                                           ttft_slo_us, tbt_slo_us, req_ttft_slo_us)])
+                                           ttft_slo_us, tbt_slo_us, req_ttft_slo_us, n_lp, n_hp)])
     oc = asc_outcomes(*[_ptr(x) for x in (first_token_us, done_us, prefill_start_us, status,
                                           digest, decisions, evaluations)])
     _check(ctx, lib().asc_simulate_batch(ctx, C.byref(tr), C.byref(oc)), "asc_simulate_batch")
@@ -254,8 +254,9 @@ class Context:
                           out["drop_cnt"], out["batch_lat_us"], out["prefill_us"], Q=Q)
         return out
 
-    def simulate_batch(self, tr, req_ttft_slo_us=None, out=None):
-        """tr: dict trace_off, arrival_us, prompt_len, output_len, ttft_slo_us, tbt_slo_us."""
+    def simulate_batch(self, tr, req_ttft_slo_us=None, out=None, n_lp=None, n_hp=None):
+        """tr: dict trace_off, arrival_us, prompt_len, output_len, ttft_slo_us, tbt_slo_us;
+        n_lp / n_hp: optional per-trace subgroup topology (int32 [T], same kind as tr)."""
         dev = not isinstance(tr["trace_off"], np.ndarray)
         T = len(tr["trace_off"]) - 1
         R = int(tr["R"]) if "R" in tr else int(tr["trace_off"][-1])
@@ -268,7 +269,7 @@ class Context:
                            tr["output_len"], tr["ttft_slo_us"], tr["tbt_slo_us"],
                            out["first_token_us"], out["done_us"], out["prefill_start_us"],
                            out["status"], out["digest"], out["decisions"], out["evaluations"],
-                           req_ttft_slo_us, R=R)
+                           req_ttft_slo_us, R=R, n_lp=n_lp, n_hp=n_hp)
         return out
 
     def goodput(self, tr, out, req_ttft_slo_us=None, res=None):

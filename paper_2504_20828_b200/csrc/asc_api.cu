@@ -57,7 +57,7 @@ asc_status collect_errors(asc_ctx* c, const char* where) {
   const int bits = *c->h_err;
   if (!bits) return ASC_OK;
   std::string w(where);
-  if (bits & 8) return fail(c, ASC_E_CONFIG, w + ": request violates liveness validation (prompt_len, output_len >= 1; prompt+output <= lp_token_budget; ceil((prompt+output)/block_tokens) < kv_blocks)");
+  if (bits & 8) return fail(c, ASC_E_CONFIG, w + ": request violates liveness validation (prompt_len, output_len >= 1; prompt+output <= lp_token_budget; ceil((prompt+output)/block_tokens) < kv_blocks), or a per-trace topology is out of range");
   if (bits & ERR_INVAL) return fail(c, ASC_E_INVAL, w + ": invalid input (eff_prompt < 1, seg_off decreasing, arrivals not sorted within a trace, or a fit record with y <= 0)");
   if (bits & ERR_RANGE) return fail(c, ASC_E_RANGE, w + ": range (F or M >= 2^53, or budget_reqs > ASC_MAX_BATCH)");
   if (bits & 16) return fail(c, ASC_E_EMPTY, w + ": goodput over a trace with 0 requests, or a fit group with fewer than 20 records");
@@ -350,9 +350,9 @@ asc_status asc_simulate_batch(asc_ctx* c, const asc_traces* tr, asc_outcomes* ou
   cudaSetDevice(c->device);
   const int kind = ptr_kind(tr->trace_off);
   if (!same_kind(kind, {tr->arrival_us, tr->prompt_len, tr->output_len, tr->ttft_slo_us,
-                        tr->tbt_slo_us, tr->req_ttft_slo_us, out->first_token_us, out->done_us,
-                        out->prefill_start_us, out->status, out->digest, out->decisions,
-                        out->evaluations}))
+                        tr->tbt_slo_us, tr->req_ttft_slo_us, tr->n_lp, tr->n_hp,
+                        out->first_token_us, out->done_us, out->prefill_start_us, out->status,
+                        out->digest, out->decisions, out->evaluations}))
     return fail(c, ASC_E_INVAL, "asc_simulate_batch: host and device pointers mixed");
   const int32_t T = tr->T;
   int64_t R = tr->R;
@@ -377,7 +377,7 @@ asc_status asc_simulate_batch(asc_ctx* c, const asc_traces* tr, asc_outcomes* ou
   }
   const size_t Tn = (size_t)T, Rn = (size_t)R;
   size_t need = rup(8 * (Tn + 1)) + rup(8 * Rn) * 2 + rup(4 * Rn) * 2 + rup(8 * Tn) * 2 +
-                rup(8 * Rn) * 3 + rup(4 * Rn) + rup(8 * Tn) * 3 + 4096;
+                rup(8 * Rn) * 3 + rup(4 * Rn) + rup(8 * Tn) * 3 + rup(4 * Tn) * 2 + 4096;
   st = ensure_stage(c, need);
   if (st) return st;
   Stager sg{c};
@@ -390,6 +390,8 @@ asc_status asc_simulate_batch(asc_ctx* c, const asc_traces* tr, asc_outcomes* ou
   dt.ttft_slo_us = sg.up(tr->ttft_slo_us, Tn);
   dt.tbt_slo_us = sg.up(tr->tbt_slo_us, Tn);
   dt.req_ttft_slo_us = sg.up(tr->req_ttft_slo_us, Rn);
+  dt.n_lp = sg.up(tr->n_lp, Tn);
+  dt.n_hp = sg.up(tr->n_hp, Tn);
   asc_outcomes doc;
   doc.first_token_us = sg.out(out->first_token_us, Rn);
   doc.done_us = sg.out(out->done_us, Rn);

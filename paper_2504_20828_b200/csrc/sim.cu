@@ -82,6 +82,7 @@ struct SimP {
   int32_t mode;                  // asc_scheduler (0 Ascendra, 1 vLLM-like, 2 Sarathi-like)
   int32_t chunk_tok;             // Sarathi-like per-batch token budget
   int32_t* rq_cdone;             // Sarathi-like: prompt tokens prefilled (after the running chunk)
+  const int32_t *tr_nlp, *tr_nhp;  // optional per-trace topology (row f3)
 };
 
 // The launch parameters live in the constant bank (one copy per device, written before each launch
@@ -92,6 +93,7 @@ __constant__ SimP P;
 
 struct TS {  // per-trace controller state (shared memory, one per warp)
   int32_t rr_lp, rr_hp, fl_head, fl_tail;
+  int32_t n_lp, n_hp, K, sw;  // the trace's subgroup topology; sw: 1 offload, 2 tickets
   int64_t base, n, tbt;  // the trace's first request, its size and its TBT SLO
 };
 
@@ -110,6 +112,11 @@ struct Wp {
   __device__ __forceinline__ int64_t base() const { return ts()->base; }
   __device__ __forceinline__ int64_t n() const { return ts()->n; }
   __device__ __forceinline__ int64_t tbt() const { return ts()->tbt; }
+  __device__ __forceinline__ int nlp() const { return ts()->n_lp; }
+  __device__ __forceinline__ int nhp() const { return ts()->n_hp; }
+  __device__ __forceinline__ int K() const { return ts()->K; }
+  __device__ __forceinline__ bool offl() const { return ts()->sw & 1; }
+  __device__ __forceinline__ bool tickets() const { return ts()->sw & 2; }
 };
 
 __device__ __forceinline__ int64_t pf_of(int32_t p) {
@@ -499,7 +506,7 @@ __device__ __noinline__ int lp_admit(Wp w, int k, int64_t T, int32_t ndrop,
   const int64_t q2 = q + nadm;
   int32_t head = I.wq_head + nadm, rem = len - nadm;
   int32_t noff = 0;
-  if (P.offl && rem > 0) {
+  if (w.offl() && rem > 0) {
     if (P.policy == ASC_POLICY_EDF_LAXITY) {
       // offload range: the prefix with key <= othr; eligible entries leave, the rest (evicted,
       // ever-prefilled requests) are packed in order at the end of the range
@@ -577,12 +584,12 @@ __device__ __noinline__ int lp_admit(Wp w, int k, int64_t T, int32_t ndrop,
     const int32_t id = P.scr_off[w.base() + j];
     const int64_t g = w.base() + id;
     const int32_t rr = w.ts()->rr_hp;
-    const int h = P.n_lp + rr;
+    const int h = w.nlp() + rr;
     const int32_t tail = w.ts()->fl_tail;
     __syncwarp();
     if (lane == 0) {
       P.rq_fl[g] |= (F_ONHP | F_OFFL);
-      w.ts()->rr_hp = (rr + 1) % P.n_hp;
+      w.ts()->rr_hp = (rr + 1) % w.nhp();
       if (P.delay != 0) {
         P.fl_t[w.base() + tail] = T + P.delay;
         P.fl_req[w.base() + tail] = id;
@@ -1003,8 +1010,8 @@ __device__ __forceinline__ void complete(Wp w, int k, int64_t T) {
 
 // --------------------------------------------------------------------- controller routing ---
 __device__ __forceinline__ void route(Wp w, int32_t id) {
-  if (P.tickets) {
-    for (int h = P.n_lp; h < P.K; h++) {
+  if (w.tickets()) {
+    for (int h = w.nlp(); h < w.K(); h++) {
       if (w.SI()[h].ticket) {
         const int32_t tk = w.SI()[h].tk_live + 1;
         __syncwarp();
@@ -1019,7 +1026,7 @@ __device__ __forceinline__ void route(Wp w, int32_t id) {
   }
   const int32_t rr = w.ts()->rr_lp;
   wq_insert(w, rr, id);
-  w.ts()->rr_lp = (rr + 1) == P.n_lp ? 0 : rr + 1;
+  w.ts()->rr_lp = (rr + 1) == w.nlp() ? 0 : rr + 1;
   __syncwarp();
 }
 
@@ -1195,7 +1202,7 @@ __device__ __noinline__ int64_t run_decode(Wp w, int k, int64_t T_limit) {
   if (total == 0) return 0;
   const int64_t hs = I.hist_sum + hsum_all;
   const int32_t hc = I.hist_cnt + hcnt_all, tk = I.tk_live - tkd_all;
-  const bool issue = hp && P.tickets && !I.ticket && I.wq_len == 0 && tk == 0;  // phase E
+  const bool issue = hp && w.tickets() && !I.ticket && I.wq_len == 0 && tk == 0;  // phase E
   __syncwarp();
   I.kv_free = kvf;
   I.ctx_sum = S;
@@ -1227,15 +1234,15 @@ __device__ __noinline__ void init_trace(Wp w, int trace) {
     P.done[g] = -1;
     P.pstart[g] = -1;
   }
-  if (lane < P.K) {
+  if (lane < w.K()) {
     SInst& I = w.SI()[lane];
-    I.hp = lane >= P.n_lp;
+    I.hp = lane >= w.nlp();
     I.kv_total = I.kv_free = I.hp ? P.kv_hp : P.kv_lp;
     I.end = INF64; I.hist_sum = 0; I.ctx_sum = 0; I.hash = 0; I.nrec = 0; I.wq_head = 0;
     I.wq_len = I.ds_len = I.bp_len = I.hist_cnt = I.need_sum = 0;
     I.batch_dec = I.tk_live = 0;
     I.papp = 1;
-    I.ticket = (I.hp && P.tickets) ? 1 : 0;  // issued at t = 0 (G29)
+    I.ticket = (I.hp && w.tickets()) ? 1 : 0;  // issued at t = 0 (G29)
   }
   __syncwarp();
 }
@@ -1244,7 +1251,7 @@ __device__ __noinline__ void finish_trace(Wp w, int trace, int64_t decisions,
                                           int64_t evals) {
   const int lane = lane_id();
   bool stuck = false;
-  if (lane < P.K) stuck = w.SI()[lane].wq_len > 0 || w.SI()[lane].ds_len > 0;
+  if (lane < w.K()) stuck = w.SI()[lane].wq_len > 0 || w.SI()[lane].ds_len > 0;
   if (__any_sync(FULL, stuck) && lane == 0) atomicOr(P.err, ERR_INVARIANT);
   for (int64_t i = lane; i < w.n(); i += 32) {
     const int64_t g = w.base() + i;
@@ -1258,7 +1265,7 @@ __device__ __noinline__ void finish_trace(Wp w, int trace, int64_t decisions,
   }
   if (lane == 0) {
     uint64_t d = 0;
-    for (int k = 0; k < P.K; k++) d = mix64(d ^ w.SI()[k].hash);
+    for (int k = 0; k < w.K(); k++) d = mix64(d ^ w.SI()[k].hash);
     P.digest[trace] = d;
     if (P.decisions) P.decisions[trace] = decisions;
     if (P.evals) P.evals[trace] = evals;
@@ -1274,7 +1281,6 @@ template <int MINB>
 __global__ void __launch_bounds__(SW * 32, MINB) sim_kernel() {
   const int lane = threadIdx.x & 31;
   Wp w;
-  const int K = P.K, n_lp = P.n_lp;
   while (true) {
     int trace = 0;
     if (lane == 0) trace = atomicAdd(P.next_trace, 1);
@@ -1286,8 +1292,13 @@ __global__ void __launch_bounds__(SW * 32, MINB) sim_kernel() {
       t->base = b;
       t->n = P.off[trace + 1] - b;
       t->tbt = P.tbt[trace];
+      t->n_lp = P.tr_nlp ? P.tr_nlp[trace] : P.n_lp;
+      t->n_hp = P.tr_nhp ? P.tr_nhp[trace] : P.n_hp;
+      t->K = t->n_lp + t->n_hp;
+      t->sw = (P.offl && t->n_hp >= 1 ? 1 : 0) | (P.tickets && t->n_hp >= 1 ? 2 : 0);
     }
     __syncwarp();
+    const int K = w.K(), n_lp = w.nlp();
     init_trace(w, trace);
     int64_t next = 0, next_arr = w.n() > 0 ? P.arr[w.base()] : INF64, decisions = 0, evals = 0;
     while (true) {
@@ -1330,7 +1341,7 @@ __global__ void __launch_bounds__(SW * 32, MINB) sim_kernel() {
         }
       }
       // E. tickets (G29)
-      if (P.tickets) {
+      if (w.tickets()) {
         if (lane >= n_lp && lane < K) {
           SInst& I = w.SI()[lane];
           if (!I.ticket && I.wq_len == 0 && I.tk_live == 0) I.ticket = 1;
@@ -1367,6 +1378,10 @@ size_t sim_smem_per_warp(int K, int32_t* o_sd = nullptr, int32_t* o_si = nullptr
 // liveness / layout validation (ASC_E_CONFIG / ASC_E_INVAL before simulating)
 __global__ void validate_traces(int64_t R) {
   if (blockIdx.x == 0 && threadIdx.x == 0 && P.off[P.T] != R) atomicOr(P.err, ERR_INVAL);
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < P.T; t += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t nl = P.tr_nlp ? P.tr_nlp[t] : P.n_lp, nh = P.tr_nhp ? P.tr_nhp[t] : P.n_hp;
+    if (nl < 1 || nh < 0 || nl + nh > P.K || (P.mode != 0 && nh != 0)) atomicOr(P.err, 8);
+  }
   for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < R;
        g += (int64_t)gridDim.x * blockDim.x) {
     const int32_t p = P.pl[g], o = P.ol[g];
@@ -1440,8 +1455,10 @@ asc_status launch_simulate(asc_ctx* c, const asc_traces* tr, asc_outcomes* out, 
   P.n_lp = cf.topo.n_lp; P.n_hp = cf.topo.n_hp; P.K = K; P.bs = cf.topo.block_tokens;
   P.lp_max = cf.topo.lp_max_batch; P.lp_tok = cf.topo.lp_token_budget; P.hp_tok = cf.topo.hp_token_budget;
   P.policy = cf.flags.policy;
-  P.offl = (cf.flags.offload && cf.topo.n_hp >= 1) ? 1 : 0;
-  P.tickets = (cf.flags.tickets && cf.topo.n_hp >= 1) ? 1 : 0;
+  P.offl = cf.flags.offload ? 1 : 0;    // per trace: and n_hp >= 1
+  P.tickets = cf.flags.tickets ? 1 : 0;
+  P.tr_nlp = tr->n_lp;
+  P.tr_nhp = tr->n_hp;
   P.elastic = cf.flags.elastic; P.drop = cf.flags.drop; P.hist_def = cf.flags.hist_default_tokens;
   P.kv_lp = cf.topo.kv_blocks_lp; P.kv_hp = cf.topo.kv_blocks_hp;
   P.W = c->w_hp; P.margin = cf.flags.offload_margin_us; P.delay = cf.flags.offload_delay_us;
@@ -1479,8 +1496,9 @@ asc_status launch_simulate(asc_ctx* c, const asc_traces* tr, asc_outcomes* out, 
   cudaError_t ue = upload_params(P, sm);
   if (ue != cudaSuccess) return cuda_check(c, ue, "simulate parameters");
   int64_t launches = 0;
-  if (R > 0) {
-    const int64_t gb = (R + 255) / 256;
+  if (R > 0 || T > 0) {
+    const int64_t n = R > T ? R : T;
+    const int64_t gb = (n + 255) / 256;
     validate_traces<<<(unsigned)(gb < 4096 ? gb : 4096), 256, 0, sm>>>(R);
     launches++;
     asc_status v = collect_errors(c, "simulate_batch validation");
