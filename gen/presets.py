@@ -7,7 +7,7 @@ are marked "reading" and listed in DESIGN.md §Readings.
 """
 from . import traces as _tr
 
-POLICY = {"EDF_LAXITY": 0, "EDF_DEADLINE": 1, "SJF": 2, "LJF": 3, "FCFS": 4}
+POLICY = {"EDF_LAXITY": 0, "EDF_DEADLINE": 1, "SJF": 2, "LJF": 3, "FCFS": 4, "WEIGHTED": 5}
 # Ascendra (LP/HP) or a baseline scheduler on homogeneous instances
 SCHEDULER = {"ascendra": 0, "vllm": 1, "sarathi": 2}
 
@@ -36,7 +36,7 @@ def topology(n_lp=2, n_hp=1, block_tokens=16, kv_blocks_lp=25000, kv_blocks_hp=2
 
 def flags(policy="EDF_LAXITY", offload=1, tickets=1, elastic=1, drop=0,
           offload_margin_us=0, offload_delay_us=0, hist_default_tokens=256, scheduler="ascendra",
-          chunk_tokens=512):
+          chunk_tokens=512, offload_rule=0, key_weights=(1, -1, 0)):
     # chunk_tokens: Sarathi-like per-batch token budget (reading G47; 512 as in SPEC S:398)
     # EDF default; offload (§5.3); tickets (§6.1); elastic (§6.2); drop off (§6.3 is a mode)
     return dict(policy=POLICY[policy] if isinstance(policy, str) else int(policy),
@@ -44,7 +44,7 @@ def flags(policy="EDF_LAXITY", offload=1, tickets=1, elastic=1, drop=0,
                 offload_margin_us=offload_margin_us, offload_delay_us=offload_delay_us,
                 hist_default_tokens=hist_default_tokens,
                 scheduler=SCHEDULER[scheduler] if isinstance(scheduler, str) else int(scheduler),
-                chunk_tokens=chunk_tokens)
+                chunk_tokens=chunk_tokens, offload_rule=offload_rule, key_weights=tuple(key_weights))
 
 
 def config(arch=None, perf=None, topo=None, flg=None):

@@ -51,10 +51,15 @@ typedef enum {
  *  EDF_DEADLINE key = deadline = arrival + TTFT SLO
  *  SJF          key = prefill_us
  *  LJF          key = -prefill_us
- *  FCFS         key = arrival  (asc_schedule_step: entry position) */
+ *  FCFS         key = arrival  (asc_schedule_step: entry position)
+ *  WEIGHTED     key = key_w[0]*deadline + key_w[1]*prefill_us + key_w[2]*arrival: an operator
+ *               value function ("any customized policy"; row f4, G51);
+ *               asc_simulate_batch only.
+ * asc_simulate_batch adds asc_traces.req_key_offset_us[i] (when given) to request i's key under
+ * every policy: service classes, e.g. premium users ahead of the free tier. */
 typedef enum {
   ASC_POLICY_EDF_LAXITY = 0, ASC_POLICY_EDF_DEADLINE = 1, ASC_POLICY_SJF = 2,
-  ASC_POLICY_LJF = 3, ASC_POLICY_FCFS = 4
+  ASC_POLICY_LJF = 3, ASC_POLICY_FCFS = 4, ASC_POLICY_WEIGHTED = 5
 } asc_policy;
 
 /* Model symbols (App. A.1): hidden h, heads n, head size s (h = n*s), KV heads n_kv,
@@ -87,6 +92,11 @@ typedef struct {
                                     instances (requires n_hp = 0, DESIGN G46-G48) */
   int32_t chunk_tokens;          /* ASC_SCHED_SARATHI: per-batch token budget, decodes + prefill
                                     chunks (G47; in [1, 2^24)); ignored otherwise */
+  int32_t offload_rule;          /* 0: the paper's rule: deadline - T <= prefill_us + W_hp
+                                    + margin.  1: look-ahead (row f4, G50): + the prefill_us of
+                                    every waiting request ahead in priority order.
+                                    asc_simulate_batch only (asc_schedule_step: ASC_E_CONFIG) */
+  int32_t key_w[3];              /* ASC_POLICY_WEIGHTED weights, each in [-1024, 1024] */
 } asc_flags;
 
 /* Schedulers asc_simulate_batch can run.  ASC_SCHED_VLLM is the vLLM-like baseline the paper
@@ -195,6 +205,8 @@ typedef struct {
                                       f3): trace t runs on n_lp[t] LP + n_hp[t] HP instances; */
   const int32_t* n_hp;             /* n_lp >= 1, n_hp >= 0, n_lp + n_hp <= the ctx's n_lp + n_hp
                                       (ASC_E_CONFIG otherwise); NULL = the ctx's topology */
+  const int64_t* req_key_offset_us; /* [R] optional value-function offset per request (service
+                                      class, G51): added to the policy key; |offset| < 2^40 */
 } asc_traces;
 
 typedef struct {

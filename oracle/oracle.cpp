@@ -8,6 +8,7 @@
 #include "oracle.h"
 
 #include <algorithm>
+#include <map>
 #include <atomic>
 #include <cmath>
 #include <cstdio>
@@ -245,12 +246,14 @@ extern "C" int32_t or_algorithm1(int32_t n, const int64_t* val, const int64_t* i
 // Priority value pi (G19): Algorithm 1 sorts by val descending; we use val = -key.
 // EDF_LAXITY key = deadline - prefill_us; EDF_DEADLINE key = deadline; SJF key = prefill_us;
 // LJF key = -prefill_us; FCFS key = arrival.
-static int64_t key_of(int policy, int64_t arrival, int64_t deadline, int64_t pf_us) {
+static int64_t key_of(int policy, int64_t arrival, int64_t deadline, int64_t pf_us,
+                      const int32_t* w = nullptr) {
   switch (policy) {
     case 0: return deadline - pf_us;
     case 1: return deadline;
     case 2: return pf_us;
     case 3: return -pf_us;
+    case 5: return (int64_t)w[0] * deadline + (int64_t)w[1] * pf_us + (int64_t)w[2] * arrival;
     default: return arrival;
   }
 }
@@ -282,6 +285,7 @@ extern "C" int or_schedule_step(const or_arch* a_in, const or_perf* pf, const or
                                 int32_t* admit_cnt, int32_t* offload_idx, int32_t* offload_cnt,
                                 int32_t* drop_idx, int32_t* drop_cnt, int64_t* batch_lat_us,
                                 int32_t* prefill_us) {
+  if (sc->policy == 5 || sc->offload_rule != 0) { set_err("step: WEIGHTED policy / look-ahead offload are simulator-only"); return 2; }
   if (!check_cfg(a_in, pf)) return 2;
   or_arch a;
   apply_tp(a_in, &a);
@@ -393,6 +397,7 @@ struct Req {
   int64_t eff;         // effective prompt (prompt + generated after preemption)
   int64_t held = 0;    // KV blocks held
   int64_t cdone = 0;   // prompt tokens already prefilled (Sarathi-like chunks, G47)
+  int64_t koff = 0;    // value-function offset of the request's service class (G51)
   bool ever = false, onhp = false, ticketed = false, offloaded = false;
   int state = UNFINISHED;
   int64_t first = -1, done = -1, pstart = -1;
@@ -433,8 +438,8 @@ struct Sim {
 
   int64_t pf_us(int64_t eff) { return prefill_us_of(a, pf, eff); }
   int64_t blk(int64_t eff) { return ceil_div(eff + 1, sc->bs); }
-  int64_t key(int i) {
-    return key_of(sc->policy, r[i].arrival, r[i].deadline, pf_us(r[i].eff));
+  int64_t key(int i) {  // value function (G19) + the request's class offset (G51)
+    return key_of(sc->policy, r[i].arrival, r[i].deadline, pf_us(r[i].eff), sc->key_w) + r[i].koff;
   }
   bool fcfs_less(int x, int y) {
     if (r[x].arrival != r[y].arrival) return r[x].arrival < r[y].arrival;
@@ -598,11 +603,22 @@ struct Sim {
     // Offload (§5.3, G24): remaining never-prefilled requests projected to miss TTFT.
     std::vector<int> off;
     if (sc->offload && sc->n_hp >= 1) {
+      // look-ahead (G50): the prefill time of every waiting request ahead in priority order
+      std::map<int, int64_t> ahead;
+      if (sc->offload_rule == 1) {
+        std::vector<int> ord = in.waiting;
+        std::sort(ord.begin(), ord.end(), [&](int x, int y) {
+          const int64_t kx = key(x), ky = key(y);
+          return kx != ky ? kx < ky : x < y;
+        });
+        int64_t sum = 0;
+        for (int i : ord) { ahead[i] = sum; sum += pf_us(r[i].eff); }
+      }
       std::vector<int> ids = in.waiting;
       std::sort(ids.begin(), ids.end());
       for (int i : ids)
         if (!r[i].ever && !r[i].onhp &&
-            r[i].deadline - T <= pf_us(r[i].eff) + Whp + sc->margin_us)
+            r[i].deadline - T <= pf_us(r[i].eff) + Whp + sc->margin_us + (sc->offload_rule == 1 ? ahead[i] : 0))
           off.push_back(i);
       for (int i : off) {
         in.waiting.erase(std::find(in.waiting.begin(), in.waiting.end(), i));
@@ -887,7 +903,8 @@ struct Sim {
 
 static int simulate_one(const or_arch* a, const or_perf* pf, const or_sched* sc, int64_t n,
                         const int64_t* arr, const int32_t* pl, const int32_t* ol, int64_t ttft,
-                        int64_t tbt, const int64_t* req_ttft, int64_t* first, int64_t* done,
+                        int64_t tbt, const int64_t* req_ttft, const int64_t* koff,
+                        int64_t* first, int64_t* done,
                         int64_t* pstart, uint32_t* status, uint64_t* digest, int64_t* decisions,
                         int64_t* evaluations, bool check, std::string& err) {
   Sim s;
@@ -899,6 +916,7 @@ static int simulate_one(const or_arch* a, const or_perf* pf, const or_sched* sc,
     q.ttft = req_ttft ? req_ttft[i] : ttft;
     q.deadline = q.arrival + q.ttft;
     q.p = pl[i]; q.o = ol[i]; q.eff = q.p;
+    q.koff = koff ? koff[i] : 0;
   }
   const int K = sc->n_lp + sc->n_hp;
   s.I.resize(K);
@@ -928,7 +946,8 @@ extern "C" int or_simulate_batch(const or_arch* a_in, const or_perf* pf, const o
                                  int32_t T, const int64_t* off, const int64_t* arr,
                                  const int32_t* pl, const int32_t* ol, const int64_t* ttft,
                                  const int64_t* tbt, const int64_t* req_ttft,
-                                 const int32_t* tr_nlp, const int32_t* tr_nhp, int64_t* first,
+                                 const int32_t* tr_nlp, const int32_t* tr_nhp,
+                                 const int64_t* req_koff, int64_t* first,
                                  int64_t* done, int64_t* pstart, uint32_t* status,
                                  uint64_t* digest, int64_t* decisions, int64_t* evaluations,
                                  int32_t nthreads, int32_t check) {
@@ -938,6 +957,9 @@ extern "C" int or_simulate_batch(const or_arch* a_in, const or_perf* pf, const o
     set_err("sched: bad topology"); return 2;
   }
   if (sc->scheduler < 0 || sc->scheduler > 2) { set_err("sched: unknown scheduler"); return 2; }
+  if (sc->policy < 0 || sc->policy > 5 || sc->offload_rule < 0 || sc->offload_rule > 1) {
+    set_err("sched: unknown policy or offload rule"); return 2;
+  }
   if (sc->scheduler == 2 && sc->chunk_tokens < 1) { set_err("sched: chunk_tokens < 1"); return 2; }
   for (int32_t t = 0; t < T; t++) {
     const int32_t nl = tr_nlp ? tr_nlp[t] : sc->n_lp, nh = tr_nhp ? tr_nhp[t] : sc->n_hp;
@@ -974,7 +996,8 @@ extern "C" int or_simulate_batch(const or_arch* a_in, const or_perf* pf, const o
       if (tr_nlp) sct.n_lp = tr_nlp[t];
       if (tr_nhp) sct.n_hp = tr_nhp[t];
       const int st = simulate_one(&a, pf, &sct, n, arr + lo, pl + lo, ol + lo, ttft[t], tbt[t],
-                                  req_ttft ? req_ttft + lo : nullptr, first + lo, done + lo,
+                                  req_ttft ? req_ttft + lo : nullptr,
+                                  req_koff ? req_koff + lo : nullptr, first + lo, done + lo,
                                   pstart + lo, status + lo, digest + t, decisions + t,
                                   evaluations + t, check != 0, e);
       if (st) {

@@ -29,6 +29,9 @@ typedef struct {
   int64_t margin_us, delay_us;
   int32_t scheduler;  /* 0 Ascendra (LP/HP); 1 vLLM-like (G46); 2 Sarathi-like (G47) */
   int32_t chunk_tokens;  /* Sarathi-like per-batch token budget (decodes + prefill chunks, G47) */
+  int32_t offload_rule;  /* 0 paper; 1 look-ahead: + prefill_us of the waiting requests
+                            ahead in priority order (row f4, G50) */
+  int32_t key_w[3];      /* policy 5 (WEIGHTED): key = w0 deadline + w1 prefill_us + w2 arrival */
 } or_sched;
 
 /* Eq. 1-3 with App. A.2/A.3 GEMM terms: exact integer F (flops) and M (bytes) of a batch of
@@ -52,7 +55,9 @@ int64_t or_batch_us(const or_arch* a, const or_perf* pf, int32_t np, const int64
                     int32_t nd, const int64_t* lhat);
 
 /* or_simulate_batch: trace_n_lp / trace_n_hp (may be NULL) give trace t its own subgroup
- * topology (row f3): n_lp >= 1, n_hp >= 0, n_lp + n_hp <= sc->n_lp + sc->n_hp. */
+ * topology (row f3): n_lp >= 1, n_hp >= 0, n_lp + n_hp <= sc->n_lp + sc->n_hp.
+ * req_key_offset_us (may be NULL): per-request value-function offset added to the key under
+ * every policy (service classes; G51). */
 
 /* Eq. 4-5 calibration ("perform a linear regression to find ... C1 ... C5", P:279
  * online refit; readings G49): for each of G groups of batch records (CSR off[],
@@ -91,6 +96,7 @@ int or_simulate_batch(const or_arch* a, const or_perf* pf, const or_sched* sc, i
                       const int64_t* ttft_slo_us, const int64_t* tbt_slo_us,
                       const int64_t* req_ttft_slo_us,
                       const int32_t* trace_n_lp, const int32_t* trace_n_hp,
+                      const int64_t* req_key_offset_us,
                       int64_t* first_token_us, int64_t* done_us, int64_t* prefill_start_us,
                       uint32_t* status, uint64_t* digest, int64_t* decisions,
                       int64_t* evaluations, int32_t nthreads, int32_t check_invariants);

@@ -27,7 +27,8 @@ class OrSched(C.Structure):
                                           "lp_tok", "hp_tok", "policy", "offload", "tickets",
                                           "elastic", "drop", "hist_default")]
                 + [("margin_us", C.c_int64), ("delay_us", C.c_int64), ("scheduler", C.c_int32),
-                   ("chunk_tokens", C.c_int32)])
+                   ("chunk_tokens", C.c_int32), ("offload_rule", C.c_int32),
+                   ("key_w", C.c_int32 * 3)])
 
 
 def build():
@@ -64,7 +65,8 @@ def sched_s(cfg):
                    t["lp_max_batch"], t["lp_token_budget"], t["hp_token_budget"], f["policy"],
                    f["offload"], f["tickets"], f["elastic"], f["drop"], f["hist_default_tokens"],
                    f["offload_margin_us"], f["offload_delay_us"], f.get("scheduler", 0),
-                   f.get("chunk_tokens", 512))
+                   f.get("chunk_tokens", 512), f.get("offload_rule", 0),
+                   (C.c_int32 * 3)(*f.get("key_weights", (1, -1, 0))))
 
 
 def _p(a, dt):
@@ -177,7 +179,7 @@ def schedule_step(cfg, seg_off, now_us, deadline_us, eff_prompt, flags, dec_coun
 
 
 def simulate_batch(cfg, batch, req_ttft_slo_us=None, nthreads=0, check_invariants=False,
-                   n_lp=None, n_hp=None):
+                   n_lp=None, n_hp=None, req_key_offset_us=None):
     """batch: gen.traces.TraceBatch; n_lp / n_hp: optional per-trace subgroup topology (row f3).
     Returns dict of per-request and per-trace outputs."""
     T, R = batch.T, batch.R
@@ -194,8 +196,10 @@ def simulate_batch(cfg, batch, req_ttft_slo_us=None, nthreads=0, check_invariant
     a, ps, sc = arch_s(cfg["arch"]), perf_s(cfg["perf"]), sched_s(cfg)
     nl = _p(n_lp, np.int32) if n_lp is not None else None
     nh = _p(n_hp, np.int32) if n_hp is not None else None
+    ko = _p(req_key_offset_us, np.int64) if req_key_offset_us is not None else None
     rc = lib().or_simulate_batch(C.byref(a), C.byref(ps), C.byref(sc), T, *[x[1] for x in ins],
                                  rt[1] if rt else None, nl[1] if nl else None, nh[1] if nh else None,
+                                 ko[1] if ko else None,
                                  *[out[k].ctypes.data_as(C.c_void_p) for k in
                                    ("first_token_us", "done_us", "prefill_start_us", "status",
                                     "digest", "decisions", "evaluations")],

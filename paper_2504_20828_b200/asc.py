@@ -47,7 +47,8 @@ class asc_flags(C.Structure):
     _fields_ = [("policy", C.c_int32), ("offload", C.c_uint8), ("tickets", C.c_uint8),
                 ("elastic", C.c_uint8), ("drop", C.c_uint8), ("offload_margin_us", C.c_int64),
                 ("offload_delay_us", C.c_int64), ("hist_default_tokens", C.c_int32),
-                ("scheduler", C.c_int32), ("chunk_tokens", C.c_int32)]
+                ("scheduler", C.c_int32), ("chunk_tokens", C.c_int32),
+                ("offload_rule", C.c_int32), ("key_w", C.c_int32 * 3)]
 
 
 class asc_config(C.Structure):
@@ -71,7 +72,7 @@ class asc_step_out(C.Structure):
 class asc_traces(C.Structure):
     _fields_ = [("T", C.c_int32), ("R", C.c_int64)] + [(k, _P) for k in (
         "trace_off", "arrival_us", "prompt_len", "output_len", "ttft_slo_us", "tbt_slo_us",
-        "req_ttft_slo_us", "n_lp", "n_hp")]
+        "req_ttft_slo_us", "n_lp", "n_hp", "req_key_offset_us")]
 
 
 class asc_fit_in(C.Structure):
@@ -124,7 +125,8 @@ def make_config(cfg):
                      t["lp_max_batch"], t["lp_token_budget"], t["hp_token_budget"]),
         asc_flags(f["policy"], f["offload"], f["tickets"], f["elastic"], f["drop"],
                   f["offload_margin_us"], f["offload_delay_us"], f["hist_default_tokens"],
-                  f.get("scheduler", 0), f.get("chunk_tokens", 512)))
+                  f.get("scheduler", 0), f.get("chunk_tokens", 512), f.get("offload_rule", 0),
+                  (C.c_int32 * 3)(*f.get("key_weights", (1, -1, 0)))))
 
 
 def _ptr(x):
@@ -183,10 +185,12 @@ def asc_schedule_step(ctx, seg_off, now_us, deadline_us, eff_prompt, flags, dec_
 
 def asc_simulate_batch(ctx, trace_off, arrival_us, prompt_len, output_len, ttft_slo_us, tbt_slo_us,
                        first_token_us, done_us, prefill_start_us, status, digest, decisions=None,
-                       evaluations=None, req_ttft_slo_us=None, R=-1, n_lp=None, n_hp=None):
+                       evaluations=None, req_ttft_slo_us=None, R=-1, n_lp=None, n_hp=None,
+                       req_key_offset_us=None):
     T = len(trace_off) - 1
     tr = asc_traces(T, R, *[_ptr(x) for x in (trace_off, arrival_us, prompt_len, output_len,
-                                           ttft_slo_us, tbt_slo_us, req_ttft_slo_us, n_lp, n_hp)])
+                                           ttft_slo_us, tbt_slo_us, req_ttft_slo_us, n_lp, n_hp,
+                                           req_key_offset_us)])
     oc = asc_outcomes(*[_ptr(x) for x in (first_token_us, done_us, prefill_start_us, status,
                                           digest, decisions, evaluations)])
     _check(ctx, lib().asc_simulate_batch(ctx, C.byref(tr), C.byref(oc)), "asc_simulate_batch")
@@ -254,7 +258,8 @@ class Context:
                           out["drop_cnt"], out["batch_lat_us"], out["prefill_us"], Q=Q)
         return out
 
-    def simulate_batch(self, tr, req_ttft_slo_us=None, out=None, n_lp=None, n_hp=None):
+    def simulate_batch(self, tr, req_ttft_slo_us=None, out=None, n_lp=None, n_hp=None,
+                       req_key_offset_us=None):
         """tr: dict trace_off, arrival_us, prompt_len, output_len, ttft_slo_us, tbt_slo_us;
         n_lp / n_hp: optional per-trace subgroup topology (int32 [T], same kind as tr)."""
         dev = not isinstance(tr["trace_off"], np.ndarray)
@@ -269,7 +274,8 @@ class Context:
                            tr["output_len"], tr["ttft_slo_us"], tr["tbt_slo_us"],
                            out["first_token_us"], out["done_us"], out["prefill_start_us"],
                            out["status"], out["digest"], out["decisions"], out["evaluations"],
-                           req_ttft_slo_us, R=R, n_lp=n_lp, n_hp=n_hp)
+                           req_ttft_slo_us, R=R, n_lp=n_lp, n_hp=n_hp,
+                           req_key_offset_us=req_key_offset_us)
         return out
 
     def goodput(self, tr, out, req_ttft_slo_us=None, res=None):

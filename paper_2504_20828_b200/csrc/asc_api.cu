@@ -116,7 +116,11 @@ asc_status asc_create(const asc_config* cfg, int device, void* cuda_stream, asc_
   CHK(t.lp_max_batch >= 1 && t.lp_max_batch <= ASC_MAX_BATCH, "topo.lp_max_batch must be in [1, ASC_MAX_BATCH]");
   CHK(t.lp_token_budget >= 1 && t.lp_token_budget < (1 << 24), "topo.lp_token_budget must be in [1, 2^24)");
   CHK(t.hp_token_budget >= 1 && t.hp_token_budget < (1 << 24), "topo.hp_token_budget must be in [1, 2^24)");
-  CHK(f.policy >= 0 && f.policy <= 4, "flags.policy must be an asc_policy");
+  CHK(f.policy >= 0 && f.policy <= 5, "flags.policy must be an asc_policy");
+  CHK(f.offload_rule == 0 || f.offload_rule == 1, "flags.offload_rule must be 0 or 1");
+  CHK(f.key_w[0] >= -1024 && f.key_w[0] <= 1024 && f.key_w[1] >= -1024 && f.key_w[1] <= 1024 &&
+          f.key_w[2] >= -1024 && f.key_w[2] <= 1024,
+      "flags.key_w must be in [-1024, 1024]");
   CHK(f.offload_margin_us >= 0 && f.offload_delay_us >= 0, "flags.offload_margin_us/offload_delay_us must be >= 0");
   CHK(f.hist_default_tokens >= 0, "flags.hist_default_tokens must be >= 0");
   CHK(f.scheduler == ASC_SCHED_ASCENDRA || f.scheduler == ASC_SCHED_VLLM || f.scheduler == ASC_SCHED_SARATHI,
@@ -266,6 +270,8 @@ extern "C" {
 
 asc_status asc_schedule_step(asc_ctx* c, const asc_step_in* in, asc_step_out* out) {
   if (!c || !in || !out) return fail(c, ASC_E_INVAL, "asc_schedule_step: NULL argument");
+  if (c->cfg.flags.policy == ASC_POLICY_WEIGHTED || c->cfg.flags.offload_rule != 0)
+    return fail(c, ASC_E_CONFIG, "asc_schedule_step: ASC_POLICY_WEIGHTED and offload_rule 1 are asc_simulate_batch only");
   c->err.clear();
   c->timed = false;
   if (in->S < 0) return fail(c, ASC_E_INVAL, "asc_schedule_step: S < 0");
@@ -350,7 +356,7 @@ asc_status asc_simulate_batch(asc_ctx* c, const asc_traces* tr, asc_outcomes* ou
   cudaSetDevice(c->device);
   const int kind = ptr_kind(tr->trace_off);
   if (!same_kind(kind, {tr->arrival_us, tr->prompt_len, tr->output_len, tr->ttft_slo_us,
-                        tr->tbt_slo_us, tr->req_ttft_slo_us, tr->n_lp, tr->n_hp,
+                        tr->tbt_slo_us, tr->req_ttft_slo_us, tr->n_lp, tr->n_hp, tr->req_key_offset_us,
                         out->first_token_us, out->done_us, out->prefill_start_us, out->status,
                         out->digest, out->decisions, out->evaluations}))
     return fail(c, ASC_E_INVAL, "asc_simulate_batch: host and device pointers mixed");
@@ -377,7 +383,7 @@ asc_status asc_simulate_batch(asc_ctx* c, const asc_traces* tr, asc_outcomes* ou
   }
   const size_t Tn = (size_t)T, Rn = (size_t)R;
   size_t need = rup(8 * (Tn + 1)) + rup(8 * Rn) * 2 + rup(4 * Rn) * 2 + rup(8 * Tn) * 2 +
-                rup(8 * Rn) * 3 + rup(4 * Rn) + rup(8 * Tn) * 3 + rup(4 * Tn) * 2 + 4096;
+                rup(8 * Rn) * 3 + rup(4 * Rn) + rup(8 * Tn) * 3 + rup(4 * Tn) * 2 + rup(8 * Rn) + 4096;
   st = ensure_stage(c, need);
   if (st) return st;
   Stager sg{c};
@@ -392,6 +398,7 @@ asc_status asc_simulate_batch(asc_ctx* c, const asc_traces* tr, asc_outcomes* ou
   dt.req_ttft_slo_us = sg.up(tr->req_ttft_slo_us, Rn);
   dt.n_lp = sg.up(tr->n_lp, Tn);
   dt.n_hp = sg.up(tr->n_hp, Tn);
+  dt.req_key_offset_us = sg.up(tr->req_key_offset_us, Rn);
   asc_outcomes doc;
   doc.first_token_us = sg.out(out->first_token_us, Rn);
   doc.done_us = sg.out(out->done_us, Rn);

@@ -83,6 +83,9 @@ struct SimP {
   int32_t chunk_tok;             // Sarathi-like per-batch token budget
   int32_t* rq_cdone;             // Sarathi-like: prompt tokens prefilled (after the running chunk)
   const int32_t *tr_nlp, *tr_nhp;  // optional per-trace topology (row f3)
+  int32_t look;                    // offload rule 1: look-ahead (G50)
+  int32_t kw0, kw1, kw2;           // ASC_POLICY_WEIGHTED weights (G51)
+  const int64_t* rq_koff;          // optional per-request value-function offsets (G51)
 };
 
 // The launch parameters live in the constant bank (one copy per device, written before each launch
@@ -129,13 +132,16 @@ __device__ __forceinline__ int32_t blk_of(int32_t eff) { return (eff + P.bs) / P
 
 // time-invariant priority key of request gid with effective prompt eff (DESIGN.md §2 Keys)
 __device__ __forceinline__ int64_t key_of(int64_t gid, int32_t eff) {
+  int64_t k;
   switch (P.policy) {
-    case 0: return P.rq_dl[gid] - pf_of(eff);
-    case 1: return P.rq_dl[gid];
-    case 2: return pf_of(eff);
-    case 3: return -pf_of(eff);
-    default: return P.arr[gid];
+    case 0: k = P.rq_dl[gid] - pf_of(eff); break;
+    case 1: k = P.rq_dl[gid]; break;
+    case 2: k = pf_of(eff); break;
+    case 3: k = -pf_of(eff); break;
+    case 5: k = (int64_t)P.kw0 * P.rq_dl[gid] + (int64_t)P.kw1 * pf_of(eff) + (int64_t)P.kw2 * P.arr[gid]; break;
+    default: k = P.arr[gid]; break;
   }
+  return P.rq_koff ? k + P.rq_koff[gid] : k;  // service-class offset (G51)
 }
 
 __device__ __forceinline__ int64_t ioff(int k, Wp w) { return (int64_t)k * P.R + w.base(); }
@@ -507,7 +513,7 @@ __device__ __noinline__ int lp_admit(Wp w, int k, int64_t T, int32_t ndrop,
   int32_t head = I.wq_head + nadm, rem = len - nadm;
   int32_t noff = 0;
   if (w.offl() && rem > 0) {
-    if (P.policy == ASC_POLICY_EDF_LAXITY) {
+    if (P.policy == ASC_POLICY_EDF_LAXITY && !P.look && !P.rq_koff) {
       // offload range: the prefix with key <= othr; eligible entries leave, the rest (evicted,
       // ever-prefilled requests) are packed in order at the end of the range
       const int64_t othr = T + P.W + P.margin;
@@ -544,19 +550,31 @@ __device__ __noinline__ int lp_admit(Wp w, int k, int64_t T, int32_t ndrop,
       head += wpos;  // wpos = number of offloaded entries
       rem -= wpos;
     } else {
+      // the whole remaining queue (in priority order); look-ahead (G50) adds the prefill time of
+      // every remaining request ahead of this one
       int32_t out = 0;
+      int64_t ahead = 0;
       for (int32_t c = 0; c < rem; c += 32) {
         const int32_t j = c + lane;
         const bool v = j < rem;
         int32_t id = 0;
         int64_t key = 0;
         bool off = false;
+        int64_t pf = 0;
         if (v) {
           id = P.wq_id[q2 + j];
           key = P.wq_key[q2 + j];
+          pf = pf_of(P.rq_eff[w.base() + id]);
+        }
+        int64_t ex = 0;
+        if (P.look) {
+          const int64_t inc = warp_incl_scan(pf);
+          ex = ahead + inc - pf;
+          ahead += __shfl_sync(FULL, inc, 31);
+        }
+        if (v) {
           const int64_t g = w.base() + id;
-          off = !(P.rq_fl[g] & (F_EVER | F_ONHP)) &&
-                P.rq_dl[g] - T <= pf_of(P.rq_eff[g]) + P.W + P.margin;
+          off = !(P.rq_fl[g] & (F_EVER | F_ONHP)) && P.rq_dl[g] - T <= pf + P.W + P.margin + ex;
         }
         const uint32_t mk = __ballot_sync(FULL, v && !off), mo = __ballot_sync(FULL, off);
         if (v && !off) {
@@ -1459,6 +1477,9 @@ asc_status launch_simulate(asc_ctx* c, const asc_traces* tr, asc_outcomes* out, 
   P.tickets = cf.flags.tickets ? 1 : 0;
   P.tr_nlp = tr->n_lp;
   P.tr_nhp = tr->n_hp;
+  P.look = cf.flags.offload_rule;
+  P.kw0 = cf.flags.key_w[0]; P.kw1 = cf.flags.key_w[1]; P.kw2 = cf.flags.key_w[2];
+  P.rq_koff = tr->req_key_offset_us;
   P.elastic = cf.flags.elastic; P.drop = cf.flags.drop; P.hist_def = cf.flags.hist_default_tokens;
   P.kv_lp = cf.topo.kv_blocks_lp; P.kv_hp = cf.topo.kv_blocks_hp;
   P.W = c->w_hp; P.margin = cf.flags.offload_margin_us; P.delay = cf.flags.offload_delay_us;

@@ -193,3 +193,38 @@ def check_vllm_fcfs_order(sim, rng, trials=4):
             for k in range(n_lp):
                 q = ps[ins == k]
                 assert np.all(np.diff(q) >= 0)
+
+
+# ----------------------------------------------------- value functions and offload rules (f4) --
+def w8_case(rule):
+    g = H.golden("w8_lookahead_offload.json")
+    t = g["topology"]
+    cfg = H.tiny_cfg(n_lp=t["n_lp"], n_hp=t["n_hp"], block_tokens=t["block_tokens"],
+                     kv_blocks=t["kv_blocks"], lp_max_batch=t["lp_max_batch"],
+                     lp_token_budget=t["lp_token_budget"], hp_token_budget=t["hp_token_budget"],
+                     policy="EDF_LAXITY", offload=1, tickets=0, elastic=0)
+    cfg["flags"]["offload_rule"] = 0 if rule == "paper" else 1
+    req = np.array(g["requests"], np.int64)
+    b = TR.make_batch([(req[:, 0] * H.SEC, req[:, 1], req[:, 2])], [g["ttft"] * H.SEC], [g["tbt"] * H.SEC])
+    return cfg, b, g["expect"][rule]
+
+
+def check_w8(sim, goodput):
+    for rule in ("paper", "lookahead"):
+        cfg, b, exp = w8_case(rule)
+        out = sim(cfg, b)
+        assert [int(x) // H.SEC for x in out["first_token_us"]] == exp["first_token"], rule
+        assert list((out["status"] >> 2) & 1) == exp["offloaded"], rule
+        g, t = goodput(b, out)
+        assert int(g[0]) == exp["good"], rule
+
+
+WEIGHTED_EQUIV = [((1, -1, 0), "EDF_LAXITY"), ((1, 0, 0), "EDF_DEADLINE"), ((0, 1, 0), "SJF"),
+                  ((0, -1, 0), "LJF"), ((0, 0, 1), "FCFS")]
+
+
+def class_offsets(b, seed, premium_us=-2_000_000):
+    """every other request (by a counter hash) is 'premium': its key moves premium_us earlier"""
+    from gen.traces import mix_np
+    h = mix_np(np.arange(b.R, dtype=np.uint64) + np.uint64(seed))
+    return np.where((h & np.uint64(1)) == 1, premium_us, 0).astype(np.int64)

@@ -32,9 +32,11 @@ def test_struct_layout_matches_header():
     assert C.sizeof(asc.asc_arch) == 36
     assert C.sizeof(asc.asc_perf) == 56
     assert C.sizeof(asc.asc_topology) == 32
-    assert C.sizeof(asc.asc_flags) == 40 and asc.asc_flags.offload_margin_us.offset == 8
+    assert C.sizeof(asc.asc_flags) == 56 and asc.asc_flags.offload_margin_us.offset == 8
     assert asc.asc_flags.scheduler.offset == 28 and asc.asc_flags.chunk_tokens.offset == 32
+    assert asc.asc_flags.offload_rule.offset == 36 and asc.asc_flags.key_w.offset == 40
     assert asc.asc_config.flags.offset == 128
+    assert C.sizeof(asc.asc_traces) == 96 and asc.asc_traces.req_key_offset_us.offset == 88
 
 
 @pytest.mark.parametrize("mut,field", [
@@ -45,6 +47,8 @@ def test_struct_layout_matches_header():
     (lambda c: c["perf"].update(M_H=0.0), "M_H"),
     (lambda c: c["flags"].update(policy=9), "policy"),
     (lambda c: c["flags"].update(scheduler=5), "flags.scheduler must be"),
+    (lambda c: c["flags"].update(offload_rule=2), "offload_rule"),
+    (lambda c: c["flags"].update(key_weights=(1, 2000, 0)), "key_w"),
     (lambda c: c["flags"].update(scheduler=1), "topo.n_hp must be 0"),
     (lambda c: (c["flags"].update(scheduler=2, chunk_tokens=0), c["topo"].update(n_hp=0)), "chunk_tokens"),
 ])
