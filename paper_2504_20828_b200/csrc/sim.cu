@@ -885,6 +885,11 @@ __device__ __forceinline__ int64_t form_sar(Wp w, int k, int64_t T) {
   return form_sarathi(w, k, T);
 }
 
+// baseline schedulers, out of line so Ascendra's event loop keeps its instruction footprint
+__device__ __noinline__ int64_t form_baseline(Wp w, int k, int64_t T) {
+  return P.mode == 1 ? form_hp(w, k, T) : form_sar(w, k, T);
+}
+
 // ------------------------------------------------------------------ phase A: batch completion --
 __device__ __forceinline__ void finish_req(int64_t g, int64_t T) {
   P.done[g] = T;
@@ -1027,9 +1032,11 @@ __device__ __forceinline__ void complete(Wp w, int k, int64_t T) {
 }
 
 // --------------------------------------------------------------------- controller routing ---
+template <bool PLAIN>
 __device__ __forceinline__ void route(Wp w, int32_t id) {
-  if (w.tickets()) {
-    for (int h = w.nlp(); h < w.K(); h++) {
+  const int n_lp = PLAIN ? P.n_lp : w.nlp(), K = PLAIN ? P.K : w.K();
+  if (PLAIN ? (P.tickets && P.n_hp >= 1) : w.tickets()) {
+    for (int h = n_lp; h < K; h++) {
       if (w.SI()[h].ticket) {
         const int32_t tk = w.SI()[h].tk_live + 1;
         __syncwarp();
@@ -1044,7 +1051,7 @@ __device__ __forceinline__ void route(Wp w, int32_t id) {
   }
   const int32_t rr = w.ts()->rr_lp;
   wq_insert(w, rr, id);
-  w.ts()->rr_lp = (rr + 1) == w.nlp() ? 0 : rr + 1;
+  w.ts()->rr_lp = (rr + 1) == n_lp ? 0 : rr + 1;
   __syncwarp();
 }
 
@@ -1295,7 +1302,10 @@ __device__ __noinline__ void finish_trace(Wp w, int trace, int64_t decisions,
 // launch picks the largest budget that still keeps every trace of the call resident at once
 // (T <= SMs x MINB x SW): a trace is a serial chain, so registers beat extra resident warps
 // only while no trace waits for a slot.
-template <int MINB>
+// PLAIN: Ascendra with the ctx's topology for every trace (the common case): topology, tickets
+// and the scheduler come from the constant bank, so none of them is live across the event loop's
+// out-of-line calls.
+template <int MINB, bool PLAIN>
 __global__ void __launch_bounds__(SW * 32, MINB) sim_kernel() {
   const int lane = threadIdx.x & 31;
   Wp w;
@@ -1316,7 +1326,7 @@ __global__ void __launch_bounds__(SW * 32, MINB) sim_kernel() {
       t->sw = (P.offl && t->n_hp >= 1 ? 1 : 0) | (P.tickets && t->n_hp >= 1 ? 2 : 0);
     }
     __syncwarp();
-    const int K = w.K(), n_lp = w.nlp();
+    const int K = PLAIN ? P.K : w.K(), n_lp = PLAIN ? P.n_lp : w.nlp();
     init_trace(w, trace);
     int64_t next = 0, next_arr = w.n() > 0 ? P.arr[w.base()] : INF64, decisions = 0, evals = 0;
     while (true) {
@@ -1338,15 +1348,14 @@ __global__ void __launch_bounds__(SW * 32, MINB) sim_kernel() {
       if (flight) deliver(w, T);
       // C. arrivals, ascending id
       while (next_arr == T) {
-        route(w, (int32_t)next);
+        route<PLAIN>(w, (int32_t)next);
         next++;
         next_arr = next < w.n() ? P.arr[w.base() + next] : INF64;
       }
       // D. formations of idle instances, LPs before HPs
       for (int k = 0; k < n_lp; k++) {
         if (w.SI()[k].end == INF64) {
-          const int64_t r = P.mode == 0 ? form_lp(w, k, T) : P.mode == 1 ? form_hp(w, k, T)
-                                                                       : form_sar(w, k, T);
+          const int64_t r = (PLAIN || P.mode == 0) ? form_lp(w, k, T) : form_baseline(w, k, T);
           decisions += r & 1;
           evals += r >> 1;
         }
@@ -1359,7 +1368,7 @@ __global__ void __launch_bounds__(SW * 32, MINB) sim_kernel() {
         }
       }
       // E. tickets (G29)
-      if (w.tickets()) {
+      if (PLAIN ? (P.tickets && P.n_hp >= 1) : w.tickets()) {
         if (lane >= n_lp && lane < K) {
           SInst& I = w.SI()[lane];
           if (!I.ticket && I.wq_len == 0 && I.tk_live == 0) I.ticket = 1;
@@ -1539,8 +1548,11 @@ asc_status launch_simulate(asc_ctx* c, const asc_traces* tr, asc_outcomes* out, 
   for (int m = 4; m < minb; m++)
     if ((int64_t)T <= (int64_t)sms * m * SW) { minb = m; break; }
   if (minb < 4) minb = 4;  // (K so large that fewer than 4 CTAs fit: the launch itself reports it)
-  void (*kern)() = minb == 4 ? sim_kernel<4> : minb == 5 ? sim_kernel<5> : minb == 6 ? sim_kernel<6>
-                 : minb == 7 ? sim_kernel<7> : sim_kernel<8>;
+  const bool plain = P.mode == 0 && !tr->n_lp && !tr->n_hp;
+  void (*const tab[2][5])() = {
+      {sim_kernel<4, false>, sim_kernel<5, false>, sim_kernel<6, false>, sim_kernel<7, false>, sim_kernel<8, false>},
+      {sim_kernel<4, true>, sim_kernel<5, true>, sim_kernel<6, true>, sim_kernel<7, true>, sim_kernel<8, true>}};
+  void (*kern)() = tab[plain ? 1 : 0][minb - 4];
   int64_t blocks = ((int64_t)T + SW - 1) / SW;
   const int64_t cap = (int64_t)sms * minb;
   if (blocks > cap) blocks = cap;
