@@ -27,6 +27,7 @@ constexpr int CH = 16384;          // entries per warp task
 constexpr int GE = 128;            // entries per warp iteration (4 per lane)
 constexpr int NG = CH / GE + 1;    // groups per task (+1: the task base is rounded down to 4)
 constexpr int MW = 4 * NG;         // mask words per task per mask (word 4g+u, bit l <-> 4l+u)
+constexpr int SMALL = 32;  // segments of <= SMALL entries: one warp, one entry per lane (k_small)
 constexpr int WARPS = 8;   // k2/k3 CTA size
 constexpr int K1W = 4;     // k1 CTA size (warps); 4 CTAs/SM -> 16 warps, 128 registers
 constexpr int SCAN_ITEMS = 4;
@@ -82,7 +83,7 @@ __global__ void plan_counts(StepP P) {
   }
   const int64_t len = P.seg_off[s + 1] - P.seg_off[s];
   if (len < 0) atomicOr(P.err, ERR_INVAL);
-  const int64_t nt = len <= CH ? 1 : (len + CH - 1) / CH;
+  const int64_t nt = len <= SMALL ? 0 : len <= CH ? 1 : (len + CH - 1) / CH;  // small: k_small
   P.task_off[s] = nt;
   P.mtask_off[s] = nt > 1 ? nt : 0;
 }
@@ -160,7 +161,7 @@ __global__ void __launch_bounds__(SCAN_THREADS) plan_small(StepP P) {
     if (s < P.S) {
       const int64_t len = P.seg_off[s + 1] - P.seg_off[s];
       if (len < 0) atomicOr(P.err, ERR_INVAL);
-      nt = len <= CH ? 1 : (len + CH - 1) / CH;
+      nt = len <= SMALL ? 0 : len <= CH ? 1 : (len + CH - 1) / CH;  // small: k_small
     } else if (s == P.S && P.seg_off[P.S] != P.Q) {
       atomicOr(P.err, ERR_INVAL);
     }
@@ -615,12 +616,115 @@ __global__ void __launch_bounds__(K1W * 32, ASC_K1_MINB) k1_tasks(const __grid_c
   }
 }
 
+// Segments of at most SMALL entries (short queues: the common case of a real LP instance): one
+// warp per segment, one entry per lane — a1 (table), a2 key, a3 as one 32-wide bitonic sort of
+// (key, position), a4 as a strict prefix-sum scan in sorted order, a5 ballots in position order,
+// a6 from the admitted moments.  Same outputs as k1 (SURVEY row S, 10^6 x 32).
+__global__ void __launch_bounds__(256, 6) k_small(const __grid_constant__ StepP P) {
+  const int lane = lane_id();
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t s = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; s < P.S; s += nw) {
+    const int64_t lo = P.seg_off[s], n = P.seg_off[s + 1] - lo;
+    if (n > SMALL || n < 0) continue;  // k1's, or invalid (the planner flags it)
+    const bool v = lane < n;
+    const int64_t e = lo + lane;
+    int64_t dl = 0;
+    int32_t p = 1;
+    uint32_t f = 0;
+    if (v) {
+      dl = __ldcs(P.dl + e);
+      p = __ldcs(P.eff + e);
+      f = __ldcs(P.fl + e);
+    }
+    bool bad = v && p < 1;
+    const int64_t pf = v ? pf_of(P, p < 1 ? 1 : p) : 0;
+    if (P.pfout && v) {
+      bad |= pf > INT32_MAX;
+      __stcs(P.pfout + e, (int32_t)pf);
+    }
+    if (__any_sync(FULL, bad) && lane == 0) atomicOr(P.err, ERR_INVAL);
+    const int64_t now = P.now[s];
+    const bool dropped = P.drop && v && !(f & 1u) && now > dl;
+    // value function (FCFS: 0, ties by position); dropped and empty lanes sort last
+    const int64_t key = (P.kdl ? dl : 0) + (P.kpf > 0 ? pf : (P.kpf < 0 ? -pf : 0));
+    const KI x = sort32(v && !dropped ? KI{key, lane} : ki_inf());
+    const bool live = x.i != INF32;
+    const int src = live ? x.i : 0;
+    const int32_t ps = __shfl_sync(FULL, p, src);
+    const int64_t pfs = __shfl_sync(FULL, pf, src);
+    const int64_t bls = live ? (int64_t)((ps + P.bs) / P.bs) : 0;
+    // Algorithm 1 lines 5-13: strict budgets N (tokens), M (blocks), C (TBT residual), R (requests)
+    int64_t R = P.bR[s];
+    if (R > ASC_MAX_BATCH) { if (lane == 0) atomicOr(P.err, ERR_RANGE); R = ASC_MAX_BATCH; }
+    const int64_t Bd = P.dcnt[s], sl = P.dctx[s];
+    int64_t C = INF64;
+    if (Bd > 0) {
+      const int64_t d = lat_decode(P.md, (uint64_t)Bd, (uint64_t)sl);
+      if (d < 0 && lane == 0) atomicOr(P.err, ERR_RANGE);
+      C = P.tbt[s] - d;
+    }
+    const int64_t St = warp_incl_scan(live ? (int64_t)ps : (int64_t)0);
+    const int64_t Sb = warp_incl_scan(bls);
+    const int64_t Sc = warp_incl_scan(live ? pfs : (int64_t)0);
+    const bool ok = live && St < (int64_t)P.bN[s] && Sb < (int64_t)P.bM[s] && Sc < C && lane < R;
+    const uint32_t m = __ballot_sync(FULL, ok);
+    const int k = (m == FULL) ? 32 : (__ffs(~m) - 1);
+    const bool adm = lane < k;
+    if (adm) P.admit_idx[lo + lane] = (int32_t)(lo + x.i);
+    const uint32_t amask = __reduce_or_sync(FULL, adm ? (1u << x.i) : 0u);
+    uint64_t sp = 0, sp2 = 0, spc = 0;
+    if (adm) {
+      const uint64_t q = (uint64_t)ps;
+      sp = q;
+      sp2 = q * q;
+      spc = q * ceil_div_u(q, P.md.b);
+    }
+    if (k > 0) {
+      sp = warp_sum(sp);
+      sp2 = warp_sum(sp2);
+      spc = warp_sum(spc);
+    }
+    // a5: offload (non-admitted, never prefilled, not on an HP) and drop lists in position order
+    const bool off = P.offl && v && !dropped && !((amask >> lane) & 1u) && !(f & 3u) &&
+                     dl - now <= pf + P.W + P.margin;
+    const uint32_t mo = __ballot_sync(FULL, off), md = __ballot_sync(FULL, dropped);
+    if (off) P.off_idx[lo + __popc(mo & lanemask_lt())] = (int32_t)e;
+    if (dropped) P.drop_idx[lo + __popc(md & lanemask_lt())] = (int32_t)e;
+    if (lane == 0) {
+      P.admit_cnt[s] = k;
+      P.off_cnt[s] = __popc(mo);
+      P.drop_cnt[s] = __popc(md);
+      int64_t l = 0;
+      if (k > 0 || Bd > 0) {
+        l = k ? lat_us(P.md, (uint64_t)k, sp, sp2, spc, (uint64_t)Bd, (uint64_t)sl)
+              : lat_decode(P.md, (uint64_t)Bd, (uint64_t)sl);
+        if (l < 0) atomicOr(P.err, ERR_RANGE);
+      }
+      P.blat[s] = l;
+    }
+  }
+}
+
 __global__ void __launch_bounds__(WARPS * 32) k2_segments(const __grid_constant__ StepP P) {
   __shared__ KI lists[WARPS][32 * KPL];
+  __shared__ int64_t segs[WARPS * 32];
+  __shared__ int nseg;
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int64_t s = blockIdx.x; s < P.S; s += gridDim.x) {
+  // find this CTA's multi-task segments up to 256 at a time (most segments have one task or
+  // none); chunks shrink with S so that few large segments still spread over the CTAs
+  int64_t chunk = P.S / gridDim.x;
+  chunk = chunk < 1 ? 1 : (chunk > WARPS * 32 ? WARPS * 32 : chunk);
+  for (int64_t base = (int64_t)blockIdx.x * chunk; base < P.S; base += (int64_t)gridDim.x * chunk) {
+    if (threadIdx.x == 0) nseg = 0;
+    __syncthreads();
+    const int64_t s0 = base + threadIdx.x;
+    if (threadIdx.x < chunk && s0 < P.S && P.task_off[s0 + 1] - P.task_off[s0] > 1)
+      segs[atomicAdd(&nseg, 1)] = s0;
+    __syncthreads();
+    const int cnt = nseg;
+  for (int q = 0; q < cnt; q++) {
+    const int64_t s = segs[q];
     const int64_t nt = P.task_off[s + 1] - P.task_off[s];
-    if (nt <= 1) continue;
     const int64_t m0 = P.mtask_off[s];
     if (m0 + nt > P.max_mt) continue;
     const int64_t lo = P.seg_off[s];
@@ -677,6 +781,8 @@ __global__ void __launch_bounds__(WARPS * 32) k2_segments(const __grid_constant_
       if (lane == 0) { P.off_cnt[s] = (int32_t)ca; P.drop_cnt[s] = (int32_t)cb; }
     }
     __syncthreads();
+  }
+    __syncthreads();  // segs is rewritten by the next round
   }
 }
 
@@ -812,6 +918,12 @@ asc_status launch_schedule_step(asc_ctx* c, const asc_step_in* in, asc_step_out*
   cudaEventRecord(c->ev1, sm);
   c->timed = true;
   launches += 1;
+  {  // short segments (after k1's timed bracket: k1 is the roofline kernel of row S's big shape)
+    int64_t gs = ((int64_t)S * 32 + 255) / 256;
+    gs = gs < (int64_t)dev_sms * 8 ? gs : (int64_t)dev_sms * 8;
+    k_small<<<(unsigned)(gs > 0 ? gs : 1), 256, 0, sm>>>(P);
+    launches += 1;
+  }
   if (Q > CH) {
     int64_t g2 = S < (int64_t)dev_sms * 4 ? S : (int64_t)dev_sms * 4;
     k2_segments<<<(unsigned)(g2 > 0 ? g2 : 1), WARPS * 32, 0, sm>>>(P);
