@@ -16,6 +16,8 @@
 //   k3     : one warp per multi-task task expands its masks into id-ascending output indices.
 // HBM traffic per entry: 13 B read (+4 B prefill_us if requested) + 4 B per output index;
 // multi-task segments add 0.25 B/entry of mask traffic and 1.5 KB per task of candidates.
+#include <type_traits>
+
 #include "asc_internal.h"
 
 using namespace asc;
@@ -504,7 +506,8 @@ __global__ void __launch_bounds__(K1W * 32, ASC_K1_MINB) k1_tasks(const __grid_c
       const uint32_t tab_hi = (uint32_t)(P.pt - 1);
       const int32_t* __restrict__ tab32 = P.pf_tab32;
       const bool has_pfout = P.pfout != nullptr;
-      const int kdl = P.kdl, kpf = P.kpf;
+      const int kpf = P.kpf;
+      const int32_t dmask = P.kdl ? -1 : 0;
 #pragma unroll
       for (int q = 0; q < NST - 1; q++) {
         if (VEC && q < ng) stage_issue(P, s_stage[w][q], b4 + (int64_t)q * GE + 4 * lane);
@@ -526,31 +529,37 @@ __global__ void __launch_bounds__(K1W * 32, ASC_K1_MINB) k1_tasks(const __grid_c
         uint64_t x[4];
         bool cnd[4];
         uint32_t mo_w = 0, md_w = 0;
+        // interior groups (every entry inside the task) skip the per-entry bounds test
+        auto body = [&](auto interior) {
+          constexpr bool IN = decltype(interior)::value;
 #pragma unroll
-        for (int u = 0; u < 4; u++) {  // branch-free: every lane runs the same instructions
-          const bool v = (uint32_t)(r0 + u - t.vlo) < vspan;
-          const uint32_t f = (cur.f4 >> (8 * u)) & 0xffu;
-          const int32_t pu = cur.p[u];
-          const bool inrange = (uint32_t)(pu - 1) < tab_hi;  // 1 <= pu < pt
-          const int32_t pf = __ldg(tab32 + (inrange ? pu : 1));
-          const int64_t d = cur.dl[u] - t.now;
-          inwin &= !v || (inrange && (uint64_t)(d + WIN) < (uint64_t)(2 * WIN) && pf < (int32_t)WIN);
-          if (has_pfout && v) __stcs(P.pfout + e0 + u, pf);
-          const int32_t d32 = (int32_t)d;
-          const bool dropped = DROP && v && !(f & 1u) && d32 < 0;
-          const bool off = OFFL && v && !dropped && !(f & 3u) && d32 - pf <= othr32;
-          if (DROP) {
-            const uint32_t md = __ballot_sync(FULL, dropped);
-            md_w = lane == u ? md : md_w;
+          for (int u = 0; u < 4; u++) {  // branch-free: every lane runs the same instructions
+            const bool v = IN || (uint32_t)(r0 + u - t.vlo) < vspan;
+            const uint32_t f = (cur.f4 >> (8 * u)) & 0xffu;
+            const int32_t pu = cur.p[u];
+            const bool inrange = (uint32_t)(pu - 1) < tab_hi;  // 1 <= pu < pt
+            const int32_t pf = __ldg(tab32 + (inrange ? pu : 1));
+            const int64_t d = cur.dl[u] - t.now;
+            inwin &= !v || (inrange && (uint64_t)(d + WIN) < (uint64_t)(2 * WIN) && pf < (int32_t)WIN);
+            if (has_pfout && v) __stcs(P.pfout + e0 + u, pf);
+            const int32_t d32 = (int32_t)d;
+            const bool dropped = DROP && v && !(f & 1u) && d32 < 0;
+            const bool off = OFFL && v && !dropped && !(f & 3u) && d32 - pf <= othr32;
+            if (DROP) {
+              const uint32_t md = __ballot_sync(FULL, dropped);
+              md_w = lane == u ? md : md_w;
+            }
+            if (OFFL) {
+              const uint32_t mo = __ballot_sync(FULL, off);
+              mo_w = lane == u ? mo : mo_w;
+            }
+            const int32_t key32 = (d32 & dmask) + kpf * pf;  // kdl * d32 + kpf * pf, branch-free
+            x[u] = ((uint64_t)((uint32_t)key32 ^ 0x80000000u) << 32) | (uint64_t)(l0 + u);
+            cnd[u] = select && v && !dropped && x[u] < st.thr;
           }
-          if (OFFL) {
-            const uint32_t mo = __ballot_sync(FULL, off);
-            mo_w = lane == u ? mo : mo_w;
-          }
-          const int32_t key32 = (kdl ? d32 : 0) + (kpf > 0 ? pf : (kpf < 0 ? -pf : 0));
-          x[u] = ((uint64_t)((uint32_t)key32 ^ 0x80000000u) << 32) | (uint64_t)(l0 + u);
-          cnd[u] = select && v && !dropped && x[u] < st.thr;
-        }
+        };
+        if (r0 - 4 * lane >= t.vlo && r0 - 4 * lane + GE <= t.vhi) body(std::true_type{});
+        else body(std::false_type{});
         if (lane < 4) {  // lanes 0-3 hold the 4 ballot words of this group
           if (DROP) s_drop[w][4 * g + lane] = md_w;
           if (OFFL) s_off[w][4 * g + lane] = mo_w;
