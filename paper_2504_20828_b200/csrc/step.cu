@@ -278,19 +278,23 @@ __device__ __forceinline__ int finalize_segment(const StepP& P, int64_t s, const
 __device__ __forceinline__ int64_t expand_groups(const uint32_t* words, int ng, int64_t b4,
                                                  int32_t* out, int64_t base) {
   const int lane = lane_id();
+  const uint32_t lt = lanemask_lt();
   for (int g = 0; g < ng; g++) {
-    const uint32_t w0 = words[4 * g], w1 = words[4 * g + 1], w2 = words[4 * g + 2], w3 = words[4 * g + 3];
-    if ((w0 | w1 | w2 | w3) == 0) continue;
-    const uint32_t nib = ((w0 >> lane) & 1u) | (((w1 >> lane) & 1u) << 1) |
-                         (((w2 >> lane) & 1u) << 2) | (((w3 >> lane) & 1u) << 3);
-    const int c = __popc(nib);
-    const int incl = warp_incl_scan(c);
-    int64_t pos = base + incl - c;
+    const uint4 wv = *reinterpret_cast<const uint4*>(words + 4 * g);  // words 4g..4g+3
+    if ((wv.x | wv.y | wv.z | wv.w) == 0) continue;
+    // set entries before this lane's first: entry 4l'+u for l' < l, any u (no shuffles)
+    int64_t pos = base + __popc(wv.x & lt) + __popc(wv.y & lt) + __popc(wv.z & lt) + __popc(wv.w & lt);
     const int32_t e0 = (int32_t)(b4 + g * GE + 4 * lane);
-#pragma unroll
-    for (int u = 0; u < 4; u++)
-      if ((nib >> u) & 1u) out[pos++] = e0 + u;
-    base += __shfl_sync(FULL, incl, 31);
+    const uint32_t b0 = (wv.x >> lane) & 1u, b1 = (wv.y >> lane) & 1u, b2 = (wv.z >> lane) & 1u,
+                   b3 = (wv.w >> lane) & 1u;
+    if (b0) out[pos] = e0;
+    pos += b0;
+    if (b1) out[pos] = e0 + 1;
+    pos += b1;
+    if (b2) out[pos] = e0 + 2;
+    pos += b2;
+    if (b3) out[pos] = e0 + 3;
+    base += __popc(wv.x) + __popc(wv.y) + __popc(wv.z) + __popc(wv.w);
   }
   return base;
 }
