@@ -176,13 +176,18 @@ __device__ __noinline__ void digest_log(Wp w, int k, int64_t T, int32_t nadm,
     }
     acc = mix64(v + (pos + 1) * GOLD);
   }
+  #pragma unroll 1
   for (int32_t j = lane; j < nadm; j += 32) acc += mix64((uint64_t)P.bp_id[o + j] + (uint64_t)(3 + j + 1) * GOLD);
+  #pragma unroll 1
   for (int32_t j = lane; j < noff; j += 32)
     acc += mix64((uint64_t)P.scr_off[w.base() + j] + (uint64_t)(5 + nadm + j + 1) * GOLD);
+  #pragma unroll 1
   for (int32_t j = lane; j < ndrop; j += 32)
     acc += mix64((uint64_t)P.scr_drop[w.base() + j] + (uint64_t)(6 + nadm + noff + j + 1) * GOLD);
+  #pragma unroll 1
   for (int32_t j = lane; j < npre; j += 32)
     acc += mix64((uint64_t)P.scr_pre[w.base() + j] + (uint64_t)(7 + nadm + noff + ndrop + j + 1) * GOLD);
+  #pragma unroll 1
   for (int32_t j = lane; j < nch; j += 32)  // Sarathi-like chunk sizes (staged in scr_off)
     acc += mix64((uint64_t)P.scr_off[w.base() + j] + (uint64_t)(8 + nadm + noff + ndrop + npre + j + 1) * GOLD);
   acc = warp_sum(acc);
@@ -224,6 +229,7 @@ __device__ __noinline__ void wq_compact(Wp w, int k) {
   const int lane = lane_id();
   const int64_t o = ioff(k, w);
   const int32_t h = I.wq_head, len = I.wq_len;
+  #pragma unroll 1
   for (int32_t c = 0; c < len; c += 32) {
     const int32_t j = c + lane;
     int32_t xi = 0;
@@ -248,6 +254,7 @@ __device__ __noinline__ void wq_insert(Wp w, int k, int32_t id) {
   const int64_t key = key_of(w.base() + id, P.rq_eff[w.base() + id]);
   const bool by_id = I.hp;
   int32_t pos = len;  // number of entries ordered before the new one
+  #pragma unroll 1
   for (int32_t c = len - 1; c >= 0; c -= 32) {
     const int32_t j = c - lane;
     bool after = false;  // entry j sorts after the new entry
@@ -260,6 +267,7 @@ __device__ __noinline__ void wq_insert(Wp w, int k, int32_t id) {
     pos -= __popc(m);
     if (m != FULL) break;  // entries are sorted: everything before this chunk sorts before
   }
+  #pragma unroll 1
   for (int32_t c = len - 1; c >= pos; c -= 32) {  // shift [pos, len) up by one
     const int32_t j = c - lane;
     int32_t xi = 0;
@@ -317,13 +325,16 @@ __device__ __noinline__ void sort_ids(Wp w, int32_t* a, int32_t n) {
     return;
   }
   int32_t* tmp = P.scr_tmp + w.base();
+  #pragma unroll 1
   for (int32_t i = lane; i < n; i += 32) {
     const int32_t x = a[i];
     int32_t r = 0;
+    #pragma unroll 1
     for (int32_t j = 0; j < n; j++) r += a[j] < x;
     tmp[r] = x;
   }
   __syncwarp();
+  #pragma unroll 1
   for (int32_t i = lane; i < n; i += 32) a[i] = tmp[i];
   __syncwarp();
 }
@@ -336,6 +347,7 @@ __device__ __noinline__ int32_t drop_step(Wp w, int k, int64_t T) {
   const int64_t q = qoff(I, k, w);
   const int32_t len = I.wq_len;
   int32_t out = 0, nd = 0, tkd = 0;
+  #pragma unroll 1
   for (int32_t c = 0; c < len; c += 32) {
     const int32_t j = c + lane;
     const bool v = j < len;
@@ -381,6 +393,7 @@ __device__ __noinline__ int32_t evict(Wp w, int k) {
   while (I.need_sum > I.kv_free) {
     const int32_t len = I.ds_len;
     int32_t best = -1, bslot = -1;
+    #pragma unroll 1
     for (int32_t c = 0; c < len; c += 32) {
       const int32_t j = c + lane;
       if (j < len) {
@@ -518,6 +531,7 @@ __device__ __noinline__ int lp_admit(Wp w, int k, int64_t T, int32_t ndrop,
       // ever-prefilled requests) are packed in order at the end of the range
       const int64_t othr = T + P.W + P.margin;
       int32_t m = 0;
+      #pragma unroll 1
       for (int32_t c = 0; c < rem; c += 32) {
         const int32_t j = c + lane;
         const uint32_t in = __ballot_sync(FULL, j < rem && P.wq_key[q2 + j] <= othr);
@@ -525,6 +539,7 @@ __device__ __noinline__ int lp_admit(Wp w, int k, int64_t T, int32_t ndrop,
         if (in != FULL) break;
       }
       int32_t wpos = m;  // backward stable compaction of the kept entries inside [0, m)
+      #pragma unroll 1
       for (int32_t c = m - 1; c >= 0; c -= 32) {
         const int32_t j = c - lane;
         const bool v = j >= 0;
@@ -554,6 +569,7 @@ __device__ __noinline__ int lp_admit(Wp w, int k, int64_t T, int32_t ndrop,
       // every remaining request ahead of this one
       int32_t out = 0;
       int64_t ahead = 0;
+      #pragma unroll 1
       for (int32_t c = 0; c < rem; c += 32) {
         const int32_t j = c + lane;
         const bool v = j < rem;
@@ -598,6 +614,7 @@ __device__ __noinline__ int lp_admit(Wp w, int k, int64_t T, int32_t ndrop,
   I.kv_free = kvf;
   __syncwarp();
   // dispatch offloads round-robin over the HPs, ascending id
+  #pragma unroll 1
   for (int32_t j = 0; j < noff; j++) {
     const int32_t id = P.scr_off[w.base() + j];
     const int64_t g = w.base() + id;
@@ -699,6 +716,7 @@ __device__ __noinline__ int32_t hp_prefill(Wp w, int k, int64_t T, uint64_t* mom
   int64_t ct = 0, cb = 0, used = 0;
   int32_t nadm = 0;
   uint64_t sp = 0, sp2 = 0, spc = 0;
+  #pragma unroll 1
   for (int32_t c = 0; c < len; c += 32) {
     const int32_t j = c + lane;
     const bool v = j < len;
@@ -802,6 +820,7 @@ __device__ __noinline__ int64_t form_sarathi(Wp w, int k, int64_t T) {
   int32_t nfull = 0, part = 0;
   uint64_t sc = 0, aF = 0, aM = 0;
   int64_t used = 0;
+  #pragma unroll 1
   for (int32_t c0 = 0; c0 < len; c0 += 32) {
     const int32_t j = c0 + lane;
     const bool v = j < len;
@@ -925,6 +944,7 @@ __device__ __noinline__ void complete_prefills(Wp w, int k, int64_t T) {
   int32_t dlen = I.ds_len;
   int64_t freed = 0, hsum = 0, cadd = 0;
   int32_t hcnt = 0, tkd = 0;
+  #pragma unroll 1
   for (int32_t c = 0; c < blen; c += 32) {
     const int32_t j = c + lane;
     const bool v = j < blen;
@@ -983,6 +1003,7 @@ __device__ __forceinline__ void complete(Wp w, int k, int64_t T) {
     bool anyfin = false;
     int64_t freed = 0, hsum = 0, cfin = 0;
     int32_t hcnt = 0, tkd = 0;
+    #pragma unroll 1
     for (int32_t c = 0; c < dlen; c += 32) {
       const int32_t j = c + lane;
       const bool v = j < dlen;
@@ -1036,6 +1057,7 @@ template <bool PLAIN>
 __device__ __forceinline__ void route(Wp w, int32_t id) {
   const int n_lp = PLAIN ? P.n_lp : w.nlp(), K = PLAIN ? P.K : w.K();
   if (PLAIN ? (P.tickets && P.n_hp >= 1) : w.tickets()) {
+    #pragma unroll 1
     for (int h = n_lp; h < K; h++) {
       if (w.SI()[h].ticket) {
         const int32_t tk = w.SI()[h].tk_live + 1;
@@ -1093,9 +1115,11 @@ __device__ __noinline__ int64_t run_decode(Wp w, int k, int64_t T_limit) {
   int64_t hsum_all = 0;
   int32_t hcnt_all = 0, tkd_all = 0;
   // pass A: histogram + minimum remaining tokens of the current slots
+  #pragma unroll 1
   for (int i = lane; i < 128; i += 32) hA[i] = 0;
   __syncwarp();
   int32_t mrem = INT32_MAX;
+  #pragma unroll 1
   for (int32_t c = 0; c < Bd; c += 32) {
     const int32_t j = c + lane;
     if (j < Bd) {
@@ -1142,11 +1166,13 @@ __device__ __noinline__ int64_t run_decode(Wp w, int k, int64_t T_limit) {
     const int32_t nstep = J + (doC ? 1 : 0);
     if (nstep == 0) break;
     // ---- pass B: apply the J decode steps (and the completion event J when doC)
+    #pragma unroll 1
     for (int i = lane; i < 128; i += 32) hB[i] = 0;
     __syncwarp();
     int32_t out = 0, mrem2 = INT32_MAX, need2 = 0;
     int64_t freed = 0, hsum = 0, csum = 0;
     int32_t hcnt = 0, tkd = 0;
+    #pragma unroll 1
     for (int32_t c0 = 0; c0 < Bd; c0 += 32) {
       const int32_t j = c0 + lane;
       const bool v = j < Bd;
@@ -1249,6 +1275,7 @@ __device__ __noinline__ void init_trace(Wp w, int trace) {
   const int lane = lane_id();
   if (lane == 0) { w.ts()->rr_lp = w.ts()->rr_hp = w.ts()->fl_head = w.ts()->fl_tail = 0; }
   const int64_t ttft = P.ttft[trace];
+  #pragma unroll 1
   for (int64_t i = lane; i < w.n(); i += 32) {
     const int64_t g = w.base() + i;
     P.rq_dl[g] = P.arr[g] + (P.rttft ? P.rttft[g] : ttft);
@@ -1278,6 +1305,7 @@ __device__ __noinline__ void finish_trace(Wp w, int trace, int64_t decisions,
   bool stuck = false;
   if (lane < w.K()) stuck = w.SI()[lane].wq_len > 0 || w.SI()[lane].ds_len > 0;
   if (__any_sync(FULL, stuck) && lane == 0) atomicOr(P.err, ERR_INVARIANT);
+  #pragma unroll 1
   for (int64_t i = lane; i < w.n(); i += 32) {
     const int64_t g = w.base() + i;
     const uint32_t f = P.rq_fl[g];
@@ -1290,6 +1318,7 @@ __device__ __noinline__ void finish_trace(Wp w, int trace, int64_t decisions,
   }
   if (lane == 0) {
     uint64_t d = 0;
+    #pragma unroll 1
     for (int k = 0; k < w.K(); k++) d = mix64(d ^ w.SI()[k].hash);
     P.digest[trace] = d;
     if (P.decisions) P.decisions[trace] = decisions;
@@ -1331,6 +1360,7 @@ __global__ void __launch_bounds__(SW * 32, MINB) sim_kernel() {
     int64_t next = 0, next_arr = w.n() > 0 ? P.arr[w.base()] : INF64, decisions = 0, evals = 0;
     while (true) {
       int64_t T = next_arr;
+      #pragma unroll 1
       for (int k = 0; k < K; k++) {
         const int64_t e = w.SI()[k].end;
         T = e < T ? e : T;
@@ -1342,6 +1372,7 @@ __global__ void __launch_bounds__(SW * 32, MINB) sim_kernel() {
       }
       if (T == INF64) break;
       // A. completions in instance order
+      #pragma unroll 1
       for (int k = 0; k < K; k++)
         if (w.SI()[k].end == T) complete(w, k, T);
       // B. offload deliveries (FIFO = time order)
@@ -1353,6 +1384,7 @@ __global__ void __launch_bounds__(SW * 32, MINB) sim_kernel() {
         next_arr = next < w.n() ? P.arr[w.base() + next] : INF64;
       }
       // D. formations of idle instances, LPs before HPs
+      #pragma unroll 1
       for (int k = 0; k < n_lp; k++) {
         if (w.SI()[k].end == INF64) {
           const int64_t r = (PLAIN || P.mode == 0) ? form_lp(w, k, T) : form_baseline(w, k, T);
@@ -1360,6 +1392,7 @@ __global__ void __launch_bounds__(SW * 32, MINB) sim_kernel() {
           evals += r >> 1;
         }
       }
+      #pragma unroll 1
       for (int k = n_lp; k < K; k++) {
         if (w.SI()[k].end == INF64) {
           const int64_t r = form_hp(w, k, T);
@@ -1381,8 +1414,10 @@ __global__ void __launch_bounds__(SW * 32, MINB) sim_kernel() {
         const int64_t tf = P.fl_t[w.base() + w.ts()->fl_head];
         tl_hp = tf < tl_hp ? tf : tl_hp;
       }
+      #pragma unroll 1
       for (int k = 0; k < n_lp; k++)
         if (w.SI()[k].wq_len > 0 && w.SI()[k].end < tl_hp) tl_hp = w.SI()[k].end;  // may offload
+      #pragma unroll 1
       for (int k = 0; k < K; k++) {
         const SInst& I = w.SI()[k];
         const int64_t lim = k < n_lp ? next_arr : tl_hp;
@@ -1405,10 +1440,12 @@ size_t sim_smem_per_warp(int K, int32_t* o_sd = nullptr, int32_t* o_si = nullptr
 // liveness / layout validation (ASC_E_CONFIG / ASC_E_INVAL before simulating)
 __global__ void validate_traces(int64_t R) {
   if (blockIdx.x == 0 && threadIdx.x == 0 && P.off[P.T] != R) atomicOr(P.err, ERR_INVAL);
+  #pragma unroll 1
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < P.T; t += (int64_t)gridDim.x * blockDim.x) {
     const int32_t nl = P.tr_nlp ? P.tr_nlp[t] : P.n_lp, nh = P.tr_nhp ? P.tr_nhp[t] : P.n_hp;
     if (nl < 1 || nh < 0 || nl + nh > P.K || (P.mode != 0 && nh != 0)) atomicOr(P.err, 8);
   }
+  #pragma unroll 1
   for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < R;
        g += (int64_t)gridDim.x * blockDim.x) {
     const int32_t p = P.pl[g], o = P.ol[g];
@@ -1432,10 +1469,12 @@ __global__ void goodput_kernel(int32_t T, const int64_t* off, const int64_t* arr
                                uint64_t* good, uint64_t* total, int* err) {
   const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   const int nw = (gridDim.x * blockDim.x) >> 5;
+  #pragma unroll 1
   for (int t = w; t < T; t += nw) {
     const int64_t lo = off[t], hi = off[t + 1];
     const int64_t tt = ttft[t], tb = tbt[t];
     uint64_t g = 0;
+    #pragma unroll 1
     for (int64_t i = lo + lane; i < hi; i += 32) {
       if ((__ldcs(status + i) & 3u) != 1u) continue;
       const int64_t f = __ldcs(first + i);
