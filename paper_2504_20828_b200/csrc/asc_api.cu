@@ -85,6 +85,15 @@ __global__ void build_tables(Model md, int64_t* tab, int32_t* tab32, int32_t n, 
   }
 }
 
+// k1's fast-path table: prefill_us(q + 1) for q in [0, n), values >= 2^30 stored as 2^30 (the fast
+// path tests bit 30 and hands such tasks to the exact 64-bit path)
+__global__ void build_fast_table(Model md, int32_t* tab, int32_t n) {
+  for (int32_t q = blockIdx.x * blockDim.x + threadIdx.x; q < n; q += gridDim.x * blockDim.x) {
+    const int64_t v = prefill_lat(md, (uint64_t)q + 1);
+    tab[q] = (int32_t)(v < 0 || v >= (int64_t(1) << 30) ? (int64_t(1) << 30) : v);
+  }
+}
+
 extern "C" {
 
 int32_t asc_abi_version(void) { return ASC_ABI_VERSION; }
@@ -172,6 +181,7 @@ asc_status asc_create(const asc_config* cfg, int device, void* cuda_stream, asc_
       cudaMallocHost(&c->h_err, sizeof(int)) != cudaSuccess ||
       cudaMalloc(&c->d_pf_tab, sizeof(int64_t) * c->pt_size) != cudaSuccess ||
       cudaMalloc(&c->d_pf_tab32_mem, sizeof(int32_t) * c->pt_size) != cudaSuccess ||
+      cudaMalloc(&c->d_pf_fast, sizeof(int32_t) * ASC_PF_FAST_N) != cudaSuccess ||
       cudaMalloc(&d_w, 2 * sizeof(int64_t)) != cudaSuccess) {
     cudaGetLastError();
     asc_destroy(c);
@@ -184,6 +194,7 @@ asc_status asc_create(const asc_config* cfg, int device, void* cuda_stream, asc_
   cudaMemsetAsync(d_w, 0, 2 * sizeof(int64_t), c->stream);
   build_tables<<<(c->pt_size + 255) / 256, 256, 0, c->stream>>>(
       c->md, c->d_pf_tab, c->d_pf_tab32_mem, c->pt_size, t.hp_token_budget, d_w, c->d_err);
+  build_fast_table<<<ASC_PF_FAST_N / 256, 256, 0, c->stream>>>(c->md, c->d_pf_fast, ASC_PF_FAST_N);
   int64_t hw[2] = {0, 0};
   e = cudaMemcpyAsync(hw, d_w, 2 * sizeof(int64_t), cudaMemcpyDeviceToHost, c->stream);
   asc_status st = e != cudaSuccess ? cuda_check(c, e, "asc_create") : collect_errors(c, "asc_create tables");
@@ -205,6 +216,7 @@ void asc_destroy(asc_ctx* ctx) {
   if (ctx->h_err) cudaFreeHost(ctx->h_err);
   if (ctx->d_pf_tab) cudaFree(ctx->d_pf_tab);
   if (ctx->d_pf_tab32_mem) cudaFree(ctx->d_pf_tab32_mem);
+  if (ctx->d_pf_fast) cudaFree(ctx->d_pf_fast);
   if (ctx->ws) cudaFree(ctx->ws);
   if (ctx->stage) cudaFree(ctx->stage);
   if (ctx->ev0) cudaEventDestroy(ctx->ev0);

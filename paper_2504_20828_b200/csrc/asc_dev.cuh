@@ -358,94 +358,4 @@ __device__ __forceinline__ uint64_t sort32_pk(uint64_t v) {
   return v;
 }
 
-template <int KPL>
-struct TopKPk {
-  uint64_t a[KPL];
-  uint64_t thr;
-  int cnt, kpos;
-  bool any;
-  uint64_t* buf;  // 160 slots in shared memory (per warp)
-
-  __device__ __forceinline__ void init(uint64_t* sbuf, int kpos_) {
-#pragma unroll
-    for (int r = 0; r < KPL; r++) a[r] = PK_INF;
-    thr = PK_INF;
-    cnt = 0;
-    kpos = kpos_;
-    any = false;
-    buf = sbuf;
-  }
-  __device__ __forceinline__ void bitonic_merge() {
-    const int l = lane_id();
-#pragma unroll
-    for (int j = KPL / 2; j > 0; j >>= 1) {
-#pragma unroll
-      for (int r = 0; r < KPL; r++) {
-        if ((r & j) == 0) {
-          const uint64_t x = a[r], y = a[r | j];
-          a[r] = x < y ? x : y;
-          a[r | j] = x < y ? y : x;
-        }
-      }
-    }
-#pragma unroll
-    for (int j = 16; j > 0; j >>= 1) {
-      const bool lower = (l & j) == 0;
-#pragma unroll
-      for (int r = 0; r < KPL; r++) a[r] = pk_keep(a[r], __shfl_xor_sync(FULL, a[r], j), lower);
-    }
-  }
-  __device__ __forceinline__ uint64_t at(int pos) const {
-    const int r = pos >> 5;
-    uint64_t x = a[0];
-#pragma unroll
-    for (int q = 1; q < KPL; q++) if (q == r) x = a[q];
-    return __shfl_sync(FULL, x, pos & 31);
-  }
-  __device__ __forceinline__ void merge_sorted32(uint64_t y) {
-    if (any) {
-      const uint64_t br = __shfl_sync(FULL, y, 31 - lane_id());
-      a[KPL - 1] = a[KPL - 1] < br ? a[KPL - 1] : br;
-      bitonic_merge();
-    } else {
-      a[0] = y;
-      any = true;
-    }
-    thr = at(kpos);
-  }
-  __device__ __forceinline__ void flush32() {
-    __syncwarp();
-    uint64_t y = buf[lane_id()];
-    __syncwarp();
-    for (int c0 = 32; c0 < cnt; c0 += 32) {
-      const int j = c0 + lane_id();
-      const uint64_t rest = j < cnt ? buf[j] : PK_INF;
-      __syncwarp();
-      if (j < cnt) buf[j - 32] = rest;
-      __syncwarp();
-    }
-    cnt -= 32;
-    merge_sorted32(sort32_pk(y));
-    __syncwarp();
-  }
-  __device__ __forceinline__ void append(uint64_t x, bool c) {
-    const uint32_t m = __ballot_sync(FULL, c);
-    if (c) buf[cnt + __popc(m & lanemask_lt())] = x;
-    cnt += __popc(m);
-  }
-  __device__ __forceinline__ void drain() {
-    while (cnt >= 32) flush32();
-  }
-  __device__ __forceinline__ void finish() {
-    drain();
-    if (cnt > 0) {
-      __syncwarp();
-      uint64_t y = lane_id() < cnt ? buf[lane_id()] : PK_INF;
-      __syncwarp();
-      cnt = 0;
-      merge_sorted32(sort32_pk(y));
-    }
-  }
-};
-
 }  // namespace asc

@@ -7,6 +7,8 @@
 #include "../../include/asc.h"
 #include "asc_dev.cuh"
 
+constexpr int32_t ASC_PF_FAST_N = 1 << 17;  // entries of asc_ctx::d_pf_fast
+
 struct asc_ctx {
   asc_config cfg;          // as given (tp not yet applied)
   int device = 0;
@@ -16,6 +18,7 @@ struct asc_ctx {
   int64_t* d_pf_tab = nullptr;  // prefill_us by eff_prompt (a1, cached per ctx)
   int32_t* d_pf_tab32 = nullptr;  // int32 copy for lookups (nullptr if some entry > INT32_MAX)
   int32_t* d_pf_tab32_mem = nullptr;
+  int32_t* d_pf_fast = nullptr;  // [2^17]: prefill_us(q + 1), clipped to 2^30 (k1's fast path)
   int64_t w_hp = 0;        // worst-case HP batch latency (G24)
   int* d_err = nullptr;    // device error bits (asc::ERR_*)
   int* h_err = nullptr;    // pinned host copy of the error bits (one sync per call)

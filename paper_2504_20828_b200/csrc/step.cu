@@ -27,7 +27,8 @@ namespace {
 constexpr int KPL = 4;             // K = 128 = ASC_MAX_BATCH
 constexpr int CH = 16384;          // entries per warp task
 constexpr int GE = 128;            // entries per warp iteration (4 per lane)
-constexpr int NG = CH / GE + 1;    // groups per task (+1: the task base is rounded down to 4)
+constexpr int ALN = 16;            // task bases are rounded down to 16 entries (16-byte flag copies)
+constexpr int NG = CH / GE + 1;    // groups per task (+1: the task base is rounded down)
 constexpr int MW = 4 * NG;         // mask words per task per mask (word 4g+u, bit l <-> 4l+u)
 constexpr int SMALL = 32;  // segments of <= SMALL entries: one warp, one entry per lane (k_small)
 constexpr int WARPS = 8;   // k2/k3 CTA size
@@ -41,6 +42,7 @@ struct StepP {
   int64_t ntask_max, max_mt;  // workspace capacities (guards against an inconsistent Q)
   const int64_t* pf_tab;
   const int32_t* pf_tab32;  // int32 copy when every entry fits (else nullptr)
+  const int32_t* pf_fast;   // [PFT_N]: prefill_us(q + 1) for q < 2^17, values >= 2^30 stored as 2^30
   int32_t pt, bs, drop, offl, kdl, kpf;
   int64_t W, margin, Q;
   int32_t S;
@@ -200,6 +202,15 @@ __global__ void __launch_bounds__(SCAN_THREADS) plan_small(StepP P) {
 // ----------------------------------------------------------- Algorithm 1 over a sorted list --
 // a[] holds the smallest live entries in (key, pos) order.  Writes admitted positions and the
 // batch latency, returns k; `adm[r]` tells each lane which of its elements were admitted.
+// TBT residual C of segment s (G22): tbt_slo - decode-only latency, or +inf without decodes
+__device__ __forceinline__ int64_t seg_tbt_budget(const StepP& P, int64_t s) {
+  const int64_t Bd = P.dcnt[s];
+  if (Bd <= 0) return INF64;
+  const int64_t d = lat_decode(P.md, (uint64_t)Bd, (uint64_t)P.dctx[s]);
+  if (d < 0) { atomicOr(P.err, ERR_RANGE); return INF64; }
+  return P.tbt[s] - d;
+}
+
 __device__ __forceinline__ int finalize_segment(const StepP& P, int64_t s, const KI (&a)[KPL],
                                                  bool (&adm)[KPL]) {
   const int lane = lane_id();
@@ -208,12 +219,7 @@ __device__ __forceinline__ int finalize_segment(const StepP& P, int64_t s, const
   int64_t R = P.bR[s];
   if (R > ASC_MAX_BATCH) { atomicOr(P.err, ERR_RANGE); R = ASC_MAX_BATCH; }
   const int64_t Bd = P.dcnt[s], sl = P.dctx[s];
-  int64_t C = INF64;
-  if (Bd > 0) {
-    const int64_t d = lat_decode(P.md, (uint64_t)Bd, (uint64_t)sl);
-    if (d < 0) atomicOr(P.err, ERR_RANGE);
-    C = P.tbt[s] - d;
-  }
+  const int64_t C = seg_tbt_budget(P, s);
   int32_t p[KPL];
   int64_t ct = 0, cb = 0, cc = 0;
   int k = 0;
@@ -274,29 +280,41 @@ __device__ __forceinline__ int finalize_segment(const StepP& P, int64_t s, const
 }
 
 // expand nibble-layout mask words (word 4g+u, bit l <-> entry b4 + 128g + 4l + u) into
-// id-ascending output indices starting at out[base]; returns the new base
+// id-ascending output indices starting at out[base]; returns the new base.  Set entries go to a
+// 256-slot shared-memory ring at their rank and leave it 128 at a time as coalesced stores (four
+// 32-lane rows with immediate offsets), instead of one 64-bit-addressed scattered store each.
 __device__ __forceinline__ int64_t expand_groups(const uint32_t* words, int ng, int64_t b4,
-                                                 int32_t* out, int64_t base) {
+                                                 int32_t* out, int64_t base, int32_t* ring) {
   const int lane = lane_id();
-  const uint32_t lt = lanemask_lt();
+  const uint32_t lt = lanemask_lt(), bit = 1u << lane;
+  int32_t* ob = out + base;
+  uint32_t head = 0, cnt = 0;  // buffered entries: ring[(head + i) & 255], i < cnt; head in {0, 128}
   for (int g = 0; g < ng; g++) {
     const uint4 wv = *reinterpret_cast<const uint4*>(words + 4 * g);  // words 4g..4g+3
     if ((wv.x | wv.y | wv.z | wv.w) == 0) continue;
-    // set entries before this lane's first: entry 4l'+u for l' < l, any u (no shuffles)
-    int64_t pos = base + __popc(wv.x & lt) + __popc(wv.y & lt) + __popc(wv.z & lt) + __popc(wv.w & lt);
+    uint32_t r = head + cnt + __popc(wv.x & lt) + __popc(wv.y & lt) + __popc(wv.z & lt) + __popc(wv.w & lt);
     const int32_t e0 = (int32_t)(b4 + g * GE + 4 * lane);
-    const uint32_t b0 = (wv.x >> lane) & 1u, b1 = (wv.y >> lane) & 1u, b2 = (wv.z >> lane) & 1u,
-                   b3 = (wv.w >> lane) & 1u;
-    if (b0) out[pos] = e0;
-    pos += b0;
-    if (b1) out[pos] = e0 + 1;
-    pos += b1;
-    if (b2) out[pos] = e0 + 2;
-    pos += b2;
-    if (b3) out[pos] = e0 + 3;
-    base += __popc(wv.x) + __popc(wv.y) + __popc(wv.z) + __popc(wv.w);
+    if (wv.x & bit) ring[r++ & 255] = e0;
+    if (wv.y & bit) ring[r++ & 255] = e0 + 1;
+    if (wv.z & bit) ring[r++ & 255] = e0 + 2;
+    if (wv.w & bit) ring[r & 255] = e0 + 3;
+    cnt += __popc(wv.x) + __popc(wv.y) + __popc(wv.z) + __popc(wv.w);
+    if (cnt >= 128) {
+      __syncwarp();
+#pragma unroll
+      for (int j = 0; j < 4; j++) ob[32 * j + lane] = ring[(head + 32 * j + lane) & 255];
+      __syncwarp();
+      ob += 128;
+      head ^= 128;
+      cnt -= 128;
+    }
   }
-  return base;
+  __syncwarp();
+#pragma unroll
+  for (int j = 0; j < 4; j++)
+    if (32 * j + lane < (int)cnt) ob[32 * j + lane] = ring[(head + 32 * j + lane) & 255];
+  __syncwarp();
+  return base + (int64_t)(ob - (out + base)) + cnt;
 }
 
 __device__ __forceinline__ void clear_admitted(uint32_t* words, int64_t loc) {
@@ -359,38 +377,151 @@ __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_grou
 template <int N>
 __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 
-// issue the copies of the group at e0 (this lane's first entry); tail groups crossing Q are read
-// directly at consume time instead
-__device__ __forceinline__ void stage_issue(const StepP& P, Stage& st, int64_t e0) {
-  const int l = lane_id();
-  if (e0 + 4 <= P.Q) {
-    cp_async16(&st.dl[2 * l], P.dl + e0);
-    cp_async16(&st.dl[2 * l + 1], P.dl + e0 + 2);
-    cp_async16(&st.eff[l], P.eff + e0);
-    cp_async4(&st.fl[l], P.fl + e0);
-  }
-}
-
-__device__ __forceinline__ void stage_read(const StepP& P, const Stage& st, int64_t e0, Grp& g) {
-  const int l = lane_id();
-  if (e0 + 4 <= P.Q) {
-    const longlong2 d01 = st.dl[2 * l], d23 = st.dl[2 * l + 1];
-    const int4 pv = st.eff[l];
-    g.f4 = st.fl[l];
-    g.dl[0] = d01.x; g.dl[1] = d01.y; g.dl[2] = d23.x; g.dl[3] = d23.y;
-    g.p[0] = pv.x; g.p[1] = pv.y; g.p[2] = pv.z; g.p[3] = pv.w;
-  } else {
-    load_grp<false>(P, e0, g);
-  }
-}
-
 __device__ __noinline__ int64_t pf_slow(const StepP& P, int32_t p) {
   const int64_t v = prefill_lat(P.md, (uint64_t)p);
   if (v < 0) { atomicOr(P.err, ERR_RANGE); return INT32_MAX; }
   return v;
 }
 
+static_assert(sizeof(Stage) * NST >= 256 * sizeof(int32_t), "expansion ring reuses the staging ring");
 constexpr size_t K1_SMEM = sizeof(Stage) * K1W * NST + sizeof(KI) * K1W * 160 + 2 * 4 * K1W * MW;
+
+// ---- budget-aware streaming selection (fast path).  A candidate packs into one uint64 whose
+// unsigned order is the (key, index) order: ((key32 + 2^31) << 32) | (task-local index << 17) | (p - 1),
+// p = the entry's effective prompt (<= 2^17).  The list is the warp's sorted 128 smallest
+// candidates (position r*32 + lane in a[r]); the low field holds p - 1.  Algorithm 1 admits the longest prefix
+// whose running sums of tokens, blocks and prefill µs stay strictly below N, M, C (and at most R
+// entries), so after every merge the threshold moves to the first list position j whose running
+// sums already reach a budget: the true prefix sum at any later key is at least the list's at j,
+// so no entry above that element can be admitted, while the element itself (the first entry
+// Algorithm 1 rejects) stays in the list.  Every entry of rank <= the first rejected one survives,
+// which is all finalize_segment / k2 read.
+constexpr int PK_LOC = 17;                          // bits of p below the local index
+constexpr uint64_t PK_PMASK = (1ull << PK_LOC) - 1;
+constexpr int32_t PFT_N = 1 << PK_LOC;              // fast table entries (p = 1 .. 2^17)
+static_assert(PFT_N == ASC_PF_FAST_N, "fast table size");
+
+struct TopKBud {
+  uint64_t a[KPL];
+  uint64_t thr;
+  int cnt, kpos;
+  bool any;
+  uint64_t* buf;  // 320 slots in shared memory (per warp); at most 159 are used
+  int32_t N, M, bs;
+  int64_t C;
+  const int32_t* tab;
+
+  __device__ __forceinline__ void init(uint64_t* sbuf, int kpos_, int32_t N_, int32_t M_, int64_t C_,
+                                       int32_t bs_, const int32_t* tab_) {
+#pragma unroll
+    for (int r = 0; r < KPL; r++) a[r] = PK_INF;
+    thr = PK_INF;
+    cnt = 0;
+    kpos = kpos_;
+    any = false;
+    buf = sbuf;
+    N = N_; M = M_; C = C_; bs = bs_; tab = tab_;
+  }
+  __device__ __forceinline__ void bitonic_merge() {
+    const int l = lane_id();
+#pragma unroll
+    for (int j = KPL / 2; j > 0; j >>= 1) {
+#pragma unroll
+      for (int r = 0; r < KPL; r++) {
+        if ((r & j) == 0) {
+          const uint64_t x = a[r], y = a[r | j];
+          a[r] = x < y ? x : y;
+          a[r | j] = x < y ? y : x;
+        }
+      }
+    }
+#pragma unroll
+    for (int j = 16; j > 0; j >>= 1) {
+      const bool lower = (l & j) == 0;
+#pragma unroll
+      for (int r = 0; r < KPL; r++) a[r] = pk_keep(a[r], __shfl_xor_sync(FULL, a[r], j), lower);
+    }
+  }
+  __device__ __forceinline__ uint64_t at(int pos) const {
+    const int r = pos >> 5;
+    uint64_t x = a[0];
+#pragma unroll
+    for (int q = 1; q < KPL; q++) if (q == r) x = a[q];
+    return __shfl_sync(FULL, x, pos & 31);
+  }
+  // first list position whose running (tokens, blocks, µs) reach (N, M, C), capped at kpos
+  __device__ __forceinline__ int budget_pos() const {
+    int pos = kpos;
+    int32_t ct = 0, cb = 0;
+    int64_t cc = 0;
+    for (int r = 0; r < KPL && r * 32 <= pos; r++) {
+      uint64_t x = a[0];
+#pragma unroll
+      for (int q = 1; q < KPL; q++) if (q == r) x = a[q];
+      const bool valid = x != PK_INF;
+      const int32_t q = (int32_t)(x & PK_PMASK);  // effective prompt - 1
+      const int32_t p = valid ? q + 1 : 0;
+      const int32_t bl = valid ? (p + bs) / bs : 0;
+      const int64_t pf = valid ? (int64_t)__ldg(tab + q) : 0;
+      const int32_t St = ct + warp_incl_scan(p);
+      const int32_t Sb = cb + warp_incl_scan(bl);
+      const int64_t Sc = cc + warp_incl_scan(pf);
+      const uint32_t m = __ballot_sync(FULL, valid && (St >= N || Sb >= M || Sc >= C));
+      if (m) return min(pos, r * 32 + __ffs(m) - 1);
+      ct = __shfl_sync(FULL, St, 31);
+      cb = __shfl_sync(FULL, Sb, 31);
+      cc = __shfl_sync(FULL, Sc, 31);
+    }
+    return pos;
+  }
+  __device__ __forceinline__ void merge_sorted32(uint64_t y) {
+    if (any) {
+      const uint64_t br = __shfl_sync(FULL, y, 31 - lane_id());
+      a[KPL - 1] = a[KPL - 1] < br ? a[KPL - 1] : br;
+      bitonic_merge();
+    } else {
+      a[0] = y;
+      any = true;
+    }
+    thr = at(budget_pos());
+  }
+  // merge the first 32 buffered candidates, then keep only the rest still below the new threshold
+  __device__ __forceinline__ void flush32() {
+    __syncwarp();
+    const uint64_t y = buf[lane_id()];
+    __syncwarp();
+    merge_sorted32(sort32_pk(y));
+    int nc = 0;
+    for (int c0 = 32; c0 < cnt; c0 += 32) {
+      const int j = c0 + lane_id();
+      const uint64_t x = j < cnt ? buf[j] : PK_INF;
+      const bool keep = x < thr;
+      const uint32_t m = __ballot_sync(FULL, keep);  // also orders the read before the writes
+      if (keep) buf[nc + __popc(m & lanemask_lt())] = x;
+      nc += __popc(m);
+    }
+    cnt = nc;
+    __syncwarp();
+  }
+  __device__ __forceinline__ void append(uint64_t x, bool c) {
+    const uint32_t m = __ballot_sync(FULL, c);
+    if (c) buf[cnt + __popc(m & lanemask_lt())] = x;
+    cnt += __popc(m);
+  }
+  __device__ __forceinline__ void drain() {
+    while (cnt >= 32) flush32();
+  }
+  __device__ __forceinline__ void finish() {
+    drain();
+    if (cnt > 0) {
+      __syncwarp();
+      const uint64_t y = lane_id() < cnt ? buf[lane_id()] : PK_INF;
+      __syncwarp();
+      cnt = 0;
+      merge_sorted32(sort32_pk(y));
+    }
+  }
+};
 
 struct TaskCtx {  // per-task constants (uniform across the warp)
   int64_t s, lo, b, e_end, b4, now, othr;
@@ -458,6 +589,142 @@ __device__ __noinline__ void task_generic(const StepP& P, const TaskCtx& t, KI* 
 
 constexpr int64_t WIN = int64_t(1) << 30;  // fast-path window: |deadline - now| < 2^30 us, pf < 2^30
 
+// Fast path of one task: 32-bit arithmetic relative to `now`.  With d = deadline - now, each
+// entry computes d' = d + 2^30 as the low word of one 64-bit add; the task is exact in 32 bits when
+// every d' lies in [0, 2^31) (|d| <= 2^30 µs), every p in [1, 2^17] and every prefill below 2^30 µs.
+// Those conditions are OR-accumulated (4 words per lane) and tested once at the end; a task that
+// fails them is redone by task_generic.  Returns false in that case.
+template <bool VEC, bool DROP, bool OFFL>
+__device__ __forceinline__ bool task_fast(const StepP& P, const TaskCtx& t, Stage (&stg)[NST], uint64_t* sbuf,
+                                          uint32_t* m_off, uint32_t* m_drop, int64_t Cb, KI (&top)[KPL]) {
+  const int lane = lane_id();
+  const int ng = t.ng;
+  const int64_t b4 = t.b4;
+  const bool select = t.kpos >= 0;
+  const int64_t nowc = WIN - t.now;  // d' = deadline + nowc
+  // offload iff deadline - prefill_us <= now + W_hp + margin  <=>  d' - pf <= othr1
+  const int32_t othr1 = (int32_t)min(P.W + P.margin + WIN, (int64_t)INT32_MAX);
+  const int32_t dmask = P.kdl ? -1 : 0;
+  const int32_t kpf = P.kpf;
+  const int32_t* __restrict__ tab = P.pf_fast;
+  const bool has_pfout = P.pfout != nullptr;
+  TopKBud st;
+  st.init(sbuf, t.kpos, P.bN[t.s], P.bM[t.s], Cb, P.bs, tab);
+  uint32_t accH = 0, accL = 0, accQ = 0, accF = 0;
+  const uint32_t vspan = (uint32_t)(t.vhi - t.vlo);
+  // groups [0, nfull) lie entirely below Q: staged through shared memory without bounds tests
+  int nfull = 0;
+  if (VEC) {
+    const int64_t nf = (P.Q - b4) / GE;
+    nfull = (int)(nf < ng ? nf : ng);
+  }
+  const int64_t* gdl = P.dl + b4 + 4 * lane;
+  const int32_t* gef = P.eff + b4 + 4 * lane;
+  const uint8_t* gfl = P.fl + b4 + 16 * (lane & 7);  // lanes 0-7 copy the group's 128 flag bytes
+  const int l = lane;
+#pragma unroll
+  for (int q = 0; q < NST - 1; q++) {
+    if (q < nfull) {
+      cp_async16(&stg[q].dl[2 * l], gdl + q * GE);
+      cp_async16(&stg[q].dl[2 * l + 1], gdl + q * GE + 2);
+      cp_async16(&stg[q].eff[l], gef + q * GE);
+      if (l < 8) cp_async16(&stg[q].fl[4 * l], gfl + q * GE);
+    }
+    cp_commit();
+  }
+  for (int g = 0; g < ng; g++) {
+    const int gi = g + NST - 1;
+    __syncwarp();  // every lane is done reading the slot lanes 0-7 refill next
+    if (gi < nfull) {
+      Stage& sg = stg[gi % NST];
+      cp_async16(&sg.dl[2 * l], gdl + gi * GE);
+      cp_async16(&sg.dl[2 * l + 1], gdl + gi * GE + 2);
+      cp_async16(&sg.eff[l], gef + gi * GE);
+      if (l < 8) cp_async16(&sg.fl[4 * l], gfl + gi * GE);
+    }
+    cp_commit();
+    const int64_t e0 = b4 + (int64_t)g * GE + 4 * lane;
+    Grp cur;
+    if (g < nfull) {
+      cp_wait<NST - 1>();
+      __syncwarp();  // flag bytes were copied by lanes 0-7
+      const Stage& sg = stg[g % NST];
+      const longlong2 d01 = sg.dl[2 * l], d23 = sg.dl[2 * l + 1];
+      const int4 pv = sg.eff[l];
+      cur.f4 = sg.fl[l];
+      cur.dl[0] = d01.x; cur.dl[1] = d01.y; cur.dl[2] = d23.x; cur.dl[3] = d23.y;
+      cur.p[0] = pv.x; cur.p[1] = pv.y; cur.p[2] = pv.z; cur.p[3] = pv.w;
+    } else {
+      load_grp<false>(P, e0, cur);
+    }
+    const int32_t r0 = g * GE + 4 * lane;
+    const uint32_t l0 = (uint32_t)r0 << PK_LOC;  // task-local index of this lane's first entry
+    uint64_t x[4];
+    bool cnd[4];
+    int32_t pfv[4];
+    uint32_t mo[4], md[4];
+    auto body = [&](auto interior) {
+      constexpr bool IN = decltype(interior)::value;
+#pragma unroll
+      for (int u = 0; u < 4; u++) {  // branch-free: every lane runs the same instructions
+        const bool v = IN || (uint32_t)(r0 + u - t.vlo) < vspan;
+        const int64_t dd = cur.dl[u] + nowc;
+        const uint32_t lo1 = (uint32_t)dd, hi1 = (uint32_t)((uint64_t)dd >> 32);
+        const int32_t q = cur.p[u] - 1;
+        const int32_t pf = __ldg(tab + (q & (int32_t)PK_PMASK));
+        accH |= v ? hi1 : 0u;
+        accL |= v ? lo1 : 0u;
+        accQ |= v ? (uint32_t)q : 0u;
+        accF |= v ? (uint32_t)pf : 0u;
+        pfv[u] = pf;
+        if (!IN && has_pfout && v) __stcs(P.pfout + e0 + u, pf);
+        const int32_t d1 = (int32_t)lo1;  // deadline - now + 2^30
+        const uint32_t f = cur.f4 >> (8 * u);
+        const bool dropped = DROP && v && !(f & 1u) && d1 < (int32_t)WIN;
+        const bool off = OFFL && v && !dropped && !(f & 3u) && d1 - pf <= othr1;
+        if (DROP) md[u] = __ballot_sync(FULL, dropped);
+        if (OFFL) mo[u] = __ballot_sync(FULL, off);
+        const int32_t key1 = (d1 & dmask) + kpf * pf;  // kdl * d' + kpf * pf, branch-free
+        x[u] = ((uint64_t)((uint32_t)key1 ^ 0x80000000u) << 32) |
+               (uint64_t)(l0 + ((uint32_t)u << PK_LOC) + ((uint32_t)q & (uint32_t)PK_PMASK));
+        cnd[u] = select && v && !dropped && x[u] < st.thr;
+      }
+    };
+    if (r0 - 4 * lane >= t.vlo && r0 - 4 * lane + GE <= t.vhi) {
+      body(std::true_type{});
+      if (has_pfout) {
+        if (VEC) __stcs(reinterpret_cast<int4*>(P.pfout + e0), make_int4(pfv[0], pfv[1], pfv[2], pfv[3]));
+        else for (int u = 0; u < 4; u++) __stcs(P.pfout + e0 + u, pfv[u]);
+      }
+    } else {
+      body(std::false_type{});
+    }
+    if (lane == 0) {  // the group's 4 ballot words
+      if (DROP) *reinterpret_cast<uint4*>(m_drop + 4 * g) = make_uint4(md[0], md[1], md[2], md[3]);
+      if (OFFL) *reinterpret_cast<uint4*>(m_off + 4 * g) = make_uint4(mo[0], mo[1], mo[2], mo[3]);
+    }
+    if (__any_sync(FULL, cnd[0] | cnd[1] | cnd[2] | cnd[3])) {
+#pragma unroll
+      for (int u = 0; u < 4; u++) st.append(x[u], cnd[u]);
+      st.drain();
+    }
+  }
+  cp_wait<0>();
+  __syncwarp();
+  const bool ok = accH == 0 && !(accL & 0x80000000u) && !(accQ & ~(uint32_t)PK_PMASK) && !(accF & 0xC0000000u);
+  if (!__all_sync(FULL, ok)) return false;
+  if (select) st.finish();
+  const int64_t kbase = P.kdl ? t.now - WIN : 0;  // key = kbase + key1
+#pragma unroll
+  for (int r = 0; r < KPL; r++) {
+    const uint64_t x = st.a[r];
+    top[r] = x == PK_INF ? ki_inf()
+                         : KI{kbase + (int64_t)(int32_t)((uint32_t)(x >> 32) ^ 0x80000000u),
+                              (int32_t)(b4 + (int64_t)((uint32_t)x >> PK_LOC))};
+  }
+  return true;
+}
+
 // TAB: 0 = int64 latency table (generic path only), 1 = int32 table (fast path)
 template <bool VEC, int TAB, bool DROP, bool OFFL>
 __global__ void __launch_bounds__(K1W * 32, ASC_K1_MINB) k1_tasks(const __grid_constant__ StepP P) {
@@ -481,7 +748,7 @@ __global__ void __launch_bounds__(K1W * 32, ASC_K1_MINB) k1_tasks(const __grid_c
     const int64_t hi = P.seg_off[s + 1];
     t.b = t.lo + c * CH;
     t.e_end = min(hi, t.b + CH);
-    t.b4 = t.b & ~int64_t(3);
+    t.b4 = t.b & ~int64_t(ALN - 1);
     t.ng = (int)((t.e_end - t.b4 + GE - 1) / GE);
     t.vlo = (int32_t)(t.b - t.b4);
     t.vhi = (int32_t)(t.e_end - t.b4);
@@ -493,101 +760,16 @@ __global__ void __launch_bounds__(K1W * 32, ASC_K1_MINB) k1_tasks(const __grid_c
     kneed = kneed < 32 * KPL ? kneed : 32 * KPL;
     kneed = kneed < (int64_t)P.bN[s] - 1 ? kneed : (int64_t)P.bN[s] - 1;
     kneed = kneed < (int64_t)P.bM[s] - 1 ? kneed : (int64_t)P.bM[s] - 1;
+    const int64_t Cb = seg_tbt_budget(P, s);  // every prefill costs >= 1 µs
+    kneed = kneed < Cb - 1 ? kneed : Cb - 1;
     t.kpos = kneed > 0 ? (int)kneed - 1 : -1;
-    const bool select = kneed > 0;
     const int64_t b4 = t.b4, lo = t.lo;
     const int ng = t.ng;
     KI top[KPL];
     bool fast_ok = (TAB == 1);
-    if (TAB == 1) {
-      // ---- fast path: 32-bit arithmetic relative to `now`, packed (key, local idx) ----------
-      const int32_t othr32 = (int32_t)max(min(P.W + P.margin, (int64_t)INT32_MAX), (int64_t)INT32_MIN);
-      const int64_t kbase = P.kdl ? t.now : 0;  // key = kbase + key32
-      TopKPk<KPL> st;
-      st.init(reinterpret_cast<uint64_t*>(sbuf[w]), t.kpos);
-      bool inwin = true;  // any entry outside the 32-bit window (or the table) -> generic path
-      const uint32_t vspan = (uint32_t)(t.vhi - t.vlo);
-      const uint32_t tab_hi = (uint32_t)(P.pt - 1);
-      const int32_t* __restrict__ tab32 = P.pf_tab32;
-      const bool has_pfout = P.pfout != nullptr;
-      const int kpf = P.kpf;
-      const int32_t dmask = P.kdl ? -1 : 0;
-#pragma unroll
-      for (int q = 0; q < NST - 1; q++) {
-        if (VEC && q < ng) stage_issue(P, s_stage[w][q], b4 + (int64_t)q * GE + 4 * lane);
-        cp_commit();
-      }
-      for (int g = 0; g < ng; g++) {
-        const int64_t e0 = b4 + (int64_t)g * GE + 4 * lane;
-        if (VEC && g + NST - 1 < ng) stage_issue(P, s_stage[w][(g + NST - 1) % NST], e0 + (NST - 1) * GE);
-        cp_commit();
-        Grp cur;
-        if (VEC) {
-          cp_wait<NST - 1>();
-          stage_read(P, s_stage[w][g % NST], e0, cur);
-        } else {
-          load_grp<false>(P, e0, cur);
-        }
-        const int32_t r0 = g * GE + 4 * lane;
-        const uint32_t l0 = (uint32_t)(e0 - lo);  // local index of this lane's first entry
-        uint64_t x[4];
-        bool cnd[4];
-        uint32_t mo_w = 0, md_w = 0;
-        // interior groups (every entry inside the task) skip the per-entry bounds test
-        auto body = [&](auto interior) {
-          constexpr bool IN = decltype(interior)::value;
-#pragma unroll
-          for (int u = 0; u < 4; u++) {  // branch-free: every lane runs the same instructions
-            const bool v = IN || (uint32_t)(r0 + u - t.vlo) < vspan;
-            const uint32_t f = (cur.f4 >> (8 * u)) & 0xffu;
-            const int32_t pu = cur.p[u];
-            const bool inrange = (uint32_t)(pu - 1) < tab_hi;  // 1 <= pu < pt
-            const int32_t pf = __ldg(tab32 + (inrange ? pu : 1));
-            const int64_t d = cur.dl[u] - t.now;
-            inwin &= !v || (inrange && (uint64_t)(d + WIN) < (uint64_t)(2 * WIN) && pf < (int32_t)WIN);
-            if (has_pfout && v) __stcs(P.pfout + e0 + u, pf);
-            const int32_t d32 = (int32_t)d;
-            const bool dropped = DROP && v && !(f & 1u) && d32 < 0;
-            const bool off = OFFL && v && !dropped && !(f & 3u) && d32 - pf <= othr32;
-            if (DROP) {
-              const uint32_t md = __ballot_sync(FULL, dropped);
-              md_w = lane == u ? md : md_w;
-            }
-            if (OFFL) {
-              const uint32_t mo = __ballot_sync(FULL, off);
-              mo_w = lane == u ? mo : mo_w;
-            }
-            const int32_t key32 = (d32 & dmask) + kpf * pf;  // kdl * d32 + kpf * pf, branch-free
-            x[u] = ((uint64_t)((uint32_t)key32 ^ 0x80000000u) << 32) | (uint64_t)(l0 + u);
-            cnd[u] = select && v && !dropped && x[u] < st.thr;
-          }
-        };
-        if (r0 - 4 * lane >= t.vlo && r0 - 4 * lane + GE <= t.vhi) body(std::true_type{});
-        else body(std::false_type{});
-        if (lane < 4) {  // lanes 0-3 hold the 4 ballot words of this group
-          if (DROP) s_drop[w][4 * g + lane] = md_w;
-          if (OFFL) s_off[w][4 * g + lane] = mo_w;
-        }
-        if (__any_sync(FULL, cnd[0] | cnd[1] | cnd[2] | cnd[3])) {
-#pragma unroll
-          for (int u = 0; u < 4; u++) st.append(x[u], cnd[u]);
-          st.drain();
-        }
-      }
-      cp_wait<0>();
-      __syncwarp();
-      fast_ok = __all_sync(FULL, inwin);
-      if (fast_ok) {
-        if (select) st.finish();
-#pragma unroll
-        for (int r = 0; r < KPL; r++) {
-          const uint64_t x = st.a[r];
-          top[r] = x == PK_INF ? ki_inf()
-                               : KI{kbase + (int64_t)(int32_t)((uint32_t)(x >> 32) ^ 0x80000000u),
-                                    (int32_t)(lo + (int64_t)(uint32_t)x)};
-        }
-      }
-    }
+    if (TAB == 1)
+      fast_ok = task_fast<VEC, DROP, OFFL>(P, t, s_stage[w], reinterpret_cast<uint64_t*>(sbuf[w]), s_off[w],
+                                           s_drop[w], Cb, top);
     if (!fast_ok) {
       KI tmp[KPL];
       task_generic<DROP, OFFL>(P, t, sbuf[w], s_off[w], s_drop[w], tmp);
@@ -603,8 +785,9 @@ __global__ void __launch_bounds__(K1W * 32, ASC_K1_MINB) k1_tasks(const __grid_c
       for (int r = 0; r < KPL; r++)
         if (OFFL && adm[r]) clear_admitted(s_off[w], top[r].i - b4);
       __syncwarp();
-      const int64_t no = OFFL ? expand_groups(s_off[w], ng, b4, P.off_idx, lo) : lo;
-      const int64_t nd = DROP ? expand_groups(s_drop[w], ng, b4, P.drop_idx, lo) : lo;
+      int32_t* ring = reinterpret_cast<int32_t*>(&s_stage[w][0]);  // the staging ring is idle now
+      const int64_t no = OFFL ? expand_groups(s_off[w], ng, b4, P.off_idx, lo, ring) : lo;
+      const int64_t nd = DROP ? expand_groups(s_drop[w], ng, b4, P.drop_idx, lo, ring) : lo;
       if (lane == 0) { P.off_cnt[s] = (int32_t)(no - lo); P.drop_cnt[s] = (int32_t)(nd - lo); }
     } else {
       const int64_t mt = P.mtask_off[s] + c;
@@ -772,7 +955,7 @@ __global__ void __launch_bounds__(WARPS * 32) k2_segments(const __grid_constant_
         if (adm[r]) {
           const int64_t e = A.a[r].i;
           const int64_t t = (e - lo) / CH;
-          const int64_t b4 = (lo + t * CH) & ~int64_t(3);
+          const int64_t b4 = (lo + t * CH) & ~int64_t(ALN - 1);
           const int64_t loc = e - b4, g = loc >> 7, rr = loc & 127;
           const uint32_t bit = 1u << (rr >> 2);
           const uint32_t old = atomicAnd(&P.moff[(m0 + t) * MW + 4 * g + (rr & 3)], ~bit);
@@ -800,6 +983,7 @@ __global__ void __launch_bounds__(WARPS * 32) k2_segments(const __grid_constant_
 }
 
 __global__ void __launch_bounds__(WARPS * 32) k3_expand(const __grid_constant__ StepP P) {
+  __shared__ int32_t s_ring[WARPS][256];
   const int w = threadIdx.x >> 5;
   const int64_t ntasks = min(P.task_off[P.S], P.ntask_max);
   for (int64_t task = blockIdx.x * (int64_t)WARPS + w; task < ntasks;
@@ -813,10 +997,10 @@ __global__ void __launch_bounds__(WARPS * 32) k3_expand(const __grid_constant__ 
     const int64_t lo = P.seg_off[s], hi = P.seg_off[s + 1];
     const int64_t b = lo + c * CH;
     const int64_t e_end = min(hi, b + CH);
-    const int64_t b4 = b & ~int64_t(3);
+    const int64_t b4 = b & ~int64_t(ALN - 1);
     const int ng = (int)((e_end - b4 + GE - 1) / GE);
-    expand_groups(P.moff + mt * MW, ng, b4, P.off_idx, lo + P.coff[mt]);
-    expand_groups(P.mdrop + mt * MW, ng, b4, P.drop_idx, lo + P.cdrop[mt]);
+    expand_groups(P.moff + mt * MW, ng, b4, P.off_idx, lo + P.coff[mt], s_ring[w]);
+    expand_groups(P.mdrop + mt * MW, ng, b4, P.drop_idx, lo + P.cdrop[mt], s_ring[w]);
   }
 }
 
@@ -824,6 +1008,10 @@ template <bool VEC, int TAB, bool DROP, bool OFFL>
 void launch_k1_t(unsigned grid, size_t, cudaStream_t sm, const StepP& P) {
   cudaFuncSetAttribute(k1_tasks<VEC, TAB, DROP, OFFL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)K1_SMEM);
+  // shared memory for ASC_K1_MINB resident CTAs and no more: the rest of the unified L1 caches the
+  // prefill table the per-entry a1 lookups gather from
+  const int carve = (int)((ASC_K1_MINB * (K1_SMEM + 1024) * 100 + 228 * 1024 - 1) / (228 * 1024));
+  cudaFuncSetAttribute(k1_tasks<VEC, TAB, DROP, OFFL>, cudaFuncAttributePreferredSharedMemoryCarveout, carve);
   k1_tasks<VEC, TAB, DROP, OFFL><<<grid, K1W * 32, K1_SMEM, sm>>>(P);
 }
 
@@ -843,10 +1031,7 @@ void launch_k1_d(int variant, unsigned grid, size_t dsm, cudaStream_t sm, const 
 }
 
 void launch_k1(int variant, unsigned grid, size_t dsm, cudaStream_t sm, const StepP& P) {
-  switch ((variant >> 1) & 3) {
-    case 1: launch_k1_d<1>(variant, grid, dsm, sm, P); break;
-    default: launch_k1_d<0>(variant, grid, dsm, sm, P); break;
-  }
+  launch_k1_d<1>(variant, grid, dsm, sm, P);  // the fast table always exists; task_generic covers the rest
 }
 
 }  // namespace
@@ -870,6 +1055,7 @@ asc_status launch_schedule_step(asc_ctx* c, const asc_step_in* in, asc_step_out*
   P.max_mt = max_mt;
   P.pf_tab = c->d_pf_tab;
   P.pf_tab32 = c->d_pf_tab32;
+  P.pf_fast = c->d_pf_fast;
   P.pt = c->pt_size;
   P.bs = c->cfg.topo.block_tokens;
   P.drop = c->cfg.flags.drop;
@@ -921,7 +1107,7 @@ asc_status launch_schedule_step(asc_ctx* c, const asc_step_in* in, asc_step_out*
   int64_t g1 = (ntask_max + K1W - 1) / K1W;
   g1 = g1 < (int64_t)dev_sms * ASC_K1_MINB ? g1 : (int64_t)dev_sms * ASC_K1_MINB;
   const bool vec = ((uintptr_t)in->deadline_us % 16 == 0) && ((uintptr_t)in->eff_prompt % 16 == 0) &&
-                   ((uintptr_t)in->flags % 4 == 0);
+                   ((uintptr_t)in->flags % 16 == 0) && ((uintptr_t)P.pfout % 16 == 0);
   const unsigned gk = (unsigned)(g1 > 0 ? g1 : 1);
   const int tab = P.pf_tab32 ? 1 : 0;
   const size_t dsm = 0;

@@ -104,6 +104,33 @@ def test_deep_segments_ample_budgets(asc, oracle):
     compare(run_gpu(asc, cfg, ins), oracle.schedule_step(cfg, **ins), ins["seg_off"])
 
 
+@pytest.mark.parametrize("bind", ["tokens", "blocks", "tbt", "reqs", "mixed"])
+def test_budget_bound_thresholds(asc, oracle, bind):
+    # k1 moves its selection threshold to the first list position whose running tokens / blocks /
+    # prefill µs reach N / M / C (Alg. 1 l.5-13): deep single- and multi-task segments
+    # where each budget binds in turn, with heavily tied keys (deadlines on a coarse grid)
+    rng = np.random.default_rng({"tokens": 11, "blocks": 12, "tbt": 13, "reqs": 14, "mixed": 15}[bind])
+    cfg = P.config(flg=P.flags(policy="EDF_LAXITY", drop=1))
+    qs = [16384, 16385, 40000, 9000, 33, 70000, 12000, 5000]
+    ins = H.random_step_inputs(rng, len(qs), 0, cfg, budgets="config", qs=qs)
+    S = len(qs)
+    ins["deadline_us"] = (ins["deadline_us"] // 250_000) * 250_000
+    if bind in ("tokens", "mixed"):
+        ins["budget_tokens"] = rng.integers(1, 3000, size=S).astype(np.int32)
+    if bind in ("blocks", "mixed"):
+        ins["budget_blocks"] = rng.integers(1, 120, size=S).astype(np.int32)
+    if bind in ("tbt", "mixed"):
+        ins["dec_count"] = rng.integers(1, 64, size=S).astype(np.int32)
+        ins["dec_ctx_sum"] = ins["dec_count"].astype(np.int64) * 500
+        ins["tbt_slo_us"] = rng.integers(20_000, 300_000, size=S).astype(np.int64)
+    if bind == "reqs":
+        ins["budget_reqs"] = rng.integers(1, 129, size=S).astype(np.int32)
+    got = run_gpu(asc, cfg, ins)
+    exp = oracle.schedule_step(cfg, **ins)
+    assert int(exp["admit_cnt"].sum()) > 0
+    compare(got, exp, ins["seg_off"])
+
+
 def test_adversarial_key_order(asc, oracle):
     # keys strictly decreasing with position: every entry beats the running threshold
     cfg = P.config(flg=P.flags(policy="EDF_DEADLINE"))
