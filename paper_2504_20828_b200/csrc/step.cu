@@ -33,7 +33,7 @@ constexpr int MW = 4 * NG;         // mask words per task per mask (word 4g+u, b
 constexpr int SMALL = 32;  // segments of <= SMALL entries: one warp, one entry per lane (k_small)
 constexpr int WARPS = 8;   // k2/k3 CTA size
 constexpr int K1W = 4;     // k1 CTA size (warps); 4 CTAs/SM -> 16 warps, 128 registers
-constexpr int SCAN_ITEMS = 4;
+constexpr int SCAN_ITEMS = 8;  // plan_small (one launch) covers S < 8192
 constexpr int SCAN_THREADS = 1024;
 constexpr int SCAN_TILE = SCAN_ITEMS * SCAN_THREADS;
 

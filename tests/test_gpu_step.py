@@ -184,3 +184,27 @@ def test_generic_path_wide_deadlines(asc, oracle):
         ins["deadline_us"][:300] += 10 ** 12
         ins["deadline_us"][5300:5400] -= 5 * 10 ** 10
         compare(run_gpu(asc, cfg, ins), oracle.schedule_step(cfg, **ins), ins["seg_off"])
+
+
+def test_row_s_full_scale_sampled(asc, oracle):
+    """SURVEY row S at full size (4096 segments x 10,000 entries) with bench.py's inputs and launch
+    configuration; the oracle checks a stratified sample of segments one by one (segments are
+    independent, so a segment's decision depends only on its own entries and budgets)."""
+    rng = np.random.default_rng(123)  # bench.py's step_microbench seed
+    cfg = P.config()
+    S, Qs = 4096, 10_000
+    ins = H.random_step_inputs(rng, S, 0, cfg, qs=np.full(S, Qs))
+    got = run_gpu(asc, cfg, ins)
+    g = H.segment_lists(got, ins["seg_off"])
+    for s in range(0, S, 128):
+        lo, hi = int(ins["seg_off"][s]), int(ins["seg_off"][s + 1])
+        one = dict(seg_off=np.array([0, hi - lo], np.int64))
+        for k in ("now_us", "dec_count", "dec_ctx_sum", "tbt_slo_us", "budget_tokens", "budget_blocks",
+                  "budget_reqs"):
+            one[k] = ins[k][s:s + 1]
+        for k in ("deadline_us", "eff_prompt", "flags"):
+            one[k] = ins[k][lo:hi]
+        exp = oracle.schedule_step(cfg, **one)
+        e = H.segment_lists(exp, one["seg_off"])[0]
+        assert [list(np.asarray(x) - lo) for x in g[s]] == [list(x) for x in e], s
+        assert got["batch_lat_us"][s] == exp["batch_lat_us"][0], s
