@@ -384,7 +384,16 @@ __device__ __noinline__ int64_t pf_slow(const StepP& P, int32_t p) {
 }
 
 static_assert(sizeof(Stage) * NST >= 256 * sizeof(int32_t), "expansion ring reuses the staging ring");
-constexpr size_t K1_SMEM = sizeof(Stage) * K1W * NST + sizeof(KI) * K1W * 160 + 2 * 4 * K1W * MW;
+// k1 shared memory: per-warp staging rings (which also hold task_generic's candidate buffer), per-warp
+// packed candidate buffers, and the per-warp masks of the enabled lists only
+static_assert(sizeof(Stage) * NST >= sizeof(KI) * 160, "task_generic's buffer reuses the staging ring");
+template <bool DROP, bool OFFL>
+struct K1L {
+  static constexpr size_t OFF_BUF = sizeof(Stage) * K1W * NST;
+  static constexpr size_t OFF_OFF = OFF_BUF + sizeof(uint64_t) * K1W * 160;
+  static constexpr size_t OFF_DROP = OFF_OFF + (OFFL ? 4 * K1W * MW : 0);
+  static constexpr size_t SMEM = OFF_DROP + (DROP ? 4 * K1W * MW : 0);
+};
 
 // ---- budget-aware streaming selection (fast path).  A candidate packs into one uint64 whose
 // unsigned order is the (key, index) order: ((key32 + 2^31) << 32) | (task-local index << 17) | (p - 1),
@@ -728,13 +737,12 @@ __device__ __forceinline__ bool task_fast(const StepP& P, const TaskCtx& t, Stag
 // TAB: 0 = int64 latency table (generic path only), 1 = int32 table (fast path)
 template <bool VEC, int TAB, bool DROP, bool OFFL>
 __global__ void __launch_bounds__(K1W * 32, ASC_K1_MINB) k1_tasks(const __grid_constant__ StepP P) {
-  extern __shared__ __align__(16) unsigned char k1_smem[];  // K1_SMEM bytes (dynamic)
+  using L = K1L<DROP, OFFL>;
+  extern __shared__ __align__(16) unsigned char k1_smem[];  // L::SMEM bytes (dynamic)
   auto& s_stage = *reinterpret_cast<Stage(*)[K1W][NST]>(k1_smem);
-  auto& sbuf = *reinterpret_cast<KI(*)[K1W][160]>(k1_smem + sizeof(Stage) * K1W * NST);
-  auto& s_off = *reinterpret_cast<uint32_t(*)[K1W][MW]>(k1_smem + sizeof(Stage) * K1W * NST +
-                                                         sizeof(KI) * K1W * 160);
-  auto& s_drop = *reinterpret_cast<uint32_t(*)[K1W][MW]>(k1_smem + sizeof(Stage) * K1W * NST +
-                                                          sizeof(KI) * K1W * 160 + 4 * K1W * MW);
+  auto& sbuf = *reinterpret_cast<uint64_t(*)[K1W][160]>(k1_smem + L::OFF_BUF);
+  auto& s_off = *reinterpret_cast<uint32_t(*)[K1W][MW]>(k1_smem + L::OFF_OFF);
+  auto& s_drop = *reinterpret_cast<uint32_t(*)[K1W][MW]>(k1_smem + L::OFF_DROP);
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t ntasks = min(P.task_off[P.S], P.ntask_max);
   for (int64_t task = blockIdx.x * (int64_t)K1W + w; task < ntasks;
@@ -768,11 +776,10 @@ __global__ void __launch_bounds__(K1W * 32, ASC_K1_MINB) k1_tasks(const __grid_c
     KI top[KPL];
     bool fast_ok = (TAB == 1);
     if (TAB == 1)
-      fast_ok = task_fast<VEC, DROP, OFFL>(P, t, s_stage[w], reinterpret_cast<uint64_t*>(sbuf[w]), s_off[w],
-                                           s_drop[w], Cb, top);
+      fast_ok = task_fast<VEC, DROP, OFFL>(P, t, s_stage[w], sbuf[w], s_off[w], s_drop[w], Cb, top);
     if (!fast_ok) {
       KI tmp[KPL];
-      task_generic<DROP, OFFL>(P, t, sbuf[w], s_off[w], s_drop[w], tmp);
+      task_generic<DROP, OFFL>(P, t, reinterpret_cast<KI*>(&s_stage[w][0]), s_off[w], s_drop[w], tmp);
 #pragma unroll
       for (int r = 0; r < KPL; r++) top[r] = tmp[r];
     }
@@ -1006,13 +1013,19 @@ __global__ void __launch_bounds__(WARPS * 32) k3_expand(const __grid_constant__ 
 
 template <bool VEC, int TAB, bool DROP, bool OFFL>
 void launch_k1_t(unsigned grid, size_t, cudaStream_t sm, const StepP& P) {
-  cudaFuncSetAttribute(k1_tasks<VEC, TAB, DROP, OFFL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)K1_SMEM);
+  constexpr size_t SMEM = K1L<DROP, OFFL>::SMEM;
+  auto* k = k1_tasks<VEC, TAB, DROP, OFFL>;
+  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM);
   // shared memory for ASC_K1_MINB resident CTAs and no more: the rest of the unified L1 caches the
   // prefill table the per-entry a1 lookups gather from
-  const int carve = (int)((ASC_K1_MINB * (K1_SMEM + 1024) * 100 + 228 * 1024 - 1) / (228 * 1024));
-  cudaFuncSetAttribute(k1_tasks<VEC, TAB, DROP, OFFL>, cudaFuncAttributePreferredSharedMemoryCarveout, carve);
-  k1_tasks<VEC, TAB, DROP, OFFL><<<grid, K1W * 32, K1_SMEM, sm>>>(P);
+  const int carve = (int)((ASC_K1_MINB * (SMEM + 1024) * 100 + 228 * 1024 - 1) / (228 * 1024));
+  cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, carve < 100 ? carve : 100);
+  int dev = 0, sms = 148, nb = ASC_K1_MINB;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k, K1W * 32, SMEM);
+  const unsigned cap = (unsigned)(sms * (nb > 0 ? nb : 1));
+  k<<<grid < cap ? grid : cap, K1W * 32, SMEM, sm>>>(P);
 }
 
 template <int TAB, bool DROP, bool OFFL>
@@ -1104,8 +1117,8 @@ asc_status launch_schedule_step(asc_ctx* c, const asc_step_in* in, asc_step_out*
     fill_task_seg<<<(unsigned)(gf < 4 * dev_sms ? (gf > 0 ? gf : 1) : 4 * dev_sms), 256, 0, sm>>>(P);
     launches += 5;
   }
-  int64_t g1 = (ntask_max + K1W - 1) / K1W;
-  g1 = g1 < (int64_t)dev_sms * ASC_K1_MINB ? g1 : (int64_t)dev_sms * ASC_K1_MINB;
+  int64_t g1 = (ntask_max + K1W - 1) / K1W;  // clamped to the resident CTAs by launch_k1_t
+  g1 = g1 < (int64_t)dev_sms * 32 ? g1 : (int64_t)dev_sms * 32;
   const bool vec = ((uintptr_t)in->deadline_us % 16 == 0) && ((uintptr_t)in->eff_prompt % 16 == 0) &&
                    ((uintptr_t)in->flags % 16 == 0) && ((uintptr_t)P.pfout % 16 == 0);
   const unsigned gk = (unsigned)(g1 > 0 ? g1 : 1);
