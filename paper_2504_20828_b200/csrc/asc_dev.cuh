@@ -144,6 +144,13 @@ __device__ __forceinline__ T warp_max(T v) {
   for (int o = 16; o > 0; o >>= 1) { T w = __shfl_xor_sync(FULL, v, o); v = w > v ? w : v; }
   return v;
 }
+// 32-bit integer reductions are one REDUX instruction each (sm_80+)
+__device__ __forceinline__ int32_t warp_sum(int32_t v) { return __reduce_add_sync(FULL, v); }
+__device__ __forceinline__ uint32_t warp_sum(uint32_t v) { return __reduce_add_sync(FULL, v); }
+__device__ __forceinline__ int32_t warp_min(int32_t v) { return __reduce_min_sync(FULL, v); }
+__device__ __forceinline__ uint32_t warp_min(uint32_t v) { return __reduce_min_sync(FULL, v); }
+__device__ __forceinline__ int32_t warp_max(int32_t v) { return __reduce_max_sync(FULL, v); }
+__device__ __forceinline__ uint32_t warp_max(uint32_t v) { return __reduce_max_sync(FULL, v); }
 // inclusive scan across the warp
 template <typename T>
 __device__ __forceinline__ T warp_incl_scan(T v) {

@@ -51,6 +51,7 @@ struct SimP {
   const int64_t* pf_tab;
   int32_t pt;
   int32_t n_lp, n_hp, K, bs, lp_max, lp_tok, hp_tok, policy, offl, tickets, elastic, drop, hist_def;
+  uint64_t bs_m;  // ceil(2^38 / bs): x / bs = (x * bs_m) >> 38 exactly for 0 <= x < 2^25 (bs <= 512)
   int32_t kv_lp, kv_hp;
   int64_t W, margin, delay;
   int32_t T;
@@ -128,7 +129,13 @@ __device__ __forceinline__ int64_t pf_of(int32_t p) {
   if (v < 0) { atomicOr(P.err, ERR_RANGE); return INT32_MAX; }
   return v;
 }
-__device__ __forceinline__ int32_t blk_of(int32_t eff) { return (eff + P.bs) / P.bs; }
+// division by the block size without a division sequence: with m = ceil(2^38 / bs) = (2^38 + e) / bs,
+// 0 <= e < bs <= 512, x * m / 2^38 = x / bs + x * e / (bs * 2^38) and x * e < 2^38 for x < 2^29, so the
+// error term stays below 1 / bs and never crosses an integer; every argument here is a token count
+// or event index below lp_token_budget + bs < 2^25 (validated), so x * m < 2^63 does not overflow
+__device__ __forceinline__ int32_t divb(int32_t x) { return (int32_t)(((uint64_t)(uint32_t)x * P.bs_m) >> 38); }
+__device__ __forceinline__ int32_t modb(int32_t x) { return x - divb(x) * P.bs; }
+__device__ __forceinline__ int32_t blk_of(int32_t eff) { return divb(eff + P.bs); }
 
 // time-invariant priority key of request gid with effective prompt eff (DESIGN.md §2 Keys)
 __device__ __forceinline__ int64_t key_of(int64_t gid, int32_t eff) {
@@ -1139,8 +1146,8 @@ __device__ __noinline__ int64_t run_decode(Wp w, int k, int64_t T_limit) {
     // ---- lane-parallel segment: events c = 0 .. Jmax-1 (no completion among them)
     while (J < Jmax) {
       const int32_t c = J + lane;
-      const int32_t cm = c % bs;
-      const int64_t need = hA[cm == 0 ? 0 : bs - cm];  // slots with (r0 + c) mod bs == 0
+      const int32_t cm = modb(c);
+      const int32_t need = hA[cm == 0 ? 0 : bs - cm];  // slots with (r0 + c) mod bs == 0
       const int64_t cum = ncarry + warp_incl_scan(need);
       const int64_t lc = lat_decode(P.md, (uint64_t)Bd, (uint64_t)(S + (int64_t)(c + 1) * Bd));
       const int64_t incl = warp_incl_scan(lc < 0 ? (int64_t)0 : lc);
@@ -1160,7 +1167,7 @@ __device__ __noinline__ int64_t run_decode(Wp w, int k, int64_t T_limit) {
     const int64_t Et = E + tcarry;  // time of event J (a completion event iff J == Jmax)
     // ---- can event J (the completion) be processed here?  Conservative KV check from the
     // histogram (finishing slots included): the main loop handles it if eviction might be needed
-    const int32_t cJ = J % bs;
+    const int32_t cJ = modb(J);
     const int64_t needJ = hA[cJ == 0 ? 0 : bs - cJ];
     const bool doC = J == Jmax && Et < T_limit && needJ <= kvf - ncarry;
     const int32_t nstep = J + (doC ? 1 : 0);
@@ -1184,10 +1191,10 @@ __device__ __noinline__ int64_t run_decode(Wp w, int k, int64_t T_limit) {
       // held after nstep completions = held_base + pend0 + #{c in [0, nstep-2] : (r0 + c) % bs == 0}
       const int32_t first = r0 == 0 ? 0 : bs - r0;
       const int32_t last = nstep - 2;
-      const int32_t grown = last >= first ? 1 + (last - first) / bs : 0;
+      const int32_t grown = last >= first ? 1 + divb(last - first) : 0;
       const int32_t held = (sl.w & HELD_MASK) + pend0 + grown;
-      const int32_t rN = (r0 + nstep) % bs;
-      const bool pend = nstep > 0 && ((r0 + nstep - 1) % bs) == 0;
+      const int32_t rN = modb(r0 + nstep);
+      const bool pend = nstep > 0 && modb(r0 + nstep - 1) == 0;
       sl.y += nstep;
       sl.z -= nstep;
       sl.w = held | (rN << R_SHIFT) | (pend ? PEND : 0);
@@ -1519,6 +1526,7 @@ asc_status launch_simulate(asc_ctx* c, const asc_traces* tr, asc_outcomes* out, 
   P.pf_tab = c->d_pf_tab;
   P.pt = c->pt_size;
   P.n_lp = cf.topo.n_lp; P.n_hp = cf.topo.n_hp; P.K = K; P.bs = cf.topo.block_tokens;
+  P.bs_m = ((uint64_t(1) << 38) + (uint64_t)P.bs - 1) / (uint64_t)P.bs;
   P.lp_max = cf.topo.lp_max_batch; P.lp_tok = cf.topo.lp_token_budget; P.hp_tok = cf.topo.hp_token_budget;
   P.policy = cf.flags.policy;
   P.offl = cf.flags.offload ? 1 : 0;    // per trace: and n_hp >= 1
