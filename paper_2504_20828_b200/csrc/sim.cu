@@ -1329,6 +1329,9 @@ __device__ __noinline__ void finish_trace(Wp w, int trace, int64_t decisions,
     for (int k = 0; k < w.K(); k++) d = mix64(d ^ w.SI()[k].hash);
     P.digest[trace] = d;
     if (P.decisions) P.decisions[trace] = decisions;
+#ifdef ASC_DEBUG_CLOCK  // experiments only: per-trace finish time (ns) in place of evaluations
+    { uint64_t tns; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tns)); evals = (int64_t)tns; }
+#endif
     if (P.evals) P.evals[trace] = evals;
   }
   __syncwarp();

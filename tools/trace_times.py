@@ -11,7 +11,7 @@ tr = asc.batch_arrays(b, "cuda:0")
 out = ctx.simulate_batch(tr)
 t = out["evaluations"][:b.T].cpu().numpy().astype(np.int64)
 d = out["decisions"][:b.T].cpu().numpy()
-t = (t - t.min()) / 1e6
+t = (t - t.min()) / 1e6  # ns -> ms after the first finisher
 order = np.argsort(-t)
 print("kernel ms", ctx.last_kernel_ms())
 for i in order[:15]:
