@@ -823,22 +823,55 @@ __global__ void __launch_bounds__(K1W * 32, ASC_K1_MINB) k1_tasks(const __grid_c
 // warp per segment, one entry per lane — a1 (table), a2 key, a3 as one 32-wide bitonic sort of
 // (key, position), a4 as a strict prefix-sum scan in sorted order, a5 ballots in position order,
 // a6 from the admitted moments.  Same outputs as k1 (SURVEY row S, 10^6 x 32).
-__global__ void __launch_bounds__(256, 6) k_small(const __grid_constant__ StepP P) {
+#ifndef ASC_KS_MINB
+#define ASC_KS_MINB 3
+#endif
+// Inputs of one short segment, loaded one segment ahead (the loop below is a chain of dependent
+// loads per segment: seg_off -> entries -> latency table; prefetching overlaps it with the work)
+struct SmallIn {
+  int64_t lo, n, dl, now, sl, tbt;
+  int32_t p, R, Bd, N, M;
+  uint32_t f;
+};
+__device__ __forceinline__ void small_load(const StepP& P, int64_t s, SmallIn& x) {
+  const int lane = lane_id();
+  x.lo = 0; x.n = -1;
+  if (s >= P.S) return;
+  x.lo = P.seg_off[s];
+  x.n = P.seg_off[s + 1] - x.lo;
+  x.dl = 0; x.p = 1; x.f = 0;
+  if (x.n > SMALL || x.n < 0) return;
+  if (lane < x.n) {
+    const int64_t e = x.lo + lane;
+    x.dl = __ldcs(P.dl + e);
+    x.p = __ldcs(P.eff + e);
+    x.f = __ldcs(P.fl + e);
+  }
+  x.now = P.now[s];
+  x.R = P.bR[s];
+  x.Bd = P.dcnt[s];
+  x.sl = P.dctx[s];
+  x.tbt = P.tbt[s];
+  x.N = P.bN[s];
+  x.M = P.bM[s];
+}
+
+__global__ void __launch_bounds__(256, ASC_KS_MINB) k_small(const __grid_constant__ StepP P) {
   const int lane = lane_id();
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t s = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; s < P.S; s += nw) {
-    const int64_t lo = P.seg_off[s], n = P.seg_off[s + 1] - lo;
+  int64_t s = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  SmallIn nx;
+  small_load(P, s, nx);
+  for (; s < P.S; s += nw) {
+    const SmallIn cu = nx;
+    small_load(P, s + nw, nx);  // next segment's inputs in flight during this one
+    const int64_t lo = cu.lo, n = cu.n;
     if (n > SMALL || n < 0) continue;  // k1's, or invalid (the planner flags it)
     const bool v = lane < n;
     const int64_t e = lo + lane;
-    int64_t dl = 0;
-    int32_t p = 1;
-    uint32_t f = 0;
-    if (v) {
-      dl = __ldcs(P.dl + e);
-      p = __ldcs(P.eff + e);
-      f = __ldcs(P.fl + e);
-    }
+    const int64_t dl = cu.dl;
+    const int32_t p = cu.p;
+    const uint32_t f = cu.f;
     bool bad = v && p < 1;
     const int64_t pf = v ? pf_of(P, p < 1 ? 1 : p) : 0;
     if (P.pfout && v) {
@@ -846,30 +879,43 @@ __global__ void __launch_bounds__(256, 6) k_small(const __grid_constant__ StepP 
       __stcs(P.pfout + e, (int32_t)pf);
     }
     if (__any_sync(FULL, bad) && lane == 0) atomicOr(P.err, ERR_INVAL);
-    const int64_t now = P.now[s];
+    const int64_t now = cu.now;
     const bool dropped = P.drop && v && !(f & 1u) && now > dl;
     // value function (FCFS: 0, ties by position); dropped and empty lanes sort last
     const int64_t key = (P.kdl ? dl : 0) + (P.kpf > 0 ? pf : (P.kpf < 0 ? -pf : 0));
-    const KI x = sort32(v && !dropped ? KI{key, lane} : ki_inf());
+    // a3: one 32-wide bitonic sort of (key, position).  Keys within 2^31 µs of the base (now for
+    // the deadline-based policies) pack with the position into one uint64 (two shuffles per step);
+    // otherwise the (int64 key, position) pairs are sorted directly.
+    const bool lv = v && !dropped;
+    const int64_t rel = key - (P.kdl ? now : 0);
+    KI x;
+    if (__all_sync(FULL, !lv || (rel >= INT32_MIN && rel <= INT32_MAX))) {
+      const uint64_t pk = lv ? ((uint64_t)((uint32_t)(int32_t)rel ^ 0x80000000u) << 32) | (uint32_t)lane : PK_INF;
+      const uint64_t y = sort32_pk(pk);
+      x.i = y == PK_INF ? INF32 : (int32_t)(uint32_t)y;
+      x.k = 0;  // unused below
+    } else {
+      x = sort32(lv ? KI{key, lane} : ki_inf());
+    }
     const bool live = x.i != INF32;
     const int src = live ? x.i : 0;
     const int32_t ps = __shfl_sync(FULL, p, src);
     const int64_t pfs = __shfl_sync(FULL, pf, src);
     const int64_t bls = live ? (int64_t)((ps + P.bs) / P.bs) : 0;
     // Algorithm 1 lines 5-13: strict budgets N (tokens), M (blocks), C (TBT residual), R (requests)
-    int64_t R = P.bR[s];
+    int64_t R = cu.R;
     if (R > ASC_MAX_BATCH) { if (lane == 0) atomicOr(P.err, ERR_RANGE); R = ASC_MAX_BATCH; }
-    const int64_t Bd = P.dcnt[s], sl = P.dctx[s];
+    const int64_t Bd = cu.Bd, sl = cu.sl;
     int64_t C = INF64;
     if (Bd > 0) {
       const int64_t d = lat_decode(P.md, (uint64_t)Bd, (uint64_t)sl);
       if (d < 0 && lane == 0) atomicOr(P.err, ERR_RANGE);
-      C = P.tbt[s] - d;
+      C = cu.tbt - d;
     }
     const int64_t St = warp_incl_scan(live ? (int64_t)ps : (int64_t)0);
     const int64_t Sb = warp_incl_scan(bls);
     const int64_t Sc = warp_incl_scan(live ? pfs : (int64_t)0);
-    const bool ok = live && St < (int64_t)P.bN[s] && Sb < (int64_t)P.bM[s] && Sc < C && lane < R;
+    const bool ok = live && St < (int64_t)cu.N && Sb < (int64_t)cu.M && Sc < C && lane < R;
     const uint32_t m = __ballot_sync(FULL, ok);
     const int k = (m == FULL) ? 32 : (__ffs(~m) - 1);
     const bool adm = lane < k;
@@ -912,6 +958,7 @@ __global__ void __launch_bounds__(WARPS * 32) k2_segments(const __grid_constant_
   __shared__ KI lists[WARPS][32 * KPL];
   __shared__ int64_t segs[WARPS * 32];
   __shared__ int nseg;
+  if (P.mtask_off[P.S] == 0) return;  // no segment has more than one task (the common case)
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // find this CTA's multi-task segments up to 256 at a time (most segments have one task or
   // none); chunks shrink with S so that few large segments still spread over the CTAs
@@ -991,6 +1038,7 @@ __global__ void __launch_bounds__(WARPS * 32) k2_segments(const __grid_constant_
 
 __global__ void __launch_bounds__(WARPS * 32) k3_expand(const __grid_constant__ StepP P) {
   __shared__ int32_t s_ring[WARPS][256];
+  if (P.mtask_off[P.S] == 0) return;  // no multi-task segment
   const int w = threadIdx.x >> 5;
   const int64_t ntasks = min(P.task_off[P.S], P.ntask_max);
   for (int64_t task = blockIdx.x * (int64_t)WARPS + w; task < ntasks;
@@ -1132,7 +1180,7 @@ asc_status launch_schedule_step(asc_ctx* c, const asc_step_in* in, asc_step_out*
   launches += 1;
   {  // short segments (after k1's timed bracket: k1 is the roofline kernel of row S's big shape)
     int64_t gs = ((int64_t)S * 32 + 255) / 256;
-    gs = gs < (int64_t)dev_sms * 8 ? gs : (int64_t)dev_sms * 8;
+    gs = gs < (int64_t)dev_sms * ASC_KS_MINB ? gs : (int64_t)dev_sms * ASC_KS_MINB;  // one resident wave
     k_small<<<(unsigned)(gs > 0 ? gs : 1), 256, 0, sm>>>(P);
     launches += 1;
   }
