@@ -200,6 +200,29 @@ def step_microbench(asc, torch, dev, stream, warmup, steps, hbm_peak):
     byts = 13 * Q + 4 * nout + S * (8 * 4 + 4 * 6) + 8
     k1ms = float(np.mean(k1))
     ctx.close()
+    others = []
+    for S2, Q2 in ((64, 1_000_000), (1_000_000, 32)):  # the other two row-S shapes
+        ins2 = H.random_step_inputs(np.random.default_rng(123), S2, 0, cfg, qs=np.full(S2, Q2))
+        d2 = {k: torch.from_numpy(np.ascontiguousarray(v)).to(dev) for k, v in ins2.items()}
+        d2["Q"] = S2 * Q2
+        c2 = asc.Context(cfg, dev.index, stream)
+        for _ in range(warmup):
+            o2 = c2.schedule_step(d2, want_prefill=False)
+        torch.cuda.synchronize()
+        e0.record(stream)
+        for _ in range(steps):
+            o2 = c2.schedule_step(d2, want_prefill=False)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms2 = e0.elapsed_time(e1) / steps
+        n2 = int(o2["admit_cnt"].sum() + o2["offload_cnt"].sum() + o2["drop_cnt"].sum())
+        b2 = 13 * S2 * Q2 + 4 * n2 + S2 * (8 * 4 + 4 * 6) + 8
+        c2.close()
+        others.append({"shape": f"S={S2} segments x Q={Q2} entries", "ms_per_call": ms2,
+                       "evaluations_per_s": S2 * Q2 / (ms2 * 1e-3),
+                       "whole_call_achieved_gbs": b2 / (ms2 * 1e-3) / 1e9,
+                       "whole_call_frac": b2 / (ms2 * 1e-3) / 1e9 / hbm_peak})
+        del d2, o2
     ach_k1 = byts / (k1ms * 1e-3) / 1e9     # single-task segments: k1 does all reads and writes
     ach_call = byts / (ms * 1e-3) / 1e9
     return {"shape": f"S={S} segments x Q={Qs} entries", "entries": Q,
@@ -210,7 +233,8 @@ def step_microbench(asc, torch, dev, stream, warmup, steps, hbm_peak):
                          "kernel": "k1_tasks (streaming pass; finishes every single-task segment)",
                          "algorithmic_bytes": byts, "kernel_ms": k1ms, "kernel_share": k1ms / ms},
             "whole_call": {"achieved": ach_call, "unit": "GB/s", "frac": ach_call / hbm_peak,
-                           "note": "asc_schedule_step incl. planner launch and the error sync"}}
+                           "note": "asc_schedule_step incl. planner launch and the error sync"},
+            "other_shapes": others}
 
 
 def main():
