@@ -191,7 +191,7 @@ def step_microbench(asc, torch, dev, stream, warmup, steps, hbm_peak):
     k1 = []
     e0.record(stream)
     for _ in range(steps):
-        out = ctx.schedule_step(dins, want_prefill=False)
+        out = ctx.schedule_step(dins, want_prefill=False, out=out)
         k1.append(ctx.last_kernel_ms())
     e1.record(stream)
     torch.cuda.synchronize()
@@ -211,7 +211,7 @@ def step_microbench(asc, torch, dev, stream, warmup, steps, hbm_peak):
         torch.cuda.synchronize()
         e0.record(stream)
         for _ in range(steps):
-            o2 = c2.schedule_step(d2, want_prefill=False)
+            o2 = c2.schedule_step(d2, want_prefill=False, out=o2)
         e1.record(stream)
         torch.cuda.synchronize()
         ms2 = e0.elapsed_time(e1) / steps
@@ -321,7 +321,8 @@ def main():
         "roofline": {"bound": "hbm", "achieved": ach, "peak": hbm_peak, "unit": "GB/s",
                      "frac": ach / hbm_peak, "traffic": ncu_traffic("sim_kernel"),
                      "kernel": "sim_kernel (event loop)", "peak_source": peak_src,
-                     "note": "latency-bound sequential event chain per trace (DESIGN.md §8); "
+                     "note": "not HBM-bound: a sequential event chain per trace, instruction-fetch "
+                             "bound (ncu no_instruction stalls, profiles/r01f_sim_kernel_ncu_full.md); "
                              "traffic is register-spill / call-save stack traffic, not data",
                      "algorithmic_bytes": algo, "kernel_ms": sim_ms,
                      "kernel_share": sim_ms / ms_step},

@@ -238,18 +238,20 @@ class Context:
     def last_kernel_ms(self):
         return asc_last_kernel_ms(self.h)
 
-    def schedule_step(self, ins, want_prefill=True):
-        """ins: dict of arrays (all torch CUDA or all numpy).  Returns dict of outputs."""
+    def schedule_step(self, ins, want_prefill=True, out=None):
+        """ins: dict of arrays (all torch CUDA or all numpy).  Returns dict of outputs; `out` (a
+        previous call's result for the same shape) is reused instead of allocating."""
         dev = not isinstance(ins["seg_off"], np.ndarray)
         S = len(ins["seg_off"]) - 1
         Q = int(ins["Q"]) if "Q" in ins else int(ins["seg_off"][-1])
-        out = _alloc(dev, self.device, dict(admit_idx=(Q, "i4"), admit_cnt=(S, "i4"),
-                                            offload_idx=(Q, "i4"), offload_cnt=(S, "i4"),
-                                            drop_idx=(Q, "i4"), drop_cnt=(S, "i4"),
-                                            batch_lat_us=(S, "i8"),
-                                            prefill_us=(Q if want_prefill else 0, "i4")))
-        if not want_prefill:
-            out["prefill_us"] = None
+        if out is None:
+            out = _alloc(dev, self.device, dict(admit_idx=(Q, "i4"), admit_cnt=(S, "i4"),
+                                                offload_idx=(Q, "i4"), offload_cnt=(S, "i4"),
+                                                drop_idx=(Q, "i4"), drop_cnt=(S, "i4"),
+                                                batch_lat_us=(S, "i8"),
+                                                prefill_us=(Q if want_prefill else 0, "i4")))
+            if not want_prefill:
+                out["prefill_us"] = None
         asc_schedule_step(self.h, ins["seg_off"], ins["now_us"], ins["deadline_us"],
                           ins["eff_prompt"], ins["flags"], ins["dec_count"], ins["dec_ctx_sum"],
                           ins["tbt_slo_us"], ins["budget_tokens"], ins["budget_blocks"],
