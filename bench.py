@@ -110,9 +110,9 @@ def load(name, rank, world, n, traces):
         return cfg, b, desc
     if name == "config5":   # 65536 traces x 100k sharded i = rank mod world
         cfg, full = P.workload("config5", n=1, max_traces=traces)
-        idx = list(range(rank, full.T, world))
-        cfg, b = P.workload("config5", n=n or 100_000, max_traces=traces)
-        return cfg, b.subset(idx), f"config5 shard {rank}/{world}"
+        idx = list(range(rank, full.T, world))   # only this rank's grid points are generated
+        cfg, b = P.workload("config5", n=n or 100_000, max_traces=traces, select=idx)
+        return cfg, b, f"config5 shard {rank}/{world}"
     if name in ("config1", "config2", "config4"):
         cfg, b = P.workload(name, n=n, max_traces=traces, base_seed=1 + rank)
         return cfg, b, name

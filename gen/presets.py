@@ -56,8 +56,9 @@ def config(arch=None, perf=None, topo=None, flg=None):
 SLO = {"sharegpt": (1_000_000, 150_000), "longbench": (2_500_000, 150_000)}
 
 
-def workload(name, n=None, max_traces=None, base_seed=1):
-    """BASELINE.json configs -> (asc config dict, TraceBatch).  DESIGN.md §Workloads."""
+def workload(name, n=None, max_traces=None, base_seed=1, select=None):
+    """BASELINE.json configs -> (asc config dict, TraceBatch).  DESIGN.md §Workloads.
+    select: optional grid-point indices (e.g. one rank's shard), generated alone and in that order."""
     if name == "config1":      # 1 trace, 1L1H, 200 req, QPS 2
         cfg = config(topo=topology(n_lp=1, n_hp=1))
         pts = [(0, 16, 16, 16)]
@@ -95,5 +96,7 @@ def workload(name, n=None, max_traces=None, base_seed=1):
         raise KeyError(name)
     if max_traces is not None:
         pts = pts[:max_traces]
+    if select is not None:
+        pts = [pts[int(i)] for i in select]
     ttft, tbt = SLO[shape]
     return cfg, _tr.grid_batch(pts, n, shape, ttft, tbt, base_seed)
