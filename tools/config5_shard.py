@@ -27,6 +27,7 @@ for rep in range(2):
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     ctx.simulate_batch(tr, out=out)
+    sim_ms = ctx.last_kernel_ms()
     good, total = ctx.goodput(tr, out)
     e1.record()
     torch.cuda.synchronize()
@@ -36,7 +37,7 @@ for rep in range(2):
     fin = int((st != 0).sum())
     g = int(good[:b.T].cpu().numpy().view(np.uint64).sum())
     tot = int(total[:b.T].cpu().numpy().view(np.uint64).sum())
-    print(f"  step {ms:.0f} ms (sim kernel {ctx.last_kernel_ms():.0f} ms): {dec / ms * 1e3:.3e} decisions/s, "
+    print(f"  step {ms:.0f} ms (sim kernel {sim_ms:.0f} ms): {dec / ms * 1e3:.3e} decisions/s, "
           f"{fin / ms * 1e3:.3e} simulated req/s, goodput {g}/{tot}", flush=True)
 if n_or > 0:
     from oracle import oracle as O
