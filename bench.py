@@ -328,6 +328,18 @@ def main():
                      "kernel_share": sim_ms / ms_step},
         "clocks": clocks,
     }
+    inst = ncu_traffic("sim_kernel_inst") if (a.workload == "config3" and a.requests is None
+                                              and a.traces is None and rank == 0) else None
+    if inst:  # the bound that applies to the event loop: instruction issue
+        sms = torch.cuda.get_device_properties(dev).multi_processor_count
+        mhz = clocks.get("sm_max_mhz") or 1965.0
+        ipk = 4 * sms * mhz * 1e6          # 4 schedulers per SM, 1 warp-instruction per cycle each
+        ach_i = inst / (sim_ms * 1e-3)
+        line["issue_roofline"] = {"bound": "issue", "achieved": ach_i, "peak": ipk, "unit": "warp-inst/s",
+                                  "frac": ach_i / ipk, "inst_per_launch": inst,
+                                  "source": "smsp__inst_executed.sum of one config-3 launch (ncu, "
+                                            "profiles/ncu_traffic.json) over the live kernel time; peak = "
+                                            "4 schedulers x SMs x max SM clock"}
     if rank == 0 and not a.no_step_bench:
         line["step_microbench"] = step_microbench(asc, torch, dev, stream, 2, max(3, a.steps), hbm_peak)
     if not a.no_e2e:

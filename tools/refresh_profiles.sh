@@ -9,7 +9,7 @@ tail -c 3000 gpurun_out/${tag}_bench.json
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
   --log-file gpurun_out/${tag}_launches.csv python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-e2e --no-baselines --no-fit-bench \
   > gpurun_out/${tag}_launches_bench.log 2>&1
-timeout 900 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum \
+timeout 900 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum,smsp__inst_executed.sum \
   --clock-control none -k regex:sim_kernel -c 1 --csv --log-file gpurun_out/${tag}_sim_dram.csv \
   python tools/profile_run.py sim --traces 4096 --n 10000 --reps 1 > gpurun_out/${tag}_sim_dram.log 2>&1
 timeout 600 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum \
