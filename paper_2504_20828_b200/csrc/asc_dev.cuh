@@ -352,6 +352,20 @@ __device__ __forceinline__ uint64_t pk_keep(uint64_t v, uint64_t o, bool keep_mi
   return ((o < v) == keep_min) ? o : v;
 }
 
+__device__ __forceinline__ uint32_t sort32_u32(uint32_t v) {  // ascending by lane
+  const int l = lane_id();
+#pragma unroll
+  for (int k = 2; k <= 32; k <<= 1) {
+#pragma unroll
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      const uint32_t o = __shfl_xor_sync(FULL, v, j);
+      const bool keep_min = ((l & j) == 0) == ((l & k) == 0);
+      v = ((o < v) == keep_min) ? o : v;
+    }
+  }
+  return v;
+}
+
 __device__ __forceinline__ uint64_t sort32_pk(uint64_t v) {
   const int l = lane_id();
 #pragma unroll

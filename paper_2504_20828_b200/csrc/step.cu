@@ -889,7 +889,13 @@ __global__ void __launch_bounds__(256, ASC_KS_MINB) k_small(const __grid_constan
     const bool lv = v && !dropped;
     const int64_t rel = key - (P.kdl ? now : 0);
     KI x;
-    if (__all_sync(FULL, !lv || (rel >= INT32_MIN && rel <= INT32_MAX))) {
+    if (__all_sync(FULL, !lv || (rel >= -(int64_t(1) << 26) && rel < (int64_t(1) << 26)))) {
+      // keys within 2^26 µs of the base: (key, position) in one uint32 (one shuffle per step)
+      const uint32_t pk = lv ? ((uint32_t)(rel + (int64_t(1) << 26)) << 5) | (uint32_t)lane : 0xffffffffu;
+      const uint32_t y = sort32_u32(pk);
+      x.i = y == 0xffffffffu ? INF32 : (int32_t)(y & 31u);
+      x.k = 0;  // unused below
+    } else if (__all_sync(FULL, !lv || (rel >= INT32_MIN && rel <= INT32_MAX))) {
       const uint64_t pk = lv ? ((uint64_t)((uint32_t)(int32_t)rel ^ 0x80000000u) << 32) | (uint32_t)lane : PK_INF;
       const uint64_t y = sort32_pk(pk);
       x.i = y == PK_INF ? INF32 : (int32_t)(uint32_t)y;
@@ -901,7 +907,7 @@ __global__ void __launch_bounds__(256, ASC_KS_MINB) k_small(const __grid_constan
     const int src = live ? x.i : 0;
     const int32_t ps = __shfl_sync(FULL, p, src);
     const int64_t pfs = __shfl_sync(FULL, pf, src);
-    const int64_t bls = live ? (int64_t)((ps + P.bs) / P.bs) : 0;
+    const int64_t bls = live ? (int64_t)(((uint32_t)ps + (uint32_t)P.bs) / (uint32_t)P.bs) : 0;  // ps < 2^31
     // Algorithm 1 lines 5-13: strict budgets N (tokens), M (blocks), C (TBT residual), R (requests)
     int64_t R = cu.R;
     if (R > ASC_MAX_BATCH) { if (lane == 0) atomicOr(P.err, ERR_RANGE); R = ASC_MAX_BATCH; }
@@ -926,7 +932,7 @@ __global__ void __launch_bounds__(256, ASC_KS_MINB) k_small(const __grid_constan
       const uint64_t q = (uint64_t)ps;
       sp = q;
       sp2 = q * q;
-      spc = q * ceil_div_u(q, P.md.b);
+      spc = q * (uint64_t)(((uint32_t)ps + (uint32_t)P.md.b - 1u) / (uint32_t)P.md.b);  // ps < 2^31, b small
     }
     if (k > 0) {
       sp = warp_sum(sp);
