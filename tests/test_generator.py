@@ -43,3 +43,16 @@ def test_workloads_valid():
         assert np.all(b.prompt_len.astype(np.int64) + b.output_len <= t["lp_token_budget"])
     cfg, b = P.workload("config3", n=10)
     assert b.T == 4096 and len(set(zip(b.qps_j, b.ttft_slo_us))) == 256
+
+
+def test_select_generates_a_shard_alone():
+    """workload(select=) (bench.py's config-5 shards) equals subsetting the full grid."""
+    from paper_2504_20828_b200 import dist as D
+    cfg, full = P.workload("config5", n=40, max_traces=64)
+    for r, W in ((0, 4), (3, 4), (1, 7)):
+        idx = D.shard(full.T, r, W)
+        _, sub = P.workload("config5", n=40, max_traces=64, select=idx)
+        ref = full.subset(idx)
+        for k in ("trace_off", "arrival_us", "prompt_len", "output_len", "ttft_slo_us", "tbt_slo_us", "qps_j"):
+            assert np.array_equal(getattr(sub, k), getattr(ref, k)), k
+        assert sub.labels == ref.labels
