@@ -159,6 +159,18 @@ def test_many_tiny_segments(asc, oracle):
     compare(run_gpu(asc, cfg, ins), oracle.schedule_step(cfg, **ins), ins["seg_off"])
 
 
+@pytest.mark.parametrize("spread_us", [3 * 10 ** 6, 10 ** 9, 10 ** 11])
+@pytest.mark.parametrize("policy", ["EDF_LAXITY", "FCFS", "SJF"])
+def test_small_segment_key_windows(asc, oracle, spread_us, policy):
+    # k_small sorts (key - now, position) packed in 32 bits when every key lies within 2^26 us of
+    # now, in 64 bits within 2^31 us, else as (int64 key, position): all three must agree
+    rng = np.random.default_rng(31)
+    cfg = P.config(flg=P.flags(policy=policy, drop=1))
+    qs = rng.integers(0, 33, size=3000)
+    ins = H.random_step_inputs(rng, 3000, 0, cfg, qs=qs, now_spread_us=spread_us)
+    compare(run_gpu(asc, cfg, ins), oracle.schedule_step(cfg, **ins), ins["seg_off"])
+
+
 def test_errors(asc):
     rng = np.random.default_rng(5)
     cfg = P.config()
