@@ -100,6 +100,22 @@ def test_config2_reduced(asc, oracle):
     assert_parity(oracle, cfg, b, gpu_sim(asc, cfg, b))
 
 
+def test_config2_full(asc, oracle):
+    # BASELINE config 2 at its full size: 8 traces (QPS 1..8) x 10,000 requests, 2 LP + 1 HP
+    cfg, b = P.workload("config2")
+    assert b.T == 8 and b.R == 80_000
+    assert_parity(oracle, cfg, b, gpu_sim(asc, cfg, b))
+
+
+def test_config4_prefix_50k(asc, oracle):
+    # BASELINE config 4's oracle scope: the first 50,000 requests of the
+    # LongBench-shaped 1M-request trace at ~2x saturation, deep queues throughout
+    cfg, b = P.workload("config4", n=50_000)
+    got = gpu_sim(asc, cfg, b)
+    assert int(got["evaluations"][0]) > 10 * int(got["decisions"][0])
+    assert_parity(oracle, cfg, b, got)
+
+
 def test_config3_subgrid(asc, oracle):
     cfg, b = P.workload("config3", n=600)
     sub = b.subset(range(0, 4096, 16))          # every 16th grid point: all QPS x SLO scales
