@@ -159,3 +159,13 @@ def test_sarathi_longbench_prefix(asc, oracle):
     cfg["topo"]["n_lp"] = 3
     cfg["flags"]["chunk_tokens"] = 2048
     assert_parity(oracle, cfg, b, gpu_sim(asc, cfg, b))
+
+
+@pytest.mark.parametrize("sched", ["vllm", "sarathi"])
+def test_baselines_config2_full(asc, oracle, sched):
+    # BASELINE config 2 at full size (8 traces, QPS 1..8, 10k requests each) on the paper's three
+    # homogeneous instances, both baseline schedulers
+    cfg, b = P.workload("config2")
+    cfg = SC.with_scheduler(cfg, sched)
+    cfg["topo"]["n_lp"] = 3
+    assert_parity(oracle, cfg, b, gpu_sim(asc, cfg, b))
