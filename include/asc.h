@@ -265,6 +265,22 @@ typedef struct {
 asc_status asc_fit_perf(asc_ctx* ctx, const asc_fit_in* in, double lambda, double* coef,
                         double* mean_err, double* max_err);
 
+/* ---------------------------------------------------------------------------------------------
+ * asc_latency — the performance model's latency of n batches given their exact costs (rows
+ * a1/a6, the evaluation every formation makes).  PAPER P:273-277 (Eq. 4-5: t = C1(tM + tF) +
+ * C2 max(tM, tF) + C3 tM + C4 tF + C5 with tM = M / M_H, tF = F / F_H), readings G17 (clamp at 0,
+ * S:187; at least 1 µs) and G18 (ceil to integer microseconds).  For i < n:
+ *     t_s[i]    = max(0, t(F[i], M[i]))      seconds, every fp64 op round-to-nearest in the order
+ *                                            above, no contraction (bitwise reproducible)
+ *     lat_us[i] = max(1, ceil(t_s[i] * 1e6))
+ * with the ctx's perf coefficients and caps.  F[i] (flops) and M[i] (bytes) as the cost model
+ * gives them (App. A; exact integers).  t_s may be NULL.  Arrays: all device pointers or all host
+ * pointers (host arrays are staged).  Errors: ASC_E_INVAL (NULL arrays, n < 0, mixed pointer
+ * kinds), ASC_E_RANGE (some F[i] or M[i] >= 2^53: the int -> double conversion would round;
+ * lat_us[i] = -1 there). */
+asc_status asc_latency(asc_ctx* ctx, int64_t n, const uint64_t* F, const uint64_t* M, int64_t* lat_us,
+                       double* t_s);
+
 #ifdef __cplusplus
 }
 #endif

@@ -199,6 +199,16 @@ extern "C" int64_t or_latency_us(const or_perf* pf, uint64_t F, uint64_t M) {
   return v < 1 ? 1 : v;
 }
 
+// Test convenience: or_latency_s / or_latency_us over n (F, M) pairs (a plain loop; no new
+// arithmetic).  t may be NULL.
+extern "C" void or_latency_n(const or_perf* pf, int64_t n, const uint64_t* F, const uint64_t* M,
+                             int64_t* lat_us, double* t) {
+  for (int64_t i = 0; i < n; i++) {
+    lat_us[i] = or_latency_us(pf, F[i], M[i]);
+    if (t) t[i] = or_latency_s(pf, F[i], M[i]);
+  }
+}
+
 extern "C" int64_t or_batch_us(const or_arch* a, const or_perf* pf, int32_t np,
                                const int64_t* p, int32_t nd, const int64_t* lhat) {
   uint64_t F, M;

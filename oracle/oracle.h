@@ -50,6 +50,9 @@ int or_cost_chunked(const or_arch* a, int32_t nc, const int64_t* l, const int64_
 double or_latency_s(const or_perf* pf, uint64_t F, uint64_t M);
 /* G18/G17: integer microseconds = max(1, ceil(t * 1e6)). */
 int64_t or_latency_us(const or_perf* pf, uint64_t F, uint64_t M);
+/* or_latency_us (and, if t != NULL, or_latency_s) of n (F, M) pairs; a loop for the tests. */
+void or_latency_n(const or_perf* pf, int64_t n, const uint64_t* F, const uint64_t* M,
+                  int64_t* lat_us, double* t);
 /* Convenience: latency of a batch in microseconds (or -1 on range error). */
 int64_t or_batch_us(const or_arch* a, const or_perf* pf, int32_t np, const int64_t* p,
                     int32_t nd, const int64_t* lhat);

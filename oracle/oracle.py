@@ -133,6 +133,19 @@ def latency_us(perf, F, M):
     return lib().or_latency_us(C.byref(ps), C.c_uint64(F), C.c_uint64(M))
 
 
+def latency_n(perf, F, M):
+    """(lat_us int64 [n], t seconds float64 [n]) of n (F, M) pairs via or_latency_n."""
+    F = np.ascontiguousarray(F, dtype=np.uint64)
+    M = np.ascontiguousarray(M, dtype=np.uint64)
+    n = len(F)
+    lat = np.zeros(n, np.int64)
+    t = np.zeros(n, np.float64)
+    ps = perf_s(perf)
+    lib().or_latency_n(C.byref(ps), C.c_int64(n), F.ctypes.data_as(C.c_void_p), M.ctypes.data_as(C.c_void_p),
+                       lat.ctypes.data_as(C.c_void_p), t.ctypes.data_as(C.c_void_p))
+    return lat, t
+
+
 def batch_us(arch, perf, p, lhat=()):
     pa, pp = _p(p, np.int64)
     la, lp = _p(lhat, np.int64)

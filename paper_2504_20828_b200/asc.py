@@ -19,7 +19,7 @@ ASC_MAX_INSTANCES = 16
 STATUS = {0: "ASC_OK", 1: "ASC_E_INVAL", 2: "ASC_E_CONFIG", 3: "ASC_E_NOMEM", 4: "ASC_E_CUDA",
           5: "ASC_E_EMPTY", 6: "ASC_E_RANGE", 7: "ASC_E_INVARIANT"}
 EXPORTS = ("asc_create", "asc_destroy", "asc_last_error", "asc_abi_version", "asc_schedule_step",
-           "asc_simulate_batch", "asc_goodput", "asc_fit_perf", "asc_last_kernel_launches",
+           "asc_simulate_batch", "asc_goodput", "asc_fit_perf", "asc_latency", "asc_last_kernel_launches",
            "asc_last_kernel_ms")
 
 
@@ -108,6 +108,8 @@ def lib():
         L.asc_fit_perf.argtypes = [C.c_void_p, C.POINTER(asc_fit_in), C.c_double, C.c_void_p,
                                    C.c_void_p, C.c_void_p]
         L.asc_fit_perf.restype = C.c_int
+        L.asc_latency.argtypes = [C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
+        L.asc_latency.restype = C.c_int
         L.asc_last_kernel_launches.argtypes = [C.c_void_p]
         L.asc_last_kernel_launches.restype = C.c_int64
         L.asc_last_kernel_ms.argtypes = [C.c_void_p]
@@ -212,6 +214,11 @@ def asc_fit_perf(ctx, rec_off, F, M, y, lam, coef, mean_err=None, max_err=None, 
                                    _ptr(max_err)), "asc_fit_perf")
 
 
+def asc_latency(ctx, F, M, lat_us, t_s=None, n=None):
+    n = len(F) if n is None else n
+    _check(ctx, lib().asc_latency(ctx, C.c_int64(n), _ptr(F), _ptr(M), _ptr(lat_us), _ptr(t_s)), "asc_latency")
+
+
 # ------------------------------------------------------------------ convenience (allocation) --
 class Context:
     """Owns a ctx; allocates outputs as torch CUDA tensors (device path) or numpy (host path)."""
@@ -307,6 +314,25 @@ class Context:
         asc_fit_perf(self.h, rec["off"], rec["F"], rec["M"], rec["y"], lam, coef, me, mx, N=N)
         coef = coef[:5 * G].reshape(G, 5)
         return coef, (me[:G] if errors else None), (mx[:G] if errors else None)
+
+
+def _latency_method(self, F, M, want_t=True):
+    """Eq. 4-5 latency of n batches from their (F, M) (uint64 numpy, or int64/uint64 torch CUDA
+    tensors) -> (lat_us int64 [n], t_s float64 [n] or None), same kind as the input."""
+    dev = not isinstance(F, np.ndarray)
+    n = len(F)
+    if dev:
+        import torch
+        lat = torch.empty(max(n, 1), dtype=torch.int64, device=f"cuda:{self.device}")
+        ts = torch.empty(max(n, 1), dtype=torch.float64, device=f"cuda:{self.device}") if want_t else None
+    else:
+        lat = np.zeros(max(n, 1), np.int64)
+        ts = np.zeros(max(n, 1), np.float64) if want_t else None
+    asc_latency(self.h, F, M, lat, ts, n=n)
+    return lat[:n], (ts[:n] if want_t else None)
+
+
+Context.latency = _latency_method
 
 
 def _alloc(dev, device, spec):

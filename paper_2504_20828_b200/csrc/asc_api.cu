@@ -520,6 +520,39 @@ asc_status asc_fit_perf(asc_ctx* c, const asc_fit_in* in, double lambda, double*
   return cuda_check(c, sg.download(), "asc_fit_perf: download");
 }
 
+asc_status asc_latency(asc_ctx* c, int64_t n, const uint64_t* F, const uint64_t* M, int64_t* lat_us,
+                       double* t_s) {
+  if (!c) return fail(c, ASC_E_INVAL, "asc_latency: NULL context");
+  c->err.clear();
+  c->timed = false;
+  if (n < 0) return fail(c, ASC_E_INVAL, "asc_latency: n < 0");
+  if (n == 0) { c->last_kernel_launches = 0; return ASC_OK; }
+  if (!F || !M || !lat_us) return fail(c, ASC_E_INVAL, "asc_latency: NULL array");
+  cudaSetDevice(c->device);
+  const int kind = ptr_kind(F);
+  if (!same_kind(kind, {M, lat_us, t_s})) return fail(c, ASC_E_INVAL, "asc_latency: host and device pointers mixed");
+  asc_status st;
+  if (kind == 1) {
+    st = launch_latency(c, n, F, M, lat_us, t_s);
+    if (st) return st;
+    return collect_errors(c, "asc_latency");
+  }
+  const size_t nn = (size_t)n;
+  st = ensure_stage(c, rup(8 * nn) * 4 + 4096);
+  if (st) return st;
+  Stager sg{c};
+  sg.base = c->stage;
+  const uint64_t* dF = sg.up(F, nn);
+  const uint64_t* dM = sg.up(M, nn);
+  int64_t* dl = sg.out(lat_us, nn);
+  double* dt = sg.out(t_s, nn);
+  st = launch_latency(c, n, dF, dM, dl, dt);
+  if (st) return st;
+  st = collect_errors(c, "asc_latency");
+  if (st) return st;
+  return cuda_check(c, sg.download(), "asc_latency: download");
+}
+
 int64_t asc_last_kernel_launches(const asc_ctx* c) { return c ? c->last_kernel_launches : 0; }
 
 double asc_last_kernel_ms(const asc_ctx* c) {

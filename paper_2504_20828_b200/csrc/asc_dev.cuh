@@ -39,7 +39,8 @@ struct Model {
 // Eq. 4-5 + G17/G18 from exact integer F, M (< 2^53): fixed fp64 RN order, ceil to microseconds.
 // Out of line: the two correctly rounded divisions expand to a long sequence, and one copy keeps
 // the event-loop kernel inside the instruction cache.
-static __device__ __noinline__ int64_t lat_from_FM(const Model& md, uint64_t F, uint64_t M) {
+// Eq. 4-5 in seconds, clamped at 0: the value lat_from_FM rounds.
+static __device__ __forceinline__ double t_from_FM(const Model& md, uint64_t F, uint64_t M) {
   const double tM = __ddiv_rn(__ull2double_rn(M), md.MH);
   const double tF = __ddiv_rn(__ull2double_rn(F), md.FH);
   const double mx = (tM > tF) ? tM : tF;
@@ -49,8 +50,14 @@ static __device__ __noinline__ int64_t lat_from_FM(const Model& md, uint64_t F, 
   t = __dadd_rn(t, __dmul_rn(md.c3, tF));
   t = __dadd_rn(t, md.c4);
   if (!(t > 0.0)) t = 0.0;
+  return t;
+}
+__device__ __forceinline__ int64_t us_of_t(double t) {  // G18 + G17
   const int64_t v = (int64_t)ceil(__dmul_rn(t, 1e6));
   return v < 1 ? 1 : v;
+}
+static __device__ __noinline__ int64_t lat_from_FM(const Model& md, uint64_t F, uint64_t M) {
+  return us_of_t(t_from_FM(md, F, M));
 }
 
 // Decode-only batch of B_d requests with context sum sl (a2's TBT term, a6 for decode steps).

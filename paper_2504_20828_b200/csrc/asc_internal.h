@@ -54,6 +54,8 @@ asc_status launch_goodput(asc_ctx* c, const asc_traces* tr, const asc_outcomes* 
                           uint64_t* good, uint64_t* total);
 asc_status launch_fit(asc_ctx* c, const asc_fit_in* in, int64_t N, double lambda, double* coef,
                       double* mean_err, double* max_err);
+asc_status launch_latency(asc_ctx* c, int64_t n, const uint64_t* F, const uint64_t* M, int64_t* lat,
+                          double* ts);
 asc_status ensure_ws(asc_ctx* c, size_t bytes);
 asc_status fail(asc_ctx* c, asc_status s, const std::string& msg);
 asc_status cuda_check(asc_ctx* c, cudaError_t e, const char* what);

@@ -248,9 +248,46 @@ __global__ void fit_resid_final(const __grid_constant__ FitP p) {
   if (p.max_err) p.max_err[g] = m;
 }
 
+// asc_latency: Eq. 4-5 (+ G17/G18) per (F, M) pair, the same t_from_FM the schedulers use.  16 B in,
+// 8 (+8) B out per pair; grid-stride over a resident grid.
+__global__ void __launch_bounds__(256) latency_kernel(Model md, int64_t n, const uint64_t* __restrict__ F,
+                                                      const uint64_t* __restrict__ M, int64_t* __restrict__ lat,
+                                                      double* __restrict__ ts, int* err) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t f = __ldcs(F + i), m = __ldcs(M + i);
+    if (f >= TWO53 || m >= TWO53) {  // int -> double would not be exact
+      atomicOr(err, ERR_RANGE);
+      lat[i] = -1;
+      if (ts) ts[i] = 0.0;
+      continue;
+    }
+    const double t = t_from_FM(md, f, m);
+    __stcs(lat + i, (long long)us_of_t(t));
+    if (ts) __stcs(ts + i, t);
+  }
+}
+
 }  // namespace
 
 namespace asc {
+
+asc_status launch_latency(asc_ctx* c, int64_t n, const uint64_t* F, const uint64_t* M, int64_t* lat,
+                          double* ts) {
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
+  int64_t grid = (n + 255) / 256;
+  if (grid > (int64_t)sms * 8) grid = (int64_t)sms * 8;
+  int64_t launches = 0;
+  if (n > 0) {
+    cudaEventRecord(c->ev0, c->stream);
+    latency_kernel<<<(unsigned)grid, 256, 0, c->stream>>>(c->md, n, F, M, lat, ts, c->d_err);
+    cudaEventRecord(c->ev1, c->stream);
+    c->timed = true;
+    launches++;
+  }
+  c->last_kernel_launches = launches;
+  return cuda_check(c, cudaGetLastError(), "latency launch");
+}
 
 asc_status launch_fit(asc_ctx* c, const asc_fit_in* in, int64_t N, double lambda, double* coef,
                       double* mean_err, double* max_err) {

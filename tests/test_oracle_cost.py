@@ -133,3 +133,15 @@ def test_range_guard(oracle):
     a = dict(P.MISTRAL7B, L=10 ** 6)
     assert oracle.cost(a, [32768])[2] == 1
     assert oracle.cost(P.MISTRAL7B, [32768])[2] == 0
+
+
+def test_latency_batch_wrapper(oracle):
+    # or_latency_n is a loop over or_latency_us / or_latency_s (the GPU latency test's reference)
+    rng = np.random.default_rng(8)
+    pf = dict(c=(0.1, 0.9, 0.05, -0.02, 3e-4), F_H=312e12, M_H=2e12)
+    F = (2.0 ** rng.uniform(0, 53, 500)).astype(np.uint64)
+    M = (2.0 ** rng.uniform(0, 53, 500)).astype(np.uint64)
+    lat, t = oracle.latency_n(pf, F, M)
+    for i in range(500):
+        assert lat[i] == oracle.latency_us(pf, int(F[i]), int(M[i]))
+        assert t[i] == oracle.latency_s(pf, int(F[i]), int(M[i]))
