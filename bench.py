@@ -134,7 +134,8 @@ def cpu_baseline(cfg, batch, budget_s=20.0):
     return {"value": dec / dt, "unit": UNIT, "cores": min(cores, len(idx)), "kind": "oracle",
             "sample": f"{len(idx)} of {T} traces (stratified over the QPS x SLO grid), "
                       f"{sub.R} requests, {dec} decisions in {dt:.2f} s",
-            "simulated_req_per_s": sub.R / dt, "seconds": dt}
+            "simulated_req_per_s": sub.R / dt,
+            "evaluations_per_s": int(out["evaluations"].sum()) / dt, "seconds": dt}
 
 
 def reference_arm(a):
