@@ -93,7 +93,7 @@ __global__ void plan_counts(StepP P) {
 }
 
 // block-local exclusive scan of (a, b) over tiles of SCAN_TILE; tile totals to tmp
-__global__ void scan_tiles(int64_t* a, int64_t* b, int64_t n, int64_t* tmp) {
+__global__ void __launch_bounds__(SCAN_THREADS) scan_tiles(int64_t* a, int64_t* b, int64_t n, int64_t* tmp) {
   __shared__ int64_t sa[SCAN_THREADS / 32], sb[SCAN_THREADS / 32];
   const int64_t base = blockIdx.x * (int64_t)SCAN_TILE + threadIdx.x * SCAN_ITEMS;
   int64_t va[SCAN_ITEMS], vb[SCAN_ITEMS], ta = 0, tb = 0;
@@ -1167,6 +1167,10 @@ asc_status launch_schedule_step(asc_ctx* c, const asc_step_in* in, asc_step_out*
     fill_task_seg<<<(unsigned)(gf < 4 * dev_sms ? (gf > 0 ? gf : 1) : 4 * dev_sms), 256, 0, sm>>>(P);
     launches += 5;
   }
+  {  // a planner that failed to launch must not leave k1 reading an unscanned task map
+    const cudaError_t pe = cudaGetLastError();
+    if (pe != cudaSuccess) return cuda_check(c, pe, "schedule_step planner launch");
+  }
   int64_t g1 = (ntask_max + K1W - 1) / K1W;  // clamped to the resident CTAs by launch_k1_t
   g1 = g1 < (int64_t)dev_sms * 32 ? g1 : (int64_t)dev_sms * 32;
   const bool vec = ((uintptr_t)in->deadline_us % 16 == 0) && ((uintptr_t)in->eff_prompt % 16 == 0) &&
@@ -1177,6 +1181,10 @@ asc_status launch_schedule_step(asc_ctx* c, const asc_step_in* in, asc_step_out*
   const int variant = (vec ? 1 : 0) | (tab << 1) | (P.drop ? 8 : 0) | (P.offl ? 16 : 0);
   cudaEventRecord(c->ev0, sm);
   launch_k1(variant, gk, dsm, sm, P);
+  {
+    const cudaError_t ke = cudaGetLastError();  // checked here: later runtime calls may not keep it
+    if (ke != cudaSuccess) return cuda_check(c, ke, "schedule_step k1 launch");
+  }
   cudaEventRecord(c->ev1, sm);
   c->timed = true;
   launches += 1;

@@ -171,6 +171,20 @@ def test_small_segment_key_windows(asc, oracle, spread_us, policy):
     compare(run_gpu(asc, cfg, ins), oracle.schedule_step(cfg, **ins), ins["seg_off"])
 
 
+def test_many_segments_mixed_sizes(asc, oracle):
+    # S > 8191 takes the multi-launch planner (count, tile scans, task map); segments of every
+    # kind in one call: short (k_small), single-task (k1), multi-task (k1 + k2 + k3)
+    rng = np.random.default_rng(41)
+    S = 12000
+    qs = rng.integers(0, 33, size=S)
+    mid = rng.random(S) < 0.25
+    qs[mid] = rng.integers(33, 1500, size=int(mid.sum()))
+    qs[[17, 5000, 11999]] = [40000, 16385, 33000]
+    cfg = P.config()
+    ins = H.random_step_inputs(rng, S, 0, cfg, qs=qs)
+    compare(run_gpu(asc, cfg, ins), oracle.schedule_step(cfg, **ins), ins["seg_off"])
+
+
 def test_errors(asc):
     rng = np.random.default_rng(5)
     cfg = P.config()
