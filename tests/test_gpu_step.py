@@ -185,6 +185,30 @@ def test_many_segments_mixed_sizes(asc, oracle):
     compare(run_gpu(asc, cfg, ins), oracle.schedule_step(cfg, **ins), ins["seg_off"])
 
 
+def test_unaligned_inputs(asc, oracle):
+    # per-entry arrays that are not 16-byte aligned (views one element into a buffer) take k1's
+    # scalar-load path (VEC = false) and k_small's; results must not depend on it
+    rng = np.random.default_rng(43)
+    cfg = P.config(flg=P.flags(drop=1))
+    qs = rng.integers(0, 33, size=600)
+    qs[::7] = rng.integers(33, 3000, size=len(qs[::7]))
+    qs[5] = 20000
+    ins = H.random_step_inputs(rng, 600, 0, cfg, qs=qs)
+    d = to_dev(ins)
+    for k in ("deadline_us", "eff_prompt", "flags"):
+        big = torch.zeros(len(ins[k]) + 1, dtype=d[k].dtype, device=d[k].device)
+        big[1:] = d[k]
+        d[k] = big[1:]
+        assert d[k].data_ptr() % 16 != 0
+    ctx = asc.Context(cfg, 0)
+    try:
+        out = ctx.schedule_step(d)
+        out = {k: (v.cpu().numpy() if v is not None else None) for k, v in out.items()}
+    finally:
+        ctx.close()
+    compare(out, oracle.schedule_step(cfg, **ins), ins["seg_off"])
+
+
 def test_errors(asc):
     rng = np.random.default_rng(5)
     cfg = P.config()
