@@ -67,3 +67,19 @@ def test_config5_shards_match_unsharded_and_oracle():
         assert np.array_equal(dec, whole["decisions"]), W
         assert np.array_equal(first, whole["first_token_us"]), W
         assert sums["good"] == int(whole["good"].sum()) and sums["total"] == int(whole["total"].sum())
+
+
+def test_more_traces_than_resident_warps():
+    """8,192 traces (the per-GPU load of config 5 on 8 GPUs) exceed the resident warp slots
+    (148 SMs x 7 CTAs x 4 warps): warps pull further traces from the atomic counter."""
+    from paper_2504_20828_b200 import asc
+    from oracle import oracle as O
+    cfg, b = P.workload("config5", n=60, select=list(range(0, 65536, 8)))
+    assert b.T == 8192
+    got = _run(asc, cfg, b)
+    exp = O.simulate_batch(cfg, b)
+    assert np.array_equal(got["digest"], exp["digest"])
+    assert np.array_equal(got["decisions"], exp["decisions"])
+    assert np.array_equal(got["first_token_us"], exp["first_token_us"])
+    assert np.array_equal(got["done_us"], exp["done_us"])
+    assert np.array_equal(got["status"], exp["status"])
