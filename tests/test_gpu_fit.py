@@ -122,3 +122,22 @@ def test_fit_errors(asc):
     with pytest.raises(asc.AscError) as e:
         _gpu(asc, rec, lam=-1.0)
     assert e.value.code == 1
+
+
+def test_fit_unaligned_records(asc, oracle):
+    # record arrays one element into their buffers (not 16-byte aligned) take fit_partials'
+    # scalar-load path; the fit must not depend on it
+    rec = RC.make_records(14, [20, 9000, 333, 8192])
+    d = {k: torch.from_numpy(np.ascontiguousarray(v)).cuda() for k, v in rec.items()}
+    for k in ("F", "M", "y"):
+        big = torch.zeros(len(rec[k]) + 1, dtype=d[k].dtype, device=d[k].device)
+        big[1:] = d[k]
+        d[k] = big[1:]
+        assert d[k].data_ptr() % 16 != 0
+    ctx = asc.Context(P.config(), 0)
+    try:
+        c, me, mx = ctx.fit_perf(d, 1e-8, True)
+        got = (c.cpu().numpy(), me.cpu().numpy(), mx.cpu().numpy())
+    finally:
+        ctx.close()
+    _check(oracle, rec, got)
