@@ -107,3 +107,20 @@ def test_step_budget_maxima(asc, oracle):
     ins["budget_tokens"][:] = (1 << 24) - 1
     ins["budget_blocks"][:] = (1 << 22) - 1
     compare(run_gpu(asc, cfg, ins), oracle.schedule_step(cfg, **ins), ins["seg_off"])
+
+
+@pytest.mark.parametrize("elastic", [0, 1])
+def test_hp_decode_set_beyond_shared_slots(asc, oracle, elastic):
+    # an offload margin of 10^6 s sends every request the LP does not admit to the HP, whose
+    # prefill batches then leave ~900 concurrent decodes: slots beyond the 128 kept in shared memory
+    # live in HBM (sim.cu DCAP), through decode runs and completions alike
+    cfg = P.config(topo=P.topology(n_lp=1, n_hp=1), flg=P.flags(offload_margin_us=10 ** 12, elastic=elastic))
+    n = 1200
+    arr = np.zeros(n, np.int64)
+    arr[600:] = 5_000_000
+    b = TR.make_batch([(arr, np.full(n, 16, np.int32), np.full(n, 300, np.int32))], [10 ** 9], [10 ** 9])
+    got = gpu_sim(asc, cfg, b)
+    st = got["status"]
+    hp = ((st >> 4) & 0xff) == 1
+    assert hp.sum() > 500
+    assert_parity(oracle, cfg, b, got)
