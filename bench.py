@@ -347,6 +347,7 @@ def main():
         line["e2e"] = e2e(asc, torch, ctx, batch, world, min(a.steps, 2), dev)
     if rank == 0 and not a.no_fit_bench:
         line["fit_microbench"] = fit_microbench(asc, torch, dev, stream, hbm_peak)
+        line["latency_microbench"] = latency_microbench(asc, torch, dev, stream, hbm_peak)
     if rank == 0 and not a.no_baselines:
         line["baselines"] = baselines(asc, torch, dev, stream, cfg, batch, good_all / max(total_all, 1))
     if rank == 0 and world == 1 and not a.no_cpu_baseline:
@@ -356,6 +357,33 @@ def main():
         print(json.dumps(line), flush=True)
     if world > 1:
         torch.distributed.destroy_process_group()
+
+
+def latency_microbench(asc, torch, dev, stream, hbm_peak, n=1 << 26, steps=5):
+    """Rows a1/a6 alone: asc_latency over n device-resident (F, M) pairs (Eq. 4-5 + G17/G18, the
+    evaluation every formation makes); 16 B read + 16 B written (lat_us, t_s) per pair."""
+    g = torch.Generator(device=dev)
+    g.manual_seed(5)
+    F = torch.floor(torch.pow(2.0, torch.rand(n, generator=g, device=dev, dtype=torch.float64) * 52)).to(torch.int64)
+    M = torch.floor(torch.pow(2.0, torch.rand(n, generator=g, device=dev, dtype=torch.float64) * 52)).to(torch.int64)
+    ctx = asc.Context(P.config(), dev.index, stream)
+    lat = torch.empty(n, dtype=torch.int64, device=dev)
+    ts = torch.empty(n, dtype=torch.float64, device=dev)
+    for _ in range(2):
+        asc.asc_latency(ctx.h, F, M, lat, ts, n=n)
+    torch.cuda.synchronize()
+    k_ms = []
+    for _ in range(steps):
+        asc.asc_latency(ctx.h, F, M, lat, ts, n=n)
+        k_ms.append(ctx.last_kernel_ms())
+    ctx.close()
+    kms = float(np.mean(k_ms))
+    byts = 32 * n
+    ach = byts / (kms * 1e-3) / 1e9
+    return {"shape": f"{n} (F, M) pairs", "evaluations_per_s": n / (kms * 1e-3),
+            "roofline": {"bound": "hbm", "achieved": ach, "peak": hbm_peak, "unit": "GB/s",
+                         "frac": ach / hbm_peak, "traffic": None, "kernel": "latency_kernel (asc_latency)",
+                         "algorithmic_bytes": byts, "kernel_ms": kms}}
 
 
 def fit_microbench(asc, torch, dev, stream, hbm_peak, groups=1024, per=65536, steps=5):
