@@ -253,17 +253,31 @@ __global__ void fit_resid_final(const __grid_constant__ FitP p) {
 __global__ void __launch_bounds__(256) latency_kernel(Model md, int64_t n, const uint64_t* __restrict__ F,
                                                       const uint64_t* __restrict__ M, int64_t* __restrict__ lat,
                                                       double* __restrict__ ts, int* err) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    const uint64_t f = __ldcs(F + i), m = __ldcs(M + i);
-    if (f >= TWO53 || m >= TWO53) {  // int -> double would not be exact
-      atomicOr(err, ERR_RANGE);
-      lat[i] = -1;
-      if (ts) ts[i] = 0.0;
-      continue;
+  // LU pairs per thread per pass, all loads issued before the arithmetic (memory-level parallelism)
+  constexpr int LU = 4;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i0 < n; i0 += LU * stride) {
+    uint64_t f[LU], m[LU];
+#pragma unroll
+    for (int u = 0; u < LU; u++) {
+      const int64_t i = i0 + u * stride;
+      f[u] = i < n ? __ldcs(F + i) : 0;
+      m[u] = i < n ? __ldcs(M + i) : 0;
     }
-    const double t = t_from_FM(md, f, m);
-    __stcs(lat + i, (long long)us_of_t(t));
-    if (ts) __stcs(ts + i, t);
+#pragma unroll
+    for (int u = 0; u < LU; u++) {
+      const int64_t i = i0 + u * stride;
+      if (i >= n) break;
+      if (f[u] >= TWO53 || m[u] >= TWO53) {  // int -> double would not be exact
+        atomicOr(err, ERR_RANGE);
+        lat[i] = -1;
+        if (ts) ts[i] = 0.0;
+        continue;
+      }
+      const double t = t_from_FM(md, f[u], m[u]);
+      __stcs(lat + i, (long long)us_of_t(t));
+      if (ts) __stcs(ts + i, t);
+    }
   }
 }
 
@@ -275,7 +289,7 @@ asc_status launch_latency(asc_ctx* c, int64_t n, const uint64_t* F, const uint64
                           double* ts) {
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
-  int64_t grid = (n + 255) / 256;
+  int64_t grid = (n + 4 * 256 - 1) / (4 * 256);
   if (grid > (int64_t)sms * 8) grid = (int64_t)sms * 8;
   int64_t launches = 0;
   if (n > 0) {
