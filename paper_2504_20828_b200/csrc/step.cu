@@ -908,9 +908,22 @@ __global__ void __launch_bounds__(256, ASC_KS_MINB) k_small(const __grid_constan
     int64_t R = cu.R;
     if (R > ASC_MAX_BATCH) { if (lane == 0) atomicOr(P.err, ERR_RANGE); R = ASC_MAX_BATCH; }
     const int64_t Bd = cu.Bd, sl = cu.sl;
+    // a6 for every prefix at once: lane j evaluates the batch {first j sorted entries} ∪ D
+    // (Eq. 3-5 from the exclusive prefix moments).  Lane 0 is the decode-only batch, whose
+    // latency also gives the TBT residual C (G22); the admitted batch is lane k's — one fused
+    // evaluation instead of two sequential ones.  Only the lanes used may raise ERR_RANGE.
+    const uint64_t qv = live ? (uint64_t)ps : 0ull;
+    const uint64_t q2 = qv * qv;
+    const uint64_t qc = live ? qv * (uint64_t)(((uint32_t)ps + (uint32_t)P.md.b - 1u) / (uint32_t)P.md.b) : 0ull;  // ps < 2^31
+    const uint64_t isp = (uint64_t)warp_incl_scan((int64_t)qv);
+    const uint64_t isp2 = (uint64_t)warp_incl_scan((int64_t)q2);
+    const uint64_t ispc = (uint64_t)warp_incl_scan((int64_t)qc);
+    const int64_t lj = (lane > 0 || Bd > 0)
+                           ? lat_us(P.md, (uint64_t)lane, isp - qv, isp2 - q2, ispc - qc, (uint64_t)Bd, (uint64_t)sl)
+                           : 0;
     int64_t C = INF64;
+    const int64_t d = __shfl_sync(FULL, lj, 0);
     if (Bd > 0) {
-      const int64_t d = lat_decode(P.md, (uint64_t)Bd, (uint64_t)sl);
       if (d < 0 && lane == 0) atomicOr(P.err, ERR_RANGE);
       C = cu.tbt - d;
     }
@@ -923,18 +936,10 @@ __global__ void __launch_bounds__(256, ASC_KS_MINB) k_small(const __grid_constan
     const bool adm = lane < k;
     if (adm) P.admit_idx[lo + lane] = (int32_t)(lo + x.i);
     const uint32_t amask = __reduce_or_sync(FULL, adm ? (1u << x.i) : 0u);
-    uint64_t sp = 0, sp2 = 0, spc = 0;
-    if (adm) {
-      const uint64_t q = (uint64_t)ps;
-      sp = q;
-      sp2 = q * q;
-      spc = q * (uint64_t)(((uint32_t)ps + (uint32_t)P.md.b - 1u) / (uint32_t)P.md.b);  // ps < 2^31, b small
-    }
-    if (k > 0) {
-      sp = warp_sum(sp);
-      sp2 = warp_sum(sp2);
-      spc = warp_sum(spc);
-    }
+    int64_t lk = __shfl_sync(FULL, lj, k & 31);  // k < 32: lane k's prefix
+    if (k == 32)                                  // every lane admitted: the full sums (lane 31's inclusive)
+      lk = lat_us(P.md, 32, __shfl_sync(FULL, isp, 31), __shfl_sync(FULL, isp2, 31), __shfl_sync(FULL, ispc, 31),
+                  (uint64_t)Bd, (uint64_t)sl);
     // a5: offload (non-admitted, never prefilled, not on an HP) and drop lists in position order
     const bool off = P.offl && v && !dropped && !((amask >> lane) & 1u) && !(f & 3u) &&
                      dl - now <= pf + P.W + P.margin;
@@ -947,8 +952,7 @@ __global__ void __launch_bounds__(256, ASC_KS_MINB) k_small(const __grid_constan
       P.drop_cnt[s] = __popc(md);
       int64_t l = 0;
       if (k > 0 || Bd > 0) {
-        l = k ? lat_us(P.md, (uint64_t)k, sp, sp2, spc, (uint64_t)Bd, (uint64_t)sl)
-              : lat_decode(P.md, (uint64_t)Bd, (uint64_t)sl);
+        l = lk;
         if (l < 0) atomicOr(P.err, ERR_RANGE);
       }
       P.blat[s] = l;
