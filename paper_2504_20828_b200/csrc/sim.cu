@@ -1484,15 +1484,32 @@ __global__ void goodput_kernel(int32_t T, const int64_t* off, const int64_t* arr
     const int64_t lo = off[t], hi = off[t + 1];
     const int64_t tt = ttft[t], tb = tbt[t];
     uint64_t g = 0;
+    // GU requests per lane per pass, every field loaded before any test (branch-free streaming:
+    // the loads of a pass are independent, so several are in flight per warp)
+    constexpr int GU = 4;
     #pragma unroll 1
-    for (int64_t i = lo + lane; i < hi; i += 32) {
-      if ((__ldcs(status + i) & 3u) != 1u) continue;
-      const int64_t f = __ldcs(first + i);
-      const int64_t slo = rttft ? rttft[i] : tt;
-      if (f - __ldcs(arr + i) > slo) continue;
-      const int32_t o = __ldcs(ol + i);
-      if (o > 1 && __ldcs(done + i) - f > tb * (int64_t)(o - 1)) continue;
-      g++;
+    for (int64_t i0 = lo + lane; i0 < hi; i0 += 32 * GU) {
+      uint32_t st[GU];
+      int64_t f[GU], a[GU], d[GU], sl[GU];
+      int32_t o[GU];
+      #pragma unroll
+      for (int u = 0; u < GU; u++) {
+        const int64_t i = i0 + 32 * u;
+        const bool v = i < hi;
+        st[u] = v ? __ldcs(status + i) : 0u;
+        f[u] = v ? __ldcs(first + i) : 0;
+        a[u] = v ? __ldcs(arr + i) : 0;
+        o[u] = v ? __ldcs(ol + i) : 1;
+        d[u] = v ? __ldcs(done + i) : 0;
+        sl[u] = (v && rttft) ? __ldcs(rttft + i) : tt;
+      }
+      #pragma unroll
+      for (int u = 0; u < GU; u++) {
+        // P:451 / G35: completed, TTFT within the SLO, mean TBT within the SLO (out = 1: no TBT)
+        const bool ok = (st[u] & 3u) == 1u && f[u] - a[u] <= sl[u] &&
+                        (o[u] <= 1 || d[u] - f[u] <= tb * (int64_t)(o[u] - 1));
+        g += ok ? 1u : 0u;
+      }
     }
     g = warp_sum(g);
     if (lane == 0) {
