@@ -243,8 +243,13 @@ static bool same_kind(int kind, std::initializer_list<const void*> ps) {
   return true;
 }
 
-struct Stager {  // copies host arrays into the staging buffer and back
+// Copies host arrays into the staging buffer and back.  The same sequence of up()/out() calls
+// runs twice: first on a dry Stager (no base, no copies) that only sums the 256-byte-aligned
+// offsets, which sizes the staging buffer, then for real -- so the size can never disagree with
+// what is staged.
+struct Stager {
   asc_ctx* c;
+  bool dry = false;
   std::vector<std::pair<void*, const void*>> downs;  // (host dst, dev src) sizes below
   std::vector<size_t> down_sizes;
   size_t off = 0;
@@ -253,19 +258,21 @@ struct Stager {  // copies host arrays into the staging buffer and back
   T* up(const T* h, size_t n) {
     if (!h) return nullptr;
     off = (off + 255) & ~size_t(255);
-    T* d = reinterpret_cast<T*>(base + off);
+    T* d = dry ? nullptr : reinterpret_cast<T*>(base + off);
     off += n * sizeof(T);
-    if (n) cudaMemcpyAsync(d, h, n * sizeof(T), cudaMemcpyHostToDevice, c->stream);
+    if (n && !dry) cudaMemcpyAsync(d, h, n * sizeof(T), cudaMemcpyHostToDevice, c->stream);
     return d;
   }
   template <typename T>
   T* out(T* h, size_t n) {
     if (!h) return nullptr;
     off = (off + 255) & ~size_t(255);
-    T* d = reinterpret_cast<T*>(base + off);
+    T* d = dry ? nullptr : reinterpret_cast<T*>(base + off);
     off += n * sizeof(T);
-    downs.push_back({(void*)h, (const void*)d});
-    down_sizes.push_back(n * sizeof(T));
+    if (!dry) {
+      downs.push_back({(void*)h, (const void*)d});
+      down_sizes.push_back(n * sizeof(T));
+    }
     return d;
   }
   cudaError_t download() {
@@ -276,7 +283,27 @@ struct Stager {  // copies host arrays into the staging buffer and back
   }
 };
 
-static size_t rup(size_t x) { return (x + 255) & ~size_t(255); }
+// Runs plan(sg) on a dry Stager to size the staging buffer, then on the real one.
+template <typename Plan>
+static asc_status stage_host(asc_ctx* c, Stager& sg, Plan plan) {
+  Stager dry{c};
+  dry.dry = true;
+  plan(dry);
+  asc_status st = ensure_stage(c, dry.off + 256);
+  if (st) return st;
+  sg.base = c->stage;
+  plan(sg);
+  return ASC_OK;
+}
+
+// Host-pointer epilogue: the outputs are copied back even when the device flagged an error (so
+// documented error markers such as asc_latency's -1 reach the caller), then the status returns.
+static asc_status finish_host(asc_ctx* c, Stager& sg, const char* where) {
+  asc_status st = collect_errors(c, where);
+  cudaError_t e = sg.download();
+  if (st) return st;
+  return cuda_check(c, e, where);
+}
 
 extern "C" {
 
@@ -322,13 +349,10 @@ asc_status asc_schedule_step(asc_ctx* c, const asc_step_in* in, asc_step_out* ou
     return collect_errors(c, "asc_schedule_step");
   }
   const size_t Sn = (size_t)S, Qn = (size_t)Q;
-  size_t need = rup(8 * (Sn + 1)) + 2 * rup(8 * Sn) + rup(8 * Qn) + rup(4 * Qn) + rup(Qn) +
-                rup(4 * Sn) + rup(8 * Sn) + 4 * rup(4 * Sn) + 4 * rup(4 * Qn) + rup(8 * Sn) + 4096;
-  st = ensure_stage(c, need);
-  if (st) return st;
   Stager sg{c};
-  sg.base = c->stage;
   asc_step_in di = *in;
+  asc_step_out dout;
+  st = stage_host(c, sg, [&](Stager& sg) {
   di.seg_off = sg.up(in->seg_off, Sn + 1);
   di.now_us = sg.up(in->now_us, Sn);
   di.deadline_us = sg.up(in->deadline_us, Qn);
@@ -340,7 +364,6 @@ asc_status asc_schedule_step(asc_ctx* c, const asc_step_in* in, asc_step_out* ou
   di.budget_tokens = sg.up(in->budget_tokens, Sn);
   di.budget_blocks = sg.up(in->budget_blocks, Sn);
   di.budget_reqs = sg.up(in->budget_reqs, Sn);
-  asc_step_out dout;
   dout.admit_idx = sg.out(out->admit_idx, Qn);
   dout.admit_cnt = sg.out(out->admit_cnt, Sn);
   dout.offload_idx = sg.out(out->offload_idx, Qn);
@@ -349,11 +372,11 @@ asc_status asc_schedule_step(asc_ctx* c, const asc_step_in* in, asc_step_out* ou
   dout.drop_cnt = sg.out(out->drop_cnt, Sn);
   dout.batch_lat_us = sg.out(out->batch_lat_us, Sn);
   dout.prefill_us = sg.out(out->prefill_us, Qn);
+  });
+  if (st) return st;
   st = launch_schedule_step(c, &di, &dout, Q);
   if (st) return st;
-  st = collect_errors(c, "asc_schedule_step");
-  if (st) return st;
-  return cuda_check(c, sg.download(), "asc_schedule_step: download");
+  return finish_host(c, sg, "asc_schedule_step");
 }
 
 asc_status asc_simulate_batch(asc_ctx* c, const asc_traces* tr, asc_outcomes* out) {
@@ -394,13 +417,10 @@ asc_status asc_simulate_batch(asc_ctx* c, const asc_traces* tr, asc_outcomes* ou
     return collect_errors(c, "asc_simulate_batch");
   }
   const size_t Tn = (size_t)T, Rn = (size_t)R;
-  size_t need = rup(8 * (Tn + 1)) + rup(8 * Rn) * 2 + rup(4 * Rn) * 2 + rup(8 * Tn) * 2 +
-                rup(8 * Rn) * 3 + rup(4 * Rn) + rup(8 * Tn) * 3 + rup(4 * Tn) * 2 + rup(8 * Rn) + 4096;
-  st = ensure_stage(c, need);
-  if (st) return st;
   Stager sg{c};
-  sg.base = c->stage;
   asc_traces dt = *tr;
+  asc_outcomes doc = *out;
+  st = stage_host(c, sg, [&](Stager& sg) {
   dt.trace_off = sg.up(tr->trace_off, Tn + 1);
   dt.arrival_us = sg.up(tr->arrival_us, Rn);
   dt.prompt_len = sg.up(tr->prompt_len, Rn);
@@ -411,7 +431,6 @@ asc_status asc_simulate_batch(asc_ctx* c, const asc_traces* tr, asc_outcomes* ou
   dt.n_lp = sg.up(tr->n_lp, Tn);
   dt.n_hp = sg.up(tr->n_hp, Tn);
   dt.req_key_offset_us = sg.up(tr->req_key_offset_us, Rn);
-  asc_outcomes doc;
   doc.first_token_us = sg.out(out->first_token_us, Rn);
   doc.done_us = sg.out(out->done_us, Rn);
   doc.prefill_start_us = sg.out(out->prefill_start_us, Rn);
@@ -419,11 +438,11 @@ asc_status asc_simulate_batch(asc_ctx* c, const asc_traces* tr, asc_outcomes* ou
   doc.digest = sg.out(out->digest, Tn);
   doc.decisions = sg.out(out->decisions, Tn);
   doc.evaluations = sg.out(out->evaluations, Tn);
+  });
+  if (st) return st;
   st = launch_simulate(c, &dt, &doc, R);
   if (st) return st;
-  st = collect_errors(c, "asc_simulate_batch");
-  if (st) return st;
-  return cuda_check(c, sg.download(), "asc_simulate_batch: download");
+  return finish_host(c, sg, "asc_simulate_batch");
 }
 
 asc_status asc_goodput(asc_ctx* c, const asc_traces* tr, const asc_outcomes* out, uint64_t* good,
@@ -446,12 +465,11 @@ asc_status asc_goodput(asc_ctx* c, const asc_traces* tr, const asc_outcomes* out
     return collect_errors(c, "asc_goodput");
   }
   const size_t Tn = (size_t)T, Rn = (size_t)tr->trace_off[T];
-  size_t need = rup(8 * (Tn + 1)) + rup(8 * Rn) * 4 + rup(4 * Rn) * 2 + rup(8 * Tn) * 4 + 4096;
-  st = ensure_stage(c, need);
-  if (st) return st;
   Stager sg{c};
-  sg.base = c->stage;
   asc_traces dt = *tr;
+  asc_outcomes doc{};
+  uint64_t *dg = nullptr, *dtt = nullptr;
+  st = stage_host(c, sg, [&](Stager& sg) {
   dt.trace_off = sg.up(tr->trace_off, Tn + 1);
   dt.arrival_us = sg.up(tr->arrival_us, Rn);
   dt.prompt_len = nullptr;
@@ -459,17 +477,16 @@ asc_status asc_goodput(asc_ctx* c, const asc_traces* tr, const asc_outcomes* out
   dt.ttft_slo_us = sg.up(tr->ttft_slo_us, Tn);
   dt.tbt_slo_us = sg.up(tr->tbt_slo_us, Tn);
   dt.req_ttft_slo_us = sg.up(tr->req_ttft_slo_us, Rn);
-  asc_outcomes doc{};
   doc.first_token_us = sg.up(out->first_token_us, Rn);
   doc.done_us = sg.up(out->done_us, Rn);
   doc.status = sg.up(out->status, Rn);
-  uint64_t* dg = sg.out(good, Tn);
-  uint64_t* dtt = sg.out(total, Tn);
+  dg = sg.out(good, Tn);
+  dtt = sg.out(total, Tn);
+  });
+  if (st) return st;
   st = launch_goodput(c, &dt, &doc, dg, dtt);
   if (st) return st;
-  st = collect_errors(c, "asc_goodput");
-  if (st) return st;
-  return cuda_check(c, sg.download(), "asc_goodput: download");
+  return finish_host(c, sg, "asc_goodput");
 }
 
 asc_status asc_fit_perf(asc_ctx* c, const asc_fit_in* in, double lambda, double* coef,
@@ -499,25 +516,23 @@ asc_status asc_fit_perf(asc_ctx* c, const asc_fit_in* in, double lambda, double*
   if (N < 0) N = in->rec_off[G];
   if (N != in->rec_off[G] || N < 0) return fail(c, ASC_E_INVAL, "asc_fit_perf: N != rec_off[G]");
   const size_t Gn = (size_t)G, Nn = (size_t)N;
-  size_t need = rup(8 * (Gn + 1)) + rup(8 * Nn) * 3 + rup(8 * Gn) * 7 + 4096;
-  asc_status st = ensure_stage(c, need);
-  if (st) return st;
   Stager sg{c};
-  sg.base = c->stage;
   asc_fit_in d = *in;
   d.N = N;
+  double *dc = nullptr, *dme = nullptr, *dmx = nullptr;
+  asc_status st = stage_host(c, sg, [&](Stager& sg) {
   d.rec_off = sg.up(in->rec_off, Gn + 1);
   d.F = sg.up(in->F, Nn);
   d.M = sg.up(in->M, Nn);
   d.y = sg.up(in->y, Nn);
-  double* dc = sg.out(coef, 5 * Gn);
-  double* dme = sg.out(mean_err, Gn);
-  double* dmx = sg.out(max_err, Gn);
+  dc = sg.out(coef, 5 * Gn);
+  dme = sg.out(mean_err, Gn);
+  dmx = sg.out(max_err, Gn);
+  });
+  if (st) return st;
   st = launch_fit(c, &d, N, lambda, dc, dme, dmx);
   if (st) return st;
-  st = collect_errors(c, "asc_fit_perf");
-  if (st) return st;
-  return cuda_check(c, sg.download(), "asc_fit_perf: download");
+  return finish_host(c, sg, "asc_fit_perf");
 }
 
 asc_status asc_latency(asc_ctx* c, int64_t n, const uint64_t* F, const uint64_t* M, int64_t* lat_us,
@@ -538,19 +553,20 @@ asc_status asc_latency(asc_ctx* c, int64_t n, const uint64_t* F, const uint64_t*
     return collect_errors(c, "asc_latency");
   }
   const size_t nn = (size_t)n;
-  st = ensure_stage(c, rup(8 * nn) * 4 + 4096);
-  if (st) return st;
   Stager sg{c};
-  sg.base = c->stage;
-  const uint64_t* dF = sg.up(F, nn);
-  const uint64_t* dM = sg.up(M, nn);
-  int64_t* dl = sg.out(lat_us, nn);
-  double* dt = sg.out(t_s, nn);
+  const uint64_t *dF = nullptr, *dM = nullptr;
+  int64_t* dl = nullptr;
+  double* dt = nullptr;
+  st = stage_host(c, sg, [&](Stager& sg) {
+    dF = sg.up(F, nn);
+    dM = sg.up(M, nn);
+    dl = sg.out(lat_us, nn);
+    dt = sg.out(t_s, nn);
+  });
+  if (st) return st;
   st = launch_latency(c, n, dF, dM, dl, dt);
   if (st) return st;
-  st = collect_errors(c, "asc_latency");
-  if (st) return st;
-  return cuda_check(c, sg.download(), "asc_latency: download");
+  return finish_host(c, sg, "asc_latency");
 }
 
 int64_t asc_last_kernel_launches(const asc_ctx* c) { return c ? c->last_kernel_launches : 0; }

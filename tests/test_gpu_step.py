@@ -152,6 +152,16 @@ def test_host_pointer_path(asc, oracle):
     compare(got, oracle.schedule_step(cfg, **ins), ins["seg_off"])
 
 
+def test_host_pointer_path_many_segments(asc, oracle):
+    # S >= 4096 with prefill_us requested: the staging buffer must hold all seven [S] int32
+    # arrays (the size formula counted five, so the last staged array overran it)
+    rng = np.random.default_rng(33)
+    cfg = P.config(flg=P.flags(drop=1))
+    ins = H.random_step_inputs(rng, 6000, 0, cfg, qs=rng.integers(0, 40, size=6000))
+    got = run_gpu(asc, cfg, ins, host=True)
+    compare(got, oracle.schedule_step(cfg, **ins), ins["seg_off"])
+
+
 def test_many_tiny_segments(asc, oracle):
     rng = np.random.default_rng(4)
     cfg = P.config()
