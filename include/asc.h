@@ -28,7 +28,7 @@
 extern "C" {
 #endif
 
-#define ASC_ABI_VERSION 2
+#define ASC_ABI_VERSION 3
 #define ASC_MAX_BATCH 128      /* max request-count budget R / lp_max_batch */
 #define ASC_MAX_INSTANCES 16   /* n_lp + n_hp per trace */
 
@@ -229,6 +229,44 @@ asc_status asc_simulate_batch(asc_ctx* ctx, const asc_traces* tr, asc_outcomes* 
  * ------------------------------------------------------------------------------------------- */
 asc_status asc_goodput(asc_ctx* ctx, const asc_traces* tr, const asc_outcomes* out,
                        uint64_t* good, uint64_t* total);
+
+/* ---------------------------------------------------------------------------------------------
+ * asc_summarize — the per-trace outcome summary behind the paper's metrics (row a8): PAPER
+ * P:579-584 (Fig. 10: "(a) P99 TTFT, (b) Mean TBT, (c) System throughput, and (d) Request
+ * scheduling delay"; "HP requests wait 4x less than LP requests"), SPEC S:543-590 (metrics
+ * module), reading G52.  For each trace t (every output is an int64 [T] array and may
+ * be NULL = not written):
+ *   completed, dropped   requests whose status state is COMPLETED / DROPPED
+ *   violating            completed requests that are not good (asc_goodput's test failed)
+ *   tokens               sum of output_len over completed requests (dropped contribute 0);
+ *                        system throughput = tokens / (last_done_us - first arrival)
+ *   ttft_p50_us, ttft_p90_us, ttft_p99_us
+ *                        nearest-rank percentiles (the ceil(q n / 100)-th smallest) of
+ *                        first_token_us - arrival_us over the n requests with a first token;
+ *                        -1 when n = 0
+ *   tbt_sum_us, tbt_tokens
+ *                        sums of done - first_token and of output_len - 1 over completed
+ *                        requests with output_len > 1: mean TBT = tbt_sum_us / tbt_tokens
+ *   delay_sum_lp_us, delay_cnt_lp, delay_sum_hp_us, delay_cnt_hp
+ *                        scheduling delay prefill_start_us - arrival_us summed and counted over
+ *                        requests with a prefill start, split by the type of the serving
+ *                        instance in the status word (index < n_lp of the trace: LP, else HP)
+ *   last_done_us         the latest done_us among completed requests (-1 if none)
+ * Inputs: tr (trace_off, arrival_us, output_len, ttft_slo_us, tbt_slo_us, optional
+ * req_ttft_slo_us and per-trace n_lp) and out (first_token_us, done_us, prefill_start_us,
+ * status) as produced by asc_simulate_batch.  All pointers device, or all host (staged).
+ * Exact integers, so per-trace results equal the CPU oracle's and sums over GPUs are exact.
+ * Errors: ASC_E_INVAL (NULL inputs, T < 0, mixed pointer kinds).
+ * ------------------------------------------------------------------------------------------- */
+typedef struct {
+  int64_t *completed, *dropped, *violating, *tokens;
+  int64_t *ttft_p50_us, *ttft_p90_us, *ttft_p99_us;
+  int64_t *tbt_sum_us, *tbt_tokens;
+  int64_t *delay_sum_lp_us, *delay_cnt_lp, *delay_sum_hp_us, *delay_cnt_hp;
+  int64_t *last_done_us;
+} asc_summary;
+asc_status asc_summarize(asc_ctx* ctx, const asc_traces* tr, const asc_outcomes* out,
+                         asc_summary* sum);
 
 /* Diagnostics: number of libasc kernels the last call on ctx launched (bench evidence). */
 int64_t asc_last_kernel_launches(const asc_ctx* ctx);

@@ -1049,3 +1049,64 @@ extern "C" int or_goodput(int32_t T, const int64_t* off, const int64_t* arr, con
   }
   return rc;
 }
+
+// Outcome summary (row a8; "(a) P99 TTFT, (b) Mean TBT, (c) System throughput, and (d)
+// Request scheduling delay"; G52).  Plain loops per trace; the percentiles sort
+// the trace's TTFTs and take the nearest-rank order statistic.
+static int64_t nearest_rank(const std::vector<int64_t>& sorted, int64_t q) {
+  const int64_t n = (int64_t)sorted.size();
+  if (n == 0) return -1;
+  int64_t k = (q * n + 99) / 100;  // ceil(q n / 100)
+  if (k < 1) k = 1;
+  return sorted[(size_t)(k - 1)];
+}
+
+extern "C" int or_summarize(int32_t T, const int64_t* off, const int64_t* arr, const int32_t* ol,
+                            const int64_t* ttft, const int64_t* tbt, const int64_t* req_ttft,
+                            const int32_t* trace_n_lp, int32_t n_lp, const int64_t* first,
+                            const int64_t* done, const int64_t* pstart, const uint32_t* status,
+                            int64_t* completed, int64_t* dropped, int64_t* violating,
+                            int64_t* tokens, int64_t* p50, int64_t* p90, int64_t* p99,
+                            int64_t* tbt_sum, int64_t* tbt_tok, int64_t* dsum_lp, int64_t* dcnt_lp,
+                            int64_t* dsum_hp, int64_t* dcnt_hp, int64_t* last_done) {
+  for (int32_t t = 0; t < T; t++) {
+    const int32_t nl = trace_n_lp ? trace_n_lp[t] : n_lp;
+    int64_t c = 0, d = 0, v = 0, tok = 0, ts = 0, tt = 0, sl = 0, cl = 0, sh = 0, ch = 0, ld = -1;
+    std::vector<int64_t> ttfts;
+    for (int64_t i = off[t]; i < off[t + 1]; i++) {
+      const uint32_t state = status[i] & 3u;
+      if (first[i] >= 0) ttfts.push_back(first[i] - arr[i]);
+      if (pstart[i] >= 0) {
+        const int32_t inst = (int32_t)((status[i] >> 4) & 255u);
+        if (inst < nl) { sl += pstart[i] - arr[i]; cl++; }
+        else { sh += pstart[i] - arr[i]; ch++; }
+      }
+      if (state == DROPPED) d++;
+      if (state != COMPLETED) continue;
+      c++;
+      tok += ol[i];
+      if (done[i] > ld) ld = done[i];
+      if (ol[i] > 1) { ts += done[i] - first[i]; tt += ol[i] - 1; }
+      const int64_t slo = req_ttft ? req_ttft[i] : ttft[t];
+      const bool good = first[i] - arr[i] <= slo &&
+                        (ol[i] == 1 || done[i] - first[i] <= tbt[t] * (int64_t)(ol[i] - 1));
+      if (!good) v++;
+    }
+    std::sort(ttfts.begin(), ttfts.end());
+    if (completed) completed[t] = c;
+    if (dropped) dropped[t] = d;
+    if (violating) violating[t] = v;
+    if (tokens) tokens[t] = tok;
+    if (p50) p50[t] = nearest_rank(ttfts, 50);
+    if (p90) p90[t] = nearest_rank(ttfts, 90);
+    if (p99) p99[t] = nearest_rank(ttfts, 99);
+    if (tbt_sum) tbt_sum[t] = ts;
+    if (tbt_tok) tbt_tok[t] = tt;
+    if (dsum_lp) dsum_lp[t] = sl;
+    if (dcnt_lp) dcnt_lp[t] = cl;
+    if (dsum_hp) dsum_hp[t] = sh;
+    if (dcnt_hp) dcnt_hp[t] = ch;
+    if (last_done) last_done[t] = ld;
+  }
+  return 0;
+}

@@ -110,6 +110,32 @@ int or_goodput(int32_t T, const int64_t* trace_off, const int64_t* arrival_us,
                const int64_t* req_ttft_slo_us, const int64_t* first_token_us,
                const int64_t* done_us, const uint32_t* status, uint64_t* good, uint64_t* total);
 
+/* Outcome summary per trace (row a8; Fig. 10 metric set; SPEC S:543-590 metrics module;
+ * DESIGN.md reading G52).  Every output array [T] may be NULL.
+ *   completed / dropped         requests in state COMPLETED / DROPPED
+ *   violating                   completed but not good (TTFT or mean-TBT SLO missed)
+ *   tokens                      sum of output_len over completed requests (dropped contribute 0)
+ *   ttft_p{50,90,99}_us         nearest-rank percentile (the ceil(q n / 100)-th smallest)
+ *                               of first_token - arrival over requests with a first token; -1 if none
+ *   tbt_sum_us / tbt_tokens     sum of (done - first) and of (output_len - 1) over completed
+ *                               requests with output_len > 1 (mean TBT = tbt_sum_us / tbt_tokens)
+ *   delay_sum_{lp,hp}_us / delay_cnt_{lp,hp}
+ *                               scheduling delay prefill_start - arrival summed over
+ *                               requests with a prefill start, split by the type of the serving
+ *                               instance (index < n_lp of the trace = LP)
+ *   last_done_us                latest done_us of the trace (-1 if none completed)
+ * trace_n_lp: per-trace LP count (may be NULL: n_lp for every trace).  Returns 0. */
+int or_summarize(int32_t T, const int64_t* trace_off, const int64_t* arrival_us,
+                 const int32_t* output_len, const int64_t* ttft_slo_us, const int64_t* tbt_slo_us,
+                 const int64_t* req_ttft_slo_us, const int32_t* trace_n_lp, int32_t n_lp,
+                 const int64_t* first_token_us, const int64_t* done_us,
+                 const int64_t* prefill_start_us, const uint32_t* status,
+                 int64_t* completed, int64_t* dropped, int64_t* violating, int64_t* tokens,
+                 int64_t* ttft_p50_us, int64_t* ttft_p90_us, int64_t* ttft_p99_us,
+                 int64_t* tbt_sum_us, int64_t* tbt_tokens,
+                 int64_t* delay_sum_lp_us, int64_t* delay_cnt_lp,
+                 int64_t* delay_sum_hp_us, int64_t* delay_cnt_hp, int64_t* last_done_us);
+
 const char* or_last_error(void);
 
 #ifdef __cplusplus

@@ -243,6 +243,30 @@ def goodput(batch, out, req_ttft_slo_us=None):
     return good[:T], total[:T]
 
 
+SUMMARY_KEYS = ("completed", "dropped", "violating", "tokens", "ttft_p50_us", "ttft_p90_us",
+                "ttft_p99_us", "tbt_sum_us", "tbt_tokens", "delay_sum_lp_us", "delay_cnt_lp",
+                "delay_sum_hp_us", "delay_cnt_hp", "last_done_us")
+
+
+def summarize(cfg, batch, out, req_ttft_slo_us=None, n_lp=None):
+    """Per-trace outcome summary (or_summarize; row a8): dict of int64 [T] arrays, SUMMARY_KEYS."""
+    T = batch.T
+    ins = [_p(x, dt) for x, dt in ((batch.trace_off, np.int64), (batch.arrival_us, np.int64),
+                                   (batch.output_len, np.int32), (batch.ttft_slo_us, np.int64),
+                                   (batch.tbt_slo_us, np.int64))]
+    rt = _p(req_ttft_slo_us, np.int64) if req_ttft_slo_us is not None else None
+    nl = _p(n_lp, np.int32) if n_lp is not None else None
+    outs = [_p(out[k], dt) for k, dt in (("first_token_us", np.int64), ("done_us", np.int64),
+                                        ("prefill_start_us", np.int64), ("status", np.uint32))]
+    res = {k: np.zeros(max(T, 1), np.int64) for k in SUMMARY_KEYS}
+    rc = lib().or_summarize(T, *[x[1] for x in ins], rt[1] if rt else None, nl[1] if nl else None,
+                            int(cfg["topo"]["n_lp"]), *[x[1] for x in outs],
+                            *[res[k].ctypes.data_as(C.c_void_p) for k in SUMMARY_KEYS])
+    if rc:
+        raise OracleError(rc, _err())
+    return {k: v[:T] for k, v in res.items()}
+
+
 # status word layout (DESIGN.md §Outputs)
 def state(st):
     return np.asarray(st) & 3

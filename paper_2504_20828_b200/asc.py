@@ -19,7 +19,7 @@ ASC_MAX_INSTANCES = 16
 STATUS = {0: "ASC_OK", 1: "ASC_E_INVAL", 2: "ASC_E_CONFIG", 3: "ASC_E_NOMEM", 4: "ASC_E_CUDA",
           5: "ASC_E_EMPTY", 6: "ASC_E_RANGE", 7: "ASC_E_INVARIANT"}
 EXPORTS = ("asc_create", "asc_destroy", "asc_last_error", "asc_abi_version", "asc_schedule_step",
-           "asc_simulate_batch", "asc_goodput", "asc_fit_perf", "asc_latency", "asc_last_kernel_launches",
+           "asc_simulate_batch", "asc_goodput", "asc_summarize", "asc_fit_perf", "asc_latency", "asc_last_kernel_launches",
            "asc_last_kernel_ms")
 
 
@@ -84,6 +84,15 @@ class asc_outcomes(C.Structure):
                                   "digest", "decisions", "evaluations")]
 
 
+SUMMARY_KEYS = ("completed", "dropped", "violating", "tokens", "ttft_p50_us", "ttft_p90_us",
+                "ttft_p99_us", "tbt_sum_us", "tbt_tokens", "delay_sum_lp_us", "delay_cnt_lp",
+                "delay_sum_hp_us", "delay_cnt_hp", "last_done_us")
+
+
+class asc_summary(C.Structure):
+    _fields_ = [(k, _P) for k in SUMMARY_KEYS]
+
+
 def lib():
     global _LIB
     if _LIB is None:
@@ -105,6 +114,9 @@ def lib():
         L.asc_goodput.argtypes = [C.c_void_p, C.POINTER(asc_traces), C.POINTER(asc_outcomes),
                                   C.c_void_p, C.c_void_p]
         L.asc_goodput.restype = C.c_int
+        L.asc_summarize.argtypes = [C.c_void_p, C.POINTER(asc_traces), C.POINTER(asc_outcomes),
+                                    C.POINTER(asc_summary)]
+        L.asc_summarize.restype = C.c_int
         L.asc_fit_perf.argtypes = [C.c_void_p, C.POINTER(asc_fit_in), C.c_double, C.c_void_p,
                                    C.c_void_p, C.c_void_p]
         L.asc_fit_perf.restype = C.c_int
@@ -208,6 +220,18 @@ def asc_goodput(ctx, trace_off, arrival_us, output_len, ttft_slo_us, tbt_slo_us,
            "asc_goodput")
 
 
+def asc_summarize(ctx, trace_off, arrival_us, output_len, ttft_slo_us, tbt_slo_us, first_token_us,
+                  done_us, prefill_start_us, status, res, req_ttft_slo_us=None, n_lp=None, R=-1):
+    """res: dict SUMMARY_KEY -> int64 [T] array (missing keys are not written)."""
+    T = len(trace_off) - 1
+    tr = asc_traces(T, R, _ptr(trace_off), _ptr(arrival_us), None, _ptr(output_len), _ptr(ttft_slo_us),
+                    _ptr(tbt_slo_us), _ptr(req_ttft_slo_us), _ptr(n_lp))
+    oc = asc_outcomes(_ptr(first_token_us), _ptr(done_us), _ptr(prefill_start_us), _ptr(status),
+                      None, None, None)
+    sm = asc_summary(*[_ptr(res.get(k)) for k in SUMMARY_KEYS])
+    _check(ctx, lib().asc_summarize(ctx, C.byref(tr), C.byref(oc), C.byref(sm)), "asc_summarize")
+
+
 def asc_fit_perf(ctx, rec_off, F, M, y, lam, coef, mean_err=None, max_err=None, N=-1):
     fi = asc_fit_in(len(rec_off) - 1, N, _ptr(rec_off), _ptr(F), _ptr(M), _ptr(y))
     _check(ctx, lib().asc_fit_perf(ctx, C.byref(fi), C.c_double(lam), _ptr(coef), _ptr(mean_err),
@@ -297,6 +321,17 @@ class Context:
                     res["good"], res["total"], req_ttft_slo_us, R=int(tr["R"]) if "R" in tr else -1)
         return res["good"], res["total"]
 
+
+    def summarize(self, tr, out, req_ttft_slo_us=None, n_lp=None, res=None):
+        """Per-trace outcome summary (asc_summarize) -> dict SUMMARY_KEY -> int64 [T]."""
+        dev = not isinstance(tr["trace_off"], np.ndarray)
+        T = len(tr["trace_off"]) - 1
+        if res is None:
+            res = _alloc(dev, self.device, {k: (T, "i8") for k in SUMMARY_KEYS})
+        asc_summarize(self.h, tr["trace_off"], tr["arrival_us"], tr["output_len"], tr["ttft_slo_us"],
+                      tr["tbt_slo_us"], out["first_token_us"], out["done_us"], out["prefill_start_us"],
+                      out["status"], res, req_ttft_slo_us, n_lp, R=int(tr["R"]) if "R" in tr else -1)
+        return {k: v[:T] for k, v in res.items()}
 
     def fit_perf(self, rec, lam=1e-8, errors=True):
         """rec: dict(off, F, M, y) numpy (host path) or torch CUDA tensors (device path)

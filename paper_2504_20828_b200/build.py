@@ -6,7 +6,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libasc.so")
-SOURCES = ["asc_api.cu", "step.cu", "sim.cu", "fit.cu"]
+SOURCES = ["asc_api.cu", "step.cu", "sim.cu", "fit.cu", "summary.cu"]
 HEADERS = ["asc_dev.cuh", "asc_internal.h", os.path.join("..", "..", "include", "asc.h")]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",

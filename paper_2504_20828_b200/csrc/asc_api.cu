@@ -489,6 +489,65 @@ asc_status asc_goodput(asc_ctx* c, const asc_traces* tr, const asc_outcomes* out
   return finish_host(c, sg, "asc_goodput");
 }
 
+asc_status asc_summarize(asc_ctx* c, const asc_traces* tr, const asc_outcomes* out, asc_summary* sum) {
+  if (!c || !tr || !out || !sum) return fail(c, ASC_E_INVAL, "asc_summarize: NULL argument");
+  c->err.clear();
+  c->timed = false;
+  if (tr->T < 0) return fail(c, ASC_E_INVAL, "asc_summarize: T < 0");
+  if (!tr->trace_off || !tr->arrival_us || !tr->output_len || !tr->ttft_slo_us || !tr->tbt_slo_us ||
+      !out->first_token_us || !out->done_us || !out->prefill_start_us || !out->status)
+    return fail(c, ASC_E_INVAL, "asc_summarize: NULL array");
+  cudaSetDevice(c->device);
+  const int kind = ptr_kind(tr->trace_off);
+  int64_t** outs[] = {&sum->completed, &sum->dropped, &sum->violating, &sum->tokens,
+                      &sum->ttft_p50_us, &sum->ttft_p90_us, &sum->ttft_p99_us, &sum->tbt_sum_us,
+                      &sum->tbt_tokens, &sum->delay_sum_lp_us, &sum->delay_cnt_lp,
+                      &sum->delay_sum_hp_us, &sum->delay_cnt_hp, &sum->last_done_us};
+  if (!same_kind(kind, {tr->arrival_us, tr->output_len, tr->ttft_slo_us, tr->tbt_slo_us,
+                        tr->req_ttft_slo_us, tr->n_lp, out->first_token_us, out->done_us,
+                        out->prefill_start_us, out->status}))
+    return fail(c, ASC_E_INVAL, "asc_summarize: host and device pointers mixed");
+  for (int64_t** o : outs)
+    if (!same_kind(kind, {*o})) return fail(c, ASC_E_INVAL, "asc_summarize: host and device pointers mixed");
+  asc_status st;
+  if (kind == 1) {
+    st = launch_summary(c, tr, out, sum);
+    if (st) return st;
+    return collect_errors(c, "asc_summarize");
+  }
+  const int32_t T = tr->T;
+  const size_t Tn = (size_t)T, Rn = (size_t)tr->trace_off[T];
+  Stager sg{c};
+  asc_traces dt = *tr;
+  asc_outcomes doc{};
+  asc_summary ds{};
+  st = stage_host(c, sg, [&](Stager& sg) {
+    dt.trace_off = sg.up(tr->trace_off, Tn + 1);
+    dt.arrival_us = sg.up(tr->arrival_us, Rn);
+    dt.prompt_len = nullptr;
+    dt.output_len = sg.up(tr->output_len, Rn);
+    dt.ttft_slo_us = sg.up(tr->ttft_slo_us, Tn);
+    dt.tbt_slo_us = sg.up(tr->tbt_slo_us, Tn);
+    dt.req_ttft_slo_us = sg.up(tr->req_ttft_slo_us, Rn);
+    dt.n_lp = sg.up(tr->n_lp, Tn);
+    dt.n_hp = nullptr;
+    dt.req_key_offset_us = nullptr;
+    doc.first_token_us = sg.up(out->first_token_us, Rn);
+    doc.done_us = sg.up(out->done_us, Rn);
+    doc.prefill_start_us = sg.up(out->prefill_start_us, Rn);
+    doc.status = sg.up(out->status, Rn);
+    int64_t** douts[] = {&ds.completed, &ds.dropped, &ds.violating, &ds.tokens, &ds.ttft_p50_us,
+                         &ds.ttft_p90_us, &ds.ttft_p99_us, &ds.tbt_sum_us, &ds.tbt_tokens,
+                         &ds.delay_sum_lp_us, &ds.delay_cnt_lp, &ds.delay_sum_hp_us,
+                         &ds.delay_cnt_hp, &ds.last_done_us};
+    for (int k = 0; k < 14; k++) *douts[k] = sg.out(*outs[k], Tn);
+  });
+  if (st) return st;
+  st = launch_summary(c, &dt, &doc, &ds);
+  if (st) return st;
+  return finish_host(c, sg, "asc_summarize");
+}
+
 asc_status asc_fit_perf(asc_ctx* c, const asc_fit_in* in, double lambda, double* coef,
                         double* mean_err, double* max_err) {
   if (!c || !in || !coef) return fail(c, ASC_E_INVAL, "asc_fit_perf: NULL argument");

@@ -52,6 +52,8 @@ asc_status launch_schedule_step(asc_ctx* c, const asc_step_in* in, asc_step_out*
 asc_status launch_simulate(asc_ctx* c, const asc_traces* tr, asc_outcomes* out, int64_t R);
 asc_status launch_goodput(asc_ctx* c, const asc_traces* tr, const asc_outcomes* out,
                           uint64_t* good, uint64_t* total);
+asc_status launch_summary(asc_ctx* c, const asc_traces* tr, const asc_outcomes* out,
+                          asc_summary* s);
 asc_status launch_fit(asc_ctx* c, const asc_fit_in* in, int64_t N, double lambda, double* coef,
                       double* mean_err, double* max_err);
 asc_status launch_latency(asc_ctx* c, int64_t n, const uint64_t* F, const uint64_t* M, int64_t* lat,

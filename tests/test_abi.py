@@ -24,7 +24,7 @@ def test_exports_every_declared_symbol():
     assert set(names) == set(asc.EXPORTS)
     for n in names:
         assert hasattr(L, n), n
-    assert L.asc_abi_version() == 2
+    assert L.asc_abi_version() == 3
 
 
 def test_struct_layout_matches_header():
