@@ -48,6 +48,7 @@ def args_():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-step-bench", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--config4", action="store_true", help="also time BASELINE config 4 in full")
     return ap.parse_args()
 
 
@@ -60,12 +61,23 @@ def peaks():
     return FALLBACK_HBM, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
+NCU_TRAFFIC = os.path.join(ROOT, "profiles", "ncu_traffic_r02.json")
+
+
 def ncu_traffic(kernel):
-    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-    if os.path.exists(p):
-        with open(p) as f:
-            return json.load(f).get(kernel)
+    """{"bytes": dram read+write bytes per launch, "inst": warp-instructions per launch (optional),
+    "source": capture} from one ncu capture of the same launch configuration at this round's code
+    (profiles/ncu_traffic_r02.json, written by tools/ncu_traffic.py), or None."""
+    if os.path.exists(NCU_TRAFFIC):
+        with open(NCU_TRAFFIC) as f:
+            v = json.load(f).get(kernel)
+        return v if isinstance(v, dict) else None
     return None
+
+
+def traffic_bytes(kernel):
+    v = ncu_traffic(kernel)
+    return v.get("bytes") if v else None
 
 
 class Clocks:
@@ -103,20 +115,41 @@ class Clocks:
 
 
 def load(name, rank, world, n, traces):
+    """-> (cfg, batch, desc, point_of_trace, grid) where grid describes the (QPS, SLO-scale) points."""
     if name == "config3":
         cfg, b = P.workload("config3", n=n, max_traces=traces, base_seed=1 + rank)
-        desc = f"config3 (4096 traces x 10k ShareGPT-shaped req, 2L1H, seed {1 + rank}"
+        desc = f"config3 (4096 traces x 10k ShareGPT-shaped req, 2L1H, calibrated perf preset, seed {1 + rank}"
         desc += ")" if world == 1 else f", one grid per rank: {world} x 4096 traces)"
-        return cfg, b, desc
-    if name == "config5":   # 65536 traces x 100k sharded i = rank mod world
+        grid = dict(n_qps=16, n_scale=16, qps=[(q + 1) / 2 for q in range(16)],
+                    scale=[(k + 1) / 4 for k in range(16)], scale1=3)
+    elif name == "config5":   # 65536 traces x 100k sharded i = rank mod world
         cfg, full = P.workload("config5", n=1, max_traces=traces)
         idx = list(range(rank, full.T, world))   # only this rank's grid points are generated
         cfg, b = P.workload("config5", n=n or 100_000, max_traces=traces, select=idx)
-        return cfg, b, f"config5 shard {rank}/{world}"
-    if name in ("config1", "config2", "config4"):
+        desc = f"config5 shard {rank}/{world} (calibrated perf preset)"
+        grid = dict(n_qps=64, n_scale=64, qps=[(q + 1) / 8 for q in range(64)],
+                    scale=[(k + 1) / 16 for k in range(64)], scale1=15)
+    elif name in ("config1", "config2", "config4"):
         cfg, b = P.workload(name, n=n, max_traces=traces, base_seed=1 + rank)
-        return cfg, b, name
-    raise SystemExit(f"unknown workload {name}")
+        desc = f"{name} ({P.DEFAULT_PERF[name]} perf preset)"
+        grid = None
+    else:
+        raise SystemExit(f"unknown workload {name}")
+    tidx = np.array([int(l.split(":")[0][1:]) for l in b.labels], np.int64)
+    point = tidx // 16 if grid else tidx
+    return cfg, b, desc, point, grid
+
+
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+    return platform.processor() or "unknown"
 
 
 def cpu_baseline(cfg, batch, budget_s=20.0):
@@ -132,6 +165,7 @@ def cpu_baseline(cfg, batch, budget_s=20.0):
     dt = time.perf_counter() - t0
     dec = int(out["decisions"].sum())
     return {"value": dec / dt, "unit": UNIT, "cores": min(cores, len(idx)), "kind": "oracle",
+            "cpu_model": cpu_model(),
             "sample": f"{len(idx)} of {T} traces (stratified over the QPS x SLO grid), "
                       f"{sub.R} requests, {dec} decisions in {dt:.2f} s",
             "simulated_req_per_s": sub.R / dt,
@@ -142,7 +176,7 @@ def reference_arm(a):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    cfg, b, desc = load(a.workload, 0, 1, a.requests, a.traces)
+    cfg, b, desc, _, _ = load(a.workload, 0, 1, a.requests, a.traces)
     from oracle import oracle as O
     cores = os.cpu_count() or 1
     per_step = min(b.T, max(4, cores))
@@ -166,6 +200,7 @@ def reference_arm(a):
             "config": {"workload": desc, "sample_traces_per_step": per_step},
             "simulated_req_per_s": sum(reqs) / sum(secs),
             "cpu_baseline": {"value": v, "unit": UNIT, "kind": "oracle", "cores": min(cores, per_step),
+                             "cpu_model": cpu_model(),
                              "sample": f"{per_step} random traces of {b.T} per step"},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -230,7 +265,7 @@ def step_microbench(asc, torch, dev, stream, warmup, steps, hbm_peak):
             "ms_per_call": ms, "evaluations_per_s": Q / (ms * 1e-3),
             "admitted": int(out["admit_cnt"].sum()), "offloaded": int(out["offload_cnt"].sum()),
             "roofline": {"bound": "hbm", "achieved": ach_k1, "peak": hbm_peak, "unit": "GB/s",
-                         "frac": ach_k1 / hbm_peak, "traffic": ncu_traffic("k1_tasks"),
+                         "frac": ach_k1 / hbm_peak, "traffic": traffic_bytes("k1_tasks"),
                          "kernel": "k1_tasks (streaming pass; finishes every single-task segment)",
                          "algorithmic_bytes": byts, "kernel_ms": k1ms, "kernel_share": k1ms / ms},
             "whole_call": {"achieved": ach_call, "unit": "GB/s", "frac": ach_call / hbm_peak,
@@ -238,15 +273,76 @@ def step_microbench(asc, torch, dev, stream, warmup, steps, hbm_peak):
             "other_shapes": others}
 
 
+def maybe_spawn(a):
+    """`bench.py --gpus N` without torchrun: re-launch under torch.distributed.run with N ranks."""
+    if a.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        import socket
+        sk = socket.socket()
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+        sk.close()
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+               f"--nproc-per-node={a.gpus}", "--master-addr", "127.0.0.1", "--master-port",
+               str(port), os.path.abspath(__file__)] + sys.argv[1:]
+        os.execv(sys.executable, cmd)
+
+
+def grid_report(grid, tab, rows_all, point_all):
+    """Per-grid-point table (all ranks) -> the goodput surface and the SLO-scale-1 row."""
+    from paper_2504_20828_b200 import dist as D
+    col = {k: tab[:, j].astype(np.float64) for j, k in enumerate(D.POINT_COUNTERS)}
+    nq, ns = grid["n_qps"], grid["n_scale"]
+    div = lambda x, y: np.where(y > 0, x / np.maximum(y, 1), np.nan)
+    gp = div(col["good"], col["total"]).reshape(nq, ns)
+    s1 = grid["scale1"]
+    at = lambda v: [None if not np.isfinite(x) else round(float(x), 4) for x in v.reshape(nq, ns)[:, s1]]
+    # p99 TTFT per point: median over the point's traces of the per-trace nearest-rank p99
+    p99 = np.full(nq * ns, np.nan)
+    for pnt in np.unique(point_all):
+        v = rows_all[point_all == pnt, 1]
+        v = v[v >= 0]
+        if len(v):
+            p99[pnt] = np.median(v) / 1e3
+    ev_req = div(col["evaluations"], col["total"])
+    batch = div(col["tokens"], col["decisions"])
+    over = slice(nq // 2, nq)
+    return {
+        "qps": grid["qps"], "slo_scale": grid["scale"],
+        "goodput_surface": [[None if not np.isfinite(x) else round(float(x), 3) for x in r] for r in gp]
+        if nq * ns <= 256 else "omitted (see at_slo_scale_1)",
+        "at_slo_scale_1": {
+            "goodput": at(div(col["good"], col["total"])),
+            "evaluations_per_request": at(ev_req), "decisions_per_request": at(div(col["decisions"], col["total"])),
+            "mean_batch_requests": at(batch), "p99_ttft_ms_median_over_seeds": at(p99),
+            "mean_tbt_ms": at(div(col["tbt_sum_us"], col["tbt_tokens"]) / 1e3),
+            "sched_delay_lp_ms": at(div(col["delay_sum_lp_us"], col["delay_cnt_lp"]) / 1e3),
+            "sched_delay_hp_ms": at(div(col["delay_sum_hp_us"], col["delay_cnt_hp"]) / 1e3),
+            "dropped_frac": at(div(col["dropped"], col["total"]))},
+        "overloaded_half_at_scale_1": {
+            "qps": grid["qps"][nq // 2:],
+            "evaluations_per_request": round(float(np.nansum(col["evaluations"].reshape(nq, ns)[over, s1])
+                                                   / np.nansum(col["total"].reshape(nq, ns)[over, s1])), 2),
+            "mean_batch_requests": round(float(np.nansum(col["tokens"].reshape(nq, ns)[over, s1])
+                                               / np.nansum(col["decisions"].reshape(nq, ns)[over, s1])), 2)},
+        "mean_batch_requests_all": round(float(col["tokens"].sum() / max(col["decisions"].sum(), 1)), 2),
+        "evaluations_per_request_all": round(float(col["evaluations"].sum() / max(col["total"].sum(), 1)), 2),
+        "note": "mean batch = generated tokens / non-empty formations (every batch member emits one token)",
+    }
+
+
 def main():
     a = args_()
+    maybe_spawn(a)
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != a.gpus:
+        raise SystemExit(f"bench.py: --gpus {a.gpus} but WORLD_SIZE={world}")
     if a.impl == "reference":
         return reference_arm(a)
     import torch
     from paper_2504_20828_b200 import asc
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    from paper_2504_20828_b200 import dist as D
     assert torch.cuda.is_available(), "bench.py needs CUDA (no CPU fallback)"
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
@@ -254,20 +350,25 @@ def main():
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=dev)
     hbm_peak, peak_src = peaks()
-    cfg, batch, desc = load(a.workload, rank, world, a.requests, a.traces)
+    cfg, batch, desc, point, grid = load(a.workload, rank, world, a.requests, a.traces)
     stream = torch.cuda.Stream(device=dev)
     ctx = asc.Context(cfg, local, stream)
     tr = asc.batch_arrays(batch, dev)
     out = ctx.simulate_batch(tr)
     res = {k: torch.empty(max(batch.T, 1), dtype=torch.int64, device=dev) for k in ("good", "total")}
+    summ = {k: torch.empty(max(batch.T, 1), dtype=torch.int64, device=dev) for k in asc.SUMMARY_KEYS}
     ctx.goodput(tr, out, res=res)
+    ctx.summarize(tr, out, res=summ)
 
     def step():
+        # one pass of the hot path: simulate (rows a1-a7) + goodput and outcome summary (row a8)
         ctx.simulate_batch(tr, out=out)
         sim_ms = ctx.last_kernel_ms()
         l1 = ctx.last_launches()
         ctx.goodput(tr, out, res=res)
-        return sim_ms, l1 + ctx.last_launches()
+        l2 = ctx.last_launches()
+        ctx.summarize(tr, out, res=summ)
+        return sim_ms, l1 + l2 + ctx.last_launches()
 
     for _ in range(max(0, a.warmup - 1)):
         step()
@@ -291,22 +392,26 @@ def main():
     barrier()
     clocks = clk.stop()
     ms_total = e0.elapsed_time(e1)
-    dec = int(out["decisions"][:batch.T].sum().item())
-    evals = int(out["evaluations"][:batch.T].sum().item())
-    st = out["status"][:batch.R].cpu().numpy().view(np.uint32) & 3
-    finished = int((st != 0).sum())
-    good = int(res["good"][:batch.T].cpu().numpy().view(np.uint64).sum())
-    total = int(res["total"][:batch.T].cpu().numpy().view(np.uint64).sum())
-    from paper_2504_20828_b200 import dist as D
-    tot = D.reduce_counters(dict(decisions=dec, evaluations=evals, finished=finished, good=good,
-                                 total=total, requests=batch.R), dev)
-    dec_all, evals_all, fin_all = tot["decisions"], tot["evaluations"], tot["finished"]
-    good_all, total_all = tot["good"], tot["total"]
+    T = batch.T
+    host = lambda x: x[:T].cpu().numpy()
+    per_trace = {k: host(summ[k]) for k in asc.SUMMARY_KEYS}
+    per_trace.update(good=host(res["good"]), total=host(res["total"]), decisions=host(out["decisions"]),
+                     evaluations=host(out["evaluations"]),
+                     finished=per_trace["completed"] + per_trace["dropped"])
+    n_points = (grid["n_qps"] * grid["n_scale"]) if grid else int(point.max()) + 1
+    tab = D.reduce_points(D.point_counters(point, n_points, per_trace), dev)
+    rows = np.stack([host(out["digest"]), per_trace["ttft_p99_us"], point], 1)
+    parts = D.gather_rows(rows, dev)
+    rows_all = np.concatenate(parts, 0)
+    col = {k: int(tab[:, j].sum()) for j, k in enumerate(D.POINT_COUNTERS)}
+    dec_all, evals_all, fin_all = col["decisions"], col["evaluations"], col["finished"]
     ms_step = D.reduce_max(ms_total, dev) / a.steps
     value = dec_all / (ms_step * 1e-3)
     sim_ms = float(np.mean(sims))
-    algo = 44 * batch.R + 12 * evals          # per launch on this rank
+    evals = int(per_trace["evaluations"].sum())
+    algo = 44 * batch.R + 12 * evals          # SURVEY §8(d)'s figure, this rank
     ach = algo / (sim_ms * 1e-3) / 1e9
+    traffic = ncu_traffic("sim_kernel") if a.workload == "config3" else None
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps,
         "warmup": a.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
@@ -314,49 +419,79 @@ def main():
         "config": {"workload": desc, "traces_per_gpu": batch.T, "requests_per_gpu": batch.R,
                    "parallelism": f"dp{world} (independent traces, no data-path collective)",
                    "l2": "inputs+workspace > 126 MB L2 (no flush needed)",
-                   "perf_model": "Mistral-7B shape, A100 caps 312 TF / 2 TB/s, C=(0,1,0,0,3e-4)"},
+                   "perf_model": "Mistral-7B shape, A100 caps 312 TF / 2 TB/s, C=" + str(tuple(cfg["perf"]["c"]))},
         "simulated_req_per_s": fin_all / (ms_step * 1e-3),
         "evaluations_per_s": evals_all / (ms_step * 1e-3),
-        "goodput": good_all / max(total_all, 1),
+        "goodput": col["good"] / max(col["total"], 1),
         "gpu_launches": launches,
         "roofline": {"bound": "hbm", "achieved": ach, "peak": hbm_peak, "unit": "GB/s",
-                     "frac": ach / hbm_peak, "traffic": ncu_traffic("sim_kernel"),
+                     "frac": ach / hbm_peak, "traffic": traffic.get("bytes") if traffic else None,
                      "kernel": "sim_kernel (event loop)", "peak_source": peak_src,
-                     "note": "not HBM-bound: a sequential event chain per trace, instruction-fetch "
-                             "bound (ncu no_instruction stalls, profiles/r01f_sim_kernel_ncu_full.md); "
-                             "traffic is register-spill / call-save stack traffic, not data",
+                     "note": "algorithmic bytes = SURVEY 8(d)'s 44 B per request + 12 B per queued-request "
+                             "evaluation; the sorted-queue kernel touches O(admitted + offloaded) entries per "
+                             "formation, not every queued one, so this credits reads it does not make (an "
+                             "upper bound); traffic = ncu dram bytes of one launch (profiles/ncu_traffic.json). "
+                             "The event loop is a dependent chain per trace: issue-bound, see issue_roofline",
                      "algorithmic_bytes": algo, "kernel_ms": sim_ms,
                      "kernel_share": sim_ms / ms_step},
         "clocks": clocks,
     }
-    inst = ncu_traffic("sim_kernel_inst") if (a.workload == "config3" and a.requests is None
-                                              and a.traces is None and rank == 0) else None
-    if inst:  # the bound that applies to the event loop: instruction issue
-        sms = torch.cuda.get_device_properties(dev).multi_processor_count
-        mhz = clocks.get("sm_max_mhz") or 1965.0
-        ipk = 4 * sms * mhz * 1e6          # 4 schedulers per SM, 1 warp-instruction per cycle each
-        ach_i = inst / (sim_ms * 1e-3)
-        line["issue_roofline"] = {"bound": "issue", "achieved": ach_i, "peak": ipk, "unit": "warp-inst/s",
-                                  "frac": ach_i / ipk, "inst_per_launch": inst,
-                                  "source": "smsp__inst_executed.sum of one config-3 launch (ncu, "
-                                            "profiles/ncu_traffic.json) over the live kernel time; peak = "
-                                            "4 schedulers x SMs x max SM clock"}
+    if grid:
+        line["grid"] = grid_report(grid, tab, rows_all, rows_all[:, 2])
+    if traffic:
+        line["roofline"]["traffic_source"] = traffic.get("source")
+        inst = traffic.get("inst")
+        if inst:
+            sms = torch.cuda.get_device_properties(dev).multi_processor_count
+            mhz = (clocks or {}).get("sm_max_mhz") or 1965.0
+            ipk = 4 * sms * mhz * 1e6          # 4 schedulers per SM, 1 warp-instruction per cycle each
+            ach_i = inst / (sim_ms * 1e-3)
+            line["issue_roofline"] = {"bound": "issue", "achieved": ach_i, "peak": ipk, "unit": "warp-inst/s",
+                                      "frac": ach_i / ipk, "inst_per_launch": inst,
+                                      "source": traffic.get("source") + " (smsp__inst_executed.sum of one launch) "
+                                                "over the live kernel time; peak = 4 schedulers x SMs x max SM clock"}
     if rank == 0 and not a.no_step_bench:
         line["step_microbench"] = step_microbench(asc, torch, dev, stream, 2, max(3, a.steps), hbm_peak)
     if not a.no_e2e:
-        line["e2e"] = e2e(asc, torch, ctx, batch, world, min(a.steps, 2), dev)
+        line["e2e"] = e2e(asc, torch, ctx, batch, world, max(3, a.steps), dev)
     if rank == 0 and not a.no_fit_bench:
         line["fit_microbench"] = fit_microbench(asc, torch, dev, stream, hbm_peak)
         line["latency_microbench"] = latency_microbench(asc, torch, dev, stream, hbm_peak)
+    ctx.close()
     if rank == 0 and not a.no_baselines:
-        line["baselines"] = baselines(asc, torch, dev, stream, cfg, batch, good_all / max(total_all, 1))
+        line["baselines"] = baselines(asc, torch, dev, stream, cfg, batch, col["good"] / max(col["total"], 1))
+    if rank == 0 and a.config4:
+        line["config4"] = config4_line(asc, torch, dev, stream, hbm_peak)
     if rank == 0 and world == 1 and not a.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(cfg, batch)
-    ctx.close()
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
         torch.distributed.destroy_process_group()
+
+
+def config4_line(asc, torch, dev, stream, hbm_peak):
+    """BASELINE config 4 in full: one LongBench-shaped trace of 10^6 requests at QPS 12 (~2x the
+    2L1H saturation), deep queues; one timed asc_simulate_batch + asc_goodput."""
+    cfg, b = P.workload("config4")
+    ctx = asc.Context(cfg, dev.index, stream)
+    tr = asc.batch_arrays(b, dev)
+    out = ctx.simulate_batch(tr)
+    ms = ctx.last_kernel_ms()
+    good, total = ctx.goodput(tr, out)
+    dec = int(out["decisions"][:1].sum().item())
+    ev = int(out["evaluations"][:1].sum().item())
+    g = int(good[:1].cpu().numpy().view(np.uint64)[0])
+    t = int(total[:1].cpu().numpy().view(np.uint64)[0])
+    ctx.close()
+    tr_ = traffic_bytes("sim_kernel_config4")
+    return {"workload": "config4: 1 trace, 10^6 LongBench-shaped requests, 2L1H, QPS 12, roofline preset",
+            "kernel_ms": ms, "decisions": dec, "evaluations": ev,
+            "decisions_per_s": dec / (ms * 1e-3), "evaluations_per_s": ev / (ms * 1e-3),
+            "simulated_req_per_s": b.R / (ms * 1e-3), "goodput": g / max(t, 1),
+            "algorithmic_gbs": (44 * b.R + 12 * ev) / (ms * 1e-3) / 1e9,
+            "dram_bytes": tr_,
+            "note": "one trace = one warp's sequential event chain"}
 
 
 def latency_microbench(asc, torch, dev, stream, hbm_peak, n=1 << 26, steps=5):
@@ -418,7 +553,7 @@ def fit_microbench(asc, torch, dev, stream, hbm_peak, groups=1024, per=65536, st
             "gpu_launches_per_call": launches / steps,
             "median_in_sample_rel_err": float(np.median(me.cpu().numpy())),
             "roofline": {"bound": "hbm", "achieved": ach, "peak": hbm_peak, "unit": "GB/s",
-                         "frac": ach / hbm_peak, "traffic": ncu_traffic("fit_partials"),
+                         "frac": ach / hbm_peak, "traffic": traffic_bytes("fit_partials"),
                          "kernel": "fit_partials (features + Gram partials, one HBM pass)",
                          "algorithmic_bytes": byts, "kernel_ms": kms, "kernel_share": kms / call_ms}}
 

@@ -6,7 +6,7 @@ mkdir -p xlib
 while [ $# -gt 0 ]; do
   name=$1; defs=$2; shift 2
   /usr/local/cuda/bin/nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC \
-    -shared -cudart static -fmad=false $defs paper_2504_20828_b200/csrc/{asc_api,step,sim,fit}.cu -o xlib/$name.so &
+    -shared -cudart static -fmad=false $defs paper_2504_20828_b200/csrc/{asc_api,step,sim,fit,summary}.cu -o xlib/$name.so &
 done
 wait
 ls -la xlib
