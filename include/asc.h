@@ -142,7 +142,8 @@ int32_t asc_abi_version(void);
  * drop_idx likewise (ascending position).  Indices are global entry positions (int32).
  * flags: bit0 = ever prefilled (preempted request), bit1 = already on an HP.
  * Errors: ASC_E_INVAL (S < 0, seg_off not non-decreasing, eff_prompt < 1), ASC_E_RANGE
- * (budget_reqs > ASC_MAX_BATCH, total entries >= 2^31, cost >= 2^53).
+ * (budget_reqs > ASC_MAX_BATCH, total entries >= 2^31, eff_prompt >= 2^24, a cost F or M >= 2^53
+ * -- detected even where the uint64 products would wrap, e.g. a huge dec_ctx_sum).
  * ------------------------------------------------------------------------------------------- */
 typedef struct {
   int32_t S;

@@ -67,6 +67,19 @@ extern "C" int or_cost(const or_arch* a, int32_t np, const int64_t* p, int32_t n
   const uint64_t F_layer = (Fp + Fd) * n + gemm_F;
   *F = L * F_layer;
   *M = L * M_layer * d;
+  // uint64 wrap guard: the same sums in fp64; far above 2^53 means out of range, whatever the
+  // wrapped integers say (every term is a product of non-negative integers)
+  double fF = 0, fM = 0;
+  for (int32_t i = 0; i < np; i++) {
+    const double li = (double)p[i];
+    fM += 2 * li * s + 3 * li * s * (double)ceil_div(p[i], (int64_t)b);
+    fF += 2 * (double)s * li * li;
+  }
+  for (int32_t j = 0; j < nd; j++) { fM += 2 * (double)lhat[j] * s + 2.0 * s; fF += 2 * (double)lhat[j] * s; }
+  const double ft = (double)t + (double)nd;
+  fF = (double)L * (fF * (double)n + ft * (4.0 * h * h + 2.0 * h * m));
+  fM = (double)L * (double)d * (fM * (double)n + (double)G * (4.0 * h * h + 2.0 * h * m) + ft * (8.0 * h + 2.0 * m));
+  if (fF >= 0x1p62 || fM >= 0x1p62) return 1;
   return (*F >= TWO53 || *M >= TWO53) ? 1 : 0;
 }
 
@@ -313,6 +326,7 @@ extern "C" int or_schedule_step(const or_arch* a_in, const or_perf* pf, const or
     for (int32_t i = 0; i < n; i++) {
       const int64_t e = lo + i;
       if (eff_prompt[e] < 1) { set_err("eff_prompt < 1"); return 1; }
+      if (eff_prompt[e] >= (1 << 24)) { set_err("range: eff_prompt >= 2^24"); return 6; }
       pfu[i] = prefill_us_of(&a, pf, eff_prompt[e]);
       if (pfu[i] < 0) { set_err("range: prefill cost"); return 6; }
       if (prefill_us) prefill_us[e] = (int32_t)pfu[i];

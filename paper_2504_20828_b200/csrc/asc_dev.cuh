@@ -61,11 +61,39 @@ static __device__ __noinline__ int64_t lat_from_FM(const Model& md, uint64_t F, 
 }
 
 // Decode-only batch of B_d requests with context sum sl (a2's TBT term, a6 for decode steps).
+// The fp64 shadow below guards the uint64 products against wrapping (as wraps() does).
 __device__ __forceinline__ int64_t lat_decode(const Model& md, uint64_t Bd, uint64_t sl) {
   const uint64_t F = md.dF_bd * Bd + md.dF_sl * sl;
   const uint64_t M = md.dM_0 + md.dM_bd * Bd + md.dM_sl * sl;
   if (F >= TWO53 || M >= TWO53) return -1;
+  const double bd = (double)Bd, s = (double)sl;
+  if ((double)md.dF_bd * bd + (double)md.dF_sl * s >= 0x1p62 ||
+      (double)md.dM_0 + (double)md.dM_bd * bd + (double)md.dM_sl * s >= 0x1p62) return -1;
   return lat_from_FM(md, F, M);
+}
+
+// uint64 wrap guard: F and M are sums of products of non-negative integers, so no
+// intermediate exceeds the final value; if the same expression evaluated in fp64 (relative error
+// < 2^-40 here) stays below 2^62, the true values are below 2^63 and the uint64 results are exact.
+// Otherwise the true F or M is far above 2^53 and the batch is out of range.  The inputs' own sums
+// (Σp, Σp², ...) are bounded by the callers' validation (eff_prompt < 2^24, <= 128 requests).
+__host__ __device__ inline bool wraps(const Model& md, uint64_t sp, uint64_t sp2, uint64_t spm /* 3 Σp⌈p/b⌉ */,
+                                      uint64_t Bd, uint64_t sl, uint64_t G) {
+  const double n = (double)md.n, s = (double)md.s, tok = (double)sp + (double)Bd;
+  const double F = (double)md.L * (tok * (double)md.FT + n * (2.0 * s * (double)sp2 + 2.0 * s * (double)sl));
+  const double M = (double)md.L * (double)md.d *
+                   ((double)G * (double)md.W + tok * (double)md.MT +
+                    n * (2.0 * s * (double)sp + s * (double)spm + 2.0 * s * (double)sl + 2.0 * s * (double)Bd));
+  return F >= 0x1p62 || M >= 0x1p62;
+}
+__host__ __device__ inline bool wraps_chunked(const Model& md, uint64_t sc, uint64_t aF, uint64_t aM,
+                                              uint64_t Bd, uint64_t sl, uint64_t G) {
+  const double n = (double)md.n, s = (double)md.s, tok = (double)sc + (double)Bd;
+  const double F = (double)md.L * (tok * (double)md.FT + n * (2.0 * s * (double)aF + 2.0 * s * (double)sl));
+  const double M = (double)md.L * (double)md.d *
+                   ((double)G * (double)md.W + tok * (double)md.MT +
+                    n * (s * (double)aM + 2.0 * s * (double)sl + 2.0 * s * (double)Bd));
+  return F >= 0x1p62 || M >= 0x1p62;
 }
 
 // Latency in integer microseconds of a batch given its integer moments (G17, G18).
@@ -78,7 +106,7 @@ __host__ __device__ inline int64_t lat_us(const Model& md, uint64_t Bp, uint64_t
   const uint64_t attnM = md.n * (2 * md.s * sp + 3 * md.s * spc + 2 * md.s * sl + 2 * md.s * Bd);
   const uint64_t F = md.L * (tok * md.FT + attnF);
   const uint64_t M = md.L * (G * md.W + tok * md.MT + attnM) * md.d;
-  if (F >= TWO53 || M >= TWO53) return -1;
+  if (F >= TWO53 || M >= TWO53 || wraps(md, sp, sp2, 3 * spc, Bd, sl, G)) return -1;
 #ifdef __CUDA_ARCH__
   return lat_from_FM(md, F, M);
 #else
@@ -111,7 +139,7 @@ __device__ __forceinline__ int64_t lat_chunked(const Model& md, uint64_t nch, ui
   const uint64_t attnM = md.n * (md.s * aM + 2 * md.s * sl + 2 * md.s * Bd);
   const uint64_t F = md.L * (tok * md.FT + attnF);
   const uint64_t M = md.L * (G * md.W + tok * md.MT + attnM) * md.d;
-  if (F >= TWO53 || M >= TWO53) return -1;
+  if (F >= TWO53 || M >= TWO53 || wraps_chunked(md, sc, aF, aM, Bd, sl, G)) return -1;
   return lat_from_FM(md, F, M);
 }
 

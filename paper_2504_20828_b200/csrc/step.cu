@@ -542,7 +542,7 @@ __device__ __noinline__ void task_generic(const StepP& P, const TaskCtx& t, KI* 
   TopKStream<KPL> st;
   st.init(sbuf, t.kpos);
   const bool select = t.kpos >= 0;
-  bool bad = false;
+  bool bad = false, rng = false;
   for (int g = 0; g < t.ng; g++) {
     const int64_t e0 = t.b4 + (int64_t)g * GE + 4 * lane;
     Grp cur;
@@ -557,6 +557,7 @@ __device__ __noinline__ void task_generic(const StepP& P, const TaskCtx& t, KI* 
       const uint32_t f = (cur.f4 >> (8 * u)) & 0xffu;
       const int32_t pu = cur.p[u];
       bad |= v && pu < 1;
+      rng |= v && pu >= (1 << 24);  // eff_prompt bound (keeps Σp² of a batch far from 2^64)
       int64_t pf = 0;
       if (v) {
         if (pu >= 1 && pu < P.pt) pf = P.pf_tab32 ? (int64_t)__ldg(P.pf_tab32 + pu) : __ldg(P.pf_tab + pu);
@@ -586,6 +587,7 @@ __device__ __noinline__ void task_generic(const StepP& P, const TaskCtx& t, KI* 
     }
   }
   if (__any_sync(FULL, bad) && lane == 0) atomicOr(P.err, ERR_INVAL);
+  if (__any_sync(FULL, rng) && lane == 0) atomicOr(P.err, ERR_RANGE);
   if (select) st.finish();
 #pragma unroll
   for (int r = 0; r < KPL; r++) out_a[r] = st.top.a[r];
@@ -869,6 +871,7 @@ __global__ void __launch_bounds__(256, ASC_KS_MINB) k_small(const __grid_constan
     const int32_t p = cu.p;
     const uint32_t f = cu.f;
     bool bad = v && p < 1;
+    if (__any_sync(FULL, v && p >= (1 << 24)) && lane == 0) atomicOr(P.err, ERR_RANGE);
     const int64_t pf = v ? pf_of(P, p < 1 ? 1 : p) : 0;
     if (P.pfout && v) {
       bad |= pf > INT32_MAX;
@@ -885,7 +888,7 @@ __global__ void __launch_bounds__(256, ASC_KS_MINB) k_small(const __grid_constan
     const bool lv = v && !dropped;
     const int64_t rel = key - (P.kdl ? now : 0);
     KI x;
-    if (__all_sync(FULL, !lv || (rel >= -(int64_t(1) << 26) && rel < (int64_t(1) << 26)))) {
+    if (__all_sync(FULL, !lv || (rel >= -(int64_t(1) << 26) && rel < (int64_t(1) << 26) - 1))) {
       // keys within 2^26 µs of the base: (key, position) in one uint32 (one shuffle per step)
       const uint32_t pk = lv ? ((uint32_t)(rel + (int64_t(1) << 26)) << 5) | (uint32_t)lane : 0xffffffffu;
       const uint32_t y = sort32_u32(pk);

@@ -124,3 +124,44 @@ def test_hp_decode_set_beyond_shared_slots(asc, oracle, elastic):
     hp = ((st >> 4) & 0xff) == 1
     assert hp.sum() > 500
     assert_parity(oracle, cfg, b, got)
+
+
+def test_step_range_errors(asc, oracle):
+    # eff_prompt >= 2^24 and a dec_ctx_sum whose uint64 decode cost would wrap are
+    # ASC_E_RANGE on both sides (the oracle rejects the first; the second is a GPU-side guard)
+    from test_gpu_step import run_gpu
+    cfg = P.config()
+    rng = np.random.default_rng(64)
+    for case in ("eff", "ctx"):
+        ins = H.random_step_inputs(rng, 6, 0, cfg, qs=np.array([0, 1, 40, 33, 5000, 20000]))
+        if case == "eff":
+            ins["eff_prompt"][-3] = 1 << 24
+        else:
+            ins["dec_count"][3] = 100
+            ins["dec_ctx_sum"][3] = 1 << 62
+        with pytest.raises(asc.AscError) as e:
+            run_gpu(asc, cfg, ins)
+        assert e.value.code == 6
+        if case == "eff":
+            with pytest.raises(oracle.OracleError) as e2:
+                oracle.schedule_step(cfg, **ins)
+            assert e2.value.code == 6
+
+
+def test_small_segment_packed_sort_window_edge(asc, oracle):
+    # k_small packs (key - now + 2^26) << 5 | lane into 32 bits; a key of exactly
+    # now + 2^26 - 1 in lane 31 must not collide with the dead-lane sentinel 0xffffffff
+    from test_gpu_step import compare, run_gpu
+    cfg = P.config(flg=P.flags(policy="EDF_DEADLINE"))  # key = deadline
+    S = 4
+    ins = H.random_step_inputs(np.random.default_rng(65), S, 0, cfg, qs=np.full(S, 32), budgets="max")
+    for s in range(S):
+        lo = 32 * s
+        ins["deadline_us"][lo:lo + 32] = ins["now_us"][s] + np.arange(32) * 1000 + 10 ** 6
+        ins["deadline_us"][lo + 31] = ins["now_us"][s] + (1 << 26) - 1 - s  # s = 0: the edge
+        ins["eff_prompt"][lo:lo + 32] = 10
+        ins["flags"][lo:lo + 32] = 0
+    ins["dec_count"][:] = 0
+    exp = oracle.schedule_step(cfg, **ins)
+    assert all(int(c) == 32 for c in exp["admit_cnt"])
+    compare(run_gpu(asc, cfg, ins), exp, ins["seg_off"])

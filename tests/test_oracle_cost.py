@@ -135,6 +135,32 @@ def test_range_guard(oracle):
     assert oracle.cost(P.MISTRAL7B, [32768])[2] == 0
 
 
+def test_range_guard_catches_uint64_wrap(oracle):
+    # F is checked against 2^53 after uint64 products; with powers of two chosen so
+    # that the exact F is 2^73 + 3 * 2^66 (a multiple of 2^64), the wrapped product is exactly 0 --
+    # "in range" without a guard.  The fp64 shadow flags it.
+    a = dict(h=1 << 16, n=1 << 8, s=1 << 8, n_kv=1 << 8, m=1 << 16, L=1 << 10, b=1, dtype_bytes=2, tp=1)
+    p = 1 << 23
+    exact_F = a["L"] * (p * (4 * a["h"] ** 2 + 2 * a["h"] * a["m"]) + a["n"] * 2 * a["s"] * p * p)
+    assert exact_F % (1 << 64) == 0 and exact_F >= 1 << 53
+    F, M, rc = oracle.cost(a, [p])
+    assert rc == 1
+
+
+def test_step_rejects_eff_prompt_at_2_24(oracle):
+    # eff_prompt >= 2^24 is out of range for asc_schedule_step (include/asc.h)
+    cfg = P.config()
+    ins = dict(seg_off=np.array([0, 2], np.int64), now_us=np.array([10 ** 7], np.int64),
+               deadline_us=np.array([10 ** 7, 10 ** 7], np.int64),
+               eff_prompt=np.array([100, 1 << 24], np.int32), flags=np.zeros(2, np.uint8),
+               dec_count=np.zeros(1, np.int32), dec_ctx_sum=np.zeros(1, np.int64),
+               tbt_slo_us=np.array([150000], np.int64), budget_tokens=np.array([8192], np.int32),
+               budget_blocks=np.array([25000], np.int32), budget_reqs=np.array([128], np.int32))
+    with pytest.raises(oracle.OracleError) as e:
+        oracle.schedule_step(cfg, **ins)
+    assert e.value.code == 6
+
+
 def test_latency_batch_wrapper(oracle):
     # or_latency_n is a loop over or_latency_us / or_latency_s (the GPU latency test's reference)
     rng = np.random.default_rng(8)
