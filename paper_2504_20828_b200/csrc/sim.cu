@@ -17,6 +17,7 @@
 // an 8-lane digest update.  Rare paths (admission with a non-empty queue, eviction, drops, HP
 // prefill, offload dispatch, prefill completions) are __noinline__ so the hot loop stays small.
 // The event order is the canonical A-E phase order of DESIGN.md §2.
+#include <cstdlib>
 #include <mutex>
 #include "asc_internal.h"
 
@@ -1615,6 +1616,10 @@ asc_status launch_simulate(asc_ctx* c, const asc_traces* tr, asc_outcomes* out, 
   for (int m = 4; m < minb; m++)
     if ((int64_t)T <= (int64_t)sms * m * SW) { minb = m; break; }
   if (minb < 4) minb = 4;  // (K so large that fewer than 4 CTAs fit: the launch itself reports it)
+  if (const char* f = getenv("ASC_SIM_MINB")) {  // experiments only: force the register budget
+    const int m = atoi(f);
+    if (m >= 4 && m <= 8) minb = m;
+  }
   const bool plain = P.mode == 0 && !tr->n_lp && !tr->n_hp;
   void (*const tab[2][5])() = {
       {sim_kernel<4, false>, sim_kernel<5, false>, sim_kernel<6, false>, sim_kernel<7, false>, sim_kernel<8, false>},
