@@ -152,17 +152,24 @@ def cpu_model():
     return platform.processor() or "unknown"
 
 
-def cpu_baseline(cfg, batch, budget_s=20.0):
-    """The oracle as it stands, on a stratified sample of traces, all host cores."""
+def cpu_baseline(cfg, batch, budget_s=12.0):
+    """The oracle as it stands, on a stratified sample of traces, all host cores.  A probe of
+    2 x cores traces sizes the measured sample to about budget_s seconds of CPU work."""
     from oracle import oracle as O
     cores = os.cpu_count() or 1
     T = batch.T
+
+    def run(m):
+        idx = sorted(set(np.linspace(0, T - 1, m).round().astype(int).tolist()))
+        sub = batch.subset(idx)
+        t0 = time.perf_counter()
+        out = O.simulate_batch(cfg, sub, nthreads=cores)
+        return idx, sub, out, time.perf_counter() - t0
+
     m = min(T, max(4, 2 * cores))
-    idx = sorted(set(np.linspace(0, T - 1, m).round().astype(int).tolist()))
-    sub = batch.subset(idx)
-    t0 = time.perf_counter()
-    out = O.simulate_batch(cfg, sub, nthreads=cores)
-    dt = time.perf_counter() - t0
+    idx, sub, out, dt = run(m)
+    if dt < 0.5 * budget_s and m < T:
+        idx, sub, out, dt = run(min(T, int(m * budget_s / max(dt, 1e-3))))
     dec = int(out["decisions"].sum())
     return {"value": dec / dt, "unit": UNIT, "cores": min(cores, len(idx)), "kind": "oracle",
             "cpu_model": cpu_model(),
@@ -182,12 +189,16 @@ def reference_arm(a):
     per_step = min(b.T, max(4, cores))
     vals, reqs, secs = [], [], []
     rng = np.random.default_rng(0)
+    # each step is a bounded random sample; the first warm-up step sizes it to ~target_s seconds
+    target_s = max(1.0, min(6.0, 150.0 / max(1, a.warmup + a.steps)))
     for step in range(a.warmup + a.steps):
         idx = sorted(rng.choice(b.T, size=per_step, replace=False).tolist())
         sub = b.subset(idx)
         t0 = time.perf_counter()
         out = O.simulate_batch(cfg, sub, nthreads=cores)
         dt = time.perf_counter() - t0
+        if step == 0:
+            per_step = int(min(b.T, max(per_step, per_step * target_s / max(dt, 1e-3))))
         if step >= a.warmup:
             vals.append(int(out["decisions"].sum()))
             reqs.append(sub.R)

@@ -141,7 +141,8 @@ int32_t asc_abi_version(void);
  * same CSR offsets: admit_idx[seg_off[s] + j], j < admit_cnt[s] (priority order); offload_idx and
  * drop_idx likewise (ascending position).  Indices are global entry positions (int32).
  * flags: bit0 = ever prefilled (preempted request), bit1 = already on an HP.
- * Errors: ASC_E_INVAL (S < 0, seg_off not non-decreasing, eff_prompt < 1), ASC_E_RANGE
+ * Errors: ASC_E_INVAL (S < 0, seg_off not non-decreasing, eff_prompt < 1, dec_count > 0 with
+ * dec_ctx_sum < dec_count), ASC_E_RANGE
  * (budget_reqs > ASC_MAX_BATCH, total entries >= 2^31, eff_prompt >= 2^24, a cost F or M >= 2^53
  * -- detected even where the uint64 products would wrap, e.g. a huge dec_ctx_sum).
  * ------------------------------------------------------------------------------------------- */
@@ -155,7 +156,7 @@ typedef struct {
   const int32_t* eff_prompt;     /* [Q] prompt (+ generated tokens after preemption), >= 1 */
   const uint8_t* flags;          /* [Q] */
   const int32_t* dec_count;      /* [S] B_d */
-  const int64_t* dec_ctx_sum;    /* [S] sum of decode contexts lhat */
+  const int64_t* dec_ctx_sum;    /* [S] sum of decode contexts lhat, >= dec_count; ignored when dec_count = 0 */
   const int64_t* tbt_slo_us;     /* [S] */
   const int32_t* budget_tokens;  /* [S] N */
   const int32_t* budget_blocks;  /* [S] M (free KV blocks) */

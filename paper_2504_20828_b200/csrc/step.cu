@@ -206,6 +206,7 @@ __global__ void __launch_bounds__(SCAN_THREADS) plan_small(StepP P) {
 __device__ __forceinline__ int64_t seg_tbt_budget(const StepP& P, int64_t s) {
   const int64_t Bd = P.dcnt[s];
   if (Bd <= 0) return INF64;
+  if (P.dctx[s] < Bd) atomicOr(P.err, ERR_INVAL);  // every context lhat >= 1 (oracle: same error)
   const int64_t d = lat_decode(P.md, (uint64_t)Bd, (uint64_t)P.dctx[s]);
   if (d < 0) { atomicOr(P.err, ERR_RANGE); return INF64; }
   return P.tbt[s] - d;
@@ -218,7 +219,7 @@ __device__ __forceinline__ int finalize_segment(const StepP& P, int64_t s, const
   const int64_t N = P.bN[s], M = P.bM[s];
   int64_t R = P.bR[s];
   if (R > ASC_MAX_BATCH) { atomicOr(P.err, ERR_RANGE); R = ASC_MAX_BATCH; }
-  const int64_t Bd = P.dcnt[s], sl = P.dctx[s];
+  const int64_t Bd = P.dcnt[s], sl = Bd > 0 ? P.dctx[s] : 0;  // no decodes: no context (oracle)
   const int64_t C = seg_tbt_budget(P, s);
   int32_t p[KPL];
   int64_t ct = 0, cb = 0, cc = 0;
@@ -848,7 +849,7 @@ __device__ __forceinline__ void small_load(const StepP& P, int64_t s, SmallIn& x
   x.now = P.now[s];
   x.R = P.bR[s];
   x.Bd = P.dcnt[s];
-  x.sl = P.dctx[s];
+  x.sl = x.Bd > 0 ? P.dctx[s] : 0;  // dec_ctx_sum is ignored without decodes
   x.tbt = P.tbt[s];
   x.N = P.bN[s];
   x.M = P.bM[s];
@@ -911,6 +912,7 @@ __global__ void __launch_bounds__(256, ASC_KS_MINB) k_small(const __grid_constan
     int64_t R = cu.R;
     if (R > ASC_MAX_BATCH) { if (lane == 0) atomicOr(P.err, ERR_RANGE); R = ASC_MAX_BATCH; }
     const int64_t Bd = cu.Bd, sl = cu.sl;
+    if (lane == 0 && Bd > 0 && sl < Bd) atomicOr(P.err, ERR_INVAL);  // every lhat >= 1
     // a6 for every prefix at once: lane j evaluates the batch {first j sorted entries} ∪ D
     // (Eq. 3-5 from the exclusive prefix moments).  Lane 0 is the decode-only batch, whose
     // latency also gives the TBT residual C (G22); the admitted batch is lane k's — one fused

@@ -165,3 +165,20 @@ def test_small_segment_packed_sort_window_edge(asc, oracle):
     exp = oracle.schedule_step(cfg, **ins)
     assert all(int(c) == 32 for c in exp["admit_cnt"])
     compare(run_gpu(asc, cfg, ins), exp, ins["seg_off"])
+
+
+def test_decode_context_sum_below_count_is_inval(asc, oracle):
+    # every decode context lhat >= 1, so dec_ctx_sum >= dec_count (oracle: "dec_ctx_sum < dec_count");
+    # dec_ctx_sum is ignored when dec_count = 0 (test above)
+    from test_gpu_step import run_gpu
+    cfg = P.config()
+    for qs in (np.array([0, 20, 30]), np.array([0, 20, 20000])):   # k_small and k1 segments
+        ins = H.random_step_inputs(np.random.default_rng(66), 3, 0, cfg, qs=qs)
+        ins["dec_count"][2] = 5
+        ins["dec_ctx_sum"][2] = 4
+        with pytest.raises(asc.AscError) as e:
+            run_gpu(asc, cfg, ins)
+        assert e.value.code == 1
+        with pytest.raises(oracle.OracleError) as e2:
+            oracle.schedule_step(cfg, **ins)
+        assert e2.value.code == 1

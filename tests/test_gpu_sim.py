@@ -116,6 +116,16 @@ def test_config4_prefix_50k(asc, oracle):
     assert_parity(oracle, cfg, b, got)
 
 
+@pytest.mark.slow
+def test_config4_prefix_200k(asc, oracle):
+    # a longer deep-queue prefix of config 4 (200,000 requests; the LP and HP
+    # queues grow to ~6,000 entries; the oracle re-sorts them at every formation, ~90 s)
+    cfg, b = P.workload("config4", n=200_000)
+    got = gpu_sim(asc, cfg, b)
+    assert int(got["evaluations"][0]) > 1000 * int(got["decisions"][0])
+    assert_parity(oracle, cfg, b, got)
+
+
 def test_config3_subgrid(asc, oracle):
     cfg, b = P.workload("config3", n=600)
     sub = b.subset(range(0, 4096, 16))          # every 16th grid point: all QPS x SLO scales
