@@ -65,6 +65,8 @@ struct StepP {
   KI* cand;
   uint32_t *moff, *mdrop;
   int32_t *coff, *cdrop;
+  int32_t* redo;       // [S]: short segments k_lane hands to k_small (outside its fast window)
+  int32_t* redo_cnt;
   int* err;
 };
 
@@ -81,6 +83,7 @@ __global__ void plan_counts(StepP P) {
   if (s > P.S) return;
   if (s == P.S) {
     if (P.seg_off[P.S] != P.Q) atomicOr(P.err, ERR_INVAL);
+    *P.redo_cnt = 0;
     P.task_off[s] = 0;
     P.mtask_off[s] = 0;
     return;
@@ -157,6 +160,7 @@ __global__ void __launch_bounds__(SCAN_THREADS) plan_small(StepP P) {
   __shared__ int64_t sa[SCAN_THREADS / 32], sb[SCAN_THREADS / 32];
   const int64_t n = (int64_t)P.S + 1;
   const int64_t base = threadIdx.x * SCAN_ITEMS;
+  if (threadIdx.x == 0) *P.redo_cnt = 0;
   int64_t va[SCAN_ITEMS], vb[SCAN_ITEMS], ta = 0, tb = 0;
 #pragma unroll
   for (int i = 0; i < SCAN_ITEMS; i++) {
@@ -855,15 +859,20 @@ __device__ __forceinline__ void small_load(const StepP& P, int64_t s, SmallIn& x
   x.M = P.bM[s];
 }
 
+// LIST: the segments k_lane handed back (P.redo[0 .. *P.redo_cnt)); otherwise every segment
+template <bool LIST>
 __global__ void __launch_bounds__(256, ASC_KS_MINB) k_small(const __grid_constant__ StepP P) {
   const int lane = lane_id();
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  int64_t s = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nseg = LIST ? (int64_t)*P.redo_cnt : (int64_t)P.S;
+  auto seg_at = [&](int64_t i) -> int64_t { return LIST ? (i < nseg ? (int64_t)P.redo[i] : (int64_t)P.S) : i; };
+  int64_t i = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   SmallIn nx;
-  small_load(P, s, nx);
-  for (; s < P.S; s += nw) {
+  small_load(P, seg_at(i), nx);
+  for (; i < nseg; i += nw) {
+    const int64_t s = seg_at(i);
     const SmallIn cu = nx;
-    small_load(P, s + nw, nx);  // next segment's inputs in flight during this one
+    small_load(P, seg_at(i + nw), nx);  // next segment's inputs in flight during this one
     const int64_t lo = cu.lo, n = cu.n;
     if (n > SMALL || n < 0) continue;  // k1's, or invalid (the planner flags it)
     const bool v = lane < n;
@@ -962,6 +971,203 @@ __global__ void __launch_bounds__(256, ASC_KS_MINB) k_small(const __grid_constan
       }
       P.blat[s] = l;
     }
+  }
+}
+
+// ------------------------------------------------------------- k_lane: one THREAD per segment --
+// Short segments (<= SMALL entries: SURVEY row S's 10^6 x 32 shape, the queue of a real LP
+// instance).  A warp takes 32 consecutive segments, stages their contiguous entry range into shared
+// memory with coalesced 16-byte cp.async copies, and then every lane decides its own segment
+// serially (§5): a1 (prefill table), the key (a2), the drop / offload predicates as
+// 32-bit position masks (a5), a3 as a 32-input bitonic network over packed (key, position) words
+// held in registers, a4 as a strict prefix scan in key order with early exit, and a6 twice
+// (decode-only batch for the TBT residual C, then the admitted batch).  No shuffles and one fp64
+// evaluation per batch instead of one per prefix: about a tenth of k_small's instructions.
+// A lane reads its entries rotated by (lane mod n) so that equal-length neighbours hit distinct
+// shared-memory banks.  Segments outside the fast window (p outside [1, 2^17], a prefill >= 2^30 µs,
+// a live key more than 2^26 µs from now, R > ASC_MAX_BATCH, an invalid decode count / context) or
+// in a group whose entry range exceeds the staging buffer go to P.redo; k_small<true> decides them
+// (and raises their errors) afterwards.
+constexpr int LW = 4;             // k_lane CTA size (warps); 4 CTAs/SM
+constexpr int LCAP = 32 * SMALL;  // staged entries per warp (32 segments of <= SMALL)
+struct __align__(16) LaneStage {
+  int64_t dl[LCAP + 2];    // chunk-aligned copies (first chunk aligned down to 16 bytes); after
+  int32_t eff[LCAP + 4];   // pass 1 the low word of dl[e] holds prefill_us of entry e
+  uint8_t fl[LCAP + 16];
+};
+static_assert(sizeof(int64_t) * (LCAP + 2) % 16 == 0 && sizeof(int32_t) * (LCAP + 4) % 16 == 0, "16-byte aligned rows");
+
+// copy g[lo0, hi) into dst (16-byte chunks from the aligned-down start a0); returns a0.  Chunks that
+// cross [0, Q) are copied element by element.
+template <typename T>
+__device__ __forceinline__ int64_t lane_stage(T* dst, const T* g, int64_t lo0, int64_t hi, int64_t Q) {
+  constexpr int K = 16 / sizeof(T);
+  const int64_t a0 = lo0 - (int64_t)(((uintptr_t)(g + lo0) & 15) / sizeof(T));
+  const int nch = (int)((hi - a0 + K - 1) / K);
+  for (int c = lane_id(); c < nch; c += 32) {
+    const int64_t e = a0 + (int64_t)c * K;
+    if (e >= 0 && e + K <= Q) {
+      cp_async16(dst + c * K, g + e);
+    } else {
+#pragma unroll
+      for (int u = 0; u < K; u++)
+        if (e + u >= 0 && e + u < Q) dst[c * K + u] = g[e + u];
+    }
+  }
+  return a0;
+}
+
+// decide segment s (entries [lo, lo + n), staged at st with chunk bases a0d / a0e / a0f); false if
+// the segment is outside the fast window (nothing written yet)
+__device__ __forceinline__ bool lane_segment(const StepP& P, LaneStage& st, int64_t s, int64_t lo, int n,
+                                             int64_t a0d, int64_t a0e, int64_t a0f) {
+  const int32_t R = P.bR[s], Bd = P.dcnt[s];
+  const int64_t sl = Bd > 0 ? P.dctx[s] : 0;  // dec_ctx_sum is ignored without decodes
+  if (R > ASC_MAX_BATCH || Bd < 0 || (Bd > 0 && sl < Bd)) return false;
+  const int64_t now = P.now[s];
+  const int od = (int)(lo - a0d), oe = (int)(lo - a0e), of = (int)(lo - a0f);
+  int32_t* pfs = reinterpret_cast<int32_t*>(st.dl);  // pf of entry j at pfs[2 * (od + j)]
+  const int rot = n > 0 ? lane_id() % n : 0;
+  uint32_t a[SMALL];
+  uint32_t dm = 0, om = 0;
+  bool ok = true;
+  const int64_t othr = P.W + P.margin;
+  // pass 1: a1, key, drop / offload candidates (position order is kept in the masks)
+#pragma unroll
+  for (int j = 0; j < SMALL; j++) {
+    a[j] = 0xffffffffu;
+    if (j < n) {
+      int jj = j + rot;
+      jj -= jj >= n ? n : 0;
+      const int64_t dl = st.dl[od + jj];
+      const int32_t p = st.eff[oe + jj];
+      const uint32_t f = st.fl[of + jj];
+      const int32_t pf = __ldg(P.pf_fast + ((p - 1) & (PFT_N - 1)));
+      ok &= (uint32_t)(p - 1) < (uint32_t)PFT_N && pf < (1 << 30);
+      const bool dropped = P.drop && !(f & 1u) && now > dl;
+      const bool offc = P.offl && !dropped && !(f & 3u) && dl - now <= (int64_t)pf + othr;
+      const int64_t rel = (P.kdl ? dl - now : 0) + (int64_t)(P.kpf * pf);
+      ok &= dropped || (rel >= -(int64_t(1) << 26) && rel < (int64_t(1) << 26) - 1);
+      a[j] = dropped ? 0xffffffffu : ((uint32_t)(rel + (int64_t(1) << 26)) << 5) | (uint32_t)jj;
+      dm |= (uint32_t)dropped << jj;
+      om |= (uint32_t)offc << jj;
+      pfs[2 * (od + jj)] = pf;  // this lane's own entry: the deadline is not read again
+    }
+  }
+  if (!ok) return false;
+  // a3: ascending (key, position); dropped entries (all ones) sort last
+#pragma unroll
+  for (int k = 2; k <= SMALL; k <<= 1)
+#pragma unroll
+    for (int j = k >> 1; j > 0; j >>= 1)
+#pragma unroll
+      for (int i = 0; i < SMALL; i++) {
+        const int l = i ^ j;
+        if (l > i) {
+          const uint32_t x = a[i], y = a[l];
+          const bool up = (i & k) == 0;
+          a[i] = up ? min(x, y) : max(x, y);
+          a[l] = up ? max(x, y) : min(x, y);
+        }
+      }
+  // C: TBT residual after the decode-only batch (G22)
+  int64_t C = INF64, d = 0;
+  if (Bd > 0) {
+    d = lat_us(P.md, 0, 0, 0, 0, (uint64_t)Bd, (uint64_t)sl);
+    if (d < 0) atomicOr(P.err, ERR_RANGE);
+    C = P.tbt[s] - d;
+  }
+  // a4: Algorithm 1 lines 5-13, strict budgets in key order
+  const int32_t N = P.bN[s], M = P.bM[s];
+  const uint32_t bs = (uint32_t)P.bs, ab = (uint32_t)P.md.b;
+  int32_t St = 0, Sb = 0;
+  int64_t Sc = 0;
+  int k = 0;
+  uint32_t am = 0;
+  uint64_t sp = 0, sp2 = 0, spc = 0;
+#pragma unroll
+  for (int j = 0; j < SMALL; j++) {
+    const uint32_t x = a[j];
+    if (x == 0xffffffffu || j >= R) break;
+    const int pos = (int)(x & 31u);
+    const int32_t p = st.eff[oe + pos];
+    St += p;
+    Sb += (int32_t)(((uint32_t)p + bs) / bs);
+    Sc += pfs[2 * (od + pos)];
+    if (!(St < N && Sb < M && Sc < C)) break;
+    P.admit_idx[lo + j] = (int32_t)(lo + pos);
+    am |= 1u << pos;
+    k = j + 1;
+    const uint64_t q = (uint64_t)p;
+    sp += q;
+    sp2 += q * q;
+    spc += q * (uint64_t)(((uint32_t)p + ab - 1u) / ab);
+  }
+  // a6: the hybrid batch {admitted} + {decodes}
+  int64_t l = 0;
+  if (k > 0 || Bd > 0) {
+    l = k ? lat_us(P.md, (uint64_t)k, sp, sp2, spc, (uint64_t)Bd, (uint64_t)sl) : d;
+    if (l < 0) atomicOr(P.err, ERR_RANGE);
+  }
+  // a5: offload (not admitted) and drop lists in ascending position
+  uint32_t mo = om & ~am;
+  int co = 0, cd = 0;
+  while (mo) {
+    P.off_idx[lo + co++] = (int32_t)(lo + __ffs(mo) - 1);
+    mo &= mo - 1;
+  }
+  while (dm) {
+    P.drop_idx[lo + cd++] = (int32_t)(lo + __ffs(dm) - 1);
+    dm &= dm - 1;
+  }
+  if (P.pfout)
+    for (int j = 0; j < n; j++) P.pfout[lo + j] = pfs[2 * (od + j)];
+  P.admit_cnt[s] = k;
+  P.off_cnt[s] = co;
+  P.drop_cnt[s] = cd;
+  P.blat[s] = l;
+  return true;
+}
+
+__global__ void __launch_bounds__(LW * 32, 4) k_lane(const __grid_constant__ StepP P) {
+  extern __shared__ __align__(16) unsigned char kl_smem[];
+  LaneStage& st = reinterpret_cast<LaneStage*>(kl_smem)[threadIdx.x >> 5];
+  const int lane = lane_id();
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int64_t ng = ((int64_t)P.S + 31) >> 5;
+  for (int64_t gi = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; gi < ng; gi += nw) {
+    const int64_t s = gi * 32 + lane;
+    const bool has = s < P.S;
+    int64_t lo = 0, hi = 0;
+    if (has) {
+      lo = P.seg_off[s];
+      hi = P.seg_off[s + 1];
+    }
+    const int last = (int)min((int64_t)31, (int64_t)P.S - 1 - gi * 32);
+    const int64_t lo0 = __shfl_sync(FULL, lo, 0), hiN = __shfl_sync(FULL, hi, last);
+    const bool fits = hiN >= lo0 && hiN - lo0 <= LCAP && lo0 >= 0 && hiN <= P.Q;  // uniform
+    // n > SMALL: k1's segment; a non-monotone seg_off is flagged by the planner
+    const bool mine = has && hi - lo >= 0 && hi - lo <= SMALL;
+    int64_t a0d = 0, a0e = 0, a0f = 0;
+    if (fits) {
+      a0d = lane_stage(st.dl, P.dl, lo0, hiN, P.Q);
+      a0e = lane_stage(st.eff, P.eff, lo0, hiN, P.Q);
+      a0f = lane_stage(st.fl, P.fl, lo0, hiN, P.Q);
+      cp_commit();
+      cp_wait<0>();
+    }
+    __syncwarp();
+    bool redo = mine;
+    if (mine && fits && lo >= lo0 && hi <= hiN)
+      redo = !lane_segment(P, st, s, lo, (int)(hi - lo), a0d, a0e, a0f);
+    const uint32_t m = __ballot_sync(FULL, redo);
+    if (m) {
+      int base = 0;
+      if (lane == 0) base = atomicAdd(P.redo_cnt, __popc(m));
+      base = __shfl_sync(FULL, base, 0);
+      if (redo) P.redo[base + __popc(m & lanemask_lt())] = (int32_t)s;
+    }
+    __syncwarp();  // the staging buffer is refilled next
   }
 }
 
@@ -1118,6 +1324,7 @@ asc_status launch_schedule_step(asc_ctx* c, const asc_step_in* in, asc_step_out*
   size_t need = 0;
   need += 2 * (size_t)(S + 1) * 8 + 2 * (size_t)ntile * 8 + (size_t)ntask_max * 4 + 8192;
   need += (size_t)max_mt * (32 * KPL) * sizeof(KI) + (size_t)max_mt * MW * 8 + (size_t)max_mt * 8 + 8192;
+  need += (size_t)(S + 1) * 4 + 1024;  // k_lane's hand-back list
   asc_status st = ensure_ws(c, need);
   if (st) return st;
   Arena ar{c->ws, c->ws_cap};
@@ -1159,6 +1366,8 @@ asc_status launch_schedule_step(asc_ctx* c, const asc_step_in* in, asc_step_out*
   P.mdrop = ar.take<uint32_t>(max_mt * MW);
   P.coff = ar.take<int32_t>(max_mt);
   P.cdrop = ar.take<int32_t>(max_mt);
+  P.redo = ar.take<int32_t>(S > 0 ? S : 1);
+  P.redo_cnt = ar.take<int32_t>(1);
   P.err = c->d_err;
   cudaStream_t sm = c->stream;
   int64_t launches = 0;
@@ -1197,11 +1406,17 @@ asc_status launch_schedule_step(asc_ctx* c, const asc_step_in* in, asc_step_out*
   cudaEventRecord(c->ev1, sm);
   c->timed = true;
   launches += 1;
-  {  // short segments (after k1's timed bracket: k1 is the roofline kernel of row S's big shape)
+  {  // short segments (after k1's timed bracket: k1 is the roofline kernel of row S's big shape):
+     // k_lane decides them one per thread, k_small the ones it hands back
+    constexpr size_t LSMEM = LW * sizeof(LaneStage);
+    cudaFuncSetAttribute(k_lane, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)LSMEM);
+    int64_t gl = (((int64_t)S + 31) / 32 + LW - 1) / LW;
+    gl = gl < (int64_t)dev_sms * 4 ? gl : (int64_t)dev_sms * 4;  // one resident wave
+    k_lane<<<(unsigned)(gl > 0 ? gl : 1), LW * 32, LSMEM, sm>>>(P);
     int64_t gs = ((int64_t)S * 32 + 255) / 256;
-    gs = gs < (int64_t)dev_sms * ASC_KS_MINB ? gs : (int64_t)dev_sms * ASC_KS_MINB;  // one resident wave
-    k_small<<<(unsigned)(gs > 0 ? gs : 1), 256, 0, sm>>>(P);
-    launches += 1;
+    gs = gs < (int64_t)dev_sms * ASC_KS_MINB ? gs : (int64_t)dev_sms * ASC_KS_MINB;
+    k_small<true><<<(unsigned)(gs > 0 ? gs : 1), 256, 0, sm>>>(P);
+    launches += 2;
   }
   if (Q > CH) {
     int64_t g2 = S < (int64_t)dev_sms * 4 ? S : (int64_t)dev_sms * 4;

@@ -268,3 +268,63 @@ def test_row_s_full_scale_sampled(asc, oracle):
         e = H.segment_lists(exp, one["seg_off"])[0]
         assert [list(np.asarray(x) - lo) for x in g[s]] == [list(x) for x in e], s
         assert got["batch_lat_us"][s] == exp["batch_lat_us"][0], s
+
+
+def compare_vec(got, exp, seg_off):
+    """compare() without per-segment Python lists (millions of segments): counts and latencies
+    element by element, then every list slot below its segment's count."""
+    S = len(seg_off) - 1
+    Q = int(seg_off[-1])
+    for k in ("admit_cnt", "offload_cnt", "drop_cnt", "batch_lat_us"):
+        assert np.array_equal(got[k][:S], exp[k][:S]), k
+    seg_of = np.repeat(np.arange(S), np.diff(seg_off))
+    local = np.arange(Q) - seg_off[:-1][seg_of]
+    for idx, cnt in (("admit_idx", "admit_cnt"), ("offload_idx", "offload_cnt"), ("drop_idx", "drop_cnt")):
+        m = local < exp[cnt][seg_of]
+        bad = np.flatnonzero(got[idx][:Q][m] != exp[idx][:Q][m])
+        assert bad.size == 0, (idx, int(seg_of[np.flatnonzero(m)[bad[0]]]))
+
+
+def test_row_s_short_queues_full_scale(asc, oracle):
+    """SURVEY row S's third shape at full size, bench.py's inputs (10^6 segments x 32 entries,
+    seed 123): k_lane decides every segment one per thread; the whole call equals the oracle."""
+    rng = np.random.default_rng(123)
+    cfg = P.config()
+    S = 1_000_000
+    ins = H.random_step_inputs(rng, S, 0, cfg, qs=np.full(S, 32))
+    got = run_gpu(asc, cfg, ins)
+    compare_vec(got, oracle.schedule_step(cfg, **ins), ins["seg_off"])
+
+
+@pytest.mark.parametrize("policy", ["EDF_LAXITY", "EDF_DEADLINE", "FCFS", "SJF", "LJF"])
+def test_lane_handback_mix(asc, oracle, policy):
+    """Groups of 32 short segments where some segments leave k_lane's fast window and are handed
+    to k_small: prompts beyond the 2^17-entry fast table, keys more than 2^26 us from now (both
+    directions), no decodes, zero budgets, empty segments; plus groups that contain a k1 segment
+    (the group's entry range exceeds the staging buffer)."""
+    rng = np.random.default_rng(77)
+    cfg = P.config(flg=P.flags(policy=policy, drop=1))
+    S = 4000
+    qs = rng.integers(0, 33, size=S)
+    qs[::211] = 200
+    ins = H.random_step_inputs(rng, S, 0, cfg, qs=qs)
+    off = ins["seg_off"]
+    for s in rng.choice(S, 300, replace=False):
+        lo, hi = int(off[s]), int(off[s + 1])
+        if hi == lo:
+            continue
+        j = int(rng.integers(lo, hi))
+        kind = s % 4
+        if kind == 0:
+            ins["eff_prompt"][j] = int(rng.integers((1 << 17) + 1, 1 << 19))
+        elif kind == 1:
+            ins["deadline_us"][j] += (1 << 27)
+        elif kind == 2:
+            ins["deadline_us"][j] -= (1 << 27)
+        else:
+            ins["deadline_us"][j] = ins["now_us"][s] + (1 << 26) - 2
+    z = rng.random(S) < 0.1
+    ins["dec_count"][z] = 0
+    ins["budget_tokens"][rng.random(S) < 0.02] = 0
+    ins["budget_reqs"][rng.random(S) < 0.02] = 0
+    compare(run_gpu(asc, cfg, ins), oracle.schedule_step(cfg, **ins), ins["seg_off"])

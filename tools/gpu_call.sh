@@ -51,6 +51,19 @@ for s in $steps; do
            ncu -i gpurun_out/${tag}_k1_full.ncu-rep --page raw --csv > gpurun_out/${tag}_k1_raw.csv
            ncu -i gpurun_out/${tag}_k1_full.ncu-rep --page source --csv --print-source sass > gpurun_out/${tag}_k1_src.csv;;
     sanitize) bash tools/sanitize.sh $tag;;
+    steptests) timeout 1200 python -m pytest tests/test_gpu_step.py tests/test_gpu_edges.py -x -q > gpurun_out/${tag}_steptests.log 2>&1
+           echo steptests_rc=$?; tail -15 gpurun_out/${tag}_steptests.log;;
+    timestep) timeout 600 python tools/time_step.py 2>&1 | tee gpurun_out/${tag}_timestep.log;;
+    klanefull) timeout 900 ncu --set full --import-source on --clock-control none -k regex:k_lane -c 1 \
+           -o gpurun_out/${tag}_kl python tools/profile_run.py step --S 1000000 --Q 32 --reps 2 > gpurun_out/${tag}_kl.log 2>&1
+           echo klanefull_rc=$?
+           ncu -i gpurun_out/${tag}_kl.ncu-rep --page raw --csv > gpurun_out/${tag}_kl_raw.csv
+           ncu -i gpurun_out/${tag}_kl.ncu-rep --page source --csv --print-source sass > gpurun_out/${tag}_kl_src.csv;;
+    c4full) timeout 1800 ncu --set full --import-source on --clock-control none -k regex:sim_kernel -c 1 \
+           -o gpurun_out/${tag}_c4 python tools/profile_run.py sim --workload config4 --traces 1 --n 100000 --reps 1 \
+           > gpurun_out/${tag}_c4.log 2>&1; echo c4full_rc=$?
+           ncu -i gpurun_out/${tag}_c4.ncu-rep --page raw --csv > gpurun_out/${tag}_c4_raw.csv
+           ncu -i gpurun_out/${tag}_c4.ncu-rep --page source --csv --print-source sass > gpurun_out/${tag}_c4_src.csv;;
     *) echo "running: $s"; timeout 1800 bash -c "$s"; echo "rc=$?";;
   esac
   echo "[$s took $(( $(date +%s) - t0 )) s]"

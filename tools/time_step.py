@@ -6,7 +6,7 @@ sys.path.insert(0, ROOT); sys.path.insert(0, os.path.join(ROOT, "tests"))
 from gen import presets as P
 from paper_2504_20828_b200 import asc
 import helpers as H
-peak = 6467.7
+peak = 6555.2
 for S, Q in ((4096, 10000), (64, 1000000), (1000000, 32)):
     rng = np.random.default_rng(123)
     cfg = P.config()
