@@ -66,6 +66,8 @@ struct StepP {
   uint32_t *moff, *mdrop;
   int32_t *coff, *cdrop;
   int32_t* redo;       // [S]: short segments k_lane hands to k_small (outside its fast window)
+  uint64_t bs_m, ab_m; // ceil(2^38 / block_tokens), ceil(2^38 / attention block b) (div_m)
+  int32_t lane_ok;     // both divisors exact by div_m for every k_lane argument (< 2^17 + divisor)
   int32_t* redo_cnt;
   int* err;
 };
@@ -994,66 +996,154 @@ struct __align__(16) LaneStage {
   int64_t dl[LCAP + 2];    // chunk-aligned copies (first chunk aligned down to 16 bytes); after
   int32_t eff[LCAP + 4];   // pass 1 the low word of dl[e] holds prefill_us of entry e
   uint8_t fl[LCAP + 16];
+  uint64_t bar;            // mbarrier: completion of the group's bulk copies
 };
 static_assert(sizeof(int64_t) * (LCAP + 2) % 16 == 0 && sizeof(int32_t) * (LCAP + 4) % 16 == 0, "16-byte aligned rows");
 
-// copy g[lo0, hi) into dst (16-byte chunks from the aligned-down start a0); returns a0.  Chunks that
-// cross [0, Q) are copied element by element.
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* bar) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(smem_u32(bar)) : "memory");
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "LAB_WAIT%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra LAB_WAIT%=;\n}\n" ::"r"(smem_u32(bar)), "r"(parity) : "memory");
+}
+// one TMA bulk copy (1-D, 16-byte aligned, size a multiple of 16) completing on bar
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
+               ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
+
+// Stage g[lo0, hi) into dst as 16-byte chunks from the aligned-down start a0 (returns a0): the chunks
+// inside [0, Q) as ONE bulk copy issued by lane 0 (bytes added to *tx), the at most two chunks that
+// cross the array ends element by element by the other lanes.
 template <typename T>
-__device__ __forceinline__ int64_t lane_stage(T* dst, const T* g, int64_t lo0, int64_t hi, int64_t Q) {
+__device__ __forceinline__ int64_t lane_stage(T* dst, const T* g, int64_t lo0, int64_t hi, int64_t Q,
+                                              uint64_t* bar, unsigned* tx) {
   constexpr int K = 16 / sizeof(T);
   const int64_t a0 = lo0 - (int64_t)(((uintptr_t)(g + lo0) & 15) / sizeof(T));
-  const int nch = (int)((hi - a0 + K - 1) / K);
-  for (int c = lane_id(); c < nch; c += 32) {
-    const int64_t e = a0 + (int64_t)c * K;
-    if (e >= 0 && e + K <= Q) {
-      cp_async16(dst + c * K, g + e);
-    } else {
-#pragma unroll
-      for (int u = 0; u < K; u++)
-        if (e + u >= 0 && e + u < Q) dst[c * K + u] = g[e + u];
-    }
+  const int64_t nch = (hi - a0 + K - 1) / K;
+  const int64_t c0 = a0 < 0 ? (-a0 + K - 1) / K : 0;           // first chunk with e >= 0
+  int64_t c1 = (Q - a0) / K;                                     // chunks [c0, c1) end <= Q
+  c1 = c1 < nch ? c1 : nch;
+  const int lane = lane_id();
+  if (c1 > c0) {
+    if (lane == 0) bulk_g2s(dst + c0 * K, g + a0 + c0 * K, (unsigned)((c1 - c0) * 16), bar);
+    *tx += (unsigned)((c1 - c0) * 16);
+  }
+  // boundary chunks [0, c0) and [t0, nch): element by element
+  const int64_t t0 = c1 > c0 ? c1 : c0;
+  const int hb = (int)(c0 < nch ? c0 : nch) * K, nb = hb + (int)(nch > t0 ? nch - t0 : 0) * K;
+  for (int i = lane; i < nb; i += 32) {
+    const int64_t x = i < hb ? (int64_t)i : t0 * K + (i - hb);  // element offset from a0
+    const int64_t e = a0 + x;
+    if (e >= 0 && e < Q) dst[x] = g[e];
   }
   return a0;
 }
 
+// per-segment inputs of k_lane, loaded (coalesced across the warp's 32 segments) while the entry
+// range is still being staged
+struct LaneSeg {
+  int64_t now, sl, tbt;
+  int32_t R, Bd, N, M;
+};
+__device__ __forceinline__ void lane_seg_load(const StepP& P, int64_t s, LaneSeg& x) {
+  x.now = P.now[s];
+  x.R = P.bR[s];
+  x.Bd = P.dcnt[s];
+  x.sl = P.dctx[s];
+  x.tbt = P.tbt[s];
+  x.N = P.bN[s];
+  x.M = P.bM[s];
+}
+// x / d for 0 <= x < 2^38 / d by one multiply: m = ceil(2^38 / d) = (2^38 + e) / d with e < d, so
+// x * m / 2^38 = x / d + x * e / (d * 2^38) and the error term stays below 1 / d (StepP::lane_div)
+__device__ __forceinline__ uint32_t div_m(uint32_t x, uint64_t m) { return (uint32_t)(((uint64_t)x * m) >> 38); }
+
 // decide segment s (entries [lo, lo + n), staged at st with chunk bases a0d / a0e / a0f); false if
-// the segment is outside the fast window (nothing written yet)
+// the segment is outside the fast window (nothing written yet).  F32: n == 32 (the row-S shape;
+// warp-uniform), so the rotation is (j + lane) & 31 and no entry test is needed.  Every deadline is
+// taken relative to now in 32 bits: d = deadline - now must lie in (-2^30, 2^30) (else: hand back),
+// so d - pf, the key d*kdl + pf*kpf and the offload test are exact int32 arithmetic.
+template <bool F32>
 __device__ __forceinline__ bool lane_segment(const StepP& P, LaneStage& st, int64_t s, int64_t lo, int n,
-                                             int64_t a0d, int64_t a0e, int64_t a0f) {
-  const int32_t R = P.bR[s], Bd = P.dcnt[s];
-  const int64_t sl = Bd > 0 ? P.dctx[s] : 0;  // dec_ctx_sum is ignored without decodes
+                                             const LaneSeg& g, int64_t a0d, int64_t a0e, int64_t a0f) {
+  const int32_t R = g.R, Bd = g.Bd;
+  const int64_t sl = Bd > 0 ? g.sl : 0;  // dec_ctx_sum is ignored without decodes
   if (R > ASC_MAX_BATCH || Bd < 0 || (Bd > 0 && sl < Bd)) return false;
-  const int64_t now = P.now[s];
+  const int64_t now = g.now;
   const int od = (int)(lo - a0d), oe = (int)(lo - a0e), of = (int)(lo - a0f);
   int32_t* pfs = reinterpret_cast<int32_t*>(st.dl);  // pf of entry j at pfs[2 * (od + j)]
-  const int rot = n > 0 ? lane_id() % n : 0;
+  const int lane = lane_id();
+  const int rot = F32 ? lane : (n > 0 ? lane % n : 0);
+  auto slot = [&](int j) {  // rotated position of the j-th visit; 0 past the end (never used)
+    if (F32) return (j + lane) & (SMALL - 1);
+    int jj = j + rot;
+    jj -= jj >= n ? n : 0;
+    return j < n ? jj : 0;
+  };
+  // two halves of 16 entries: all 16 a1 table gathers of a half in flight at once (branch-free, no
+  // dependence between entries), then the key, drop and offload candidates of that half (position
+  // order is kept in the masks)
+  constexpr int H = SMALL / 2;
   uint32_t a[SMALL];
-  uint32_t dm = 0, om = 0;
-  bool ok = true;
-  const int64_t othr = P.W + P.margin;
-  // pass 1: a1, key, drop / offload candidates (position order is kept in the masks)
+  uint32_t dm = 0, om = 0, bad = 0, mxw = 0;
+  const int32_t othr = (int32_t)max((int64_t)INT32_MIN, min((int64_t)INT32_MAX, P.W + P.margin));
+  const bool kdl = P.kdl != 0, drop = P.drop != 0, offl = P.offl != 0;
+  const int32_t kpf = P.kpf;
+  int32_t pfv[H];
 #pragma unroll
-  for (int j = 0; j < SMALL; j++) {
-    a[j] = 0xffffffffu;
-    if (j < n) {
-      int jj = j + rot;
-      jj -= jj >= n ? n : 0;
-      const int64_t dl = st.dl[od + jj];
-      const int32_t p = st.eff[oe + jj];
+  for (int h = 0; h < SMALL; h += H) {
+#pragma unroll
+    for (int j = h; j < h + H; j++) {
+      const int32_t p = st.eff[oe + slot(j)];
+      pfv[j - h] = __ldg(P.pf_fast + ((p - 1) & (PFT_N - 1)));
+      if (F32 || j < n) bad |= (uint32_t)(p - 1) & ~(uint32_t)(PFT_N - 1);  // p outside [1, 2^17]
+    }
+#pragma unroll
+    for (int j = h; j < h + H; j++) {
+      const int jj = slot(j);
+      const bool v = F32 || j < n;
+      const int64_t d64 = st.dl[od + jj] - now;
+      const int32_t d = (int32_t)d64, pf = pfv[j - h];
       const uint32_t f = st.fl[of + jj];
-      const int32_t pf = __ldg(P.pf_fast + ((p - 1) & (PFT_N - 1)));
-      ok &= (uint32_t)(p - 1) < (uint32_t)PFT_N && pf < (1 << 30);
-      const bool dropped = P.drop && !(f & 1u) && now > dl;
-      const bool offc = P.offl && !dropped && !(f & 3u) && dl - now <= (int64_t)pf + othr;
-      const int64_t rel = (P.kdl ? dl - now : 0) + (int64_t)(P.kpf * pf);
-      ok &= dropped || (rel >= -(int64_t(1) << 26) && rel < (int64_t(1) << 26) - 1);
-      a[j] = dropped ? 0xffffffffu : ((uint32_t)(rel + (int64_t(1) << 26)) << 5) | (uint32_t)jj;
-      dm |= (uint32_t)dropped << jj;
-      om |= (uint32_t)offc << jj;
-      pfs[2 * (od + jj)] = pf;  // this lane's own entry: the deadline is not read again
+      // window (else hand back): d = deadline - now in [-2^30, 2^30) (d64 is d sign-extended, and
+      // d + 2^30 < 2^31), pf < 2^30, the packed key field rel + 2^26 < 2^27 - 1; so d - pf and the
+      // key are exact int32 and the packed word of a live entry is never the all-ones sentinel
+      const uint32_t u = (uint32_t)((kdl ? d : 0) + kpf * pf + (1 << 26));
+      if (v) {
+        bad |= (uint32_t)(d64 >> 32) ^ (uint32_t)(d >> 31);
+        mxw = max(mxw, max((uint32_t)(d + (1 << 30)) >> 4, (uint32_t)pf >> 3));  // < 2^27 iff both in range
+        mxw = max(mxw, u);
+      }
+      const bool dropped = v && drop && !(f & 1u) && d < 0;
+      const bool offc = v && offl && !dropped && !(f & 3u) && d - pf <= othr;
+      a[j] = (!v || dropped) ? 0xffffffffu : (u << 5) | (uint32_t)jj;
+      if (F32) {  // bits in visit order; rotated to positions once below
+        dm |= dropped ? (1u << j) : 0u;
+        om |= offc ? (1u << j) : 0u;
+      } else {
+        dm |= (uint32_t)dropped << jj;
+        om |= (uint32_t)offc << jj;
+      }
+      if (v) pfs[2 * (od + jj)] = pf;  // this entry's deadline is not read again: keep pf in its place
+                                       // (v: an empty segment's slot 0 is the next lane's entry)
     }
   }
+  if (F32) {  // visit j is position (j + lane) & 31: rotate left by lane
+    dm = __funnelshift_l(dm, dm, lane);
+    om = __funnelshift_l(om, om, lane);
+  }
+  bad |= mxw >= (1u << 27) - 1 ? 1u : 0u;
+  const bool ok = bad == 0;
   if (!ok) return false;
   // a3: ascending (key, position); dropped entries (all ones) sort last
 #pragma unroll
@@ -1075,33 +1165,40 @@ __device__ __forceinline__ bool lane_segment(const StepP& P, LaneStage& st, int6
   if (Bd > 0) {
     d = lat_us(P.md, 0, 0, 0, 0, (uint64_t)Bd, (uint64_t)sl);
     if (d < 0) atomicOr(P.err, ERR_RANGE);
-    C = P.tbt[s] - d;
+    C = g.tbt - d;
   }
-  // a4: Algorithm 1 lines 5-13, strict budgets in key order
-  const int32_t N = P.bN[s], M = P.bM[s];
-  const uint32_t bs = (uint32_t)P.bs, ab = (uint32_t)P.md.b;
+  // a4: Algorithm 1 lines 5-13, strict budgets in key order; the next entry's (p, pf) is loaded
+  // before the current one is tested
+  const int32_t N = g.N, M = g.M;
+  const uint32_t bs = (uint32_t)P.bs;
   int32_t St = 0, Sb = 0;
   int64_t Sc = 0;
   int k = 0;
   uint32_t am = 0;
   uint64_t sp = 0, sp2 = 0, spc = 0;
+  int32_t pn = st.eff[oe + (int)(a[0] & 31u)], pfn = pfs[2 * (od + (int)(a[0] & 31u))];
 #pragma unroll
   for (int j = 0; j < SMALL; j++) {
     const uint32_t x = a[j];
+    const int32_t p = pn, pf = pfn;
+    if (j + 1 < SMALL) {
+      const int q = (int)(a[j + 1 < SMALL ? j + 1 : j] & 31u);
+      pn = st.eff[oe + q];
+      pfn = pfs[2 * (od + q)];
+    }
     if (x == 0xffffffffu || j >= R) break;
-    const int pos = (int)(x & 31u);
-    const int32_t p = st.eff[oe + pos];
     St += p;
-    Sb += (int32_t)(((uint32_t)p + bs) / bs);
-    Sc += pfs[2 * (od + pos)];
+    Sb += (int32_t)div_m((uint32_t)p + bs, P.bs_m);
+    Sc += pf;
     if (!(St < N && Sb < M && Sc < C)) break;
+    const int pos = (int)(x & 31u);
     P.admit_idx[lo + j] = (int32_t)(lo + pos);
     am |= 1u << pos;
     k = j + 1;
     const uint64_t q = (uint64_t)p;
     sp += q;
     sp2 += q * q;
-    spc += q * (uint64_t)(((uint32_t)p + ab - 1u) / ab);
+    spc += q * (uint64_t)div_m((uint32_t)p + (uint32_t)P.md.b - 1u, P.ab_m);
   }
   // a6: the hybrid batch {admitted} + {decodes}
   int64_t l = 0;
@@ -1129,37 +1226,57 @@ __device__ __forceinline__ bool lane_segment(const StepP& P, LaneStage& st, int6
   return true;
 }
 
-__global__ void __launch_bounds__(LW * 32, 4) k_lane(const __grid_constant__ StepP P) {
+#ifndef ASC_KL_MINB
+#define ASC_KL_MINB 4
+#endif
+// the general (n != 32) case out of line: its register pressure stays out of the F32 path's
+__device__ __noinline__ bool lane_segment_any(const StepP& P, LaneStage& st, int64_t s, int64_t lo, int n,
+                                              const LaneSeg& g, int64_t a0d, int64_t a0e, int64_t a0f) {
+  return lane_segment<false>(P, st, s, lo, n, g, a0d, a0e, a0f);
+}
+
+__global__ void __launch_bounds__(LW * 32, ASC_KL_MINB) k_lane(const __grid_constant__ StepP P) {
   extern __shared__ __align__(16) unsigned char kl_smem[];
   LaneStage& st = reinterpret_cast<LaneStage*>(kl_smem)[threadIdx.x >> 5];
   const int lane = lane_id();
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const int64_t ng = ((int64_t)P.S + 31) >> 5;
+  if (lane == 0) mbar_init(&st.bar);
+  __syncwarp();
+  unsigned phase = 0;
   for (int64_t gi = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; gi < ng; gi += nw) {
     const int64_t s = gi * 32 + lane;
     const bool has = s < P.S;
     int64_t lo = 0, hi = 0;
+    LaneSeg sg{};
     if (has) {
       lo = P.seg_off[s];
       hi = P.seg_off[s + 1];
+      lane_seg_load(P, s, sg);  // in flight during the staging below
     }
     const int last = (int)min((int64_t)31, (int64_t)P.S - 1 - gi * 32);
     const int64_t lo0 = __shfl_sync(FULL, lo, 0), hiN = __shfl_sync(FULL, hi, last);
-    const bool fits = hiN >= lo0 && hiN - lo0 <= LCAP && lo0 >= 0 && hiN <= P.Q;  // uniform
+    const bool fits = P.lane_ok && hiN >= lo0 && hiN - lo0 <= LCAP && lo0 >= 0 && hiN <= P.Q;  // uniform
     // n > SMALL: k1's segment; a non-monotone seg_off is flagged by the planner
     const bool mine = has && hi - lo >= 0 && hi - lo <= SMALL;
     int64_t a0d = 0, a0e = 0, a0f = 0;
     if (fits) {
-      a0d = lane_stage(st.dl, P.dl, lo0, hiN, P.Q);
-      a0e = lane_stage(st.eff, P.eff, lo0, hiN, P.Q);
-      a0f = lane_stage(st.fl, P.fl, lo0, hiN, P.Q);
-      cp_commit();
-      cp_wait<0>();
+      // the previous group's generic-proxy accesses to the buffer come before the async writes
+      if (lane == 0) asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+      unsigned tx = 0;
+      a0d = lane_stage(st.dl, P.dl, lo0, hiN, P.Q, &st.bar, &tx);
+      a0e = lane_stage(st.eff, P.eff, lo0, hiN, P.Q, &st.bar, &tx);
+      a0f = lane_stage(st.fl, P.fl, lo0, hiN, P.Q, &st.bar, &tx);
+      if (lane == 0) mbar_arrive_tx(&st.bar, tx);
+      mbar_wait(&st.bar, phase);
+      phase ^= 1u;
     }
     __syncwarp();
     bool redo = mine;
+    const bool all32 = __all_sync(FULL, !has || hi - lo == SMALL);
     if (mine && fits && lo >= lo0 && hi <= hiN)
-      redo = !lane_segment(P, st, s, lo, (int)(hi - lo), a0d, a0e, a0f);
+      redo = all32 ? !lane_segment<true>(P, st, s, lo, SMALL, sg, a0d, a0e, a0f)
+                   : !lane_segment_any(P, st, s, lo, (int)(hi - lo), sg, a0d, a0e, a0f);
     const uint32_t m = __ballot_sync(FULL, redo);
     if (m) {
       int base = 0;
@@ -1255,6 +1372,7 @@ __global__ void __launch_bounds__(WARPS * 32) k2_segments(const __grid_constant_
 
 __global__ void __launch_bounds__(WARPS * 32) k3_expand(const __grid_constant__ StepP P) {
   __shared__ int32_t s_ring[WARPS][256];
+  __shared__ __align__(16) uint32_t s_words[WARPS][2][MW];
   if (P.mtask_off[P.S] == 0) return;  // no multi-task segment
   const int w = threadIdx.x >> 5;
   const int64_t ntasks = min(P.task_off[P.S], P.ntask_max);
@@ -1271,8 +1389,17 @@ __global__ void __launch_bounds__(WARPS * 32) k3_expand(const __grid_constant__ 
     const int64_t e_end = min(hi, b + CH);
     const int64_t b4 = b & ~int64_t(ALN - 1);
     const int ng = (int)((e_end - b4 + GE - 1) / GE);
-    expand_groups(P.moff + mt * MW, ng, b4, P.off_idx, lo + P.coff[mt], s_ring[w]);
-    expand_groups(P.mdrop + mt * MW, ng, b4, P.drop_idx, lo + P.cdrop[mt], s_ring[w]);
+    // the task's mask words come to shared memory in one coalesced pass first: expand_groups reads
+    // one 16-byte word group per iteration, a dependent global load each time otherwise
+    const int nw4 = 4 * ng;
+    for (int j = lane_id(); j < nw4; j += 32) {
+      s_words[w][0][j] = P.moff[mt * MW + j];
+      s_words[w][1][j] = P.mdrop[mt * MW + j];
+    }
+    __syncwarp();
+    expand_groups(s_words[w][0], ng, b4, P.off_idx, lo + P.coff[mt], s_ring[w]);
+    expand_groups(s_words[w][1], ng, b4, P.drop_idx, lo + P.cdrop[mt], s_ring[w]);
+    __syncwarp();
   }
 }
 
@@ -1367,6 +1494,12 @@ asc_status launch_schedule_step(asc_ctx* c, const asc_step_in* in, asc_step_out*
   P.coff = ar.take<int32_t>(max_mt);
   P.cdrop = ar.take<int32_t>(max_mt);
   P.redo = ar.take<int32_t>(S > 0 ? S : 1);
+  {  // div_m is exact for x < 2^38 / d; k_lane's arguments stay below 2^17 + d
+    const uint64_t bsd = (uint64_t)P.bs, abd = (uint64_t)P.md.b;
+    P.bs_m = ((uint64_t(1) << 38) + bsd - 1) / bsd;
+    P.ab_m = ((uint64_t(1) << 38) + abd - 1) / abd;
+    P.lane_ok = bsd <= (1u << 16) && abd <= (1u << 16);
+  }
   P.redo_cnt = ar.take<int32_t>(1);
   P.err = c->d_err;
   cudaStream_t sm = c->stream;

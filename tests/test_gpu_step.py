@@ -316,7 +316,7 @@ def test_lane_handback_mix(asc, oracle, policy):
         j = int(rng.integers(lo, hi))
         kind = s % 4
         if kind == 0:
-            ins["eff_prompt"][j] = int(rng.integers((1 << 17) + 1, 1 << 19))
+            ins["eff_prompt"][j] = int(rng.integers((1 << 17) + 1, (1 << 17) + 5000))
         elif kind == 1:
             ins["deadline_us"][j] += (1 << 27)
         elif kind == 2:

@@ -2,7 +2,7 @@
 # One gpurun call's worth of evidence at HEAD (GPU box only): bash tools/gpu_call.sh <tag> [steps...]
 # steps: smoke tests bench launches traffic simfull ksfull k1full sanitize  (default: all but sanitize)
 tag=$1; shift
-steps=${*:-"smoke tests bench launches traffic simfull"}
+[ $# -eq 0 ] && set -- smoke tests bench launches traffic simfull
 mkdir -p gpurun_out
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv,noheader
 M="dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum,smsp__inst_executed.sum"
@@ -13,7 +13,7 @@ cap() { # name kernel-regex count args...
     --log-file gpurun_out/${tag}_${name}_dram.csv python tools/profile_run.py "$@" > gpurun_out/${tag}_${name}_dram.log 2>&1
   echo "cap $name rc=$?"
 }
-for s in $steps; do
+for s in "$@"; do
   t0=$(date +%s)
   case $s in
     smoke) timeout 600 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/${tag}_smoke.log 2>&1
