@@ -150,6 +150,7 @@ asc_status asc_create(const asc_config* cfg, int device, void* cuda_stream, asc_
   asc_ctx* c = new asc_ctx();
   c->cfg = *cfg;
   c->device = device;
+  cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, device);
   c->stream = (cudaStream_t)cuda_stream;
   // tp division
   const uint64_t tp = (uint64_t)a.tp;

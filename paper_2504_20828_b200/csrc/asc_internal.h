@@ -12,6 +12,7 @@ constexpr int32_t ASC_PF_FAST_N = 1 << 17;  // entries of asc_ctx::d_pf_fast
 struct asc_ctx {
   asc_config cfg;          // as given (tp not yet applied)
   int device = 0;
+  int sms = 148;           // multiprocessors of `device` (queried once in asc_create)
   cudaStream_t stream = nullptr;
   asc::Model md;           // tp-divided model constants
   int32_t pt_size = 0;     // prefill table covers eff_prompt in [0, pt_size)

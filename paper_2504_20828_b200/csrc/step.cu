@@ -16,6 +16,7 @@
 //   k3     : one warp per multi-task task expands its masks into id-ascending output indices.
 // HBM traffic per entry: 13 B read (+4 B prefill_us if requested) + 4 B per output index;
 // multi-task segments add 0.25 B/entry of mask traffic and 1.5 KB per task of candidates.
+#include <mutex>
 #include <type_traits>
 
 #include "asc_internal.h"
@@ -154,6 +155,85 @@ __global__ void fill_task_seg(StepP P) {
        s += (int64_t)gridDim.x * blockDim.x) {
     for (int64_t t = P.task_off[s]; t < P.task_off[s + 1] && t < P.ntask_max; t++)
       P.task_seg[t] = (int32_t)s;
+  }
+}
+
+// two-launch planner for S >= SCAN_TILE: plan_tiles counts every segment's tasks from seg_off and
+// scans them tile-locally (tile totals to scan_tmp); plan_fix adds the sum of the preceding tile
+// totals (read directly: at most PLAN_FIX_TILES tiles) and writes the task -> segment map
+constexpr int64_t PLAN_FIX_TILES = 4096;
+__device__ __forceinline__ int64_t seg_tasks(const StepP& P, int64_t s) {
+  const int64_t len = P.seg_off[s + 1] - P.seg_off[s];
+  if (len < 0) atomicOr(P.err, ERR_INVAL);
+  return len <= SMALL ? 0 : len <= CH ? 1 : (len + CH - 1) / CH;  // small: k_lane / k_small
+}
+__global__ void __launch_bounds__(SCAN_THREADS) plan_tiles(StepP P) {
+  __shared__ int64_t sa[SCAN_THREADS / 32], sb[SCAN_THREADS / 32];
+  const int64_t n = (int64_t)P.S + 1;
+  const int64_t base = blockIdx.x * (int64_t)SCAN_TILE + threadIdx.x * SCAN_ITEMS;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    *P.redo_cnt = 0;
+    if (P.seg_off[P.S] != P.Q) atomicOr(P.err, ERR_INVAL);
+  }
+  int64_t va[SCAN_ITEMS], vb[SCAN_ITEMS], ta = 0, tb = 0;
+#pragma unroll
+  for (int i = 0; i < SCAN_ITEMS; i++) {
+    const int64_t s = base + i;
+    const int64_t nt = s < P.S ? seg_tasks(P, s) : 0;
+    va[i] = nt;
+    vb[i] = nt > 1 ? nt : 0;
+    ta += va[i];
+    tb += vb[i];
+  }
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  const int64_t ia = warp_incl_scan(ta), ib = warp_incl_scan(tb);
+  if (l == 31) { sa[w] = ia; sb[w] = ib; }
+  __syncthreads();
+  if (w == 0) {
+    const int64_t x = sa[l], y = sb[l];
+    const int64_t xi = warp_incl_scan(x), yi = warp_incl_scan(y);
+    sa[l] = xi - x;
+    sb[l] = yi - y;
+    if (l == 31) { P.scan_tmp[2 * blockIdx.x] = xi; P.scan_tmp[2 * blockIdx.x + 1] = yi; }
+  }
+  __syncthreads();
+  int64_t ea = sa[w] + ia - ta, eb = sb[w] + ib - tb;
+#pragma unroll
+  for (int i = 0; i < SCAN_ITEMS; i++) {
+    if (base + i < n) { P.task_off[base + i] = ea; P.mtask_off[base + i] = eb; }
+    ea += va[i];
+    eb += vb[i];
+  }
+}
+__global__ void __launch_bounds__(SCAN_THREADS) plan_fix(StepP P) {
+  __shared__ int64_t ra[SCAN_THREADS / 32], rb[SCAN_THREADS / 32];
+  int64_t pa = 0, pb = 0;  // totals of the tiles before this one
+  for (int64_t t = threadIdx.x; t < blockIdx.x; t += SCAN_THREADS) {
+    pa += P.scan_tmp[2 * t];
+    pb += P.scan_tmp[2 * t + 1];
+  }
+  pa = warp_sum(pa);
+  pb = warp_sum(pb);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  if (l == 0) { ra[w] = pa; rb[w] = pb; }
+  __syncthreads();
+  pa = 0;
+  pb = 0;
+  for (int i = 0; i < SCAN_THREADS / 32; i++) { pa += ra[i]; pb += rb[i]; }
+  const int64_t n = (int64_t)P.S + 1;
+  const int64_t base = blockIdx.x * (int64_t)SCAN_TILE + threadIdx.x * SCAN_ITEMS;
+#pragma unroll
+  for (int i = 0; i < SCAN_ITEMS; i++) {
+    const int64_t s = base + i;
+    if (s >= n) break;
+    const int64_t t0 = P.task_off[s] + pa;
+    P.task_off[s] = t0;
+    P.mtask_off[s] += pb;
+    if (s < P.S) {
+      const int64_t len = P.seg_off[s + 1] - P.seg_off[s];
+      const int64_t nt = len <= SMALL ? 0 : len <= CH ? 1 : (len + CH - 1) / CH;
+      for (int64_t t = t0; t < t0 + nt && t < P.ntask_max; t++) P.task_seg[t] = (int32_t)s;
+    }
   }
 }
 
@@ -1407,16 +1487,29 @@ template <bool VEC, int TAB, bool DROP, bool OFFL>
 void launch_k1_t(unsigned grid, size_t, cudaStream_t sm, const StepP& P) {
   constexpr size_t SMEM = K1L<DROP, OFFL>::SMEM;
   auto* k = k1_tasks<VEC, TAB, DROP, OFFL>;
-  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM);
-  // shared memory for ASC_K1_MINB resident CTAs and no more: the rest of the unified L1 caches the
-  // prefill table the per-entry a1 lookups gather from
-  const int carve = (int)((ASC_K1_MINB * (SMEM + 1024) * 100 + 228 * 1024 - 1) / (228 * 1024));
-  cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, carve < 100 ? carve : 100);
-  int dev = 0, sms = 148, nb = ASC_K1_MINB;
+  // attributes and the resident-CTA cap once per device (host work between launches is GPU idle
+  // time of every call)
+  static std::mutex mu;
+  static unsigned caps[64] = {};
+  int dev = 0;
   cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k, K1W * 32, SMEM);
-  const unsigned cap = (unsigned)(sms * (nb > 0 ? nb : 1));
+  unsigned cap = 0;
+  {
+    std::lock_guard<std::mutex> g(mu);
+    cap = dev < 64 ? caps[dev] : 0;
+    if (!cap) {
+      cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM);
+      // shared memory for ASC_K1_MINB resident CTAs and no more: the rest of the unified L1 caches
+      // the prefill table the per-entry a1 lookups gather from
+      const int carve = (int)((ASC_K1_MINB * (SMEM + 1024) * 100 + 228 * 1024 - 1) / (228 * 1024));
+      cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, carve < 100 ? carve : 100);
+      int sms = 148, nb = ASC_K1_MINB;
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k, K1W * 32, SMEM);
+      cap = (unsigned)(sms * (nb > 0 ? nb : 1));
+      if (dev < 64) caps[dev] = cap;
+    }
+  }
   k<<<grid < cap ? grid : cap, K1W * 32, SMEM, sm>>>(P);
 }
 
@@ -1504,11 +1597,14 @@ asc_status launch_schedule_step(asc_ctx* c, const asc_step_in* in, asc_step_out*
   P.err = c->d_err;
   cudaStream_t sm = c->stream;
   int64_t launches = 0;
-  int dev_sms = 148;
-  cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, c->device);
+  const int dev_sms = c->sms;
   if (S + 1 <= SCAN_TILE) {
     plan_small<<<1, SCAN_THREADS, 0, sm>>>(P);
     launches += 1;
+  } else if (ntile <= PLAN_FIX_TILES) {
+    plan_tiles<<<ntile, SCAN_THREADS, 0, sm>>>(P);
+    plan_fix<<<ntile, SCAN_THREADS, 0, sm>>>(P);
+    launches += 2;
   } else {
     plan_counts<<<(S + 1 + 255) / 256, 256, 0, sm>>>(P);
     scan_tiles<<<ntile, SCAN_THREADS, 0, sm>>>(P.task_off, P.mtask_off, S + 1, P.scan_tmp);
@@ -1542,7 +1638,15 @@ asc_status launch_schedule_step(asc_ctx* c, const asc_step_in* in, asc_step_out*
   {  // short segments (after k1's timed bracket: k1 is the roofline kernel of row S's big shape):
      // k_lane decides them one per thread, k_small the ones it hands back
     constexpr size_t LSMEM = LW * sizeof(LaneStage);
-    cudaFuncSetAttribute(k_lane, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)LSMEM);
+    {
+      static std::mutex mu;
+      static uint64_t set = 0;  // devices whose k_lane attribute is set
+      std::lock_guard<std::mutex> g(mu);
+      if (c->device >= 64 || !(set >> c->device & 1)) {
+        cudaFuncSetAttribute(k_lane, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)LSMEM);
+        if (c->device < 64) set |= uint64_t(1) << c->device;
+      }
+    }
     int64_t gl = (((int64_t)S + 31) / 32 + LW - 1) / LW;
     gl = gl < (int64_t)dev_sms * 4 ? gl : (int64_t)dev_sms * 4;  // one resident wave
     k_lane<<<(unsigned)(gl > 0 ? gl : 1), LW * 32, LSMEM, sm>>>(P);

@@ -7,7 +7,7 @@ from gen import presets as P
 from paper_2504_20828_b200 import asc
 import helpers as H
 peak = 6555.2
-for S, Q in ((4096, 10000), (64, 1000000), (1000000, 32)):
+for S, Q in ((4096, 10000), (64, 1000000), (1000000, 32), (1, 1), (100000, 32)):
     rng = np.random.default_rng(123)
     cfg = P.config()
     ins = H.random_step_inputs(rng, S, 0, cfg, qs=np.full(S, Q))
