@@ -1,5 +1,7 @@
+#include <chrono>
 // asc_api.cu — the C ABI of include/asc.h: validation, context, workspace, host staging.
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -11,6 +13,17 @@ using namespace asc;
 static thread_local std::string g_create_err;
 
 namespace asc {
+
+HostProf g_prof;
+static double now_us_host() {
+  return std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+void HostProf::mark(int i) {
+  if (!on) return;
+  const double t = now_us_host();
+  if (i >= 0) acc[i] += t - last;
+  last = t;
+}
 
 asc_status fail(asc_ctx* c, asc_status s, const std::string& msg) {
   if (c) c->err = msg; else g_create_err = msg;
@@ -103,6 +116,7 @@ const char* asc_last_error(const asc_ctx* ctx) {
 }
 
 asc_status asc_create(const asc_config* cfg, int device, void* cuda_stream, asc_ctx** out) {
+  { const char* e = getenv("ASC_HOST_PROF"); g_prof.on = e && *e == '1'; }
   if (!cfg || !out) return fail(nullptr, ASC_E_INVAL, "asc_create: NULL argument");
   *out = nullptr;
   const asc_arch& a = cfg->arch;
@@ -213,6 +227,13 @@ asc_status asc_create(const asc_config* cfg, int device, void* cuda_stream, asc_
 
 void asc_destroy(asc_ctx* ctx) {
   if (!ctx) return;
+  if (g_prof.on && g_prof.calls) {
+    static const char* nm[] = {"checks", "ws+params", "planner", "k1", "k_lane+k_small", "k2+k3", "errors+sync"};
+    fprintf(stderr, "asc host profile over %ld asc_schedule_step calls (us/call):", g_prof.calls);
+    for (int i = 0; i < 7; i++) fprintf(stderr, " %s %.1f", nm[i], g_prof.acc[i] / g_prof.calls);
+    fprintf(stderr, "\n");
+    g_prof = HostProf{true};
+  }
   if (ctx->d_err) cudaFree(ctx->d_err);
   if (ctx->h_err) cudaFreeHost(ctx->h_err);
   if (ctx->d_pf_tab) cudaFree(ctx->d_pf_tab);
@@ -309,6 +330,8 @@ static asc_status finish_host(asc_ctx* c, Stager& sg, const char* where) {
 extern "C" {
 
 asc_status asc_schedule_step(asc_ctx* c, const asc_step_in* in, asc_step_out* out) {
+  g_prof.mark(-1);
+  if (g_prof.on) g_prof.calls++;
   if (!c || !in || !out) return fail(c, ASC_E_INVAL, "asc_schedule_step: NULL argument");
   if (c->cfg.flags.policy == ASC_POLICY_WEIGHTED || c->cfg.flags.offload_rule != 0)
     return fail(c, ASC_E_CONFIG, "asc_schedule_step: ASC_POLICY_WEIGHTED and offload_rule 1 are asc_simulate_batch only");
@@ -345,9 +368,12 @@ asc_status asc_schedule_step(asc_ctx* c, const asc_step_in* in, asc_step_out* ou
   if (Q >= INT32_MAX) return fail(c, ASC_E_RANGE, "asc_schedule_step: total entries >= 2^31");
   asc_status st;
   if (kind == 1) {
+    g_prof.mark(0);  // argument checks and pointer kinds
     st = launch_schedule_step(c, in, out, Q);
     if (st) return st;
-    return collect_errors(c, "asc_schedule_step");
+    st = collect_errors(c, "asc_schedule_step");
+    g_prof.mark(6);  // error read-back and stream sync
+    return st;
   }
   const size_t Sn = (size_t)S, Qn = (size_t)Q;
   Stager sg{c};

@@ -35,6 +35,17 @@ struct asc_ctx {
 
 namespace asc {
 
+// Host-side phase timer (experiments: ASC_HOST_PROF=1 prints the mean time per phase of
+// asc_schedule_step at asc_destroy).  Off: one branch per mark.
+struct HostProf {
+  bool on = false;
+  double acc[12] = {};
+  long calls = 0;
+  double last = 0;
+  void mark(int i);
+};
+extern HostProf g_prof;
+
 // bump allocator over a device buffer
 struct Arena {
   char* base;

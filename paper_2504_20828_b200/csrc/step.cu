@@ -162,11 +162,6 @@ __global__ void fill_task_seg(StepP P) {
 // scans them tile-locally (tile totals to scan_tmp); plan_fix adds the sum of the preceding tile
 // totals (read directly: at most PLAN_FIX_TILES tiles) and writes the task -> segment map
 constexpr int64_t PLAN_FIX_TILES = 4096;
-__device__ __forceinline__ int64_t seg_tasks(const StepP& P, int64_t s) {
-  const int64_t len = P.seg_off[s + 1] - P.seg_off[s];
-  if (len < 0) atomicOr(P.err, ERR_INVAL);
-  return len <= SMALL ? 0 : len <= CH ? 1 : (len + CH - 1) / CH;  // small: k_lane / k_small
-}
 __global__ void __launch_bounds__(SCAN_THREADS) plan_tiles(StepP P) {
   __shared__ int64_t sa[SCAN_THREADS / 32], sb[SCAN_THREADS / 32];
   const int64_t n = (int64_t)P.S + 1;
@@ -175,16 +170,23 @@ __global__ void __launch_bounds__(SCAN_THREADS) plan_tiles(StepP P) {
     *P.redo_cnt = 0;
     if (P.seg_off[P.S] != P.Q) atomicOr(P.err, ERR_INVAL);
   }
+  int64_t o[SCAN_ITEMS + 1];
+#pragma unroll
+  for (int i = 0; i <= SCAN_ITEMS; i++) o[i] = P.seg_off[min(base + i, (int64_t)P.S)];
   int64_t va[SCAN_ITEMS], vb[SCAN_ITEMS], ta = 0, tb = 0;
+  bool bad = false;
 #pragma unroll
   for (int i = 0; i < SCAN_ITEMS; i++) {
     const int64_t s = base + i;
-    const int64_t nt = s < P.S ? seg_tasks(P, s) : 0;
+    const int64_t len = o[i + 1] - o[i];
+    bad |= s < P.S && len < 0;
+    const int64_t nt = s >= P.S || len <= SMALL ? 0 : len <= CH ? 1 : (len + CH - 1) / CH;
     va[i] = nt;
     vb[i] = nt > 1 ? nt : 0;
     ta += va[i];
     tb += vb[i];
   }
+  if (bad) atomicOr(P.err, ERR_INVAL);
   const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
   const int64_t ia = warp_incl_scan(ta), ib = warp_incl_scan(tb);
   if (l == 31) { sa[w] = ia; sb[w] = ib; }
@@ -222,6 +224,9 @@ __global__ void __launch_bounds__(SCAN_THREADS) plan_fix(StepP P) {
   for (int i = 0; i < SCAN_THREADS / 32; i++) { pa += ra[i]; pb += rb[i]; }
   const int64_t n = (int64_t)P.S + 1;
   const int64_t base = blockIdx.x * (int64_t)SCAN_TILE + threadIdx.x * SCAN_ITEMS;
+  int64_t o[SCAN_ITEMS + 1];
+#pragma unroll
+  for (int i = 0; i <= SCAN_ITEMS; i++) o[i] = P.seg_off[min(base + i, (int64_t)P.S)];
 #pragma unroll
   for (int i = 0; i < SCAN_ITEMS; i++) {
     const int64_t s = base + i;
@@ -230,7 +235,7 @@ __global__ void __launch_bounds__(SCAN_THREADS) plan_fix(StepP P) {
     P.task_off[s] = t0;
     P.mtask_off[s] += pb;
     if (s < P.S) {
-      const int64_t len = P.seg_off[s + 1] - P.seg_off[s];
+      const int64_t len = o[i + 1] - o[i];
       const int64_t nt = len <= SMALL ? 0 : len <= CH ? 1 : (len + CH - 1) / CH;
       for (int64_t t = t0; t < t0 + nt && t < P.ntask_max; t++) P.task_seg[t] = (int32_t)s;
     }
@@ -243,23 +248,30 @@ __global__ void __launch_bounds__(SCAN_THREADS) plan_small(StepP P) {
   const int64_t n = (int64_t)P.S + 1;
   const int64_t base = threadIdx.x * SCAN_ITEMS;
   if (threadIdx.x == 0) *P.redo_cnt = 0;
+  // every offset this thread needs in flight at once (one dependent load each costs a DRAM
+  // round trip on the launch's critical path otherwise)
+  int64_t o[SCAN_ITEMS + 1];
+#pragma unroll
+  for (int i = 0; i <= SCAN_ITEMS; i++) o[i] = P.seg_off[min(base + i, (int64_t)P.S)];
   int64_t va[SCAN_ITEMS], vb[SCAN_ITEMS], ta = 0, tb = 0;
+  bool bad = false;
 #pragma unroll
   for (int i = 0; i < SCAN_ITEMS; i++) {
     const int64_t s = base + i;
     int64_t nt = 0;
     if (s < P.S) {
-      const int64_t len = P.seg_off[s + 1] - P.seg_off[s];
-      if (len < 0) atomicOr(P.err, ERR_INVAL);
-      nt = len <= SMALL ? 0 : len <= CH ? 1 : (len + CH - 1) / CH;  // small: k_small
-    } else if (s == P.S && P.seg_off[P.S] != P.Q) {
-      atomicOr(P.err, ERR_INVAL);
+      const int64_t len = o[i + 1] - o[i];
+      bad |= len < 0;
+      nt = len <= SMALL ? 0 : len <= CH ? 1 : (len + CH - 1) / CH;  // small: k_lane / k_small
+    } else if (s == P.S) {
+      bad |= o[i] != P.Q;
     }
     va[i] = nt;
     vb[i] = nt > 1 ? nt : 0;
     ta += va[i];
     tb += vb[i];
   }
+  if (bad) atomicOr(P.err, ERR_INVAL);
   const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
   const int64_t ia = warp_incl_scan(ta), ib = warp_incl_scan(tb);
   if (l == 31) { sa[w] = ia; sb[w] = ib; }
@@ -1196,12 +1208,13 @@ __device__ __forceinline__ bool lane_segment(const StepP& P, LaneStage& st, int6
       const int32_t d = (int32_t)d64, pf = pfv[j - h];
       const uint32_t f = st.fl[of + jj];
       // window (else hand back): d = deadline - now in [-2^30, 2^30) (d64 is d sign-extended, and
-      // d + 2^30 < 2^31), pf < 2^30, the packed key field rel + 2^26 < 2^27 - 1; so d - pf and the
-      // key are exact int32 and the packed word of a live entry is never the all-ones sentinel
+      // d + 2^30 < 2^31), pf < 2^26, the packed key field rel + 2^26 < 2^27 - 1; so d - pf and the
+      // key are exact int32, 32 prefill times sum below 2^31, and the packed word of a live entry
+      // is never the all-ones sentinel
       const uint32_t u = (uint32_t)((kdl ? d : 0) + kpf * pf + (1 << 26));
       if (v) {
         bad |= (uint32_t)(d64 >> 32) ^ (uint32_t)(d >> 31);
-        mxw = max(mxw, max((uint32_t)(d + (1 << 30)) >> 4, (uint32_t)pf >> 3));  // < 2^27 iff both in range
+        mxw = max(mxw, max((uint32_t)(d + (1 << 30)) >> 4, (uint32_t)pf << 1));  // < 2^27 iff both in range
         mxw = max(mxw, u);
       }
       const bool dropped = v && drop && !(f & 1u) && d < 0;
@@ -1214,8 +1227,9 @@ __device__ __forceinline__ bool lane_segment(const StepP& P, LaneStage& st, int6
         dm |= (uint32_t)dropped << jj;
         om |= (uint32_t)offc << jj;
       }
-      if (v) pfs[2 * (od + jj)] = pf;  // this entry's deadline is not read again: keep pf in its place
-                                       // (v: an empty segment's slot 0 is the next lane's entry)
+      if (v)  // this entry's deadline is not read again: keep (pf, p) in its place (v: an empty
+              // segment's slot 0 is the next lane's entry)
+        reinterpret_cast<int2*>(st.dl)[od + jj] = make_int2(pf, st.eff[oe + jj]);
     }
   }
   if (F32) {  // visit j is position (j + lane) & 31: rotate left by lane
@@ -1247,43 +1261,55 @@ __device__ __forceinline__ bool lane_segment(const StepP& P, LaneStage& st, int6
     if (d < 0) atomicOr(P.err, ERR_RANGE);
     C = g.tbt - d;
   }
-  // a4: Algorithm 1 lines 5-13, strict budgets in key order; the next entry's (p, pf) is loaded
-  // before the current one is tested
+  // the sorted keys go to this lane's own eff slots (its p values now sit beside pf), so that
+  // Algorithm 1's loop below can index them without unrolling
+  uint32_t* ks = reinterpret_cast<uint32_t*>(st.eff) + oe;
+#pragma unroll
+  for (int j = 0; j < SMALL; j++)
+    if (F32 || j < n) ks[slot(j)] = a[j];
+  // a4: Algorithm 1 lines 5-13, strict budgets in key order (prefix sums of tokens, blocks and
+  // prefill µs strictly below N, M, C; at most R).  Σpf < 2^31, so the µs budget compares in 32
+  // bits against C clamped to [0, 2^32 - 1].  The next entry is fetched before the current one is
+  // tested.
   const int32_t N = g.N, M = g.M;
-  const uint32_t bs = (uint32_t)P.bs;
+  const uint32_t bs = (uint32_t)P.bs, ab1 = (uint32_t)P.md.b - 1u;
+  const uint32_t Cc = C <= 0 ? 0u : (C >= (int64_t)0xffffffff ? 0xffffffffu : (uint32_t)C);
+  const int2* ent = reinterpret_cast<const int2*>(st.dl) + od;  // (pf, p) by position
+  const int jmax = min(F32 ? SMALL : n, (int)max(R, 0));
   int32_t St = 0, Sb = 0;
-  int64_t Sc = 0;
+  uint32_t Sc = 0, sp = 0;
   int k = 0;
   uint32_t am = 0;
-  uint64_t sp = 0, sp2 = 0, spc = 0;
-  int32_t pn = st.eff[oe + (int)(a[0] & 31u)], pfn = pfs[2 * (od + (int)(a[0] & 31u))];
-#pragma unroll
-  for (int j = 0; j < SMALL; j++) {
-    const uint32_t x = a[j];
-    const int32_t p = pn, pf = pfn;
-    if (j + 1 < SMALL) {
-      const int q = (int)(a[j + 1 < SMALL ? j + 1 : j] & 31u);
-      pn = st.eff[oe + q];
-      pfn = pfs[2 * (od + q)];
+  uint64_t sp2 = 0, spc = 0;
+  uint32_t xn = jmax > 0 ? ks[slot(0)] : 0xffffffffu;
+  int2 en = ent[xn & 31u];
+  int32_t* adm = P.admit_idx + lo;
+#pragma unroll 2
+  for (int j = 0; j < jmax; j++) {
+    const uint32_t x = xn;
+    const int2 e = en;
+    if (j + 1 < jmax) {
+      xn = ks[slot(j + 1)];
+      en = ent[xn & 31u];
     }
-    if (x == 0xffffffffu || j >= R) break;
-    St += p;
-    Sb += (int32_t)div_m((uint32_t)p + bs, P.bs_m);
-    Sc += pf;
-    if (!(St < N && Sb < M && Sc < C)) break;
-    const int pos = (int)(x & 31u);
-    P.admit_idx[lo + j] = (int32_t)(lo + pos);
+    if (x == 0xffffffffu) break;
+    const uint32_t p = (uint32_t)e.y;
+    St += (int32_t)p;
+    Sb += (int32_t)div_m(p + bs, P.bs_m);
+    Sc += (uint32_t)e.x;
+    if (!(St < N && Sb < M && Sc < Cc)) break;
+    const uint32_t pos = x & 31u;
+    adm[j] = (int32_t)(lo + pos);
     am |= 1u << pos;
     k = j + 1;
-    const uint64_t q = (uint64_t)p;
-    sp += q;
-    sp2 += q * q;
-    spc += q * (uint64_t)div_m((uint32_t)p + (uint32_t)P.md.b - 1u, P.ab_m);
+    sp += p;
+    sp2 += (uint64_t)p * p;
+    spc += (uint64_t)p * div_m(p + ab1, P.ab_m);
   }
   // a6: the hybrid batch {admitted} + {decodes}
   int64_t l = 0;
   if (k > 0 || Bd > 0) {
-    l = k ? lat_us(P.md, (uint64_t)k, sp, sp2, spc, (uint64_t)Bd, (uint64_t)sl) : d;
+    l = k ? lat_us(P.md, (uint64_t)k, (uint64_t)sp, sp2, spc, (uint64_t)Bd, (uint64_t)sl) : d;
     if (l < 0) atomicOr(P.err, ERR_RANGE);
   }
   // a5: offload (not admitted) and drop lists in ascending position
@@ -1596,6 +1622,7 @@ asc_status launch_schedule_step(asc_ctx* c, const asc_step_in* in, asc_step_out*
   P.redo_cnt = ar.take<int32_t>(1);
   P.err = c->d_err;
   cudaStream_t sm = c->stream;
+  g_prof.mark(1);
   int64_t launches = 0;
   const int dev_sms = c->sms;
   if (S + 1 <= SCAN_TILE) {
@@ -1614,6 +1641,7 @@ asc_status launch_schedule_step(asc_ctx* c, const asc_step_in* in, asc_step_out*
     fill_task_seg<<<(unsigned)(gf < 4 * dev_sms ? (gf > 0 ? gf : 1) : 4 * dev_sms), 256, 0, sm>>>(P);
     launches += 5;
   }
+  g_prof.mark(2);
   {  // a planner that failed to launch must not leave k1 reading an unscanned task map
     const cudaError_t pe = cudaGetLastError();
     if (pe != cudaSuccess) return cuda_check(c, pe, "schedule_step planner launch");
@@ -1635,6 +1663,7 @@ asc_status launch_schedule_step(asc_ctx* c, const asc_step_in* in, asc_step_out*
   cudaEventRecord(c->ev1, sm);
   c->timed = true;
   launches += 1;
+  g_prof.mark(3);
   {  // short segments (after k1's timed bracket: k1 is the roofline kernel of row S's big shape):
      // k_lane decides them one per thread, k_small the ones it hands back
     constexpr size_t LSMEM = LW * sizeof(LaneStage);
@@ -1655,6 +1684,7 @@ asc_status launch_schedule_step(asc_ctx* c, const asc_step_in* in, asc_step_out*
     k_small<true><<<(unsigned)(gs > 0 ? gs : 1), 256, 0, sm>>>(P);
     launches += 2;
   }
+  g_prof.mark(4);
   if (Q > CH) {
     int64_t g2 = S < (int64_t)dev_sms * 4 ? S : (int64_t)dev_sms * 4;
     k2_segments<<<(unsigned)(g2 > 0 ? g2 : 1), WARPS * 32, 0, sm>>>(P);
@@ -1664,7 +1694,9 @@ asc_status launch_schedule_step(asc_ctx* c, const asc_step_in* in, asc_step_out*
     launches += 2;
   }
   c->last_kernel_launches = launches;
-  return cuda_check(c, cudaGetLastError(), "schedule_step launch");
+  const asc_status lst = cuda_check(c, cudaGetLastError(), "schedule_step launch");
+  g_prof.mark(5);
+  return lst;
 }
 
 }  // namespace asc

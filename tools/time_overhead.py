@@ -8,11 +8,12 @@ from gen import presets as P
 from paper_2504_20828_b200 import asc
 import helpers as H
 cfg = P.config()
-for S, Q in ((1, 1), (1000000, 32)):
+for S, Q, strm in ((1, 1, None), (1, 1, 'torch'), (1000000, 32, None), (1000000, 32, 'torch')):
     ins = H.random_step_inputs(np.random.default_rng(1), S, 0, cfg, qs=np.full(S, Q))
     d = {k: torch.from_numpy(np.ascontiguousarray(v)).cuda() for k, v in ins.items()}
     d["Q"] = S * Q
-    ctx = asc.Context(cfg, 0)
+    sobj = torch.cuda.Stream() if strm else None
+    ctx = asc.Context(cfg, 0, sobj)
     out = ctx.schedule_step(d, want_prefill=False)
     n = 200 if S == 1 else 20
     torch.cuda.synchronize()
@@ -30,6 +31,6 @@ for S, Q in ((1, 1), (1000000, 32)):
     for _ in range(n):
         L.asc_schedule_step(ctx.h, C.byref(i), C.byref(o))
     t3 = time.perf_counter()
-    print(f"S={S} Q={Q}: python API {1e6*(t1-t0)/n:.1f} us/call, C call alone {1e6*(t3-t2)/n:.1f} us/call, "
+    print(f"S={S} Q={Q} stream={strm}: python API {1e6*(t1-t0)/n:.1f} us/call, C call alone {1e6*(t3-t2)/n:.1f} us/call, "
           f"launches {ctx.last_launches()}")
     ctx.close()
