@@ -382,8 +382,36 @@ __device__ __forceinline__ int finalize_segment(const StepP& P, int64_t s, const
 // id-ascending output indices starting at out[base]; returns the new base.  Set entries go to a
 // 256-slot shared-memory ring at their rank and leave it 128 at a time as coalesced stores (four
 // 32-lane rows with immediate offsets), instead of one 64-bit-addressed scattered store each.
+#ifndef ASC_K1_EXPAND
+#define ASC_K1_EXPAND 0
+#endif
+// direct variant: each lane stores its (at most four) set entries of a group straight to their
+// ranks -- fewer instructions than the ring; the warp's stores for one group stay inside a
+// 512-byte window, so they still coalesce into a few sectors
+__device__ __forceinline__ int64_t expand_direct(const uint32_t* words, int ng, int64_t b4,
+                                                 int32_t* out, int64_t base) {
+  const int lane = lane_id();
+  const uint32_t lt = lanemask_lt(), bit = 1u << lane;
+  int32_t* ob = out + base;
+  uint32_t cnt = 0;
+  const int32_t e00 = (int32_t)b4 + 4 * lane;
+  for (int g = 0; g < ng; g++) {
+    const uint4 wv = *reinterpret_cast<const uint4*>(words + 4 * g);  // words 4g..4g+3
+    if ((wv.x | wv.y | wv.z | wv.w) == 0) continue;
+    uint32_t r = cnt + __popc(wv.x & lt) + __popc(wv.y & lt) + __popc(wv.z & lt) + __popc(wv.w & lt);
+    const int32_t e0 = e00 + g * GE;
+    if (wv.x & bit) ob[r++] = e0;
+    if (wv.y & bit) ob[r++] = e0 + 1;
+    if (wv.z & bit) ob[r++] = e0 + 2;
+    if (wv.w & bit) ob[r] = e0 + 3;
+    cnt += __popc(wv.x) + __popc(wv.y) + __popc(wv.z) + __popc(wv.w);
+  }
+  return base + cnt;
+}
+
 __device__ __forceinline__ int64_t expand_groups(const uint32_t* words, int ng, int64_t b4,
                                                  int32_t* out, int64_t base, int32_t* ring) {
+  if (ASC_K1_EXPAND) return expand_direct(words, ng, b4, out, base);
   const int lane = lane_id();
   const uint32_t lt = lanemask_lt(), bit = 1u << lane;
   int32_t* ob = out + base;
@@ -777,7 +805,7 @@ __device__ __forceinline__ bool task_fast(const StepP& P, const TaskCtx& t, Stag
         const int64_t dd = cur.dl[u] + nowc;
         const uint32_t lo1 = (uint32_t)dd, hi1 = (uint32_t)((uint64_t)dd >> 32);
         const int32_t q = cur.p[u] - 1;
-        const int32_t pf = __ldg(tab + (q & (int32_t)PK_PMASK));
+        const int32_t pf = __ldg(tab + ((uint32_t)q & (uint32_t)PK_PMASK));  // unsigned: one IMAD.WIDE
         accH |= v ? hi1 : 0u;
         accL |= v ? lo1 : 0u;
         accQ |= v ? (uint32_t)q : 0u;

@@ -20,10 +20,13 @@ ap.add_argument("--S", type=int, default=4096)
 ap.add_argument("--Q", type=int, default=10000)
 ap.add_argument("--reps", type=int, default=2)
 ap.add_argument("--workload", default="config3")
+ap.add_argument("--select", default=None, help="comma-separated trace indices (sim)")
 a = ap.parse_args()
 if a.what == "sim":
     cfg, b = P.workload(a.workload, n=a.n)
-    if a.traces < b.T:
+    if a.select:
+        b = b.subset([int(x) for x in a.select.split(",")])
+    elif a.traces < b.T:
         b = b.subset(np.linspace(0, b.T - 1, a.traces).round().astype(int))
     ctx = asc.Context(cfg, 0)
     tr = asc.batch_arrays(b, "cuda:0")
