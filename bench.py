@@ -48,7 +48,8 @@ def args_():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-step-bench", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--config4", action="store_true", help="also time BASELINE config 4 in full")
+    ap.add_argument("--no-config4", action="store_true", help="skip the BASELINE config 4 sub-line")
+    ap.add_argument("--no-config5", action="store_true", help="skip the BASELINE config 5 shard sub-line")
     return ap.parse_args()
 
 
@@ -256,19 +257,28 @@ def step_microbench(asc, torch, dev, stream, warmup, steps, hbm_peak):
         for _ in range(warmup):
             o2 = c2.schedule_step(d2, want_prefill=False)
         torch.cuda.synchronize()
+        kl = []
         e0.record(stream)
         for _ in range(steps):
             o2 = c2.schedule_step(d2, want_prefill=False, out=o2)
+            kl.append(c2.last_kernel2_ms())
         e1.record(stream)
         torch.cuda.synchronize()
         ms2 = e0.elapsed_time(e1) / steps
         n2 = int(o2["admit_cnt"].sum() + o2["offload_cnt"].sum() + o2["drop_cnt"].sum())
         b2 = 13 * S2 * Q2 + 4 * n2 + S2 * (8 * 4 + 4 * 6) + 8
         c2.close()
-        others.append({"shape": f"S={S2} segments x Q={Q2} entries", "ms_per_call": ms2,
-                       "evaluations_per_s": S2 * Q2 / (ms2 * 1e-3),
-                       "whole_call_achieved_gbs": b2 / (ms2 * 1e-3) / 1e9,
-                       "whole_call_frac": b2 / (ms2 * 1e-3) / 1e9 / hbm_peak})
+        sh = {"shape": f"S={S2} segments x Q={Q2} entries", "ms_per_call": ms2,
+              "evaluations_per_s": S2 * Q2 / (ms2 * 1e-3),
+              "whole_call_achieved_gbs": b2 / (ms2 * 1e-3) / 1e9,
+              "whole_call_frac": b2 / (ms2 * 1e-3) / 1e9 / hbm_peak}
+        if Q2 <= 32:  # every segment is k_lane's (one thread per segment)
+            klm = float(np.mean(kl))
+            sh["roofline"] = {"bound": "hbm", "kernel": "k_lane (one thread per short segment)",
+                              "achieved": b2 / (klm * 1e-3) / 1e9, "peak": hbm_peak, "unit": "GB/s",
+                              "frac": b2 / (klm * 1e-3) / 1e9 / hbm_peak, "kernel_ms": klm,
+                              "algorithmic_bytes": b2, "traffic": traffic_bytes("k_lane")}
+        others.append(sh)
         del d2, o2
     ach_k1 = byts / (k1ms * 1e-3) / 1e9     # single-task segments: k1 does all reads and writes
     ach_call = byts / (ms * 1e-3) / 1e9
@@ -471,8 +481,12 @@ def main():
     ctx.close()
     if rank == 0 and not a.no_baselines:
         line["baselines"] = baselines(asc, torch, dev, stream, cfg, batch, col["good"] / max(col["total"], 1))
-    if rank == 0 and a.config4:
+    if rank == 0 and not a.no_config4:
         line["config4"] = config4_line(asc, torch, dev, stream, hbm_peak)
+    if rank == 0 and not a.no_config5:
+        del tr, out, res, summ
+        torch.cuda.empty_cache()
+        line["config5_shard"] = config5_line(asc, torch, dev, stream)
     if rank == 0 and world == 1 and not a.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(cfg, batch)
     if rank == 0:
@@ -503,6 +517,42 @@ def config4_line(asc, torch, dev, stream, hbm_peak):
             "algorithmic_gbs": (44 * b.R + 12 * ev) / (ms * 1e-3) / 1e9,
             "dram_bytes": tr_,
             "note": "one trace = one warp's sequential event chain"}
+
+
+def config5_line(asc, torch, dev, stream, W=16, r=0):
+    """BASELINE config 5's per-GPU unit: shard r of W of the 65,536-trace x 100k-request QPS x SLO
+    grid (traces i = r mod W, as dist.py shards it across ranks) = 4096 traces x 10^5 requests
+    (4.1e8) on one B200; one timed asc_simulate_batch + asc_goodput after the uploads."""
+    from paper_2504_20828_b200 import dist as D
+    t0 = time.perf_counter()
+    cfg, full = P.workload("config5", n=1)
+    cfg, b = P.workload("config5", n=100_000, select=D.shard(full.T, r, W))
+    gen_s = time.perf_counter() - t0
+    ctx = asc.Context(cfg, dev.index, stream)
+    tr = asc.batch_arrays(b, dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record(stream)
+    out = ctx.simulate_batch(tr)
+    sim_ms = ctx.last_kernel_ms()
+    good, total = ctx.goodput(tr, out)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    dec = int(out["decisions"][:b.T].sum().item())
+    ev = int(out["evaluations"][:b.T].sum().item())
+    g = int(good[:b.T].cpu().numpy().view(np.uint64).sum())
+    t = int(total[:b.T].cpu().numpy().view(np.uint64).sum())
+    ctx.close()
+    del tr, out, good, total
+    torch.cuda.empty_cache()
+    return {"workload": f"config5 shard {r}/{W}: {b.T} traces x 100k ShareGPT-shaped requests "
+                        f"({b.R} requests), 2L1H, QPS 1/8..8 x SLO scale 1/16..4, calibrated preset",
+            "ms": ms, "kernel_ms": sim_ms, "decisions": dec, "evaluations": ev,
+            "decisions_per_s": dec / (ms * 1e-3), "simulated_req_per_s": b.R / (ms * 1e-3),
+            "evaluations_per_s": ev / (ms * 1e-3), "goodput": g / max(t, 1), "host_gen_s": gen_s,
+            "note": "one GPU's share of the 8-GPU config-5 grid (W = 16 shards; bench.py --gpus N "
+                    "--workload config5 runs the grid sharded across N ranks)"}
 
 
 def latency_microbench(asc, torch, dev, stream, hbm_peak, n=1 << 26, steps=5):

@@ -276,6 +276,9 @@ int64_t asc_last_kernel_launches(const asc_ctx* ctx);
  * kernel (simulate: the step loop; schedule_step: the streaming pass; goodput: the reduction),
  * or -1 if none ran. */
 double asc_last_kernel_ms(const asc_ctx* ctx);
+/* Diagnostics: device time (ms) of the last call's secondary kernel (schedule_step: k_lane, the
+ * one-thread-per-segment pass over segments of <= 32 entries), or -1 if the call has none. */
+double asc_last_kernel2_ms(const asc_ctx* ctx);
 
 /* ---------------------------------------------------------------------------------------------
  * asc_fit_perf — batched calibration of the performance model.

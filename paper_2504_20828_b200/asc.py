@@ -20,7 +20,7 @@ STATUS = {0: "ASC_OK", 1: "ASC_E_INVAL", 2: "ASC_E_CONFIG", 3: "ASC_E_NOMEM", 4:
           5: "ASC_E_EMPTY", 6: "ASC_E_RANGE", 7: "ASC_E_INVARIANT"}
 EXPORTS = ("asc_create", "asc_destroy", "asc_last_error", "asc_abi_version", "asc_schedule_step",
            "asc_simulate_batch", "asc_goodput", "asc_summarize", "asc_fit_perf", "asc_latency", "asc_last_kernel_launches",
-           "asc_last_kernel_ms")
+           "asc_last_kernel_ms", "asc_last_kernel2_ms")
 
 
 class AscError(RuntimeError):
@@ -126,6 +126,8 @@ def lib():
         L.asc_last_kernel_launches.restype = C.c_int64
         L.asc_last_kernel_ms.argtypes = [C.c_void_p]
         L.asc_last_kernel_ms.restype = C.c_double
+        L.asc_last_kernel2_ms.argtypes = [C.c_void_p]
+        L.asc_last_kernel2_ms.restype = C.c_double
         _LIB = L
     return _LIB
 
@@ -182,6 +184,10 @@ def asc_last_kernel_launches(ctx):
 
 def asc_last_kernel_ms(ctx):
     return float(lib().asc_last_kernel_ms(ctx))
+
+
+def asc_last_kernel2_ms(ctx):
+    return float(lib().asc_last_kernel2_ms(ctx))
 
 
 def asc_schedule_step(ctx, seg_off, now_us, deadline_us, eff_prompt, flags, dec_count, dec_ctx_sum,
@@ -268,6 +274,9 @@ class Context:
 
     def last_kernel_ms(self):
         return asc_last_kernel_ms(self.h)
+
+    def last_kernel2_ms(self):
+        return asc_last_kernel2_ms(self.h)
 
     def schedule_step(self, ins, want_prefill=True, out=None):
         """ins: dict of arrays (all torch CUDA or all numpy).  Returns dict of outputs; `out` (a

@@ -205,6 +205,8 @@ asc_status asc_create(const asc_config* cfg, int device, void* cuda_stream, asc_
   }
   cudaEventCreate(&c->ev0);
   cudaEventCreate(&c->ev1);
+  cudaEventCreate(&c->ev2);
+  cudaEventCreate(&c->ev3);
   cudaMemsetAsync(c->d_err, 0, sizeof(int), c->stream);
   cudaMemsetAsync(d_w, 0, 2 * sizeof(int64_t), c->stream);
   build_tables<<<(c->pt_size + 255) / 256, 256, 0, c->stream>>>(
@@ -243,6 +245,8 @@ void asc_destroy(asc_ctx* ctx) {
   if (ctx->stage) cudaFree(ctx->stage);
   if (ctx->ev0) cudaEventDestroy(ctx->ev0);
   if (ctx->ev1) cudaEventDestroy(ctx->ev1);
+  if (ctx->ev2) cudaEventDestroy(ctx->ev2);
+  if (ctx->ev3) cudaEventDestroy(ctx->ev3);
   delete ctx;
 }
 
@@ -337,6 +341,7 @@ asc_status asc_schedule_step(asc_ctx* c, const asc_step_in* in, asc_step_out* ou
     return fail(c, ASC_E_CONFIG, "asc_schedule_step: ASC_POLICY_WEIGHTED and offload_rule 1 are asc_simulate_batch only");
   c->err.clear();
   c->timed = false;
+  c->timed2 = false;
   if (in->S < 0) return fail(c, ASC_E_INVAL, "asc_schedule_step: S < 0");
   if (!in->seg_off || !in->now_us || !in->deadline_us || !in->eff_prompt || !in->flags ||
       !in->dec_count || !in->dec_ctx_sum || !in->tbt_slo_us || !in->budget_tokens ||
@@ -410,6 +415,7 @@ asc_status asc_simulate_batch(asc_ctx* c, const asc_traces* tr, asc_outcomes* ou
   if (!c || !tr || !out) return fail(c, ASC_E_INVAL, "asc_simulate_batch: NULL argument");
   c->err.clear();
   c->timed = false;
+  c->timed2 = false;
   if (tr->T < 0) return fail(c, ASC_E_INVAL, "asc_simulate_batch: T < 0");
   if (!tr->trace_off || !tr->arrival_us || !tr->prompt_len || !tr->output_len || !tr->ttft_slo_us ||
       !tr->tbt_slo_us || !out->first_token_us || !out->done_us || !out->prefill_start_us ||
@@ -477,6 +483,7 @@ asc_status asc_goodput(asc_ctx* c, const asc_traces* tr, const asc_outcomes* out
   if (!c || !tr || !out || !good || !total) return fail(c, ASC_E_INVAL, "asc_goodput: NULL argument");
   c->err.clear();
   c->timed = false;
+  c->timed2 = false;
   if (tr->T < 0) return fail(c, ASC_E_INVAL, "asc_goodput: T < 0");
   cudaSetDevice(c->device);
   const int kind = ptr_kind(tr->trace_off);
@@ -520,6 +527,7 @@ asc_status asc_summarize(asc_ctx* c, const asc_traces* tr, const asc_outcomes* o
   if (!c || !tr || !out || !sum) return fail(c, ASC_E_INVAL, "asc_summarize: NULL argument");
   c->err.clear();
   c->timed = false;
+  c->timed2 = false;
   if (tr->T < 0) return fail(c, ASC_E_INVAL, "asc_summarize: T < 0");
   if (!tr->trace_off || !tr->arrival_us || !tr->output_len || !tr->ttft_slo_us || !tr->tbt_slo_us ||
       !out->first_token_us || !out->done_us || !out->prefill_start_us || !out->status)
@@ -580,6 +588,7 @@ asc_status asc_fit_perf(asc_ctx* c, const asc_fit_in* in, double lambda, double*
   if (!c || !in || !coef) return fail(c, ASC_E_INVAL, "asc_fit_perf: NULL argument");
   c->err.clear();
   c->timed = false;
+  c->timed2 = false;
   if (in->G < 0) return fail(c, ASC_E_INVAL, "asc_fit_perf: G < 0");
   if (!(lambda >= 0.0 && lambda < HUGE_VAL)) return fail(c, ASC_E_INVAL, "asc_fit_perf: lambda must be finite and >= 0");
   if (!in->rec_off || !in->F || !in->M || !in->y) return fail(c, ASC_E_INVAL, "asc_fit_perf: NULL array");
@@ -626,6 +635,7 @@ asc_status asc_latency(asc_ctx* c, int64_t n, const uint64_t* F, const uint64_t*
   if (!c) return fail(c, ASC_E_INVAL, "asc_latency: NULL context");
   c->err.clear();
   c->timed = false;
+  c->timed2 = false;
   if (n < 0) return fail(c, ASC_E_INVAL, "asc_latency: n < 0");
   if (n == 0) { c->last_kernel_launches = 0; return ASC_OK; }
   if (!F || !M || !lat_us) return fail(c, ASC_E_INVAL, "asc_latency: NULL array");
@@ -661,6 +671,13 @@ double asc_last_kernel_ms(const asc_ctx* c) {
   if (!c || !c->timed) return -1.0;
   float ms = -1.0f;
   if (cudaEventElapsedTime(&ms, c->ev0, c->ev1) != cudaSuccess) { cudaGetLastError(); return -1.0; }
+  return (double)ms;
+}
+
+double asc_last_kernel2_ms(const asc_ctx* c) {
+  if (!c || !c->timed2) return -1.0;
+  float ms = -1.0f;
+  if (cudaEventElapsedTime(&ms, c->ev2, c->ev3) != cudaSuccess) { cudaGetLastError(); return -1.0; }
   return (double)ms;
 }
 

@@ -30,7 +30,8 @@ struct asc_ctx {
   std::string err;
   int64_t last_kernel_launches = 0;  // kernels launched by the last call (bench evidence)
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;  // bracket the dominant kernel of the last call
-  bool timed = false;
+  cudaEvent_t ev2 = nullptr, ev3 = nullptr;  // bracket its secondary kernel (schedule_step: k_lane)
+  bool timed = false, timed2 = false;
 };
 
 namespace asc {

@@ -1706,7 +1706,10 @@ asc_status launch_schedule_step(asc_ctx* c, const asc_step_in* in, asc_step_out*
     }
     int64_t gl = (((int64_t)S + 31) / 32 + LW - 1) / LW;
     gl = gl < (int64_t)dev_sms * 4 ? gl : (int64_t)dev_sms * 4;  // one resident wave
+    cudaEventRecord(c->ev2, sm);
     k_lane<<<(unsigned)(gl > 0 ? gl : 1), LW * 32, LSMEM, sm>>>(P);
+    cudaEventRecord(c->ev3, sm);
+    c->timed2 = true;
     int64_t gs = ((int64_t)S * 32 + 255) / 256;
     gs = gs < (int64_t)dev_sms * ASC_KS_MINB ? gs : (int64_t)dev_sms * ASC_KS_MINB;
     k_small<true><<<(unsigned)(gs > 0 ? gs : 1), 256, 0, sm>>>(P);

@@ -22,7 +22,7 @@ for s in "$@"; do
            echo pytest_rc=$?; tail -22 gpurun_out/${tag}_pytest_gpu.log;;
     testsfast) timeout 1500 python -m pytest tests -m "gpu and not slow" -x -q > gpurun_out/${tag}_pytest_gpu.log 2>&1
            echo pytest_rc=$?; tail -5 gpurun_out/${tag}_pytest_gpu.log;;
-    bench) timeout 1500 python bench.py --config4 > gpurun_out/${tag}_bench.json 2> gpurun_out/${tag}_bench.err
+    bench) timeout 1500 python bench.py > gpurun_out/${tag}_bench.json 2> gpurun_out/${tag}_bench.err
            echo bench_rc=$?; tail -c 6000 gpurun_out/${tag}_bench.json; tail -5 gpurun_out/${tag}_bench.err;;
     benchref) timeout 900 python bench.py --impl reference > gpurun_out/${tag}_bench_ref.json 2>&1; echo ref_rc=$?
            cat gpurun_out/${tag}_bench_ref.json | tail -c 1500;;
@@ -33,11 +33,11 @@ for s in "$@"; do
       cap sim sim_kernel 1 sim --traces 4096 --n 10000 --reps 1
       cap sim_config4 sim_kernel 1 sim --workload config4 --traces 1 --n 1000000 --reps 1
       cap k1 k1_tasks 2 step --S 4096 --Q 10000 --reps 2
-      cap ksmall k_small 2 step --S 1000000 --Q 32 --reps 2
+      cap klane k_lane 2 step --S 1000000 --Q 32 --reps 2
       cap fit fit_partials 2 fit --reps 2
       python tools/ncu_traffic.py gpurun_out/${tag}_ncu_traffic.json \
         sim_kernel=gpurun_out/${tag}_sim_dram.csv sim_kernel_config4=gpurun_out/${tag}_sim_config4_dram.csv \
-        k1_tasks=gpurun_out/${tag}_k1_dram.csv k_small=gpurun_out/${tag}_ksmall_dram.csv \
+        k1_tasks=gpurun_out/${tag}_k1_dram.csv k_lane=gpurun_out/${tag}_klane_dram.csv \
         fit_partials=gpurun_out/${tag}_fit_dram.csv;;
     simfull) timeout 2400 ncu --set full --import-source on --clock-control none -k regex:sim_kernel -c 1 \
            -o gpurun_out/${tag}_sim_full python tools/profile_run.py sim --traces 4096 --n 10000 --reps 1 \
