@@ -53,6 +53,8 @@ struct SimP {
   int32_t pt;
   int32_t n_lp, n_hp, K, bs, lp_max, lp_tok, hp_tok, policy, offl, tickets, elastic, drop, hist_def;
   uint64_t bs_m;  // ceil(2^38 / bs): x / bs = (x * bs_m) >> 38 exactly for 0 <= x < 2^25 (bs <= 512)
+  uint64_t ab_m;  // ceil(2^38 / b) for the attention block b (ceilb), used when ab_fast
+  int32_t ab_fast;  // b <= 4096: (x * ab_m) >> 38 == x / b for every x < 2^25 + b
   int32_t kv_lp, kv_hp;
   int64_t W, margin, delay;
   int32_t T;
@@ -124,11 +126,23 @@ struct Wp {
   __device__ __forceinline__ bool tickets() const { return ts()->sw & 2; }
 };
 
-__device__ __forceinline__ int64_t pf_of(int32_t p) {
-  if (p < P.pt) return __ldg(P.pf_tab + p);
+// Out-of-line copies of the rarely taken latency evaluations: inlined, each call site would carry
+// its own copy of the integer moments, the wrap guard and the fp64 regression, and the event loop's
+// hot code would outgrow the instruction cache (the kernel is instruction-fetch bound).
+__device__ __noinline__ int64_t pf_slow(int32_t p) {  // prompts beyond the per-ctx table
   const int64_t v = prefill_lat(P.md, (uint64_t)p);
   if (v < 0) { atomicOr(P.err, ERR_RANGE); return INT32_MAX; }
   return v;
+}
+__device__ __forceinline__ int64_t pf_of(int32_t p) {
+  return p < P.pt ? __ldg(P.pf_tab + p) : pf_slow(p);
+}
+__device__ __noinline__ int64_t lat_dec_call(int64_t Bd, int64_t sl) {  // decode-only batch, Eq. 4-5
+  return lat_decode(P.md, (uint64_t)Bd, (uint64_t)sl);
+}
+__device__ __noinline__ int64_t lat_batch(uint64_t nadm, uint64_t sp, uint64_t sp2, uint64_t spc, uint64_t Bd,
+                                         uint64_t sl) {  // hybrid batch from its moments, Eq. 3-5
+  return lat_us(P.md, nadm, sp, sp2, spc, Bd, sl);
 }
 // division by the block size without a division sequence: with m = ceil(2^38 / bs) = (2^38 + e) / bs,
 // 0 <= e < bs <= 512, x * m / 2^38 = x / bs + x * e / (bs * 2^38) and x * e < 2^38 for x < 2^29, so the
@@ -137,6 +151,11 @@ __device__ __forceinline__ int64_t pf_of(int32_t p) {
 __device__ __forceinline__ int32_t divb(int32_t x) { return (int32_t)(((uint64_t)(uint32_t)x * P.bs_m) >> 38); }
 __device__ __forceinline__ int32_t modb(int32_t x) { return x - divb(x) * P.bs; }
 __device__ __forceinline__ int32_t blk_of(int32_t eff) { return divb(eff + P.bs); }
+// ceil(u / b), b = the attention block (App. A.1, G15); u < 2^25 (a token count)
+__device__ __forceinline__ uint64_t ceilb(uint64_t u) {
+  const uint32_t x = (uint32_t)u + (uint32_t)P.md.b - 1u;
+  return P.ab_fast ? (uint64_t)(((uint64_t)x * P.ab_m) >> 38) : (uint64_t)(x / (uint32_t)P.md.b);
+}
 
 // time-invariant priority key of request gid with effective prompt eff (DESIGN.md §2 Keys)
 __device__ __forceinline__ int64_t key_of(int64_t gid, int32_t eff) {
@@ -486,15 +505,20 @@ __device__ __noinline__ int lp_admit(Wp w, int k, int64_t T, int32_t ndrop,
   const int64_t N = P.lp_tok, M = I.kv_free, Rb = P.lp_max - Bd;
   int64_t C = INF64, ldec = 0;
   if (Bd) {
-    ldec = lat_decode(P.md, (uint64_t)Bd, (uint64_t)sl);
+    ldec = lat_dec_call(Bd, (int64_t)sl);
     if (ldec < 0) atomicOr(P.err, ERR_RANGE);
     C = w.tbt() - ldec;
   }
   const int32_t len = I.wq_len;
-  // Algorithm 1 lines 5-13 as a strict prefix-sum scan over the sorted prefix
+  // Algorithm 1 lines 5-13 as a strict prefix-sum scan over the sorted prefix.  Token and block
+  // sums run in 32 bits: a chunk of 32 is reached only if every running sum of the previous one
+  // stayed below N (< 2^25) / M (< 2^31), and a chunk adds < 2^30 (p < 2^25), so they stay < 2^32;
+  // the admitted sums are below N and M.  The µs sum (prefill times up to 2^31) stays 64-bit.
   int32_t nadm = 0;
-  uint64_t sp = 0, sp2 = 0, spc = 0;
-  int64_t used = 0, ct = 0, cb = 0, cc = 0;
+  uint64_t sp2 = 0, spc = 0;
+  uint32_t sp = 0, used = 0, ct = 0, cb = 0;
+  int64_t cc = 0;
+  const uint32_t N32 = (uint32_t)N, M32 = (uint32_t)M;
 #pragma unroll 1
   for (int r = 0; r < KPL; r++) {
     const int pos = r * 32 + lane;
@@ -503,20 +527,20 @@ __device__ __noinline__ int lp_admit(Wp w, int k, int64_t T, int32_t ndrop,
     const int64_t g = w.base() + id;
     const int32_t p = valid ? P.rq_eff[g] : 0;
     const int64_t pf = valid ? pf_of(p) : 0;
-    const int64_t bl = valid ? blk_of(p) : 0;
-    const int64_t St = ct + warp_incl_scan((int64_t)p);
-    const int64_t Sb = cb + warp_incl_scan(bl);
+    const uint32_t bl = valid ? (uint32_t)blk_of(p) : 0u;
+    const uint32_t St = ct + warp_incl_scan((uint32_t)p);
+    const uint32_t Sb = cb + warp_incl_scan(bl);
     const int64_t Sc = cc + warp_incl_scan(pf);
-    const bool ok = valid && St < N && Sb < M && Sc < C && pos < Rb;
+    const bool ok = valid && St < N32 && Sb < M32 && Sc < C && pos < Rb;
     const uint32_t m = __ballot_sync(FULL, ok);
     const int cnt = (m == FULL) ? 32 : (__ffs(~m) - 1);
     if (lane < cnt) {
       admit_req(g, k, T);
       P.bp_id[o + pos] = id;
       const uint64_t u = (uint64_t)p;
-      sp += u;
+      sp += (uint32_t)p;
       sp2 += u * u;
-      spc += u * ceil_div_u(u, P.md.b);
+      spc += u * ceilb(u);
       used += bl;
     }
     nadm += cnt;
@@ -647,7 +671,7 @@ __device__ __noinline__ int lp_admit(Wp w, int k, int64_t T, int32_t ndrop,
   const bool nonempty = nadm > 0 || Bd > 0;
   int64_t l = 0;
   if (nonempty) {
-    l = nadm ? lat_us(P.md, (uint64_t)nadm, sp, sp2, spc, (uint64_t)Bd, (uint64_t)sl) : ldec;
+    l = nadm ? lat_batch((uint64_t)nadm, sp, sp2, spc, (uint64_t)Bd, (uint64_t)sl) : ldec;
     set_batch(I, T, l, Bd > 0, nadm);
   }
   if (nonempty || noff || ndrop || npre)
@@ -658,7 +682,7 @@ __device__ __noinline__ int lp_admit(Wp w, int k, int64_t T, int32_t ndrop,
 // one decode-only batch of the whole decode set (LP with an empty queue, or HP) — the hot path
 __device__ __forceinline__ void decode_batch(SInst& I, int k, int64_t T) {
   const int32_t bd = I.ds_len;
-  const int64_t l = lat_decode(P.md, (uint64_t)bd, (uint64_t)I.ctx_sum);
+  const int64_t l = lat_dec_call(bd, I.ctx_sum);
   if (l < 0) atomicOr(P.err, ERR_RANGE);
   const uint64_t nr = I.nrec + 1;
   const uint64_t h = digest_decode(I.hash, nr, k, T, bd, l);
@@ -691,7 +715,7 @@ __device__ __forceinline__ int64_t form_lp(Wp w, int k, int64_t T) {
     const int64_t Bd = I.ds_len;
     int64_t l = 0;
     if (Bd) {
-      l = lat_decode(P.md, (uint64_t)Bd, (uint64_t)I.ctx_sum);
+      l = lat_dec_call(Bd, I.ctx_sum);
       set_batch(I, T, l, 1, 0);
     }
     digest_log(w, k, T, 0, Bd, 0, ndrop, 0, l);  // ndrop > 0 here
@@ -742,7 +766,7 @@ __device__ __noinline__ int32_t hp_prefill(Wp w, int k, int64_t T, uint64_t* mom
       const uint64_t u = (uint64_t)p;
       sp += u;
       sp2 += u * u;
-      spc += u * ceil_div_u(u, P.md.b);
+      spc += u * ceilb(u);
       used += bl;
     }
     nadm += cnt;
@@ -785,8 +809,7 @@ __device__ __noinline__ int64_t form_hp_general(Wp w, int k, int64_t T) {
   }
   int64_t l = 0;
   if (batch) {
-    l = bd ? lat_decode(P.md, (uint64_t)bd, (uint64_t)I.ctx_sum)
-           : lat_us(P.md, (uint64_t)nadm, mom[0], mom[1], mom[2], 0, 0);
+    l = bd ? lat_dec_call(bd, I.ctx_sum) : lat_batch((uint64_t)nadm, mom[0], mom[1], mom[2], 0, 0);
     set_batch(I, T, l, bd > 0, bd ? 0 : nadm);
   }
   if (batch || ndrop || npre) digest_log(w, k, T, bd ? 0 : nadm, bd, 0, ndrop, npre, l);
@@ -974,7 +997,7 @@ __device__ __noinline__ void complete_prefills(Wp w, int k, int64_t T) {
       } else {
         stay = true;
         const int32_t ctx = p + gen;
-        s = make_int4(id, ctx, out_len - gen, held | ((ctx % P.bs) << R_SHIFT));
+        s = make_int4(id, ctx, out_len - gen, held | (modb(ctx) << R_SHIFT));
         cadd += ctx;
       }
     }
@@ -1028,8 +1051,9 @@ __device__ __forceinline__ void complete(Wp w, int k, int64_t T) {
       const uint32_t mf = __ballot_sync(FULL, fin);
       const uint32_t mk = __ballot_sync(FULL, v && !fin);
       need += __popc(__ballot_sync(FULL, v && !fin && pend));
-      // stable compaction (positions == j until the first completion); every lane has read its
-      // slot before the ballots above, so in-place writes are safe
+      // stable compaction (positions == j until the first completion): every lane's read is
+      // ordered before the in-place writes
+      __syncwarp();
       if (v && !fin) *slotp(w, k, out + __popc(mk & lanemask_lt())) = s;
       if (mf) {
         anyfin = true;
@@ -1202,6 +1226,7 @@ __device__ __noinline__ int64_t run_decode(Wp w, int k, int64_t T_limit) {
       const bool fin = v && doC && sl.z == 0;
       const bool keep = v && !fin;
       const uint32_t mk = __ballot_sync(FULL, keep);
+      __syncwarp();  // every lane's slot read is ordered before the in-place compaction below
       if (keep) {
         *slotp(w, k, out + __popc(mk & lanemask_lt())) = sl;
         mrem2 = min(mrem2, sl.z);
@@ -1247,7 +1272,7 @@ __device__ __noinline__ int64_t run_decode(Wp w, int k, int64_t T_limit) {
       break;
     }
     kvf -= need2;  // growth for the survivors' next token (fits: needJ <= kvf - ncarry above)
-    const int64_t l = lat_decode(P.md, (uint64_t)Bd, (uint64_t)S);
+    const int64_t l = lat_dec_call(Bd, S);
     if (l < 0) atomicOr(P.err, ERR_RANGE);
     nr += 1;
     h = digest_decode(h, nr, k, Et, Bd, l);
@@ -1548,6 +1573,8 @@ asc_status launch_simulate(asc_ctx* c, const asc_traces* tr, asc_outcomes* out, 
   P.pt = c->pt_size;
   P.n_lp = cf.topo.n_lp; P.n_hp = cf.topo.n_hp; P.K = K; P.bs = cf.topo.block_tokens;
   P.bs_m = ((uint64_t(1) << 38) + (uint64_t)P.bs - 1) / (uint64_t)P.bs;
+  P.ab_m = ((uint64_t(1) << 38) + c->md.b - 1) / c->md.b;
+  P.ab_fast = c->md.b <= 4096 ? 1 : 0;
   P.lp_max = cf.topo.lp_max_batch; P.lp_tok = cf.topo.lp_token_budget; P.hp_tok = cf.topo.hp_token_budget;
   P.policy = cf.flags.policy;
   P.offl = cf.flags.offload ? 1 : 0;    // per trace: and n_hp >= 1

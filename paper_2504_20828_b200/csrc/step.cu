@@ -1220,6 +1220,7 @@ __device__ __forceinline__ bool lane_segment(const StepP& P, LaneStage& st, int6
   const bool kdl = P.kdl != 0, drop = P.drop != 0, offl = P.offl != 0;
   const int32_t kpf = P.kpf;
   int32_t pfv[H];
+  if (F32 || n > 0) {  // (an empty segment reads nothing: its slot 0 is the next lane's entry)
 #pragma unroll
   for (int h = 0; h < SMALL; h += H) {
 #pragma unroll
@@ -1259,6 +1260,7 @@ __device__ __forceinline__ bool lane_segment(const StepP& P, LaneStage& st, int6
               // segment's slot 0 is the next lane's entry)
         reinterpret_cast<int2*>(st.dl)[od + jj] = make_int2(pf, st.eff[oe + jj]);
     }
+  }
   }
   if (F32) {  // visit j is position (j + lane) & 31: rotate left by lane
     dm = __funnelshift_l(dm, dm, lane);
@@ -1309,8 +1311,9 @@ __device__ __forceinline__ bool lane_segment(const StepP& P, LaneStage& st, int6
   int k = 0;
   uint32_t am = 0;
   uint64_t sp2 = 0, spc = 0;
+  // (a sentinel's position field is read as entry 0: never outside this lane's segment)
   uint32_t xn = jmax > 0 ? ks[slot(0)] : 0xffffffffu;
-  int2 en = ent[xn & 31u];
+  int2 en = ent[xn == 0xffffffffu ? 0u : (xn & 31u)];
   int32_t* adm = P.admit_idx + lo;
 #pragma unroll 2
   for (int j = 0; j < jmax; j++) {
@@ -1318,7 +1321,7 @@ __device__ __forceinline__ bool lane_segment(const StepP& P, LaneStage& st, int6
     const int2 e = en;
     if (j + 1 < jmax) {
       xn = ks[slot(j + 1)];
-      en = ent[xn & 31u];
+      en = ent[xn == 0xffffffffu ? 0u : (xn & 31u)];
     }
     if (x == 0xffffffffu) break;
     const uint32_t p = (uint32_t)e.y;

@@ -56,6 +56,29 @@ def step_case():
     print("ok step mixed", int(qs.sum()), "entries")
 
 
+def lane_case():
+    # k_lane: full 32-entry groups (n == 32 path), mixed short groups (general path), segments
+    # handed back to k_small (a key outside the 2^26 us window, a prompt beyond the fast table),
+    # and S > 8191 for the two-launch planner
+    cfg = P.config(flg=P.flags(drop=1))
+    rng = np.random.default_rng(11)
+    S = 8300
+    qs = rng.integers(0, 33, size=S)
+    qs[:96] = 32
+    ins = H.random_step_inputs(rng, S, 0, cfg, qs=qs)
+    off = ins["seg_off"]
+    ins["deadline_us"][off[100]] += 1 << 28
+    ins["eff_prompt"][off[200]] = (1 << 17) + 7
+    ctx = asc.Context(cfg, 0)
+    got = ctx.schedule_step(dev(ins))
+    torch.cuda.synchronize()
+    exp = O.schedule_step(cfg, **ins)
+    for k in ("admit_cnt", "offload_cnt", "drop_cnt", "batch_lat_us"):
+        assert np.array_equal(got[k].cpu().numpy()[:S], exp[k][:S]), k
+    ctx.close()
+    print("ok step lanes", int(qs.sum()), "entries")
+
+
 def fit_case():
     from gen import records as RC
     rec = RC.make_records(3, [40, 9000, 20000])
@@ -85,6 +108,7 @@ if __name__ == "__main__":
         sim_case("config4", 3000)
     if "step" in which:
         step_case()
+        lane_case()
     if "fit" in which:
         fit_case()
     if "latency" in which:
