@@ -780,8 +780,9 @@ __device__ __noinline__ int32_t hp_prefill(Wp w, int k, int64_t T, uint64_t* mom
   mom[2] = warp_sum(spc);
   used = warp_sum(used);
   const int32_t kvn = I.kv_free - (int32_t)used;
+  const int32_t h0 = I.wq_head;  // read by every lane before any lane stores
   __syncwarp();
-  I.wq_head = len > nadm ? I.wq_head + nadm : 0;  // the admitted prefix leaves the queue
+  I.wq_head = len > nadm ? h0 + nadm : 0;  // the admitted prefix leaves the queue
   I.wq_len = len - nadm;
   I.kv_free = kvn;
   __syncwarp();
@@ -906,9 +907,10 @@ __device__ __noinline__ int64_t form_sarathi(Wp w, int k, int64_t T) {
   aM = warp_sum(aM);
   used = warp_sum(used);
   const int32_t nch = nfull + part;
+  const int32_t h0 = I.wq_head;  // read by every lane before any lane stores
   __syncwarp();
   if (part && lane == 0) P.wq_key[q + nfull] = INT64_MIN;  // the partial request leads the queue
-  I.wq_head = len > nfull ? I.wq_head + nfull : 0;            // whole prompts leave the queue
+  I.wq_head = len > nfull ? h0 + nfull : 0;                  // whole prompts leave the queue
   I.wq_len = len - nfull;
   I.kv_free = (int32_t)(kvf - used);
   __syncwarp();
