@@ -1365,6 +1365,21 @@ __device__ __noinline__ void finish_trace(Wp w, int trace, int64_t decisions,
   __syncwarp();
 }
 
+// minimum over the lanes < K (<= 16) of a warp, lanes >= K holding INF64; returned to every lane
+__device__ __forceinline__ int64_t kmin64(int64_t v, int K) {
+  int64_t o = __shfl_xor_sync(FULL, v, 1);
+  v = o < v ? o : v;
+  o = __shfl_xor_sync(FULL, v, 2);
+  v = o < v ? o : v;
+  if (K > 4) {
+    o = __shfl_xor_sync(FULL, v, 4);
+    v = o < v ? o : v;
+    o = __shfl_xor_sync(FULL, v, 8);
+    v = o < v ? o : v;
+  }
+  return __shfl_sync(FULL, v, 0);
+}
+
 // MINB = CTAs per SM the register budget must allow (8 -> 64 registers/thread ... 4 -> 128).  The
 // launch picks the largest budget that still keeps every trace of the call resident at once
 // (T <= SMs x MINB x SW): a trace is a serial chain, so registers beat extra resident warps
@@ -1396,13 +1411,15 @@ __global__ void __launch_bounds__(SW * 32, MINB) sim_kernel() {
     const int K = PLAIN ? P.K : w.K(), n_lp = PLAIN ? P.n_lp : w.nlp();
     init_trace(w, trace);
     int64_t next = 0, next_arr = w.n() > 0 ? P.arr[w.base()] : INF64, decisions = 0, evals = 0;
+    // Lane k < K mirrors instance k in the checks below (one shared-memory load per lane, minima
+    // by shuffles, instance sets by ballots), instead of serial loops over the instances.  Every
+    // phase only changes the instance it processes, so taking each set before the phase visits it
+    // in ascending instance order is the canonical A-E order of DESIGN.md §2.
+    const bool inst = lane < K;
     while (true) {
-      int64_t T = next_arr;
-      #pragma unroll 1
-      for (int k = 0; k < K; k++) {
-        const int64_t e = w.SI()[k].end;
-        T = e < T ? e : T;
-      }
+      const int64_t e = inst ? w.SI()[lane].end : INF64;
+      int64_t T = kmin64(e, K);
+      T = next_arr < T ? next_arr : T;
       const bool flight = w.ts()->fl_head < w.ts()->fl_tail;
       if (flight) {
         const int64_t tf = P.fl_t[w.base() + w.ts()->fl_head];
@@ -1410,9 +1427,7 @@ __global__ void __launch_bounds__(SW * 32, MINB) sim_kernel() {
       }
       if (T == INF64) break;
       // A. completions in instance order
-      #pragma unroll 1
-      for (int k = 0; k < K; k++)
-        if (w.SI()[k].end == T) complete(w, k, T);
+      for (uint32_t m = __ballot_sync(FULL, inst && e == T); m; m &= m - 1) complete(w, __ffs(m) - 1, T);
       // B. offload deliveries (FIFO = time order)
       if (flight) deliver(w, T);
       // C. arrivals, ascending id
@@ -1421,22 +1436,13 @@ __global__ void __launch_bounds__(SW * 32, MINB) sim_kernel() {
         next++;
         next_arr = next < w.n() ? P.arr[w.base() + next] : INF64;
       }
-      // D. formations of idle instances, LPs before HPs
-      #pragma unroll 1
-      for (int k = 0; k < n_lp; k++) {
-        if (w.SI()[k].end == INF64) {
-          const int64_t r = (PLAIN || P.mode == 0) ? form_lp(w, k, T) : form_baseline(w, k, T);
-          decisions += r & 1;
-          evals += r >> 1;
-        }
-      }
-      #pragma unroll 1
-      for (int k = n_lp; k < K; k++) {
-        if (w.SI()[k].end == INF64) {
-          const int64_t r = form_hp(w, k, T);
-          decisions += r & 1;
-          evals += r >> 1;
-        }
+      // D. formations of idle instances, LPs (lower indices) before HPs
+      for (uint32_t m = __ballot_sync(FULL, inst && w.SI()[lane].end == INF64); m; m &= m - 1) {
+        const int k = __ffs(m) - 1;
+        const int64_t r = k >= n_lp ? form_hp(w, k, T)
+                                    : ((PLAIN || P.mode == 0) ? form_lp(w, k, T) : form_baseline(w, k, T));
+        decisions += r & 1;
+        evals += r >> 1;
       }
       // E. tickets (G29)
       if (PLAIN ? (P.tickets && P.n_hp >= 1) : w.tickets()) {
@@ -1446,21 +1452,27 @@ __global__ void __launch_bounds__(SW * 32, MINB) sim_kernel() {
         }
         __syncwarp();
       }
-      // F. decode runs of independent instances up to their next possible interaction
-      int64_t tl_hp = next_arr;
+      // F. decode runs of independent instances up to their next possible interaction: an LP until
+      // the next arrival; an HP also until any LP formation that could offload, or a delivery
+      int64_t ef = INF64;
+      int32_t wl = 0, bd = 0, bp = 0;
+      if (inst) {
+        const SInst& I = w.SI()[lane];
+        ef = I.end;
+        wl = I.wq_len;
+        bd = I.batch_dec;
+        bp = I.bp_len;
+      }
+      int64_t tl_hp = kmin64(lane < n_lp && wl > 0 ? ef : INF64, K);
+      tl_hp = next_arr < tl_hp ? next_arr : tl_hp;
       if (w.ts()->fl_head < w.ts()->fl_tail) {
         const int64_t tf = P.fl_t[w.base() + w.ts()->fl_head];
         tl_hp = tf < tl_hp ? tf : tl_hp;
       }
-      #pragma unroll 1
-      for (int k = 0; k < n_lp; k++)
-        if (w.SI()[k].wq_len > 0 && w.SI()[k].end < tl_hp) tl_hp = w.SI()[k].end;  // may offload
-      #pragma unroll 1
-      for (int k = 0; k < K; k++) {
-        const SInst& I = w.SI()[k];
-        const int64_t lim = k < n_lp ? next_arr : tl_hp;
-        if (I.end < lim && I.batch_dec && I.bp_len == 0 && I.wq_len == 0)
-          decisions += run_decode(w, k, lim);
+      const int64_t lim = lane < n_lp ? next_arr : tl_hp;
+      for (uint32_t m = __ballot_sync(FULL, inst && ef < lim && bd && bp == 0 && wl == 0); m; m &= m - 1) {
+        const int k = __ffs(m) - 1;
+        decisions += run_decode(w, k, k < n_lp ? next_arr : tl_hp);
       }
     }
     finish_trace(w, trace, decisions, evals);
