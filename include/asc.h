@@ -223,6 +223,38 @@ typedef struct {
 
 asc_status asc_simulate_batch(asc_ctx* ctx, const asc_traces* tr, asc_outcomes* out);
 
+/* Diagnostics: decision snapshots of the simulator (SURVEY §8(d) config-4 self-check: "sampled
+ * formations replayed through asc_schedule_step must equal the simulator's admissions").  Arms the
+ * NEXT asc_simulate_batch on ctx (device-pointer calls only) to record, at every Algorithm-1 LP
+ * formation of LP instance `instance` of trace `trace` whose ordinal o (1 + the formations of that
+ * instance recorded in its digest so far) is a multiple of `every`, the inputs the decision used
+ * and the decision it made:
+ *   hdr[16 s + 0..14] = T (now), instance, N (lp_token_budget), M (free KV blocks after decode
+ *     preparation), B_d (decodes), sum of their contexts, tbt SLO, R (lp_max_batch - B_d), queue
+ *     length q, first entry in the entry arrays, admitted count, offloaded count, first id in
+ *     out_ids, batch latency (µs), o;
+ *   ids / deadline_us / eff_prompt / flags [e0, e0 + q): the waiting queue in the simulator's
+ *     (key, id) order: request id within the trace, deadline, effective prompt, bit0 = ever
+ *     prefilled, bit1 = on an HP -- exactly asc_schedule_step's per-entry inputs;
+ *   out_ids [o0, o0 + admitted + offloaded): admitted ids in priority order, then offloaded ids
+ *     ascending.
+ * Snapshots stop when max_snaps, entry_cap or out_cap would be exceeded; counts[0..2] (device,
+ * int64) receive the snapshots, entries and out ids used.  The arming is consumed by the next
+ * asc_simulate_batch.  All pointers are device memory owned by the caller. */
+typedef struct {
+  int32_t trace, instance;
+  int64_t every;
+  int32_t max_snaps;
+  int64_t entry_cap, out_cap;
+  int64_t *hdr, *counts;
+  int32_t* ids;
+  int64_t* deadline_us;
+  int32_t* eff_prompt;
+  uint8_t* flags;
+  int32_t* out_ids;
+} asc_snapshots;
+asc_status asc_arm_snapshots(asc_ctx* ctx, const asc_snapshots* snap);
+
 /* ---------------------------------------------------------------------------------------------
  * asc_goodput — per trace, good = #requests that COMPLETED with first_token - arrival <= TTFT SLO
  * and (output_len = 1 or done - first_token <= TBT SLO * (output_len - 1)), i.e. mean TBT within

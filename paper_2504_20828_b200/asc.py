@@ -20,7 +20,15 @@ STATUS = {0: "ASC_OK", 1: "ASC_E_INVAL", 2: "ASC_E_CONFIG", 3: "ASC_E_NOMEM", 4:
           5: "ASC_E_EMPTY", 6: "ASC_E_RANGE", 7: "ASC_E_INVARIANT"}
 EXPORTS = ("asc_create", "asc_destroy", "asc_last_error", "asc_abi_version", "asc_schedule_step",
            "asc_simulate_batch", "asc_goodput", "asc_summarize", "asc_fit_perf", "asc_latency", "asc_last_kernel_launches",
-           "asc_last_kernel_ms", "asc_last_kernel2_ms")
+           "asc_last_kernel_ms", "asc_last_kernel2_ms", "asc_arm_snapshots")
+
+
+class asc_snapshots(C.Structure):
+    _fields_ = [("trace", C.c_int32), ("instance", C.c_int32), ("every", C.c_int64),
+                ("max_snaps", C.c_int32), ("entry_cap", C.c_int64), ("out_cap", C.c_int64),
+                ("hdr", C.c_void_p), ("counts", C.c_void_p), ("ids", C.c_void_p),
+                ("deadline_us", C.c_void_p), ("eff_prompt", C.c_void_p), ("flags", C.c_void_p),
+                ("out_ids", C.c_void_p)]
 
 
 class AscError(RuntimeError):
@@ -128,6 +136,8 @@ def lib():
         L.asc_last_kernel_ms.restype = C.c_double
         L.asc_last_kernel2_ms.argtypes = [C.c_void_p]
         L.asc_last_kernel2_ms.restype = C.c_double
+        L.asc_arm_snapshots.argtypes = [C.c_void_p, C.POINTER(asc_snapshots)]
+        L.asc_arm_snapshots.restype = C.c_int
         _LIB = L
     return _LIB
 
@@ -277,6 +287,24 @@ class Context:
 
     def last_kernel2_ms(self):
         return asc_last_kernel2_ms(self.h)
+
+    def arm_snapshots(self, trace, instance, every, max_snaps, entry_cap, out_cap):
+        """asc_arm_snapshots with freshly allocated device buffers (returned; read them after the
+        next simulate_batch)."""
+        import torch
+        dev = torch.device("cuda", self.device)
+        b = dict(hdr=torch.full((max(max_snaps, 1) * 16,), -1, dtype=torch.int64, device=dev),
+                 counts=torch.zeros(3, dtype=torch.int64, device=dev),
+                 ids=torch.empty(max(entry_cap, 1), dtype=torch.int32, device=dev),
+                 deadline_us=torch.empty(max(entry_cap, 1), dtype=torch.int64, device=dev),
+                 eff_prompt=torch.empty(max(entry_cap, 1), dtype=torch.int32, device=dev),
+                 flags=torch.empty(max(entry_cap, 1), dtype=torch.uint8, device=dev),
+                 out_ids=torch.empty(max(out_cap, 1), dtype=torch.int32, device=dev))
+        sn = asc_snapshots(trace, instance, every, max_snaps, entry_cap, out_cap,
+                           *[_ptr(b[k]) for k in ("hdr", "counts", "ids", "deadline_us", "eff_prompt",
+                                                  "flags", "out_ids")])
+        _check(self.h, lib().asc_arm_snapshots(self.h, C.byref(sn)), "asc_arm_snapshots")
+        return b
 
     def schedule_step(self, ins, want_prefill=True, out=None):
         """ins: dict of arrays (all torch CUDA or all numpy).  Returns dict of outputs; `out` (a

@@ -665,6 +665,19 @@ asc_status asc_latency(asc_ctx* c, int64_t n, const uint64_t* F, const uint64_t*
   return finish_host(c, sg, "asc_latency");
 }
 
+asc_status asc_arm_snapshots(asc_ctx* c, const asc_snapshots* s) {
+  if (!c || !s) return fail(c, ASC_E_INVAL, "asc_arm_snapshots: NULL argument");
+  if (s->every < 1 || s->max_snaps < 0 || s->entry_cap < 0 || s->out_cap < 0 || s->instance < 0 ||
+      s->trace < 0 || !s->hdr || !s->counts || !s->ids || !s->deadline_us || !s->eff_prompt || !s->flags ||
+      !s->out_ids)
+    return fail(c, ASC_E_INVAL, "asc_arm_snapshots: bad argument");
+  if (ptr_kind(s->hdr) != 1 || ptr_kind(s->counts) != 1 || ptr_kind(s->ids) != 1 || ptr_kind(s->out_ids) != 1)
+    return fail(c, ASC_E_INVAL, "asc_arm_snapshots: device pointers only");
+  c->snap = *s;
+  c->snap_armed = true;
+  return ASC_OK;
+}
+
 int64_t asc_last_kernel_launches(const asc_ctx* c) { return c ? c->last_kernel_launches : 0; }
 
 double asc_last_kernel_ms(const asc_ctx* c) {

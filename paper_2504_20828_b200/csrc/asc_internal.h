@@ -32,6 +32,8 @@ struct asc_ctx {
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;  // bracket the dominant kernel of the last call
   cudaEvent_t ev2 = nullptr, ev3 = nullptr;  // bracket its secondary kernel (schedule_step: k_lane)
   bool timed = false, timed2 = false;
+  asc_snapshots snap{};     // armed decision snapshots for the next asc_simulate_batch
+  bool snap_armed = false;
 };
 
 namespace asc {

@@ -90,6 +90,12 @@ struct SimP {
   int32_t look;                    // offload rule 1: look-ahead (G50)
   int32_t kw0, kw1, kw2;           // ASC_POLICY_WEIGHTED weights (G51)
   const int64_t* rq_koff;          // optional per-request value-function offsets (G51)
+  // decision snapshots (asc_arm_snapshots; sn_hdr == nullptr when not armed)
+  int64_t *sn_hdr, *sn_cnt, *sn_dl;
+  int32_t *sn_ids, *sn_eff, *sn_out;
+  uint8_t* sn_fl;
+  int32_t sn_trace, sn_inst, sn_max;
+  int64_t sn_every, sn_ecap, sn_ocap;
 };
 
 // The launch parameters live in the constant bank (one copy per device, written before each launch
@@ -488,6 +494,59 @@ __device__ __forceinline__ void set_batch(SInst& I, int64_t T, int64_t l,
   __syncwarp();
 }
 
+// ---------------------------------------------------------------- decision snapshots (diag) --
+// asc_arm_snapshots: the inputs of a sampled Algorithm-1 formation (queue in (key, id) order with
+// the per-entry fields asc_schedule_step takes, and the budgets) ...
+__device__ __noinline__ int snap_begin(Wp w, int k, int64_t T, int64_t M, int64_t Bd, int64_t sl,
+                                       int64_t Rb, int32_t len, int64_t q) {
+  const SInst& I = w.SI()[k];
+  if (k != P.sn_inst || w.base() != P.off[P.sn_trace]) return -1;
+  const int64_t ord = (int64_t)I.nrec + 1;
+  if (ord % P.sn_every != 0) return -1;
+  const int64_t ns = P.sn_cnt[0], e0 = P.sn_cnt[1];
+  if (ns >= P.sn_max || e0 + len > P.sn_ecap) return -1;
+  const int lane = lane_id();
+  for (int32_t j = lane; j < len; j += 32) {
+    const int32_t id = P.wq_id[q + j];
+    const int64_t g = w.base() + id;
+    const uint32_t f = P.rq_fl[g];
+    P.sn_ids[e0 + j] = id;
+    P.sn_dl[e0 + j] = P.rq_dl[g];
+    P.sn_eff[e0 + j] = P.rq_eff[g];
+    P.sn_fl[e0 + j] = (uint8_t)(((f & F_EVER) ? 1u : 0u) | ((f & F_ONHP) ? 2u : 0u));
+  }
+  if (lane == 0) {
+    int64_t* h = P.sn_hdr + 16 * ns;
+    h[0] = T; h[1] = k; h[2] = P.lp_tok; h[3] = M; h[4] = Bd; h[5] = sl; h[6] = w.tbt(); h[7] = Rb;
+    h[8] = len; h[9] = e0; h[14] = ord;
+    P.sn_cnt[0] = ns + 1;
+    P.sn_cnt[1] = e0 + len;
+  }
+  __syncwarp();
+  return (int)ns;
+}
+// ... and the decision it made: admitted ids in priority order, offloaded ids ascending, latency
+__device__ __noinline__ void snap_end(Wp w, int ns, int k, int32_t nadm, int32_t noff, int64_t lat) {
+  const int64_t o0 = P.sn_cnt[2];
+  const int lane = lane_id();
+  int64_t* h = P.sn_hdr + 16 * ns;
+  const bool fits = o0 + nadm + noff <= P.sn_ocap;
+  if (fits) {
+    const int64_t o = ioff(k, w);
+    for (int32_t j = lane; j < nadm; j += 32) P.sn_out[o0 + j] = P.bp_id[o + j];
+    for (int32_t j = lane; j < noff; j += 32) P.sn_out[o0 + nadm + j] = P.scr_off[w.base() + j];
+  }
+  __syncwarp();
+  if (lane == 0) {
+    h[10] = fits ? nadm : -1;  // -1: the decision did not fit out_ids
+    h[11] = noff;
+    h[12] = o0;
+    h[13] = lat;
+    if (fits) P.sn_cnt[2] = o0 + nadm + noff;
+  }
+  __syncwarp();
+}
+
 // --------------------------------------------------------------- LP admission (non-empty queue)
 // The queue is sorted by the time-invariant (key, id), i.e. already in Algorithm 1's
 // line-3 order: lines 5-13 read its prefix.  Offload (§5.3, G24) under EDF_LAXITY is the range
@@ -510,6 +569,7 @@ __device__ __noinline__ int lp_admit(Wp w, int k, int64_t T, int32_t ndrop,
     C = w.tbt() - ldec;
   }
   const int32_t len = I.wq_len;
+  const int snap = P.sn_hdr ? snap_begin(w, k, T, M, Bd, (int64_t)sl, Rb, len, q) : -1;
   // Algorithm 1 lines 5-13 as a strict prefix-sum scan over the sorted prefix.  Token and block
   // sums run in 32 bits: a chunk of 32 is reached only if every running sum of the previous one
   // stayed below N (< 2^25) / M (< 2^31), and a chunk adds < 2^30 (p < 2^25), so they stay < 2^32;
@@ -676,6 +736,7 @@ __device__ __noinline__ int lp_admit(Wp w, int k, int64_t T, int32_t ndrop,
   }
   if (nonempty || noff || ndrop || npre)
     digest_log(w, k, T, nadm, nonempty ? Bd : 0, noff, ndrop, npre, l);
+  if (snap >= 0) snap_end(w, snap, k, nadm, noff, l);
   return nonempty ? 1 : 0;
 }
 
@@ -1626,6 +1687,17 @@ asc_status launch_simulate(asc_ctx* c, const asc_traces* tr, asc_outcomes* out, 
   }
   P.next_trace = ar.take<int>(1);
   P.err = c->d_err;
+  P.sn_hdr = nullptr;
+  if (c->snap_armed) {  // consumed by this call
+    const asc_snapshots& sn = c->snap;
+    P.sn_hdr = sn.hdr; P.sn_cnt = sn.counts; P.sn_ids = sn.ids; P.sn_dl = sn.deadline_us;
+    P.sn_eff = sn.eff_prompt; P.sn_fl = sn.flags; P.sn_out = sn.out_ids;
+    P.sn_trace = sn.trace; P.sn_inst = sn.instance; P.sn_max = sn.max_snaps;
+    P.sn_every = sn.every; P.sn_ecap = sn.entry_cap; P.sn_ocap = sn.out_cap;
+    cudaMemsetAsync(sn.counts, 0, 3 * sizeof(int64_t), c->stream);
+    if (sn.trace >= T) P.sn_hdr = nullptr;
+    c->snap_armed = false;
+  }
   P.pw = (int32_t)sim_smem_per_warp(K, &P.o_sd, &P.o_si, &P.o_ts);
   P.mode = cf.flags.scheduler;
   P.chunk_tok = cf.flags.chunk_tokens;
