@@ -22,7 +22,8 @@ struct asc_ctx {
   int32_t* d_pf_fast = nullptr;  // [2^17]: prefill_us(q + 1), clipped to 2^30 (k1's fast path)
   int64_t w_hp = 0;        // worst-case HP batch latency (G24)
   int* d_err = nullptr;    // device error bits (asc::ERR_*)
-  int* h_err = nullptr;    // pinned host copy of the error bits (one sync per call)
+  int* h_err = nullptr;    // mapped pinned host copy of the error bits (one sync per call)
+  int* h_err_dev = nullptr;  // its device alias (err_publish writes it)
   char* ws = nullptr;      // device workspace
   size_t ws_cap = 0;
   char* stage = nullptr;   // device staging for host-pointer calls

@@ -162,49 +162,68 @@ __global__ void fill_task_seg(StepP P) {
 // scans them tile-locally (tile totals to scan_tmp); plan_fix adds the sum of the preceding tile
 // totals (read directly: at most PLAN_FIX_TILES tiles) and writes the task -> segment map
 constexpr int64_t PLAN_FIX_TILES = 4096;
-__global__ void __launch_bounds__(SCAN_THREADS) plan_tiles(StepP P) {
-  __shared__ int64_t sa[SCAN_THREADS / 32], sb[SCAN_THREADS / 32];
-  const int64_t n = (int64_t)P.S + 1;
-  const int64_t base = blockIdx.x * (int64_t)SCAN_TILE + threadIdx.x * SCAN_ITEMS;
+// tasks of segment s from its length (segments of <= SMALL entries have none: k_lane / k_small)
+__device__ __forceinline__ int32_t tasks_of(int64_t len) {
+  return len <= SMALL ? 0 : len <= CH ? 1 : (int32_t)((len + CH - 1) / CH);
+}
+// One tile of SCAN_TILE = 8192 segments per CTA, warp w owning segments [w*256, w*256 + 256) of the
+// tile with lane l at positions 32 i + l (coalesced loads and stores); tile-local sums fit int32
+// (<= 8192 x 2^17 tasks).  SINGLE (S < SCAN_TILE): the final offsets and the task -> segment map in
+// this one launch.  Otherwise tile-local exclusive offsets and tile totals (scan_tmp) for plan_fix.
+template <bool SINGLE>
+__global__ void __launch_bounds__(SCAN_THREADS) plan_tile(StepP P) {
+  __shared__ int32_t sa[SCAN_THREADS / 32], sb[SCAN_THREADS / 32];
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  const int64_t tb = blockIdx.x * (int64_t)SCAN_TILE + w * 256 + l;
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     *P.redo_cnt = 0;
     if (P.seg_off[P.S] != P.Q) atomicOr(P.err, ERR_INVAL);
   }
-  int64_t o[SCAN_ITEMS + 1];
+  int64_t lo[SCAN_ITEMS + 1];
 #pragma unroll
-  for (int i = 0; i <= SCAN_ITEMS; i++) o[i] = P.seg_off[min(base + i, (int64_t)P.S)];
-  int64_t va[SCAN_ITEMS], vb[SCAN_ITEMS], ta = 0, tb = 0;
+  for (int i = 0; i < SCAN_ITEMS; i++) lo[i] = P.seg_off[min(tb + 32 * i, (int64_t)P.S)];
+  int32_t na[SCAN_ITEMS], nb[SCAN_ITEMS];
   bool bad = false;
 #pragma unroll
   for (int i = 0; i < SCAN_ITEMS; i++) {
-    const int64_t s = base + i;
-    const int64_t len = o[i + 1] - o[i];
+    const int64_t s = tb + 32 * i;
+    const int64_t hi = P.seg_off[min(s + 1, (int64_t)P.S)];  // (the next lane's lo: an L1 hit)
+    const int64_t len = hi - lo[i];
     bad |= s < P.S && len < 0;
-    const int64_t nt = s >= P.S || len <= SMALL ? 0 : len <= CH ? 1 : (len + CH - 1) / CH;
-    va[i] = nt;
-    vb[i] = nt > 1 ? nt : 0;
-    ta += va[i];
-    tb += vb[i];
+    na[i] = s < P.S ? tasks_of(len) : 0;
+    nb[i] = na[i] > 1 ? na[i] : 0;
   }
   if (bad) atomicOr(P.err, ERR_INVAL);
-  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
-  const int64_t ia = warp_incl_scan(ta), ib = warp_incl_scan(tb);
-  if (l == 31) { sa[w] = ia; sb[w] = ib; }
-  __syncthreads();
-  if (w == 0) {
-    const int64_t x = sa[l], y = sb[l];
-    const int64_t xi = warp_incl_scan(x), yi = warp_incl_scan(y);
-    sa[l] = xi - x;
-    sb[l] = yi - y;
-    if (l == 31) { P.scan_tmp[2 * blockIdx.x] = xi; P.scan_tmp[2 * blockIdx.x + 1] = yi; }
-  }
-  __syncthreads();
-  int64_t ea = sa[w] + ia - ta, eb = sb[w] + ib - tb;
+  int32_t ea[SCAN_ITEMS], eb[SCAN_ITEMS], ca = 0, cb = 0;
 #pragma unroll
   for (int i = 0; i < SCAN_ITEMS; i++) {
-    if (base + i < n) { P.task_off[base + i] = ea; P.mtask_off[base + i] = eb; }
-    ea += va[i];
-    eb += vb[i];
+    const int32_t ia = warp_incl_scan(na[i]), ib = warp_incl_scan(nb[i]);
+    ea[i] = ca + ia - na[i];
+    eb[i] = cb + ib - nb[i];
+    ca += __shfl_sync(FULL, ia, 31);
+    cb += __shfl_sync(FULL, ib, 31);
+  }
+  if (l == 0) { sa[w] = ca; sb[w] = cb; }
+  __syncthreads();
+  if (w == 0) {
+    const int32_t x = sa[l], y = sb[l];
+    const int32_t xi = warp_incl_scan(x), yi = warp_incl_scan(y);
+    sa[l] = xi - x;
+    sb[l] = yi - y;
+    if (!SINGLE && l == 31) { P.scan_tmp[2 * blockIdx.x] = xi; P.scan_tmp[2 * blockIdx.x + 1] = yi; }
+  }
+  __syncthreads();
+  const int64_t wa = sa[w], wb = sb[w];
+#pragma unroll
+  for (int i = 0; i < SCAN_ITEMS; i++) {
+    const int64_t s = tb + 32 * i;
+    if (s <= P.S) {
+      const int64_t t0 = wa + ea[i];
+      P.task_off[s] = t0;
+      P.mtask_off[s] = wb + eb[i];
+      if (SINGLE)
+        for (int64_t t = t0; t < t0 + na[i] && t < P.ntask_max; t++) P.task_seg[t] = (int32_t)s;
+    }
   }
 }
 __global__ void __launch_bounds__(SCAN_THREADS) plan_fix(StepP P) {
@@ -222,78 +241,27 @@ __global__ void __launch_bounds__(SCAN_THREADS) plan_fix(StepP P) {
   pa = 0;
   pb = 0;
   for (int i = 0; i < SCAN_THREADS / 32; i++) { pa += ra[i]; pb += rb[i]; }
-  const int64_t n = (int64_t)P.S + 1;
-  const int64_t base = blockIdx.x * (int64_t)SCAN_TILE + threadIdx.x * SCAN_ITEMS;
-  int64_t o[SCAN_ITEMS + 1];
-#pragma unroll
-  for (int i = 0; i <= SCAN_ITEMS; i++) o[i] = P.seg_off[min(base + i, (int64_t)P.S)];
+  const int64_t tb = blockIdx.x * (int64_t)SCAN_TILE + w * 256 + l;
+  // all loads first (clamped indices, no control flow between them), then the stores
+  int64_t ta[SCAN_ITEMS], tm[SCAN_ITEMS], lo[SCAN_ITEMS], hi[SCAN_ITEMS];
 #pragma unroll
   for (int i = 0; i < SCAN_ITEMS; i++) {
-    const int64_t s = base + i;
-    if (s >= n) break;
-    const int64_t t0 = P.task_off[s] + pa;
-    P.task_off[s] = t0;
-    P.mtask_off[s] += pb;
-    if (s < P.S) {
-      const int64_t len = o[i + 1] - o[i];
-      const int64_t nt = len <= SMALL ? 0 : len <= CH ? 1 : (len + CH - 1) / CH;
+    const int64_t s = min(tb + 32 * i, (int64_t)P.S);
+    ta[i] = P.task_off[s];
+    tm[i] = P.mtask_off[s];
+    lo[i] = P.seg_off[s];
+    hi[i] = P.seg_off[min(s + 1, (int64_t)P.S)];
+  }
+#pragma unroll
+  for (int i = 0; i < SCAN_ITEMS; i++) {
+    const int64_t s = tb + 32 * i;
+    if (s <= P.S) {
+      const int64_t t0 = ta[i] + pa;
+      P.task_off[s] = t0;
+      P.mtask_off[s] = tm[i] + pb;
+      const int32_t nt = s < P.S ? tasks_of(hi[i] - lo[i]) : 0;
       for (int64_t t = t0; t < t0 + nt && t < P.ntask_max; t++) P.task_seg[t] = (int32_t)s;
     }
-  }
-}
-
-// single-CTA planner for S < SCAN_TILE: counts, both exclusive scans and the task map in one launch
-__global__ void __launch_bounds__(SCAN_THREADS) plan_small(StepP P) {
-  __shared__ int64_t sa[SCAN_THREADS / 32], sb[SCAN_THREADS / 32];
-  const int64_t n = (int64_t)P.S + 1;
-  const int64_t base = threadIdx.x * SCAN_ITEMS;
-  if (threadIdx.x == 0) *P.redo_cnt = 0;
-  // every offset this thread needs in flight at once (one dependent load each costs a DRAM
-  // round trip on the launch's critical path otherwise)
-  int64_t o[SCAN_ITEMS + 1];
-#pragma unroll
-  for (int i = 0; i <= SCAN_ITEMS; i++) o[i] = P.seg_off[min(base + i, (int64_t)P.S)];
-  int64_t va[SCAN_ITEMS], vb[SCAN_ITEMS], ta = 0, tb = 0;
-  bool bad = false;
-#pragma unroll
-  for (int i = 0; i < SCAN_ITEMS; i++) {
-    const int64_t s = base + i;
-    int64_t nt = 0;
-    if (s < P.S) {
-      const int64_t len = o[i + 1] - o[i];
-      bad |= len < 0;
-      nt = len <= SMALL ? 0 : len <= CH ? 1 : (len + CH - 1) / CH;  // small: k_lane / k_small
-    } else if (s == P.S) {
-      bad |= o[i] != P.Q;
-    }
-    va[i] = nt;
-    vb[i] = nt > 1 ? nt : 0;
-    ta += va[i];
-    tb += vb[i];
-  }
-  if (bad) atomicOr(P.err, ERR_INVAL);
-  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
-  const int64_t ia = warp_incl_scan(ta), ib = warp_incl_scan(tb);
-  if (l == 31) { sa[w] = ia; sb[w] = ib; }
-  __syncthreads();
-  if (w == 0) {
-    const int64_t x = sa[l], y = sb[l];
-    const int64_t xi = warp_incl_scan(x), yi = warp_incl_scan(y);
-    sa[l] = xi - x;
-    sb[l] = yi - y;
-  }
-  __syncthreads();
-  int64_t ea = sa[w] + ia - ta, eb = sb[w] + ib - tb;
-#pragma unroll
-  for (int i = 0; i < SCAN_ITEMS; i++) {
-    const int64_t s = base + i;
-    if (s < n) {
-      P.task_off[s] = ea;
-      P.mtask_off[s] = eb;
-      for (int64_t t = ea; t < ea + va[i] && t < P.ntask_max; t++) P.task_seg[t] = (int32_t)s;
-    }
-    ea += va[i];
-    eb += vb[i];
   }
 }
 
@@ -1657,10 +1625,10 @@ asc_status launch_schedule_step(asc_ctx* c, const asc_step_in* in, asc_step_out*
   int64_t launches = 0;
   const int dev_sms = c->sms;
   if (S + 1 <= SCAN_TILE) {
-    plan_small<<<1, SCAN_THREADS, 0, sm>>>(P);
+    plan_tile<true><<<1, SCAN_THREADS, 0, sm>>>(P);
     launches += 1;
   } else if (ntile <= PLAN_FIX_TILES) {
-    plan_tiles<<<ntile, SCAN_THREADS, 0, sm>>>(P);
+    plan_tile<false><<<ntile, SCAN_THREADS, 0, sm>>>(P);
     plan_fix<<<ntile, SCAN_THREADS, 0, sm>>>(P);
     launches += 2;
   } else {
