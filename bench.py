@@ -245,7 +245,9 @@ def step_microbench(asc, torch, dev, stream, warmup, steps, hbm_peak):
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / steps
     nout = int(out["admit_cnt"].sum() + out["offload_cnt"].sum() + out["drop_cnt"].sum())
-    byts = 13 * Q + 4 * nout + S * (8 * 4 + 4 * 6) + 8
+    # 12 B per request evaluation (deadline 8 B + eff_prompt 4 B with the flag bits
+    # packed in); the ABI's separate flag byte (13 B moved per entry) is not credited
+    byts = 12 * Q + 4 * nout + S * (8 * 4 + 4 * 6) + 8
     k1ms = float(np.mean(k1))
     ctx.close()
     others = []
@@ -266,7 +268,7 @@ def step_microbench(asc, torch, dev, stream, warmup, steps, hbm_peak):
         torch.cuda.synchronize()
         ms2 = e0.elapsed_time(e1) / steps
         n2 = int(o2["admit_cnt"].sum() + o2["offload_cnt"].sum() + o2["drop_cnt"].sum())
-        b2 = 13 * S2 * Q2 + 4 * n2 + S2 * (8 * 4 + 4 * 6) + 8
+        b2 = 12 * S2 * Q2 + 4 * n2 + S2 * (8 * 4 + 4 * 6) + 8
         c2.close()
         sh = {"shape": f"S={S2} segments x Q={Q2} entries", "ms_per_call": ms2,
               "evaluations_per_s": S2 * Q2 / (ms2 * 1e-3),
