@@ -1475,14 +1475,21 @@ __global__ void __launch_bounds__(WARPS * 32) k2_segments(const __grid_constant_
   }
 }
 
+// K3P warps per multi-task task, each expanding a contiguous quarter of its 128-entry groups (more
+// independent warps in flight than one per task): a part's output offset is the task's (k2's scan)
+// plus the set bits of the task's earlier mask words
+constexpr int K3P = 4;
+constexpr int K3W = (NG + K3P - 1) / K3P;  // groups per part
 __global__ void __launch_bounds__(WARPS * 32) k3_expand(const __grid_constant__ StepP P) {
   __shared__ int32_t s_ring[WARPS][256];
-  __shared__ __align__(16) uint32_t s_words[WARPS][2][MW];
+  __shared__ __align__(16) uint32_t s_words[WARPS][2][4 * K3W];
   if (P.mtask_off[P.S] == 0) return;  // no multi-task segment
-  const int w = threadIdx.x >> 5;
+  const int w = threadIdx.x >> 5, lane = lane_id();
   const int64_t ntasks = min(P.task_off[P.S], P.ntask_max);
-  for (int64_t task = blockIdx.x * (int64_t)WARPS + w; task < ntasks;
-       task += (int64_t)gridDim.x * WARPS) {
+  for (int64_t item = blockIdx.x * (int64_t)WARPS + w; item < ntasks * K3P;
+       item += (int64_t)gridDim.x * WARPS) {
+    const int64_t task = item / K3P;
+    const int part = (int)(item % K3P);
     const int64_t s = P.task_seg[task];
     const int64_t nt = P.task_off[s + 1] - P.task_off[s];
     if (nt <= 1) continue;
@@ -1494,16 +1501,28 @@ __global__ void __launch_bounds__(WARPS * 32) k3_expand(const __grid_constant__ 
     const int64_t e_end = min(hi, b + CH);
     const int64_t b4 = b & ~int64_t(ALN - 1);
     const int ng = (int)((e_end - b4 + GE - 1) / GE);
-    // the task's mask words come to shared memory in one coalesced pass first: expand_groups reads
-    // one 16-byte word group per iteration, a dependent global load each time otherwise
-    const int nw4 = 4 * ng;
-    for (int j = lane_id(); j < nw4; j += 32) {
-      s_words[w][0][j] = P.moff[mt * MW + j];
-      s_words[w][1][j] = P.mdrop[mt * MW + j];
+    const int g0 = part * K3W, g1 = min(ng, g0 + K3W);
+    if (g0 >= g1) continue;
+    const uint32_t* wo = P.moff + mt * MW;
+    const uint32_t* wd = P.mdrop + mt * MW;
+    int32_t po = 0, pd = 0;  // set bits of the words before this part
+    for (int j = lane; j < 4 * g0; j += 32) {
+      po += __popc(wo[j]);
+      pd += __popc(wd[j]);
+    }
+    po = warp_sum(po);
+    pd = warp_sum(pd);
+    // this part's mask words to shared memory in one coalesced pass: expand_groups reads one
+    // 16-byte word group per iteration, a dependent global load each time otherwise
+    const int nw4 = 4 * (g1 - g0);
+    for (int j = lane; j < nw4; j += 32) {
+      s_words[w][0][j] = wo[4 * g0 + j];
+      s_words[w][1][j] = wd[4 * g0 + j];
     }
     __syncwarp();
-    expand_groups(s_words[w][0], ng, b4, P.off_idx, lo + P.coff[mt], s_ring[w]);
-    expand_groups(s_words[w][1], ng, b4, P.drop_idx, lo + P.cdrop[mt], s_ring[w]);
+    const int64_t bg = b4 + (int64_t)g0 * GE;
+    expand_groups(s_words[w][0], g1 - g0, bg, P.off_idx, lo + P.coff[mt] + po, s_ring[w]);
+    expand_groups(s_words[w][1], g1 - g0, bg, P.drop_idx, lo + P.cdrop[mt] + pd, s_ring[w]);
     __syncwarp();
   }
 }
@@ -1690,7 +1709,7 @@ asc_status launch_schedule_step(asc_ctx* c, const asc_step_in* in, asc_step_out*
   if (Q > CH) {
     int64_t g2 = S < (int64_t)dev_sms * 4 ? S : (int64_t)dev_sms * 4;
     k2_segments<<<(unsigned)(g2 > 0 ? g2 : 1), WARPS * 32, 0, sm>>>(P);
-    int64_t g3 = (ntask_max + WARPS - 1) / WARPS;
+    int64_t g3 = (ntask_max * K3P + WARPS - 1) / WARPS;
     g3 = g3 < (int64_t)dev_sms * 8 ? g3 : (int64_t)dev_sms * 8;
     k3_expand<<<(unsigned)(g3 > 0 ? g3 : 1), WARPS * 32, 0, sm>>>(P);
     launches += 2;

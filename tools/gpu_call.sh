@@ -38,7 +38,8 @@ for s in "$@"; do
       python tools/ncu_traffic.py gpurun_out/${tag}_ncu_traffic.json \
         sim_kernel=gpurun_out/${tag}_sim_dram.csv sim_kernel_config4=gpurun_out/${tag}_sim_config4_dram.csv \
         k1_tasks=gpurun_out/${tag}_k1_dram.csv k_lane=gpurun_out/${tag}_klane_dram.csv \
-        fit_partials=gpurun_out/${tag}_fit_dram.csv;;
+        fit_partials=gpurun_out/${tag}_fit_dram.csv
+      cp gpurun_out/${tag}_ncu_traffic.json profiles/ncu_traffic_r02.json;;  # read by the bench step after it
     simfull) timeout 2400 ncu --set full --import-source on --clock-control none -k regex:sim_kernel -c 1 \
            -o gpurun_out/${tag}_sim_full python tools/profile_run.py sim --traces 4096 --n 10000 --reps 1 \
            > gpurun_out/${tag}_sim_full.log 2>&1; echo simfull_rc=$?
