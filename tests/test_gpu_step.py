@@ -328,3 +328,16 @@ def test_lane_handback_mix(asc, oracle, policy):
     ins["budget_tokens"][rng.random(S) < 0.02] = 0
     ins["budget_reqs"][rng.random(S) < 0.02] = 0
     compare(run_gpu(asc, cfg, ins), oracle.schedule_step(cfg, **ins), ins["seg_off"])
+
+
+@pytest.mark.slow
+def test_row_s_deep_segments_full_scale(asc, oracle):
+    """SURVEY row S's second shape at full size, bench.py's inputs (64 segments x 10^6 entries,
+    seed 123): multi-task segments through k1, the k2 merge and the k3 expansion; every slot of
+    every list equals the oracle."""
+    rng = np.random.default_rng(123)
+    cfg = P.config()
+    S = 64
+    ins = H.random_step_inputs(rng, S, 0, cfg, qs=np.full(S, 1_000_000))
+    got = run_gpu(asc, cfg, ins)
+    compare_vec(got, oracle.schedule_step(cfg, **ins), ins["seg_off"])
