@@ -1280,16 +1280,19 @@ __device__ __forceinline__ bool lane_segment(const StepP& P, LaneStage& st, int6
   uint32_t am = 0;
   uint64_t sp2 = 0, spc = 0;
   // (a sentinel's position field is read as entry 0: never outside this lane's segment)
-  uint32_t xn = jmax > 0 ? ks[slot(0)] : 0xffffffffu;
-  int2 en = ent[xn == 0xffffffffu ? 0u : (xn & 31u)];
+  // two entries in flight ahead of the one being tested (the key -> entry loads are dependent)
+  uint32_t xn = jmax > 0 ? ks[slot(0)] : 0xffffffffu, xn2 = jmax > 1 ? ks[slot(1)] : 0xffffffffu;
+  int2 en = ent[xn == 0xffffffffu ? 0u : (xn & 31u)], en2 = ent[xn2 == 0xffffffffu ? 0u : (xn2 & 31u)];
   int32_t* adm = P.admit_idx + lo;
 #pragma unroll 2
   for (int j = 0; j < jmax; j++) {
     const uint32_t x = xn;
     const int2 e = en;
-    if (j + 1 < jmax) {
-      xn = ks[slot(j + 1)];
-      en = ent[xn == 0xffffffffu ? 0u : (xn & 31u)];
+    xn = xn2;
+    en = en2;
+    if (j + 2 < jmax) {
+      xn2 = ks[slot(j + 2)];
+      en2 = ent[xn2 == 0xffffffffu ? 0u : (xn2 & 31u)];
     }
     if (x == 0xffffffffu) break;
     const uint32_t p = (uint32_t)e.y;
