@@ -241,6 +241,9 @@ __global__ void __launch_bounds__(SCAN_THREADS) plan_fix(StepP P) {
   pa = 0;
   pb = 0;
   for (int i = 0; i < SCAN_THREADS / 32; i++) { pa += ra[i]; pb += rb[i]; }
+  // nothing before this tile and no task in it (every segment short: the usual LP queue): its
+  // tile-local offsets are already the global ones and there is no task to map
+  if (pa == 0 && pb == 0 && P.scan_tmp[2 * blockIdx.x] == 0) return;
   const int64_t tb = blockIdx.x * (int64_t)SCAN_TILE + w * 256 + l;
   // all loads first (clamped indices, no control flow between them), then the stores
   int64_t ta[SCAN_ITEMS], tm[SCAN_ITEMS], lo[SCAN_ITEMS], hi[SCAN_ITEMS];
