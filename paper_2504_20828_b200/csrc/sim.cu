@@ -1419,7 +1419,13 @@ __device__ __noinline__ void finish_trace(Wp w, int trace, int64_t decisions,
     P.digest[trace] = d;
     if (P.decisions) P.decisions[trace] = decisions;
 #ifdef ASC_DEBUG_CLOCK  // experiments only: per-trace finish time (ns) in place of evaluations
-    { uint64_t tns; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tns)); evals = (int64_t)tns; }
+    {  // finish time (ns, low 48 bits) and the SM the trace ran on (bits 48-63)
+      uint64_t tns;
+      uint32_t smid;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tns));
+      asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+      evals = (int64_t)(((uint64_t)smid << 48) | (tns & ((1ull << 48) - 1)));
+    }
 #endif
     if (P.evals) P.evals[trace] = evals;
   }

@@ -9,7 +9,7 @@ cfg, b = P.workload("config3")
 ctx = asc.Context(cfg, 0)
 tr = asc.batch_arrays(b, "cuda:0")
 out = ctx.simulate_batch(tr)
-t = out["evaluations"][:b.T].cpu().numpy().astype(np.int64)
+t = (out["evaluations"][:b.T].cpu().numpy().view(np.uint64) & ((1 << 48) - 1)).astype(np.int64)
 d = out["decisions"][:b.T].cpu().numpy()
 t = (t - t.min()) / 1e6  # ns -> ms after the first finisher
 order = np.argsort(-t)
