@@ -1536,10 +1536,17 @@ __global__ void __launch_bounds__(SW * 32, MINB) sim_kernel() {
         const int64_t tf = P.fl_t[w.base() + w.ts()->fl_head];
         tl_hp = tf < tl_hp ? tf : tl_hp;
       }
-      const int64_t lim = lane < n_lp ? next_arr : tl_hp;
+      // LP k only receives arrivals: round-robin from rr_lp (an arrival taken by an HP's ticket
+      // does not advance it), so none reaches k before the ((k - rr_lp) mod n_lp)-th upcoming one
+      int64_t lim = tl_hp;
+      if (lane < n_lp) {
+        const int32_t rr = w.ts()->rr_lp;
+        const int64_t j = next + (lane >= rr ? lane - rr : lane - rr + n_lp);
+        lim = j < w.n() ? P.arr[w.base() + j] : INF64;
+      }
       for (uint32_t m = __ballot_sync(FULL, inst && ef < lim && bd && bp == 0 && wl == 0); m; m &= m - 1) {
         const int k = __ffs(m) - 1;
-        decisions += run_decode(w, k, k < n_lp ? next_arr : tl_hp);
+        decisions += run_decode(w, k, __shfl_sync(FULL, lim, k));
       }
     }
     finish_trace(w, trace, decisions, evals);
