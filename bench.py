@@ -483,9 +483,10 @@ def main():
     ctx.close()
     if rank == 0 and not a.no_baselines:
         line["baselines"] = baselines(asc, torch, dev, stream, cfg, batch, col["good"] / max(col["total"], 1))
-    if rank == 0 and not a.no_config4:
+    # configs 4 and 5 (one trace / one GPU's shard) are single-GPU lines: the N = 1 run carries them
+    if rank == 0 and world == 1 and not a.no_config4:
         line["config4"] = config4_line(asc, torch, dev, stream, hbm_peak)
-    if rank == 0 and not a.no_config5:
+    if rank == 0 and world == 1 and not a.no_config5:
         del tr, out, res, summ
         torch.cuda.empty_cache()
         line["config5_shard"] = config5_line(asc, torch, dev, stream)

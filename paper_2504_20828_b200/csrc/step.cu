@@ -764,7 +764,11 @@ __device__ __forceinline__ bool task_fast(const StepP& P, const TaskCtx& t, Stag
     }
     const int32_t r0 = g * GE + 4 * lane;
     const uint32_t l0 = (uint32_t)r0 << PK_LOC;  // task-local index of this lane's first entry
-    uint64_t x[4];
+    // candidates are filtered on the packed word's high half (the key) only: key <= the
+    // threshold's key keeps every entry below the threshold (plus, rarely, ties above it, which the
+    // merge sorts past it); the full word is packed only for the candidates, in the append below
+    const uint32_t thr_hi = (uint32_t)(st.thr >> 32);
+    uint32_t kw[4];
     bool cnd[4];
     int32_t pfv[4];
     uint32_t mo[4], md[4];
@@ -790,9 +794,8 @@ __device__ __forceinline__ bool task_fast(const StepP& P, const TaskCtx& t, Stag
         if (DROP) md[u] = __ballot_sync(FULL, dropped);
         if (OFFL) mo[u] = __ballot_sync(FULL, off);
         const int32_t key1 = (d1 & dmask) + kpf * pf;  // kdl * d' + kpf * pf, branch-free
-        x[u] = ((uint64_t)((uint32_t)key1 ^ 0x80000000u) << 32) |
-               (uint64_t)(l0 + ((uint32_t)u << PK_LOC) + ((uint32_t)q & (uint32_t)PK_PMASK));
-        cnd[u] = select && v && !dropped && x[u] < st.thr;
+        kw[u] = (uint32_t)key1 ^ 0x80000000u;
+        cnd[u] = select && v && !dropped && kw[u] <= thr_hi;
       }
     };
     if (r0 - 4 * lane >= t.vlo && r0 - 4 * lane + GE <= t.vhi) {
@@ -810,7 +813,10 @@ __device__ __forceinline__ bool task_fast(const StepP& P, const TaskCtx& t, Stag
     }
     if (__any_sync(FULL, cnd[0] | cnd[1] | cnd[2] | cnd[3])) {
 #pragma unroll
-      for (int u = 0; u < 4; u++) st.append(x[u], cnd[u]);
+      for (int u = 0; u < 4; u++)
+        st.append(((uint64_t)kw[u] << 32) |
+                      (uint64_t)(l0 + ((uint32_t)u << PK_LOC) + ((uint32_t)(cur.p[u] - 1) & (uint32_t)PK_PMASK)),
+                  cnd[u]);
       st.drain();
     }
   }
