@@ -14,7 +14,7 @@ static thread_local std::string g_create_err;
 
 namespace asc {
 
-HostProf g_prof;
+thread_local HostProf g_prof;
 
 __global__ void err_publish(int* d_err, int* h_err) {
   *h_err = *d_err;
@@ -678,7 +678,8 @@ asc_status asc_arm_snapshots(asc_ctx* c, const asc_snapshots* s) {
       s->trace < 0 || !s->hdr || !s->counts || !s->ids || !s->deadline_us || !s->eff_prompt || !s->flags ||
       !s->out_ids)
     return fail(c, ASC_E_INVAL, "asc_arm_snapshots: bad argument");
-  if (ptr_kind(s->hdr) != 1 || ptr_kind(s->counts) != 1 || ptr_kind(s->ids) != 1 || ptr_kind(s->out_ids) != 1)
+  if (ptr_kind(s->hdr) != 1 || ptr_kind(s->counts) != 1 || ptr_kind(s->ids) != 1 || ptr_kind(s->out_ids) != 1 ||
+      ptr_kind(s->deadline_us) != 1 || ptr_kind(s->eff_prompt) != 1 || ptr_kind(s->flags) != 1)
     return fail(c, ASC_E_INVAL, "asc_arm_snapshots: device pointers only");
   c->snap = *s;
   c->snap_armed = true;

@@ -48,7 +48,7 @@ struct HostProf {
   double last = 0;
   void mark(int i);
 };
-extern HostProf g_prof;
+extern thread_local HostProf g_prof;  // per host thread (calls on one ctx come from one thread)
 
 // bump allocator over a device buffer
 struct Arena {
