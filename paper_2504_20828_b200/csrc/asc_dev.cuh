@@ -186,6 +186,18 @@ __device__ __forceinline__ int32_t warp_min(int32_t v) { return __reduce_min_syn
 __device__ __forceinline__ uint32_t warp_min(uint32_t v) { return __reduce_min_sync(FULL, v); }
 __device__ __forceinline__ int32_t warp_max(int32_t v) { return __reduce_max_sync(FULL, v); }
 __device__ __forceinline__ uint32_t warp_max(uint32_t v) { return __reduce_max_sync(FULL, v); }
+// 64-bit sums (mod 2^64, so signed values too) as three REDUX sums of 22/21/21-bit slices: each slice
+// sum over 32 lanes stays below 2^27, so the recombined total is exact; no shuffle chain (and no
+// divergent-path copy of one)
+__device__ __forceinline__ uint64_t warp_sum(uint64_t v) {
+  const uint32_t lo = __reduce_add_sync(FULL, (uint32_t)v & 0x3fffffu);
+  const uint32_t mi = __reduce_add_sync(FULL, (uint32_t)(v >> 22) & 0x1fffffu);
+  const uint32_t hi = __reduce_add_sync(FULL, (uint32_t)(v >> 43));
+  return (uint64_t)lo + ((uint64_t)mi << 22) + ((uint64_t)hi << 43);
+}
+__device__ __forceinline__ int64_t warp_sum(int64_t v) { return (int64_t)warp_sum((uint64_t)v); }
+__device__ __forceinline__ unsigned long long warp_sum(unsigned long long v) { return warp_sum((uint64_t)v); }
+__device__ __forceinline__ long long warp_sum(long long v) { return (long long)warp_sum((uint64_t)v); }
 // inclusive scan across the warp
 template <typename T>
 __device__ __forceinline__ T warp_incl_scan(T v) {

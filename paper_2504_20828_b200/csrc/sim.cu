@@ -27,7 +27,10 @@ namespace {
 
 constexpr int KPL = 4;
 constexpr int SW = 4;      // warps (traces in flight) per CTA
-constexpr int DCAP = 128;  // decode slots per instance kept in shared memory
+#ifndef ASC_DCAP
+#define ASC_DCAP 64
+#endif
+constexpr int DCAP = ASC_DCAP;  // decode slots per instance kept in shared memory
 constexpr uint64_t GOLD = 0x9E3779B97F4A7C15ull;
 constexpr uint64_t GOLD2 = 0xD1B54A32D192ED03ull;  // formation-index key of the instance digest
 
@@ -187,11 +190,19 @@ __device__ __forceinline__ void set_state(int64_t g, uint32_t st) {
 }
 
 // ------------------------------------------------------------------------------- digest ------
+#ifdef ASC_MIX1
+__device__ __forceinline__ uint64_t mixi(uint64_t x) { return (x ^ (x >> 32)) * 0xbf58476d1ce4e5b9ull; }
+#else
+__device__ __forceinline__ uint64_t mixi(uint64_t x) { return mix64(x); }
+#endif
 // record = Σ_pos mix(v_pos + (pos+1)·G) over (T, k, B_p, admitted…, B_d, #off, off…, #drop,
 // drop…, #evicted, evicted…, lat) — positions as in the oracle; lanes hash in parallel.
 __device__ __noinline__ void digest_log(Wp w, int k, int64_t T, int32_t nadm,
                                         int64_t bd, int32_t noff, int32_t ndrop, int32_t npre,
                                         int64_t lat, int32_t nch = 0) {
+#if defined(ASC_DIGEST_OFF) || defined(ASC_DIGEST_OFF_LOG)  // experiments only: the checker digest's cost
+  return;
+#endif
   const int lane = lane_id();
   const int64_t o = ioff(k, w);
   uint64_t acc = 0;
@@ -207,22 +218,22 @@ __device__ __noinline__ void digest_log(Wp w, int k, int64_t T, int32_t nadm,
       case 6: v = (uint64_t)npre; pos = 6 + nadm + noff + ndrop; break;
       default: v = (uint64_t)lat; pos = 7 + nadm + noff + ndrop + npre; break;
     }
-    acc = mix64(v + (pos + 1) * GOLD);
+    acc = mixi(v + (pos + 1) * GOLD);
   }
   #pragma unroll 1
-  for (int32_t j = lane; j < nadm; j += 32) acc += mix64((uint64_t)P.bp_id[o + j] + (uint64_t)(3 + j + 1) * GOLD);
+  for (int32_t j = lane; j < nadm; j += 32) acc += mixi((uint64_t)P.bp_id[o + j] + (uint64_t)(3 + j + 1) * GOLD);
   #pragma unroll 1
   for (int32_t j = lane; j < noff; j += 32)
-    acc += mix64((uint64_t)P.scr_off[w.base() + j] + (uint64_t)(5 + nadm + j + 1) * GOLD);
+    acc += mixi((uint64_t)P.scr_off[w.base() + j] + (uint64_t)(5 + nadm + j + 1) * GOLD);
   #pragma unroll 1
   for (int32_t j = lane; j < ndrop; j += 32)
-    acc += mix64((uint64_t)P.scr_drop[w.base() + j] + (uint64_t)(6 + nadm + noff + j + 1) * GOLD);
+    acc += mixi((uint64_t)P.scr_drop[w.base() + j] + (uint64_t)(6 + nadm + noff + j + 1) * GOLD);
   #pragma unroll 1
   for (int32_t j = lane; j < npre; j += 32)
-    acc += mix64((uint64_t)P.scr_pre[w.base() + j] + (uint64_t)(7 + nadm + noff + ndrop + j + 1) * GOLD);
+    acc += mixi((uint64_t)P.scr_pre[w.base() + j] + (uint64_t)(7 + nadm + noff + ndrop + j + 1) * GOLD);
   #pragma unroll 1
   for (int32_t j = lane; j < nch; j += 32)  // Sarathi-like chunk sizes (staged in scr_off)
-    acc += mix64((uint64_t)P.scr_off[w.base() + j] + (uint64_t)(8 + nadm + noff + ndrop + npre + j + 1) * GOLD);
+    acc += mixi((uint64_t)P.scr_off[w.base() + j] + (uint64_t)(8 + nadm + noff + ndrop + npre + j + 1) * GOLD);
   acc = warp_sum(acc);
   const uint64_t nr = w.SI()[k].nrec + 1;
   const uint64_t h = w.SI()[k].hash + mix64(acc + nr * GOLD2);
@@ -236,14 +247,13 @@ __device__ __noinline__ void digest_log(Wp w, int k, int64_t T, int32_t nadm,
 // formation index (1-based) on the instance
 __device__ __forceinline__ uint64_t digest_decode(uint64_t h, uint64_t nr, int k, int64_t T, int64_t bd,
                                                   int64_t lat) {
+#if defined(ASC_DIGEST_OFF) || defined(ASC_DIGEST_OFF_DEC)
+  return h;
+#endif
   const int lane = lane_id();
   const uint64_t v = lane == 0 ? (uint64_t)T : lane == 1 ? (uint64_t)k : lane == 3 ? (uint64_t)bd
                    : lane == 7 ? (uint64_t)lat : 0ull;
-  uint64_t acc = mix64(v + (uint64_t)(lane + 1) * GOLD);
-  acc += __shfl_xor_sync(FULL, acc, 4);
-  acc += __shfl_xor_sync(FULL, acc, 2);
-  acc += __shfl_xor_sync(FULL, acc, 1);
-  acc = __shfl_sync(FULL, acc, 0);
+  const uint64_t acc = warp_sum(lane < 8 ? mixi(v + (uint64_t)(lane + 1) * GOLD) : (uint64_t)0);
   return h + mix64(acc + nr * GOLD2);
 }
 
@@ -1226,8 +1236,8 @@ __device__ __noinline__ int64_t run_decode(Wp w, int k, int64_t T_limit) {
   mrem = warp_min(mrem);
   __syncwarp();
   while (true) {
-    const uint64_t cpart = mix64((uint64_t)k + 2 * GOLD) + mix64(3 * GOLD) + mix64((uint64_t)Bd + 4 * GOLD) +
-                           mix64(5 * GOLD) + mix64(6 * GOLD) + mix64(7 * GOLD);
+    const uint64_t cpart = mixi((uint64_t)k + 2 * GOLD) + mixi(3 * GOLD) + mixi((uint64_t)Bd + 4 * GOLD) +
+                           mixi(5 * GOLD) + mixi(6 * GOLD) + mixi(7 * GOLD);
     const int32_t Jmax = mrem - 1;  // decode-only events before the next completion
     int32_t J = 0;
     int64_t tcarry = 0, ncarry = 0;
@@ -1243,8 +1253,10 @@ __device__ __noinline__ int64_t run_decode(Wp w, int k, int64_t T_limit) {
       const bool ok = c < Jmax && tc < T_limit && cum <= kvf && lc > 0;
       const uint32_t m = __ballot_sync(FULL, ok);
       const int n = (m == FULL) ? 32 : (__ffs(~m) - 1);
-      const uint64_t rec = cpart + mix64((uint64_t)tc + GOLD) + mix64((uint64_t)lc + 8 * GOLD);
+      const uint64_t rec = cpart + mixi((uint64_t)tc + GOLD) + mixi((uint64_t)lc + 8 * GOLD);
+#if !defined(ASC_DIGEST_OFF) && !defined(ASC_DIGEST_OFF_DEC)
       h += warp_sum(lane < n ? mix64(rec + (nr + (uint64_t)c + 1) * GOLD2) : 0ull);
+#endif
       if (n > 0) {
         ncarry = __shfl_sync(FULL, cum, n - 1);
         tcarry = __shfl_sync(FULL, incl, n - 1) + tcarry;
@@ -1433,18 +1445,13 @@ __device__ __noinline__ void finish_trace(Wp w, int trace, int64_t decisions,
 }
 
 // minimum over the lanes < K (<= 16) of a warp, lanes >= K holding INF64; returned to every lane
+// minimum over the warp (lanes past the instances hold INF64): the high words by one REDUX, then the
+// low words of the lanes holding that high word by another
 __device__ __forceinline__ int64_t kmin64(int64_t v, int K) {
-  int64_t o = __shfl_xor_sync(FULL, v, 1);
-  v = o < v ? o : v;
-  o = __shfl_xor_sync(FULL, v, 2);
-  v = o < v ? o : v;
-  if (K > 4) {
-    o = __shfl_xor_sync(FULL, v, 4);
-    v = o < v ? o : v;
-    o = __shfl_xor_sync(FULL, v, 8);
-    v = o < v ? o : v;
-  }
-  return __shfl_sync(FULL, v, 0);
+  const int32_t hi = (int32_t)(v >> 32);
+  const int32_t mh = __reduce_min_sync(FULL, hi);
+  const uint32_t ml = __reduce_min_sync(FULL, hi == mh ? (uint32_t)v : 0xffffffffu);
+  return (int64_t)(((uint64_t)(uint32_t)mh << 32) | ml);
 }
 
 // MINB = CTAs per SM the register budget must allow (8 -> 64 registers/thread ... 4 -> 128).  The
