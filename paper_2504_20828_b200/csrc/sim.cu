@@ -429,7 +429,7 @@ __device__ __noinline__ int32_t drop_step(Wp w, int k, int64_t T) {
 // §5.4; grow each decode's KV by the blocks its next token needs (precomputed by the
 // completion pass as pending bits); while short of blocks, evict the latest-arrived decode (LIFO,
 // G31) by recomputation: generated tokens join its prompt, it re-enters the queue.
-__device__ __noinline__ int32_t evict(Wp w, int k) {
+__device__ __forceinline__ int32_t evict(Wp w, int k) {
   SInst& I = w.SI()[k];
   const int lane = lane_id();
   int32_t np = 0;
@@ -562,7 +562,12 @@ __device__ __noinline__ void snap_end(Wp w, int ns, int k, int32_t nadm, int32_t
 // line-3 order: lines 5-13 read its prefix.  Offload (§5.3, G24) under EDF_LAXITY is the range
 // key <= T + W_hp + margin right after the admitted prefix (key = deadline - prefill_us makes the
 // offload test a key bound); other policies scan the whole queue.
-__device__ __noinline__ int lp_admit(Wp w, int k, int64_t T, int32_t ndrop,
+#ifdef ASC_LA_NOINLINE  // experiments only
+#define LA_ATTR __noinline__
+#else
+#define LA_ATTR __forceinline__
+#endif
+__device__ LA_ATTR int lp_admit(Wp w, int k, int64_t T, int32_t ndrop,
                                      int32_t npre) {
   SInst& I = w.SI()[k];
   const int lane = lane_id();
@@ -769,30 +774,32 @@ __device__ __forceinline__ void decode_batch(SInst& I, int k, int64_t T) {
 // returns (waiting-queue entries evaluated << 1) | (1 if a batch was formed)
 __device__ __forceinline__ int64_t form_lp(Wp w, int k, int64_t T) {
   SInst& I = w.SI()[k];
+  int32_t ndrop = 0, npre = 0;
   if (I.wq_len == 0) {
     if (I.ds_len == 0) return 0;  // parked
-    const int32_t np = decode_prep(w, k);
-    if (np == 0) {  // no eviction: the common case, a pure decode step
+    npre = decode_prep(w, k);
+    if (npre == 0) {  // no eviction: the common case, a pure decode step
       decode_batch(I, k, T);
       return 1;
     }
-    const int64_t ev = (int64_t)I.wq_len << 1;  // the queue now holds the evicted decodes
-    return ev | lp_admit(w, k, T, 0, np);
-  }
-  const int32_t ndrop = P.drop ? drop_step(w, k, T) : 0;
-  const int32_t npre = I.ds_len ? decode_prep(w, k) : 0;
-  const int64_t ev = (int64_t)I.wq_len << 1;
-  if (I.wq_len == 0) {
-    const int64_t Bd = I.ds_len;
-    int64_t l = 0;
-    if (Bd) {
-      l = lat_dec_call(Bd, I.ctx_sum);
-      set_batch(I, T, l, 1, 0);
+    // the queue now holds the evicted decodes
+  } else {
+    ndrop = P.drop ? drop_step(w, k, T) : 0;
+    npre = I.ds_len ? decode_prep(w, k) : 0;
+    if (I.wq_len == 0) {
+      const int64_t ev = (int64_t)I.wq_len << 1;
+      const int64_t Bd = I.ds_len;
+      int64_t l = 0;
+      if (Bd) {
+        l = lat_dec_call(Bd, I.ctx_sum);
+        set_batch(I, T, l, 1, 0);
+      }
+      digest_log(w, k, T, 0, Bd, 0, ndrop, 0, l);  // ndrop > 0 here
+      return ev | (Bd ? 1 : 0);
     }
-    digest_log(w, k, T, 0, Bd, 0, ndrop, 0, l);  // ndrop > 0 here
-    return ev | (Bd ? 1 : 0);
   }
-  return ev | lp_admit(w, k, T, ndrop, npre);
+  const int64_t ev = (int64_t)I.wq_len << 1;
+  return ev | lp_admit(w, k, T, ndrop, npre);  // (one call site: inlined)
 }
 
 // --------------------------------------------------------------------------- HP formation ---
@@ -860,7 +867,7 @@ __device__ __noinline__ int32_t hp_prefill(Wp w, int k, int64_t T, uint64_t* mom
   return nadm;
 }
 
-__device__ __noinline__ int64_t form_hp_general(Wp w, int k, int64_t T) {
+__device__ __forceinline__ int64_t form_hp_general(Wp w, int k, int64_t T) {
   SInst& I = w.SI()[k];
   const int32_t ndrop = (P.drop && I.wq_len) ? drop_step(w, k, T) : 0;
   const int64_t ev = (int64_t)I.wq_len << 1;
@@ -1020,7 +1027,7 @@ __device__ __forceinline__ void finish_req(int64_t g, int64_t T) {
 }
 
 // per finished request: blocks freed, HP history, resident-ticket release (G29)
-__device__ __noinline__ void finish_sums(Wp w, int k, int64_t freed, int64_t hsum,
+__device__ __forceinline__ void finish_sums(Wp w, int k, int64_t freed, int64_t hsum,
                                          int32_t hcnt, int32_t tkd, int64_t cfin) {
   freed = warp_sum(freed);
   hsum = warp_sum(hsum);
@@ -1040,7 +1047,12 @@ __device__ __noinline__ void finish_sums(Wp w, int k, int64_t freed, int64_t hsu
 }
 
 // prefill completions: first token, then completion or entry into the decode set
-__device__ __noinline__ void complete_prefills(Wp w, int k, int64_t T) {
+#ifdef ASC_CP_NOINLINE  // experiments only
+#define CP_ATTR __noinline__
+#else
+#define CP_ATTR __forceinline__  // one call site (complete)
+#endif
+__device__ CP_ATTR void complete_prefills(Wp w, int k, int64_t T) {
   SInst& I = w.SI()[k];
   const int lane = lane_id();
   const int64_t o = ioff(k, w);
@@ -1202,7 +1214,12 @@ __device__ __noinline__ void deliver(Wp w, int64_t T) {
 // from a histogram of l̂ mod bs, Σl̂ in closed form, latencies in parallel (Eq. 4-5), start times by
 // a prefix sum, and the per-instance digest chain applied in order.  Exactly the same formations,
 // times and digest as stepping them one by one through the event loop.
-__device__ __noinline__ int64_t run_decode(Wp w, int k, int64_t T_limit) {
+#ifdef ASC_RD_NOINLINE  // experiments only
+#define RD_ATTR __noinline__
+#else
+#define RD_ATTR __forceinline__  // one call site (phase F): no call, no callee-saved register traffic
+#endif
+__device__ RD_ATTR int64_t run_decode(Wp w, int k, int64_t T_limit) {
   SInst& I = w.SI()[k];
   const int lane = lane_id();
   const int32_t bs = P.bs;
