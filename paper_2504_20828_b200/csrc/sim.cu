@@ -146,10 +146,15 @@ __device__ __noinline__ int64_t pf_slow(int32_t p) {  // prompts beyond the per-
 __device__ __forceinline__ int64_t pf_of(int32_t p) {
   return p < P.pt ? __ldg(P.pf_tab + p) : pf_slow(p);
 }
-__device__ __noinline__ int64_t lat_dec_call(int64_t Bd, int64_t sl) {  // decode-only batch, Eq. 4-5
+#ifdef ASC_LDC_INLINE  // experiments only
+#define LDC_ATTR __forceinline__
+#else
+#define LDC_ATTR __noinline__
+#endif
+__device__ LDC_ATTR int64_t lat_dec_call(int64_t Bd, int64_t sl) {  // decode-only batch, Eq. 4-5
   return lat_decode(P.md, (uint64_t)Bd, (uint64_t)sl);
 }
-__device__ __noinline__ int64_t lat_batch(uint64_t nadm, uint64_t sp, uint64_t sp2, uint64_t spc, uint64_t Bd,
+__device__ LDC_ATTR int64_t lat_batch(uint64_t nadm, uint64_t sp, uint64_t sp2, uint64_t spc, uint64_t Bd,
                                          uint64_t sl) {  // hybrid batch from its moments, Eq. 3-5
   return lat_us(P.md, nadm, sp, sp2, spc, Bd, sl);
 }
@@ -197,7 +202,12 @@ __device__ __forceinline__ uint64_t mixi(uint64_t x) { return mix64(x); }
 #endif
 // record = Σ_pos mix(v_pos + (pos+1)·G) over (T, k, B_p, admitted…, B_d, #off, off…, #drop,
 // drop…, #evicted, evicted…, lat) — positions as in the oracle; lanes hash in parallel.
-__device__ __noinline__ void digest_log(Wp w, int k, int64_t T, int32_t nadm,
+#ifdef ASC_DL_NOINLINE  // experiments only
+#define DL_ATTR __noinline__
+#else
+#define DL_ATTR __forceinline__  // one call site per plain kernel (log_rec in the event loop)
+#endif
+__device__ DL_ATTR void digest_log(Wp w, int k, int64_t T, int32_t nadm,
                                         int64_t bd, int32_t noff, int32_t ndrop, int32_t npre,
                                         int64_t lat, int32_t nch = 0) {
 #if defined(ASC_DIGEST_OFF) || defined(ASC_DIGEST_OFF_LOG)  // experiments only: the checker digest's cost
@@ -241,6 +251,17 @@ __device__ __noinline__ void digest_log(Wp w, int k, int64_t T, int32_t nadm,
   w.SI()[k].hash = h;  // uniform values, every lane stores the same words
   w.SI()[k].nrec = nr;
   __syncwarp();
+}
+
+// One formation's digest record, filled by the formation and logged by its caller: the event loop
+// then holds the only digest_log call of the plain kernel.
+struct DRec {
+  int64_t T, bd, lat;
+  int32_t nadm, noff, ndrop, npre;
+  bool on;
+};
+__device__ __forceinline__ void log_rec(Wp w, int k, const DRec& r) {
+  if (r.on) digest_log(w, k, r.T, r.nadm, r.bd, r.noff, r.ndrop, r.npre, r.lat);
 }
 
 // the pure-decode record (T, k, 0, B_d, 0, 0, 0, lat): 8 lanes, 3 shuffle steps; nr = its
@@ -568,7 +589,7 @@ __device__ __noinline__ void snap_end(Wp w, int ns, int k, int32_t nadm, int32_t
 #define LA_ATTR __forceinline__
 #endif
 __device__ LA_ATTR int lp_admit(Wp w, int k, int64_t T, int32_t ndrop,
-                                     int32_t npre) {
+                                     int32_t npre, DRec& rec) {
   SInst& I = w.SI()[k];
   const int lane = lane_id();
   const int64_t o = ioff(k, w);  // running-batch list base
@@ -749,8 +770,7 @@ __device__ LA_ATTR int lp_admit(Wp w, int k, int64_t T, int32_t ndrop,
     l = nadm ? lat_batch((uint64_t)nadm, sp, sp2, spc, (uint64_t)Bd, (uint64_t)sl) : ldec;
     set_batch(I, T, l, Bd > 0, nadm);
   }
-  if (nonempty || noff || ndrop || npre)
-    digest_log(w, k, T, nadm, nonempty ? Bd : 0, noff, ndrop, npre, l);
+  rec = DRec{T, nonempty ? Bd : 0, l, nadm, noff, ndrop, npre, nonempty || noff || ndrop || npre};
   if (snap >= 0) snap_end(w, snap, k, nadm, noff, l);
   return nonempty ? 1 : 0;
 }
@@ -772,7 +792,7 @@ __device__ __forceinline__ void decode_batch(SInst& I, int k, int64_t T) {
 }
 
 // returns (waiting-queue entries evaluated << 1) | (1 if a batch was formed)
-__device__ __forceinline__ int64_t form_lp(Wp w, int k, int64_t T) {
+__device__ __forceinline__ int64_t form_lp(Wp w, int k, int64_t T, DRec& rec) {
   SInst& I = w.SI()[k];
   int32_t ndrop = 0, npre = 0;
   if (I.wq_len == 0) {
@@ -794,12 +814,12 @@ __device__ __forceinline__ int64_t form_lp(Wp w, int k, int64_t T) {
         l = lat_dec_call(Bd, I.ctx_sum);
         set_batch(I, T, l, 1, 0);
       }
-      digest_log(w, k, T, 0, Bd, 0, ndrop, 0, l);  // ndrop > 0 here
+      rec = DRec{T, Bd, l, 0, 0, ndrop, 0, true};  // ndrop > 0 here
       return ev | (Bd ? 1 : 0);
     }
   }
   const int64_t ev = (int64_t)I.wq_len << 1;
-  return ev | lp_admit(w, k, T, ndrop, npre);  // (one call site: inlined)
+  return ev | lp_admit(w, k, T, ndrop, npre, rec);  // (one call site: inlined)
 }
 
 // --------------------------------------------------------------------------- HP formation ---
@@ -867,7 +887,7 @@ __device__ __noinline__ int32_t hp_prefill(Wp w, int k, int64_t T, uint64_t* mom
   return nadm;
 }
 
-__device__ __forceinline__ int64_t form_hp_general(Wp w, int k, int64_t T) {
+__device__ __forceinline__ int64_t form_hp_general(Wp w, int k, int64_t T, DRec& rec) {
   SInst& I = w.SI()[k];
   const int32_t ndrop = (P.drop && I.wq_len) ? drop_step(w, k, T) : 0;
   const int64_t ev = (int64_t)I.wq_len << 1;
@@ -891,11 +911,11 @@ __device__ __forceinline__ int64_t form_hp_general(Wp w, int k, int64_t T) {
     l = bd ? lat_dec_call(bd, I.ctx_sum) : lat_batch((uint64_t)nadm, mom[0], mom[1], mom[2], 0, 0);
     set_batch(I, T, l, bd > 0, bd ? 0 : nadm);
   }
-  if (batch || ndrop || npre) digest_log(w, k, T, bd ? 0 : nadm, bd, 0, ndrop, npre, l);
+  rec = DRec{T, bd, l, bd ? 0 : nadm, 0, ndrop, npre, batch || ndrop || npre};
   return ev | (batch ? 1 : 0);
 }
 
-__device__ __forceinline__ int64_t form_hp(Wp w, int k, int64_t T) {
+__device__ __forceinline__ int64_t form_hp(Wp w, int k, int64_t T, DRec& rec) {
   SInst& I = w.SI()[k];
   if (I.wq_len == 0) {
     if (I.ds_len == 0) return 0;  // parked
@@ -905,7 +925,7 @@ __device__ __forceinline__ int64_t form_hp(Wp w, int k, int64_t T) {
       return 1;
     }
   }
-  return form_hp_general(w, k, T);
+  return form_hp_general(w, k, T, rec);
 }
 
 // ------------------------------------------------------------- Sarathi-like baseline (G47) ---
@@ -1017,7 +1037,12 @@ __device__ __forceinline__ int64_t form_sar(Wp w, int k, int64_t T) {
 
 // baseline schedulers, out of line so Ascendra's event loop keeps its instruction footprint
 __device__ __noinline__ int64_t form_baseline(Wp w, int k, int64_t T) {
-  return P.mode == 1 ? form_hp(w, k, T) : form_sar(w, k, T);
+  if (P.mode != 1) return form_sar(w, k, T);
+  DRec rec;
+  rec.on = false;
+  const int64_t r = form_hp(w, k, T, rec);
+  log_rec(w, k, rec);
+  return r;
 }
 
 // ------------------------------------------------------------------ phase A: batch completion --
@@ -1530,8 +1555,11 @@ __global__ void __launch_bounds__(SW * 32, MINB) sim_kernel() {
       // D. formations of idle instances, LPs (lower indices) before HPs
       for (uint32_t m = __ballot_sync(FULL, inst && w.SI()[lane].end == INF64); m; m &= m - 1) {
         const int k = __ffs(m) - 1;
-        const int64_t r = k >= n_lp ? form_hp(w, k, T)
-                                    : ((PLAIN || P.mode == 0) ? form_lp(w, k, T) : form_baseline(w, k, T));
+        DRec rec;
+        rec.on = false;
+        const int64_t r = k >= n_lp ? form_hp(w, k, T, rec)
+                                    : ((PLAIN || P.mode == 0) ? form_lp(w, k, T, rec) : form_baseline(w, k, T));
+        log_rec(w, k, rec);
         decisions += r & 1;
         evals += r >> 1;
       }
