@@ -146,15 +146,10 @@ __device__ __noinline__ int64_t pf_slow(int32_t p) {  // prompts beyond the per-
 __device__ __forceinline__ int64_t pf_of(int32_t p) {
   return p < P.pt ? __ldg(P.pf_tab + p) : pf_slow(p);
 }
-#ifdef ASC_LDC_INLINE  // experiments only
-#define LDC_ATTR __forceinline__
-#else
-#define LDC_ATTR __noinline__
-#endif
-__device__ LDC_ATTR int64_t lat_dec_call(int64_t Bd, int64_t sl) {  // decode-only batch, Eq. 4-5
+__device__ __noinline__ int64_t lat_dec_call(int64_t Bd, int64_t sl) {  // decode-only batch, Eq. 4-5
   return lat_decode(P.md, (uint64_t)Bd, (uint64_t)sl);
 }
-__device__ LDC_ATTR int64_t lat_batch(uint64_t nadm, uint64_t sp, uint64_t sp2, uint64_t spc, uint64_t Bd,
+__device__ __noinline__ int64_t lat_batch(uint64_t nadm, uint64_t sp, uint64_t sp2, uint64_t spc, uint64_t Bd,
                                          uint64_t sl) {  // hybrid batch from its moments, Eq. 3-5
   return lat_us(P.md, nadm, sp, sp2, spc, Bd, sl);
 }
