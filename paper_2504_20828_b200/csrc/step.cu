@@ -27,10 +27,10 @@ namespace {
 
 constexpr int KPL = 4;             // K = 128 = ASC_MAX_BATCH
 constexpr int CH = 16384;          // entries per warp task
-constexpr int GE = 128;            // entries per warp iteration (4 per lane)
+constexpr int GE = 128;            // entries per warp iteration (lane l: entries l, 32+l, 64+l, 96+l)
 constexpr int ALN = 16;            // task bases are rounded down to 16 entries (16-byte flag copies)
 constexpr int NG = CH / GE + 1;    // groups per task (+1: the task base is rounded down)
-constexpr int MW = 4 * NG;         // mask words per task per mask (word 4g+u, bit l <-> 4l+u)
+constexpr int MW = 4 * NG;         // mask words per task per mask (word j, bit l <-> entry 32j + l)
 constexpr int SMALL = 32;  // segments of <= SMALL entries: one warp, one entry per lane (k_small)
 constexpr int WARPS = 8;   // k2/k3 CTA size
 constexpr int K1W = 4;     // k1 CTA size (warps); 4 CTAs/SM -> 16 warps, 128 registers
@@ -349,101 +349,51 @@ __device__ __forceinline__ int finalize_segment(const StepP& P, int64_t s, const
   return k;
 }
 
-// expand nibble-layout mask words (word 4g+u, bit l <-> entry b4 + 128g + 4l + u) into
-// id-ascending output indices starting at out[base]; returns the new base.  Set entries go to a
-// 256-slot shared-memory ring at their rank and leave it 128 at a time as coalesced stores (four
-// 32-lane rows with immediate offsets), instead of one 64-bit-addressed scattered store each.
-#ifndef ASC_K1_EXPAND
-#define ASC_K1_EXPAND 0
-#endif
-// direct variant: each lane stores its (at most four) set entries of a group straight to their
-// ranks -- fewer instructions than the ring; the warp's stores for one group stay inside a
-// 512-byte window, so they still coalesce into a few sectors
-__device__ __forceinline__ int64_t expand_direct(const uint32_t* words, int ng, int64_t b4,
+// expand linear-layout mask words (word j, bit l <-> entry b4 + 32j + l) into id-ascending output
+// indices starting at out[base]; returns the new base.  Each word's set lanes store their entries
+// at consecutive ranks (one coalesced store per word, no staging ring).
+__device__ __forceinline__ int64_t expand_groups(const uint32_t* words, int ng, int64_t b4,
                                                  int32_t* out, int64_t base) {
   const int lane = lane_id();
   const uint32_t lt = lanemask_lt(), bit = 1u << lane;
-  int32_t* ob = out + base;
-  uint32_t cnt = 0;
-  const int32_t e00 = (int32_t)b4 + 4 * lane;
+  int32_t* op = out + base;
+  const int32_t e00 = (int32_t)b4 + lane;
   for (int g = 0; g < ng; g++) {
     const uint4 wv = *reinterpret_cast<const uint4*>(words + 4 * g);  // words 4g..4g+3
     if ((wv.x | wv.y | wv.z | wv.w) == 0) continue;
-    uint32_t r = cnt + __popc(wv.x & lt) + __popc(wv.y & lt) + __popc(wv.z & lt) + __popc(wv.w & lt);
     const int32_t e0 = e00 + g * GE;
-    if (wv.x & bit) ob[r++] = e0;
-    if (wv.y & bit) ob[r++] = e0 + 1;
-    if (wv.z & bit) ob[r++] = e0 + 2;
-    if (wv.w & bit) ob[r] = e0 + 3;
-    cnt += __popc(wv.x) + __popc(wv.y) + __popc(wv.z) + __popc(wv.w);
+    if (wv.x & bit) op[__popc(wv.x & lt)] = e0;
+    op += __popc(wv.x);
+    if (wv.y & bit) op[__popc(wv.y & lt)] = e0 + 32;
+    op += __popc(wv.y);
+    if (wv.z & bit) op[__popc(wv.z & lt)] = e0 + 64;
+    op += __popc(wv.z);
+    if (wv.w & bit) op[__popc(wv.w & lt)] = e0 + 96;
+    op += __popc(wv.w);
   }
-  return base + cnt;
-}
-
-__device__ __forceinline__ int64_t expand_groups(const uint32_t* words, int ng, int64_t b4,
-                                                 int32_t* out, int64_t base, int32_t* ring) {
-  if (ASC_K1_EXPAND) return expand_direct(words, ng, b4, out, base);
-  const int lane = lane_id();
-  const uint32_t lt = lanemask_lt(), bit = 1u << lane;
-  int32_t* ob = out + base;
-  uint32_t head = 0, cnt = 0;  // buffered entries: ring[(head + i) & 255], i < cnt; head in {0, 128}
-  for (int g = 0; g < ng; g++) {
-    const uint4 wv = *reinterpret_cast<const uint4*>(words + 4 * g);  // words 4g..4g+3
-    if ((wv.x | wv.y | wv.z | wv.w) == 0) continue;
-    uint32_t r = head + cnt + __popc(wv.x & lt) + __popc(wv.y & lt) + __popc(wv.z & lt) + __popc(wv.w & lt);
-    const int32_t e0 = (int32_t)(b4 + g * GE + 4 * lane);
-    if (wv.x & bit) ring[r++ & 255] = e0;
-    if (wv.y & bit) ring[r++ & 255] = e0 + 1;
-    if (wv.z & bit) ring[r++ & 255] = e0 + 2;
-    if (wv.w & bit) ring[r & 255] = e0 + 3;
-    cnt += __popc(wv.x) + __popc(wv.y) + __popc(wv.z) + __popc(wv.w);
-    if (cnt >= 128) {
-      __syncwarp();
-#pragma unroll
-      for (int j = 0; j < 4; j++) ob[32 * j + lane] = ring[(head + 32 * j + lane) & 255];
-      __syncwarp();
-      ob += 128;
-      head ^= 128;
-      cnt -= 128;
-    }
-  }
-  __syncwarp();
-#pragma unroll
-  for (int j = 0; j < 4; j++)
-    if (32 * j + lane < (int)cnt) ob[32 * j + lane] = ring[(head + 32 * j + lane) & 255];
-  __syncwarp();
-  return base + (int64_t)(ob - (out + base)) + cnt;
+  return base + (int64_t)(op - (out + base));
 }
 
 __device__ __forceinline__ void clear_admitted(uint32_t* words, int64_t loc) {
-  const int64_t g = loc >> 7, r = loc & 127;
-  atomicAnd(&words[4 * g + (r & 3)], ~(1u << (r >> 2)));
+  atomicAnd(&words[loc >> 5], ~(1u << (loc & 31)));
 }
 
-struct Grp {  // one lane's 4 consecutive entries
+struct Grp {  // one lane's 4 entries of a group: l, 32 + l, 64 + l, 96 + l
   int64_t dl[4];
   int32_t p[4];
-  uint32_t f4;
+  uint32_t f[4];
 };
 
-template <bool VEC>
-__device__ __forceinline__ void load_grp(const StepP& P, int64_t e0, Grp& g) {
-  if (VEC && e0 + 4 <= P.Q) {
-    const longlong2 d01 = __ldcs(reinterpret_cast<const longlong2*>(P.dl + e0));
-    const longlong2 d23 = __ldcs(reinterpret_cast<const longlong2*>(P.dl + e0 + 2));
-    const int4 pv = __ldcs(reinterpret_cast<const int4*>(P.eff + e0));
-    g.f4 = __ldcs(reinterpret_cast<const unsigned int*>(P.fl + e0));
-    g.dl[0] = d01.x; g.dl[1] = d01.y; g.dl[2] = d23.x; g.dl[3] = d23.y;
-    g.p[0] = pv.x; g.p[1] = pv.y; g.p[2] = pv.z; g.p[3] = pv.w;
-  } else {
-    g.f4 = 0;
+// one lane's entries gb + 32u + lane of the group starting at gb, bounds-checked (tails, generic path)
+__device__ __forceinline__ void load_grp_s(const StepP& P, int64_t gb, Grp& g) {
+  const int lane = lane_id();
 #pragma unroll
-    for (int u = 0; u < 4; u++) {
-      const bool in = e0 + u >= 0 && e0 + u < P.Q;
-      g.dl[u] = in ? P.dl[e0 + u] : 0;
-      g.p[u] = in ? P.eff[e0 + u] : 1;
-      g.f4 |= (in ? (uint32_t)P.fl[e0 + u] : 0u) << (8 * u);
-    }
+  for (int u = 0; u < 4; u++) {
+    const int64_t e = gb + 32 * u + lane;
+    const bool in = e >= 0 && e < P.Q;
+    g.dl[u] = in ? P.dl[e] : 0;
+    g.p[u] = in ? P.eff[e] : 1;
+    g.f[u] = in ? (uint32_t)P.fl[e] : 0u;
   }
 }
 
@@ -477,7 +427,6 @@ __device__ __noinline__ int64_t pf_slow(const StepP& P, int32_t p) {
   return v;
 }
 
-static_assert(sizeof(Stage) * NST >= 256 * sizeof(int32_t), "expansion ring reuses the staging ring");
 // k1 shared memory: per-warp staging rings (which also hold task_generic's candidate buffer), per-warp
 // packed candidate buffers, and the per-warp masks of the enabled lists only
 static_assert(sizeof(Stage) * NST >= sizeof(KI) * 160, "task_generic's buffer reuses the staging ring");
@@ -642,17 +591,17 @@ __device__ __noinline__ void task_generic(const StepP& P, const TaskCtx& t, KI* 
   const bool select = t.kpos >= 0;
   bool bad = false, rng = false;
   for (int g = 0; g < t.ng; g++) {
-    const int64_t e0 = t.b4 + (int64_t)g * GE + 4 * lane;
+    const int64_t gb = t.b4 + (int64_t)g * GE;
     Grp cur;
-    load_grp<false>(P, e0, cur);
-    const int32_t r0 = g * GE + 4 * lane;
+    load_grp_s(P, gb, cur);
+    const int32_t r0 = g * GE + lane;  // entry u of this lane: r0 + 32u (task-local), gb + lane + 32u
     KI x[4];
     bool cnd[4];
     uint32_t mo_w = 0, md_w = 0;
 #pragma unroll
     for (int u = 0; u < 4; u++) {
-      const bool v = r0 + u >= t.vlo && r0 + u < t.vhi;
-      const uint32_t f = (cur.f4 >> (8 * u)) & 0xffu;
+      const bool v = r0 + 32 * u >= t.vlo && r0 + 32 * u < t.vhi;
+      const uint32_t f = cur.f[u];
       const int32_t pu = cur.p[u];
       bad |= v && pu < 1;
       rng |= v && pu >= (1 << 24);  // eff_prompt bound (keeps Σp² of a batch far from 2^64)
@@ -663,7 +612,7 @@ __device__ __noinline__ void task_generic(const StepP& P, const TaskCtx& t, KI* 
       }
       if (P.pfout && v) {
         bad |= pf > INT32_MAX;
-        __stcs(P.pfout + e0 + u, (int32_t)pf);
+        __stcs(P.pfout + gb + lane + 32 * u, (int32_t)pf);
       }
       const bool dropped = DROP && v && !(f & 1u) && t.now > cur.dl[u];
       const bool off = OFFL && v && !dropped && !(f & 3u) && cur.dl[u] - pf <= t.othr;
@@ -671,7 +620,7 @@ __device__ __noinline__ void task_generic(const StepP& P, const TaskCtx& t, KI* 
       md_w = lane == u ? md : md_w;
       mo_w = lane == u ? mo : mo_w;
       const int64_t spf = P.kpf > 0 ? pf : (P.kpf < 0 ? -pf : 0);
-      x[u] = KI{(P.kdl ? cur.dl[u] : 0) + spf, (int32_t)(e0 + u)};
+      x[u] = KI{(P.kdl ? cur.dl[u] : 0) + spf, (int32_t)(gb + lane + 32 * u)};
       cnd[u] = select && v && !dropped && ki_less(x[u], st.thr);
     }
     if (lane < 4) {
@@ -748,22 +697,26 @@ __device__ __forceinline__ bool task_fast(const StepP& P, const TaskCtx& t, Stag
       if (l < 8) cp_async16(&sg.fl[4 * l], gfl + gi * GE);
     }
     cp_commit();
-    const int64_t e0 = b4 + (int64_t)g * GE + 4 * lane;
+    const int64_t gb = b4 + (int64_t)g * GE;  // this lane's entries: gb + lane + 32u
     Grp cur;
     if (g < nfull) {
       cp_wait<NST - 1>();
-      __syncwarp();  // flag bytes were copied by lanes 0-7
+      __syncwarp();  // every lane reads entries other lanes copied
       const Stage& sg = stg[g % NST];
-      const longlong2 d01 = sg.dl[2 * l], d23 = sg.dl[2 * l + 1];
-      const int4 pv = sg.eff[l];
-      cur.f4 = sg.fl[l];
-      cur.dl[0] = d01.x; cur.dl[1] = d01.y; cur.dl[2] = d23.x; cur.dl[3] = d23.y;
-      cur.p[0] = pv.x; cur.p[1] = pv.y; cur.p[2] = pv.z; cur.p[3] = pv.w;
+      const int64_t* sd = reinterpret_cast<const int64_t*>(sg.dl);
+      const int32_t* se = reinterpret_cast<const int32_t*>(sg.eff);
+      const uint8_t* sf = reinterpret_cast<const uint8_t*>(sg.fl);
+#pragma unroll
+      for (int u = 0; u < 4; u++) {  // consecutive lanes, consecutive entries: conflict-free
+        cur.dl[u] = sd[32 * u + l];
+        cur.p[u] = se[32 * u + l];
+        cur.f[u] = sf[32 * u + l];
+      }
     } else {
-      load_grp<false>(P, e0, cur);
+      load_grp_s(P, gb, cur);
     }
-    const int32_t r0 = g * GE + 4 * lane;
-    const uint32_t l0 = (uint32_t)r0 << PK_LOC;  // task-local index of this lane's first entry
+    const int32_t r0 = g * GE + lane;            // task-local index of this lane's entry u: r0 + 32u
+    const uint32_t l0 = (uint32_t)r0 << PK_LOC;
     // candidates are filtered on the packed word's high half (the key) only: key <= the
     // threshold's key keeps every entry below the threshold (plus, rarely, ties above it, which the
     // merge sorts past it); the full word is packed only for the candidates, in the append below
@@ -776,7 +729,7 @@ __device__ __forceinline__ bool task_fast(const StepP& P, const TaskCtx& t, Stag
       constexpr bool IN = decltype(interior)::value;
 #pragma unroll
       for (int u = 0; u < 4; u++) {  // branch-free: every lane runs the same instructions
-        const bool v = IN || (uint32_t)(r0 + u - t.vlo) < vspan;
+        const bool v = IN || (uint32_t)(r0 + 32 * u - t.vlo) < vspan;
         const int64_t dd = cur.dl[u] + nowc;
         const uint32_t lo1 = (uint32_t)dd, hi1 = (uint32_t)((uint64_t)dd >> 32);
         const int32_t q = cur.p[u] - 1;
@@ -786,9 +739,9 @@ __device__ __forceinline__ bool task_fast(const StepP& P, const TaskCtx& t, Stag
         accQ |= v ? (uint32_t)q : 0u;
         accF |= v ? (uint32_t)pf : 0u;
         pfv[u] = pf;
-        if (!IN && has_pfout && v) __stcs(P.pfout + e0 + u, pf);
+        if (!IN && has_pfout && v) __stcs(P.pfout + gb + l + 32 * u, pf);
         const int32_t d1 = (int32_t)lo1;  // deadline - now + 2^30
-        const uint32_t f = cur.f4 >> (8 * u);
+        const uint32_t f = cur.f[u];
         const bool dropped = DROP && v && !(f & 1u) && d1 < (int32_t)WIN;
         const bool off = OFFL && v && !dropped && !(f & 3u) && d1 - pf <= othr1;
         if (DROP) md[u] = __ballot_sync(FULL, dropped);
@@ -798,12 +751,11 @@ __device__ __forceinline__ bool task_fast(const StepP& P, const TaskCtx& t, Stag
         cnd[u] = select && v && !dropped && kw[u] <= thr_hi;
       }
     };
-    if (r0 - 4 * lane >= t.vlo && r0 - 4 * lane + GE <= t.vhi) {
+    if (r0 - lane >= t.vlo && r0 - lane + GE <= t.vhi) {
       body(std::true_type{});
-      if (has_pfout) {
-        if (VEC) __stcs(reinterpret_cast<int4*>(P.pfout + e0), make_int4(pfv[0], pfv[1], pfv[2], pfv[3]));
-        else for (int u = 0; u < 4; u++) __stcs(P.pfout + e0 + u, pfv[u]);
-      }
+      if (has_pfout)
+#pragma unroll
+        for (int u = 0; u < 4; u++) __stcs(P.pfout + gb + l + 32 * u, pfv[u]);  // coalesced per u
     } else {
       body(std::false_type{});
     }
@@ -815,7 +767,7 @@ __device__ __forceinline__ bool task_fast(const StepP& P, const TaskCtx& t, Stag
 #pragma unroll
       for (int u = 0; u < 4; u++)
         st.append(((uint64_t)kw[u] << 32) |
-                      (uint64_t)(l0 + ((uint32_t)u << PK_LOC) + ((uint32_t)(cur.p[u] - 1) & (uint32_t)PK_PMASK)),
+                      (uint64_t)(l0 + ((uint32_t)(32 * u) << PK_LOC) + ((uint32_t)(cur.p[u] - 1) & (uint32_t)PK_PMASK)),
                   cnd[u]);
       st.drain();
     }
@@ -894,9 +846,8 @@ __global__ void __launch_bounds__(K1W * 32, ASC_K1_MINB) k1_tasks(const __grid_c
       for (int r = 0; r < KPL; r++)
         if (OFFL && adm[r]) clear_admitted(s_off[w], top[r].i - b4);
       __syncwarp();
-      int32_t* ring = reinterpret_cast<int32_t*>(&s_stage[w][0]);  // the staging ring is idle now
-      const int64_t no = OFFL ? expand_groups(s_off[w], ng, b4, P.off_idx, lo, ring) : lo;
-      const int64_t nd = DROP ? expand_groups(s_drop[w], ng, b4, P.drop_idx, lo, ring) : lo;
+      const int64_t no = OFFL ? expand_groups(s_off[w], ng, b4, P.off_idx, lo) : lo;
+      const int64_t nd = DROP ? expand_groups(s_drop[w], ng, b4, P.drop_idx, lo) : lo;
       if (lane == 0) { P.off_cnt[s] = (int32_t)(no - lo); P.drop_cnt[s] = (int32_t)(nd - lo); }
     } else {
       const int64_t mt = P.mtask_off[s] + c;
@@ -1461,9 +1412,9 @@ __global__ void __launch_bounds__(WARPS * 32) k2_segments(const __grid_constant_
           const int64_t e = A.a[r].i;
           const int64_t t = (e - lo) / CH;
           const int64_t b4 = (lo + t * CH) & ~int64_t(ALN - 1);
-          const int64_t loc = e - b4, g = loc >> 7, rr = loc & 127;
-          const uint32_t bit = 1u << (rr >> 2);
-          const uint32_t old = atomicAnd(&P.moff[(m0 + t) * MW + 4 * g + (rr & 3)], ~bit);
+          const int64_t loc = e - b4;
+          const uint32_t bit = 1u << (loc & 31);
+          const uint32_t old = atomicAnd(&P.moff[(m0 + t) * MW + (loc >> 5)], ~bit);
           if (old & bit) atomicSub(&P.coff[m0 + t], 1);
         }
       }
@@ -1493,7 +1444,6 @@ __global__ void __launch_bounds__(WARPS * 32) k2_segments(const __grid_constant_
 constexpr int K3P = 4;
 constexpr int K3W = (NG + K3P - 1) / K3P;  // groups per part
 __global__ void __launch_bounds__(WARPS * 32) k3_expand(const __grid_constant__ StepP P) {
-  __shared__ int32_t s_ring[WARPS][256];
   __shared__ __align__(16) uint32_t s_words[WARPS][2][4 * K3W];
   if (P.mtask_off[P.S] == 0) return;  // no multi-task segment
   const int w = threadIdx.x >> 5, lane = lane_id();
@@ -1533,8 +1483,8 @@ __global__ void __launch_bounds__(WARPS * 32) k3_expand(const __grid_constant__ 
     }
     __syncwarp();
     const int64_t bg = b4 + (int64_t)g0 * GE;
-    expand_groups(s_words[w][0], g1 - g0, bg, P.off_idx, lo + P.coff[mt] + po, s_ring[w]);
-    expand_groups(s_words[w][1], g1 - g0, bg, P.drop_idx, lo + P.cdrop[mt] + pd, s_ring[w]);
+    expand_groups(s_words[w][0], g1 - g0, bg, P.off_idx, lo + P.coff[mt] + po);
+    expand_groups(s_words[w][1], g1 - g0, bg, P.drop_idx, lo + P.cdrop[mt] + pd);
     __syncwarp();
   }
 }
