@@ -62,6 +62,8 @@ static __device__ __noinline__ int64_t lat_from_FM(const Model& md, uint64_t F, 
 
 // Decode-only batch of B_d requests with context sum sl (a2's TBT term, a6 for decode steps).
 // The fp64 shadow below guards the uint64 products against wrapping (as wraps() does).
+// INL: the fp64 evaluation inlined (one hot call site) instead of the shared out-of-line copy
+template <bool INL = false>
 __device__ __forceinline__ int64_t lat_decode(const Model& md, uint64_t Bd, uint64_t sl) {
   const uint64_t F = md.dF_bd * Bd + md.dF_sl * sl;
   const uint64_t M = md.dM_0 + md.dM_bd * Bd + md.dM_sl * sl;
@@ -69,7 +71,7 @@ __device__ __forceinline__ int64_t lat_decode(const Model& md, uint64_t Bd, uint
   const double bd = (double)Bd, s = (double)sl;
   if ((double)md.dF_bd * bd + (double)md.dF_sl * s >= 0x1p62 ||
       (double)md.dM_0 + (double)md.dM_bd * bd + (double)md.dM_sl * s >= 0x1p62) return -1;
-  return lat_from_FM(md, F, M);
+  return INL ? us_of_t(t_from_FM(md, F, M)) : lat_from_FM(md, F, M);
 }
 
 // uint64 wrap guard: F and M are sums of products of non-negative integers, so no
@@ -98,6 +100,7 @@ __host__ __device__ inline bool wraps_chunked(const Model& md, uint64_t sc, uint
 
 // Latency in integer microseconds of a batch given its integer moments (G17, G18).
 // Returns -1 (and the caller raises ERR_RANGE) when F or M reaches 2^53.
+template <bool INL = false>  // INL: the fp64 evaluation inlined (device), as lat_decode<true>
 __host__ __device__ inline int64_t lat_us(const Model& md, uint64_t Bp, uint64_t sp, uint64_t sp2,
                                           uint64_t spc, uint64_t Bd, uint64_t sl) {
   const uint64_t tok = sp + Bd;
@@ -108,7 +111,7 @@ __host__ __device__ inline int64_t lat_us(const Model& md, uint64_t Bp, uint64_t
   const uint64_t M = md.L * (G * md.W + tok * md.MT + attnM) * md.d;
   if (F >= TWO53 || M >= TWO53 || wraps(md, sp, sp2, 3 * spc, Bd, sl, G)) return -1;
 #ifdef __CUDA_ARCH__
-  return lat_from_FM(md, F, M);
+  return INL ? us_of_t(t_from_FM(md, F, M)) : lat_from_FM(md, F, M);
 #else
   volatile double tM = (double)M / md.MH;
   volatile double tF = (double)F / md.FH;

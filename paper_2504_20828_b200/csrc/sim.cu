@@ -1284,7 +1284,8 @@ __device__ RD_ATTR int64_t run_decode(Wp w, int k, int64_t T_limit) {
       const int32_t cm = modb(c);
       const int32_t need = hA[cm == 0 ? 0 : bs - cm];  // slots with (r0 + c) mod bs == 0
       const int64_t cum = ncarry + warp_incl_scan(need);
-      const int64_t lc = lat_decode(P.md, (uint64_t)Bd, (uint64_t)(S + (int64_t)(c + 1) * Bd));
+      // (the fp64 evaluation inlined here: one lane per decode event, the hottest latency site)
+      const int64_t lc = lat_decode<true>(P.md, (uint64_t)Bd, (uint64_t)(S + (int64_t)(c + 1) * Bd));
       const int64_t incl = warp_incl_scan(lc < 0 ? (int64_t)0 : lc);
       const int64_t tc = E + tcarry + incl - (lc < 0 ? 0 : lc);  // formation time of event c
       const bool ok = c < Jmax && tc < T_limit && cum <= kvf && lc > 0;
