@@ -453,7 +453,7 @@ def main():
                      "note": "algorithmic bytes = SURVEY 8(d)'s 44 B per request + 12 B per queued-request "
                              "evaluation; the sorted-queue kernel touches O(admitted + offloaded) entries per "
                              "formation, not every queued one, so this credits reads it does not make (an "
-                             "upper bound); traffic = ncu dram bytes of one launch (profiles/ncu_traffic.json). "
+                             "upper bound); traffic = ncu dram bytes of one launch (profiles/ncu_traffic_r02.json). "
                              "The event loop is a dependent chain per trace: issue-bound, see issue_roofline",
                      "algorithmic_bytes": algo, "kernel_ms": sim_ms,
                      "kernel_share": sim_ms / ms_step},
