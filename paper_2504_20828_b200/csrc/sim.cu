@@ -254,6 +254,7 @@ struct DRec {
   int64_t T, bd, lat;
   int32_t nadm, noff, ndrop, npre;
   bool on;
+  bool dec;  // the formation is a plain decode step, left to the caller's decode_batch
 };
 __device__ __forceinline__ void log_rec(Wp w, int k, const DRec& r) {
   if (r.on) digest_log(w, k, r.T, r.nadm, r.bd, r.noff, r.ndrop, r.npre, r.lat);
@@ -793,8 +794,8 @@ __device__ __forceinline__ int64_t form_lp(Wp w, int k, int64_t T, DRec& rec) {
   if (I.wq_len == 0) {
     if (I.ds_len == 0) return 0;  // parked
     npre = decode_prep(w, k);
-    if (npre == 0) {  // no eviction: the common case, a pure decode step
-      decode_batch(I, k, T);
+    if (npre == 0) {  // no eviction: the common case, a pure decode step (the caller runs it)
+      rec.dec = true;
       return 1;
     }
     // the queue now holds the evicted decodes
@@ -916,7 +917,7 @@ __device__ __forceinline__ int64_t form_hp(Wp w, int k, int64_t T, DRec& rec) {
     if (I.ds_len == 0) return 0;  // parked
     if (I.papp || I.need_sum <= I.kv_free) {  // decode-only batch without eviction: hot path
       decode_prep(w, k);
-      decode_batch(I, k, T);
+      rec.dec = true;  // (the caller runs it)
       return 1;
     }
   }
@@ -1035,7 +1036,9 @@ __device__ __noinline__ int64_t form_baseline(Wp w, int k, int64_t T) {
   if (P.mode != 1) return form_sar(w, k, T);
   DRec rec;
   rec.on = false;
+  rec.dec = false;
   const int64_t r = form_hp(w, k, T, rec);
+  if (rec.dec) decode_batch(w.SI()[k], k, T);
   log_rec(w, k, rec);
   return r;
 }
@@ -1553,8 +1556,10 @@ __global__ void __launch_bounds__(SW * 32, MINB) sim_kernel() {
         const int k = __ffs(m) - 1;
         DRec rec;
         rec.on = false;
+        rec.dec = false;
         const int64_t r = k >= n_lp ? form_hp(w, k, T, rec)
                                     : ((PLAIN || P.mode == 0) ? form_lp(w, k, T, rec) : form_baseline(w, k, T));
+        if (rec.dec) decode_batch(w.SI()[k], k, T);  // one site for both instance kinds
         log_rec(w, k, rec);
         decisions += r & 1;
         evals += r >> 1;
