@@ -438,7 +438,7 @@ __device__ __noinline__ int32_t drop_step(Wp w, int k, int64_t T) {
   I.wq_len = out;
   I.tk_live = tk;
   __syncwarp();
-  if (!I.hp) sort_ids(w, P.scr_drop + w.base(), nd);  // LP queue order is key order
+  if (!I.hp && nd > 1) sort_ids(w, P.scr_drop + w.base(), nd);  // LP queue order is key order
   return nd;
 }
 
@@ -729,7 +729,7 @@ __device__ LA_ATTR int lp_admit(Wp w, int k, int64_t T, int32_t ndrop,
       }
       rem = out;
     }
-    sort_ids(w, P.scr_off + w.base(), noff);  // dispatch and digest in ascending id order
+    if (noff > 1) sort_ids(w, P.scr_off + w.base(), noff);  // dispatch and digest in ascending id order
   }
   const int32_t kvf = I.kv_free - (int32_t)used;
   __syncwarp();
@@ -822,7 +822,7 @@ __device__ __forceinline__ int64_t form_lp(Wp w, int k, int64_t T, DRec& rec) {
 // FCFS prefill-first under the (elastic) token limit (G27-G28).  The
 // vLLM-like baseline (G46) is the same prefill-first rule on an LP-type instance: its queue is in
 // policy-key order, the limit is lp_token_budget and the batch cap applies.
-__device__ __noinline__ int32_t hp_prefill(Wp w, int k, int64_t T, uint64_t* mom) {
+__device__ __forceinline__ int32_t hp_prefill(Wp w, int k, int64_t T, uint64_t* mom) {
   SInst& I = w.SI()[k];
   const int lane = lane_id();
   const int64_t o = ioff(k, w);
@@ -891,16 +891,24 @@ __device__ __forceinline__ int64_t form_hp_general(Wp w, int k, int64_t T, DRec&
   int32_t nadm = 0, npre = 0;
   int64_t bd = 0;
   bool batch = false;
-  if (I.wq_len > 0) { nadm = hp_prefill(w, k, T, mom); batch = nadm > 0; }  // prefill first
-  if (!batch && I.ds_len > 0) {
+  // prefill first; if nothing is admitted, the decodes (after eviction); if every decode was evicted
+  // (G43), prefill again -- one hp_prefill call site for both attempts
+  bool try_pf = I.wq_len > 0;
+  #pragma unroll 1
+  for (int pass = 0; pass < 2; pass++) {
+    if (try_pf) {
+      nadm = hp_prefill(w, k, T, mom);
+      batch = nadm > 0;
+    }
+    if (batch || pass == 1 || I.ds_len == 0) break;
     npre = decode_prep(w, k);
     if (I.ds_len > 0) {
       batch = true;
       bd = I.ds_len;
-    } else if (I.wq_len > 0) {  // every decode was evicted (G43)
-      nadm = hp_prefill(w, k, T, mom);
-      batch = nadm > 0;
+      break;
     }
+    try_pf = I.wq_len > 0;
+    if (!try_pf) break;
   }
   int64_t l = 0;
   if (batch) {
